@@ -1,0 +1,166 @@
+/*
+ * fsx.h — C ABI of the B200-native StencilFFT-P periodic solver
+ * (libfsx.so, paper_2105_06676_b200/csrc).
+ *
+ * Drop-in boundary for the reference C++ library's periodic hot path
+ * (/root/reference/proj/include/fftstencil/periodic.hpp:43-65 and the
+ * spectral/FFT building blocks it is built from).  Plain pointers and sizes;
+ * no C++ or torch types.  Every entry point returns an fsx_status; the
+ * thread-local message of the last failure is fsx_last_error().
+ *
+ * Data layout (proj/include/fftstencil/grid.hpp:17-20): a grid of
+ * prod(dims) cells x `fields` values, row-major over the dims with the field
+ * index innermost, fp64.  Complex arrays are interleaved (re, im) fp64.
+ * A stencil kernel is `ntaps` offsets (ntaps x rank int64, row-major) and
+ * `ntaps` blocks (ntaps x fields x fields fp64, row-major); repeated offsets
+ * accumulate and the taps are used in sorted-offset order
+ * (proj/src/kernel.cpp:7-22).
+ *
+ * Reference error types map to status codes: SpecError -> FSX_ERR_SPEC,
+ * NumericError -> FSX_ERR_NUMERIC (proj/include/fftstencil/errors.hpp:9-37).
+ */
+#ifndef FSX_H_
+#define FSX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum fsx_status {
+    FSX_OK = 0,
+    FSX_ERR_SPEC = 1,      /* reference SpecError: invalid shapes, kernels, arguments */
+    FSX_ERR_NUMERIC = 2,   /* reference NumericError: non-finite result / residue blow-up */
+    FSX_ERR_CUDA = 3,      /* CUDA runtime failure (no device, launch error, ...) */
+    FSX_ERR_NCCL = 4,      /* reserved for the multi-GPU path */
+    FSX_ERR_OOM = 5        /* device allocation failed */
+} fsx_status;
+
+#define FSX_MAX_RANK 8
+
+/* GridShape (proj/include/fftstencil/grid.hpp:21-83) */
+typedef struct fsx_shape {
+    int32_t rank;
+    int32_t fields;
+    int64_t dims[FSX_MAX_RANK];
+} fsx_shape;
+
+/* StencilKernel (proj/include/fftstencil/kernel.hpp:19-56) */
+typedef struct fsx_kernel {
+    int32_t rank;
+    int32_t fields;
+    int64_t ntaps;
+    const int64_t* offsets; /* ntaps * rank */
+    const double* blocks;   /* ntaps * fields * fields */
+} fsx_kernel;
+
+/* StageTimings (proj/include/fftstencil/periodic.hpp:14-23): seconds,
+ * ACCUMULATED (+=) like the reference's Stopwatch sinks.  On the GPU the
+ * stages are CUDA-event intervals on the solve's stream: forward_fft = the
+ * forward passes before the fused spectral pass, squaring = the fused pass
+ * (last forward line FFT + symbol^T + multiply + first inverse line FFT),
+ * hadamard = 0 when fused, inverse_fft = remaining inverse passes, the C2R
+ * and the non-finite scan. */
+typedef struct fsx_stage_timings {
+    double forward_fft;
+    double squaring;
+    double hadamard;
+    double inverse_fft;
+    double boundary_recursion;
+} fsx_stage_timings;
+
+/* Options (NULL = defaults). */
+typedef struct fsx_options {
+    int32_t device;     /* CUDA device ordinal (default 0) */
+    int32_t path;       /* 0 = auto (fused fast path when eligible), 1 = force general path */
+    int32_t reserved0;
+    int32_t reserved1;
+    void* stream;       /* cudaStream_t to enqueue on (NULL = library stream) */
+} fsx_options;
+
+/* Opaque spectrum/plan cache (proj/include/fftstencil/periodic.hpp:28-35). */
+typedef struct fsx_spectrum_cache fsx_spectrum_cache;
+
+/* ---------------------------------------------------------------- solvers
+ * Host pointers; `out` may alias `a0`.  T == 0 copies a0 bit-exactly after
+ * validation (proj/src/periodic.cpp:78-79). */
+
+/* solve_periodic (proj/src/periodic.cpp:76-86) */
+fsx_status fsx_solve_periodic(const fsx_shape* shape, const double* a0, const fsx_kernel* k,
+                              uint64_t T, double* out, const fsx_options* opt,
+                              fsx_stage_timings* st);
+
+/* solve_periodic_vector (proj/src/periodic.cpp:101-106): requires fields >= 2 */
+fsx_status fsx_solve_periodic_vector(const fsx_shape* shape, const double* a0, const fsx_kernel* k,
+                                     uint64_t T, double* out, const fsx_options* opt,
+                                     fsx_stage_timings* st);
+
+/* solve_periodic_cached + SpectrumCache (proj/src/periodic.cpp:67-99): the
+ * cache memoises the device plan (symbol tables, workspaces) by dims, like
+ * the reference memoises the spectrum by dims only. */
+fsx_spectrum_cache* fsx_spectrum_cache_create(void);
+void fsx_spectrum_cache_destroy(fsx_spectrum_cache* cache);
+fsx_status fsx_solve_periodic_cached(const fsx_shape* shape, const double* a0, const fsx_kernel* k,
+                                     uint64_t T, fsx_spectrum_cache* cache, double* out,
+                                     const fsx_options* opt, fsx_stage_timings* st);
+
+/* solve_periodic_implicit (proj/src/periodic.cpp:108-124): scalar q, s */
+fsx_status fsx_solve_periodic_implicit(const fsx_shape* shape, const double* a0, const fsx_kernel* q,
+                                       const fsx_kernel* s, uint64_t T, double* out,
+                                       const fsx_options* opt, fsx_stage_timings* st);
+
+/* Device-resident variant: d_a0 / d_out are device pointers (may alias);
+ * the work is enqueued on opt->stream and the call returns without
+ * synchronizing.  The non-finite check is deferred: fsx_device_check()
+ * synchronizes that stream and reports FSX_ERR_NUMERIC if any solve
+ * enqueued since the last check produced a non-finite value. */
+fsx_status fsx_solve_periodic_device(const fsx_shape* shape, const double* d_a0, const fsx_kernel* k,
+                                     uint64_t T, double* d_out, const fsx_options* opt);
+fsx_status fsx_device_check(const fsx_options* opt);
+
+/* ---------------------------------------------------------------- building blocks
+ * (host pointers, complex = interleaved fp64) */
+
+/* multi_fft / multi_ifft (proj/src/fft.cpp:159-192): per-axis DFT, fields
+ * transformed independently; inverse carries 1/n per axis. */
+fsx_status fsx_multi_fft(const fsx_shape* shape, const double* in, double* out, int32_t inverse);
+
+/* spectrum_from_kernel (proj/src/spectrum.cpp:21-45): cells * m * m blocks */
+fsx_status fsx_spectrum_from_kernel(const fsx_shape* shape, const fsx_kernel* k, double* out);
+
+/* pow_spectrum (proj/src/spectrum.cpp:47-83) */
+fsx_status fsx_pow_spectrum(const fsx_shape* shape, const double* blocks, uint64_t T, double* out);
+
+/* pseudo_inverse_spectrum (proj/src/spectrum.cpp:85-96), scalar only */
+fsx_status fsx_pseudo_inverse_spectrum(const fsx_shape* shape, const double* blocks, double* out);
+
+/* multiply_spectra (proj/src/spectrum.cpp:98-109) */
+fsx_status fsx_multiply_spectra(const fsx_shape* shape, const double* a, const double* b, double* out);
+
+/* hadamard (proj/src/spectrum.cpp:111-134): y = lam x per frequency */
+fsx_status fsx_hadamard(const fsx_shape* shape, const double* lam, const double* x, double* y);
+
+/* ---------------------------------------------------------------- introspection */
+const char* fsx_last_error(void);
+int32_t fsx_version(void);
+int32_t fsx_device_count(void);
+
+/* Plan description for measurement: which path a problem takes, how many
+ * of our kernels one solve launches and the algorithmic HBM bytes of the
+ * minimal pass schedule. */
+typedef struct fsx_plan_info {
+    int32_t path;            /* 1 = fused R2C (rank 2/3), 2 = 1D four-step row-pair, 3 = general */
+    int32_t launches;        /* kernels per solve */
+    int64_t alg_bytes;       /* algorithmic bytes per solve (all passes) */
+    int64_t fused_bytes;     /* algorithmic bytes of the dominant (fused) kernel */
+    int64_t work_bytes;      /* device workspace of the plan */
+} fsx_plan_info;
+fsx_status fsx_plan_describe(const fsx_shape* shape, const fsx_kernel* k, const fsx_options* opt,
+                             fsx_plan_info* info);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSX_H_ */

@@ -1,0 +1,41 @@
+"""B200-native StencilFFT-P (arXiv 2105.06676) periodic stencil solver.
+
+Drop-in for the reference fftstencil library's periodic hot path
+(solve_periodic / solve_periodic_vector / _cached / _implicit and the FFT /
+spectrum building blocks).  The numerical path is hand-written sm_100a CUDA
+in ``csrc/`` behind the C ABI ``include/fsx.h`` (``libfsx.so``); this package
+is the Python host mirror of the reference interface.
+"""
+from .fftstencil import (  # noqa: F401
+    ComplexGrid,
+    CudaError,
+    DiagonalSpectrum,
+    Error,
+    FieldGrid,
+    GridShape,
+    NumericError,
+    SpecError,
+    SpectrumCache,
+    StageTimings,
+    StencilKernel,
+    device_check,
+    device_count,
+    fft,
+    fold_kernels,
+    hadamard,
+    multi_fft,
+    multi_ifft,
+    multiply_spectra,
+    plan_describe,
+    pow_spectrum,
+    pseudo_inverse_spectrum,
+    solve_periodic,
+    solve_periodic_cached,
+    solve_periodic_device,
+    solve_periodic_implicit,
+    solve_periodic_vector,
+    spectrum_from_kernel,
+)
+from . import _lib  # noqa: F401
+
+__all__ = [n for n in dir() if not n.startswith("_")]

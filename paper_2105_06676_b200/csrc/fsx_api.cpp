@@ -1,0 +1,1067 @@
+// Host orchestration + C ABI of the B200 StencilFFT-P solver (include/fsx.h).
+//
+// Mirrors the reference periodic solver's contract (proj/src/periodic.cpp,
+// proj/src/kernel.cpp:7-49): validation and error types, T == 0 short cut,
+// stage timings accumulated with +=, NumericError on non-finite output (and
+// on the imaginary residue where a complex pipeline exists).  The numerical
+// work runs only on the GPU: there is no CPU fallback; a missing or failing
+// device surfaces as FSX_ERR_CUDA.
+//
+// Three plan kinds:
+//   1  fused R2C, rank 2/3, m = 1, pow2 dims: r2c rows -> strided passes ->
+//      fused (axis-0 FFT, symbol^T, inverse FFT) -> strided passes -> c2r rows
+//   2  1D, m in {1, 2}, pow2: four-step column pass -> fused row-pair pass
+//      -> inverse column pass (real packing or two-for-one pairing)
+//   3  general: complex promotion, per-axis passes (pow2 <= 8192 in one CTA,
+//      pow2 up to 2^26 as a four-step split, other lengths by direct DFT),
+//      m x m spectral kernel, inverse passes, real part + residue scan.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "fsx.h"
+#include "fsx_kernels.h"
+
+namespace {
+
+using fsx::i64;
+using fsx::u64;
+
+struct SpecErr : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct NumErr : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaErr : std::runtime_error {
+    cudaError_t code;
+    CudaErr(cudaError_t c, const std::string& what)
+        : std::runtime_error(what + ": " + cudaGetErrorString(c)), code(c) {}
+};
+
+thread_local std::string g_err;
+
+#define FSX_CK(x)                                     \
+    do {                                              \
+        cudaError_t e_ = (x);                         \
+        if (e_ != cudaSuccess) throw CudaErr(e_, #x); \
+    } while (0)
+
+bool is_pow2(i64 n) { return n > 0 && (n & (n - 1)) == 0; }
+int ilog2(i64 n) {
+    int r = 0;
+    while ((i64(1) << r) < n) ++r;
+    return r;
+}
+
+// ------------------------------------------------------------------ device buffers
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void ensure(size_t b) {
+        if (b == 0) b = 16;
+        if (b <= bytes && p) return;
+        release();
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            throw CudaErr(e, "cudaMalloc(" + std::to_string(b) + " bytes)");
+        }
+        bytes = b;
+    }
+    template <class T>
+    T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// ------------------------------------------------------------------ shapes and kernels
+struct Shape {
+    std::vector<i64> dims;
+    int fields = 1;
+    i64 cells = 1;
+    int rank() const { return (int)dims.size(); }
+    i64 values() const { return cells * fields; }
+};
+
+// GridShape invariants (proj/include/fftstencil/grid.hpp:21-45)
+Shape parse_shape(const fsx_shape* s) {
+    if (!s) throw SpecErr("GridShape: null shape");
+    if (s->rank < 1 || s->rank > FSX_MAX_RANK) throw SpecErr("GridShape: need at least one dimension");
+    if (s->fields < 1) throw SpecErr("GridShape: fields must be >= 1");
+    Shape r;
+    r.fields = s->fields;
+    __int128 n = 1;
+    for (int a = 0; a < s->rank; ++a) {
+        if (s->dims[a] < 1) throw SpecErr("GridShape: every dimension must be >= 1");
+        n *= s->dims[a];
+        if (n * r.fields > (__int128)INT64_MAX) throw SpecErr("GridShape: total value count overflows");
+        r.dims.push_back(s->dims[a]);
+    }
+    r.cells = (i64)n;
+    return r;
+}
+
+struct Taps {
+    int rank = 1, m = 1;
+    std::map<std::vector<i64>, std::vector<double>> map;  // sorted offset -> m*m block
+};
+
+// StencilKernel + add_tap (proj/src/kernel.cpp:7-22): accumulate repeats,
+// reject non-finite coefficients.
+Taps parse_kernel(const fsx_kernel* k) {
+    if (!k) throw SpecErr("StencilKernel: null kernel");
+    if (k->rank < 1) throw SpecErr("StencilKernel: rank must be >= 1");
+    if (k->fields < 1) throw SpecErr("StencilKernel: fields must be >= 1");
+    if (k->ntaps < 0 || (k->ntaps > 0 && (!k->offsets || !k->blocks)))
+        throw SpecErr("StencilKernel: bad tap arrays");
+    Taps t;
+    t.rank = k->rank;
+    t.m = k->fields;
+    const int mm = t.m * t.m;
+    for (i64 j = 0; j < k->ntaps; ++j) {
+        const double* b = k->blocks + j * mm;
+        for (int i = 0; i < mm; ++i)
+            if (!std::isfinite(b[i])) throw SpecErr("StencilKernel: non-finite coefficient");
+        std::vector<i64> off(k->offsets + j * t.rank, k->offsets + (j + 1) * t.rank);
+        auto it = t.map.find(off);
+        if (it == t.map.end()) t.map.emplace(off, std::vector<double>(b, b + mm));
+        else
+            for (int i = 0; i < mm; ++i) it->second[i] += b[i];
+    }
+    return t;
+}
+
+// require_fits (proj/src/kernel.cpp:38-49)
+void require_fits(const Taps& t, const Shape& s) {
+    if (t.map.empty()) throw SpecErr("StencilKernel: at least one tap required");
+    if (s.rank() != t.rank) throw SpecErr("StencilKernel: grid rank mismatch");
+    if (s.fields != t.m) throw SpecErr("StencilKernel: grid field count mismatch");
+    for (int a = 0; a < t.rank; ++a) {
+        i64 reach = 0;
+        for (const auto& kv : t.map) reach = std::max<i64>(reach, kv.first[a] < 0 ? -kv.first[a] : kv.first[a]);
+        if (reach >= s.dims[a]) throw SpecErr("StencilKernel: tap offset exceeds dimension " + std::to_string(a));
+    }
+}
+
+// ------------------------------------------------------------------ twiddle / phase tables
+double2 expi_neg(i64 x, i64 n) {
+    // exp(-2 pi i x / n) rounded from x87 long double
+    const long double pi = 3.141592653589793238462643383279502884L;
+    long double f = (long double)(x % n) / (long double)n;
+    if (f > 0.5L) f -= 1.0L;
+    const long double ang = -2.0L * pi * f;
+    return make_double2((double)cosl(ang), (double)sinl(ang));
+}
+
+struct HostTable {
+    std::vector<double2> lo, hi;
+    int shift = 0;
+    i64 mask = 0, n = 1;
+};
+
+HostTable make_phase(i64 n) {
+    HostTable t;
+    t.n = n;
+    if (n <= 65536) {
+        t.lo.resize(n);
+        for (i64 x = 0; x < n; ++x) t.lo[x] = expi_neg(x, n);
+        return t;
+    }
+    int bits = ilog2(n);
+    int h = (bits + 1) / 2;
+    const i64 lo_n = i64(1) << h;
+    t.shift = h;
+    t.mask = lo_n - 1;
+    t.lo.resize(lo_n);
+    for (i64 x = 0; x < lo_n; ++x) t.lo[x] = expi_neg(x, n);
+    const i64 hi_n = (n + lo_n - 1) / lo_n;
+    t.hi.resize(hi_n);
+    for (i64 j = 0; j < hi_n; ++j) t.hi[j] = expi_neg(j * lo_n, n);
+    return t;
+}
+
+// Packs several host tables into one device buffer; returns PhaseTables
+// pointing into it.
+struct TableSet {
+    std::vector<double2> host;
+    struct Ref {
+        size_t lo, hi;
+        int shift;
+        i64 mask, n;
+    };
+    std::vector<Ref> refs;
+    DevBuf dev;
+    int add(const HostTable& t) {
+        Ref r{host.size(), 0, t.shift, t.mask, t.n};
+        host.insert(host.end(), t.lo.begin(), t.lo.end());
+        r.hi = host.size();
+        host.insert(host.end(), t.hi.begin(), t.hi.end());
+        refs.push_back(r);
+        return (int)refs.size() - 1;
+    }
+    void upload() {
+        dev.ensure(host.size() * sizeof(double2));
+        FSX_CK(cudaMemcpy(dev.p, host.data(), host.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    }
+    fsx::PhaseTable get(int i) const {
+        fsx::PhaseTable p;
+        const Ref& r = refs[i];
+        p.lo = dev.as<double2>() + r.lo;
+        p.hi = dev.as<double2>() + r.hi;
+        p.shift = r.shift;
+        p.mask = r.mask;
+        p.n = r.n;
+        return p;
+    }
+};
+
+// ------------------------------------------------------------------ plans
+enum PlanKind { kFusedR2C = 1, kRowPair1D = 2, kGeneral = 3 };
+
+struct AxisStep {
+    int kind = 0;  // 0 pow2 pass, 1 direct DFT
+    fsx::AxisGeom g;
+    fsx::StepTwiddle tw;
+    int table = -1;  // direct DFT phase table
+};
+
+struct GenAxis {
+    i64 n = 1, n1 = 0, n2 = 0;  // split: n = n1 * n2 (n1 == 0: not split)
+    int direct = 0;
+    int table = -1;             // phase table for n
+};
+
+struct Plan {
+    int kind = 0;
+    Shape full;                 // the caller's shape
+    std::vector<i64> dims;      // squeezed dims (length-1 axes dropped)
+    std::vector<int> axes;      // original axis index of each squeezed axis
+    int m = 1;
+    i64 cells = 1;
+    TableSet tables;
+    // kind 1
+    i64 L = 0, M = 0, P = 0, rows = 0;
+    fsx::AxisGeom ax1, ax0;
+    // kind 2
+    i64 N1 = 1, N2 = 1, Mc = 0;
+    int t_M = -1, t_wk = -1;
+    fsx::AxisGeom colg;
+    // kind 3
+    std::vector<GenAxis> gax;
+    int gtab[fsx::kMaxRank];
+    // workspaces
+    DevBuf work;      // H (kind 1) / complex Z (kind 3)
+    DevBuf d_in, d_out;
+    DevBuf taps_dev;  // general path tap arrays
+    std::vector<char> taps_host;
+    int launches = 0;
+    i64 alg_bytes = 0, fused_bytes = 0;
+};
+
+struct Device {
+    int ordinal = 0;
+    cudaStream_t stream = nullptr;
+    DevBuf tw_all;
+    DevBuf flags;  // fsx::Flags
+    std::map<std::string, std::unique_ptr<Plan>> plans;
+    cudaEvent_t ev[8];
+    bool events = false;
+};
+
+std::mutex g_mu;
+std::map<int, std::unique_ptr<Device>> g_devices;
+
+Device& device_for(int ordinal) {
+    auto it = g_devices.find(ordinal);
+    if (it != g_devices.end()) {
+        FSX_CK(cudaSetDevice(ordinal));
+        return *it->second;
+    }
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        throw CudaErr(e == cudaSuccess ? cudaErrorNoDevice : e, "fsx: no CUDA device (the GPU path has no CPU fallback)");
+    }
+    if (ordinal < 0 || ordinal >= count) throw SpecErr("fsx: device ordinal out of range");
+    FSX_CK(cudaSetDevice(ordinal));
+    auto d = std::make_unique<Device>();
+    d->ordinal = ordinal;
+    FSX_CK(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+    // pow2 line twiddles: tw_all[N + x] = exp(-2 pi i x / N)
+    std::vector<double2> tw(2 * fsx::kMaxTwPow2);
+    tw[0] = make_double2(0, 0);
+    for (i64 N = 1; N <= fsx::kMaxTwPow2; N <<= 1)
+        for (i64 x = 0; x < N; ++x) tw[N + x] = expi_neg(x, N);
+    d->tw_all.ensure(tw.size() * sizeof(double2));
+    FSX_CK(cudaMemcpy(d->tw_all.p, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    d->flags.ensure(sizeof(fsx::Flags));
+    FSX_CK(cudaMemset(d->flags.p, 0, sizeof(fsx::Flags)));
+    for (auto& e2 : d->ev) FSX_CK(cudaEventCreate(&e2));
+    d->events = true;
+    auto& ref = *d;
+    g_devices.emplace(ordinal, std::move(d));
+    return ref;
+}
+
+// Splits a pow2 length into n1 * n2 with both <= kMaxLine.
+bool split_pow2(i64 n, i64& n1, i64& n2) {
+    const int b = ilog2(n);
+    if (b > 2 * ilog2(fsx::kMaxLine)) return false;
+    const int b2 = std::min(ilog2(fsx::kMaxLine), (b + 1) / 2);
+    n2 = i64(1) << b2;
+    n1 = n / n2;
+    return n1 <= fsx::kMaxLine;
+}
+
+int choose_kind(const Plan& p, const Taps& taps, int force_general) {
+    if (force_general) return kGeneral;
+    const int r = (int)p.dims.size();
+    for (i64 d : p.dims)
+        if (!is_pow2(d)) return kGeneral;
+    if ((i64)taps.map.size() > fsx::kMaxFusedTaps) return kGeneral;
+    if (p.m == 1 && (r == 2 || r == 3)) {
+        const i64 L = p.dims[r - 1];
+        if (L < 16 || L > 2 * fsx::kMaxLine) return kGeneral;
+        for (int a = 0; a + 1 < r; ++a)
+            if (p.dims[a] < 2 || p.dims[a] > fsx::kMaxLine) return kGeneral;
+        std::map<i64, int> groups;
+        for (const auto& kv : taps.map) groups[kv.first[p.axes[0]]] = 1;
+        if ((int)groups.size() > fsx::kMaxGroups) return kGeneral;
+        return kFusedR2C;
+    }
+    if (r == 1 && (p.m == 1 || p.m == 2)) {
+        const i64 n = p.dims[0];
+        const i64 Mc = p.m == 1 ? n / 2 : n;
+        if (Mc < 16) return kGeneral;
+        if (Mc <= 256) return kRowPair1D;
+        const int b = ilog2(Mc);
+        const int b2 = std::min(12, (b + 1) / 2);
+        if (b - b2 > ilog2(fsx::kMaxLine)) return kGeneral;
+        return kRowPair1D;
+    }
+    return kGeneral;
+}
+
+std::string plan_key(const Shape& s, int kind_hint) {
+    std::string k = std::to_string(s.fields) + "|" + std::to_string(kind_hint);
+    for (i64 d : s.dims) k += ":" + std::to_string(d);
+    return k;
+}
+
+Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general) {
+    // squeeze length-1 axes (their offsets are 0 by require_fits)
+    Plan probe;
+    probe.full = s;
+    probe.m = s.fields;
+    for (int a = 0; a < s.rank(); ++a)
+        if (s.dims[a] > 1) {
+            probe.dims.push_back(s.dims[a]);
+            probe.axes.push_back(a);
+        }
+    if (probe.dims.empty()) {
+        probe.dims.push_back(1);
+        probe.axes.push_back(0);
+    }
+    const int kind = choose_kind(probe, taps, force_general);
+    const std::string key = plan_key(s, kind);
+    auto it = dev.plans.find(key);
+    if (it != dev.plans.end()) return *it->second;
+    if (dev.plans.size() >= 8) dev.plans.clear();  // bounded cache
+
+    auto p = std::make_unique<Plan>();
+    p->full = probe.full;
+    p->dims = probe.dims;
+    p->axes = probe.axes;
+    p->m = probe.m;
+    p->kind = kind;
+    p->cells = s.cells;
+    const int r = (int)p->dims.size();
+    const i64 R = s.values() * 8;  // real bytes
+    if (kind == kFusedR2C) {
+        p->L = p->dims[r - 1];
+        p->M = p->L / 2;
+        p->P = p->M + 8;
+        p->rows = s.cells / p->L;
+        p->work.ensure((size_t)p->rows * p->P * sizeof(double2));
+        const i64 plane = (r == 3) ? p->dims[1] * p->P : p->P;
+        if (r == 3) {
+            p->ax1.n = p->dims[1];
+            p->ax1.inner = p->P;
+            p->ax1.outer = p->dims[0];
+            p->ax1.block = p->dims[1] * p->P;
+            p->ax1.ncols = p->M + 1;
+        }
+        p->ax0.n = p->dims[0];
+        p->ax0.inner = plane;
+        p->ax0.outer = 1;
+        p->ax0.block = p->dims[0] * plane;
+        p->ax0.ncols = (r == 3) ? plane : p->M + 1;
+        const i64 H = p->rows * (p->M + 1) * 16;
+        p->fused_bytes = 2 * H;
+        p->alg_bytes = 2 * R + (r == 3 ? 8 : 4) * H;
+        p->launches = (r == 3) ? 5 : 3;
+    } else if (kind == kRowPair1D) {
+        const i64 n = p->dims[0];
+        p->Mc = p->m == 1 ? n / 2 : n;
+        if (p->Mc <= 256) {
+            p->N1 = 1;
+            p->N2 = p->Mc;
+        } else {
+            const int b = ilog2(p->Mc);
+            const int b2 = std::min(12, (b + 1) / 2);
+            p->N2 = i64(1) << b2;
+            p->N1 = p->Mc / p->N2;
+        }
+        p->t_M = p->tables.add(make_phase(p->Mc));
+        p->t_wk = p->tables.add(make_phase(p->m == 1 ? n : p->Mc));
+        p->tables.upload();
+        p->colg.n = p->N1;
+        p->colg.inner = p->N2;
+        p->colg.outer = 1;
+        p->colg.block = p->Mc;
+        p->colg.ncols = p->N2;
+        p->fused_bytes = 2 * R;
+        p->alg_bytes = (p->N1 > 1 ? 6 : 2) * R + R;
+        p->launches = (p->N1 > 1 ? 3 : 1) + 1;
+    } else {
+        // general: complex Z of cells * m
+        p->work.ensure((size_t)s.values() * sizeof(double2));
+        i64 nl = 0;
+        for (int a = 0; a < r; ++a) {
+            GenAxis ga;
+            ga.n = p->dims[a];
+            if (ga.n > 1) {
+                if (is_pow2(ga.n) && ga.n <= fsx::kMaxLine) {
+                    nl += 2;
+                } else if (is_pow2(ga.n)) {
+                    if (!split_pow2(ga.n, ga.n1, ga.n2))
+                        throw SpecErr("fsx: axis length " + std::to_string(ga.n) + " exceeds the GPU path limit (2^26)");
+                    nl += 4;
+                } else {
+                    if (ga.n > fsx::kMaxDirect)
+                        throw SpecErr("fsx: non-power-of-two axis length " + std::to_string(ga.n) +
+                                      " exceeds the GPU direct-DFT limit (" + std::to_string(fsx::kMaxDirect) + ")");
+                    ga.direct = 1;
+                    nl += 2;
+                }
+            }
+            ga.table = p->tables.add(make_phase(ga.n));
+            p->gax.push_back(ga);
+        }
+        p->tables.upload();
+        p->launches = (int)nl + 3;
+        const i64 Z = s.values() * 16;
+        p->fused_bytes = 2 * Z;
+        p->alg_bytes = R + Z + (nl) * 2 * Z / 1 + 2 * Z + Z + R;
+    }
+    auto& ref = *p;
+    dev.plans.emplace(key, std::move(p));
+    return ref;
+}
+
+// ------------------------------------------------------------------ symbol setup
+fsx::FusedSymbol fused_symbol(const Plan& p, const Taps& taps, u64 T) {
+    fsx::FusedSymbol s;
+    const int r = (int)p.dims.size();
+    s.rank = r;
+    s.n0 = p.dims[0];
+    s.n1 = r == 3 ? p.dims[1] : 1;
+    s.L = p.L;
+    s.P = p.P;
+    s.M = p.M;
+    s.T = T;
+    s.scale = 1.0 / (double)p.cells;
+    std::map<i64, int> gid;
+    int j = 0;
+    for (const auto& kv : taps.map) {
+        const auto& off = kv.first;
+        const i64 o0 = off[p.axes[0]];
+        auto it = gid.find(o0);
+        int g;
+        if (it == gid.end()) {
+            g = (int)gid.size();
+            gid.emplace(o0, g);
+            s.group_off[g] = (int)o0;
+        } else {
+            g = it->second;
+        }
+        s.tap_group[j] = g;
+        s.tap_o1[j] = r == 3 ? (int)off[p.axes[1]] : 0;
+        s.tap_olast[j] = (int)off[p.axes[r - 1]];
+        s.tap_c[j] = kv.second[0];
+        ++j;
+    }
+    s.ntaps = j;
+    s.ngroups = (int)gid.size();
+    return s;
+}
+
+fsx::RowPairArgs rowpair_args(const Plan& p, const Taps& taps, u64 T, double2* z, const Device& dev) {
+    fsx::RowPairArgs a;
+    a.z = z;
+    a.N1 = p.N1;
+    a.N2 = p.N2;
+    a.mode = p.m == 1 ? 0 : 1;
+    a.tw_all = dev.tw_all.as<double2>();
+    a.wk = p.tables.get(p.t_wk);
+    a.T = T;
+    a.scale = 1.0 / (double)(p.m == 1 ? p.dims[0] : p.Mc);
+    int j = 0;
+    for (const auto& kv : taps.map) {
+        a.tap_off[j] = (int)kv.first[p.axes[0]];
+        for (int i = 0; i < p.m * p.m; ++i) a.tap_b[j][i] = kv.second[i];
+        ++j;
+    }
+    a.ntaps = j;
+    return a;
+}
+
+// General symbol: uploads the (squeezed) tap arrays into the plan.
+fsx::GeneralSymbol general_symbol(Plan& p, const Taps& taps, const Taps* q, u64 T, cudaStream_t st) {
+    fsx::GeneralSymbol s;
+    const int r = (int)p.dims.size();
+    s.rank = r;
+    s.m = p.m;
+    s.cells = p.cells;
+    for (int a = 0; a < r; ++a) {
+        s.dims[a] = p.dims[a];
+        s.split[a] = p.gax[a].n1;
+        s.tab[a] = p.tables.get(p.gax[a].table);
+    }
+    s.T = T;
+    s.scale = 1.0 / (double)p.cells;
+    const int mm = p.m * p.m;
+    auto pack = [&](const Taps& t, std::vector<long long>& off, std::vector<double>& blk) {
+        for (const auto& kv : t.map) {
+            for (int a = 0; a < r; ++a) off.push_back(kv.first[p.axes[a]]);
+            blk.insert(blk.end(), kv.second.begin(), kv.second.end());
+        }
+    };
+    std::vector<long long> off, offq;
+    std::vector<double> blk, blkq;
+    pack(taps, off, blk);
+    if (q) pack(*q, offq, blkq);
+    const size_t b_off = off.size() * 8, b_blk = blk.size() * 8, b_offq = offq.size() * 8, b_blkq = blkq.size() * 8;
+    const size_t total = b_off + b_blk + b_offq + b_blkq + 64;
+    p.taps_host.assign(total, 0);
+    std::memcpy(p.taps_host.data(), off.data(), b_off);
+    std::memcpy(p.taps_host.data() + b_off, blk.data(), b_blk);
+    std::memcpy(p.taps_host.data() + b_off + b_blk, offq.data(), b_offq);
+    std::memcpy(p.taps_host.data() + b_off + b_blk + b_offq, blkq.data(), b_blkq);
+    p.taps_dev.ensure(total);
+    FSX_CK(cudaMemcpyAsync(p.taps_dev.p, p.taps_host.data(), total, cudaMemcpyHostToDevice, st));
+    char* base = p.taps_dev.as<char>();
+    s.ntaps = (int)taps.map.size();
+    s.offsets = reinterpret_cast<const long long*>(base);
+    s.blocks = reinterpret_cast<const double*>(base + b_off);
+    if (q) {
+        s.implicit = 1;
+        s.ntaps_q = (int)q->map.size();
+        s.offsets_q = reinterpret_cast<const long long*>(base + b_off + b_blk);
+        s.blocks_q = reinterpret_cast<const double*>(base + b_off + b_blk + b_offq);
+        s.qmax = reinterpret_cast<const double*>(base + total - 8);
+    }
+    (void)mm;
+    return s;
+}
+
+// ------------------------------------------------------------------ general axis passes
+void general_axes(Plan& p, const Device& dev, double2* Z, bool inverse, cudaStream_t st) {
+    const int r = (int)p.dims.size();
+    const int sign = inverse ? +1 : -1;
+    auto run_axis = [&](int a) {
+        const GenAxis& ga = p.gax[a];
+        if (ga.n <= 1) return;
+        i64 inner = p.m, outer = 1;
+        for (int b = a + 1; b < r; ++b) inner *= p.dims[b];
+        for (int b = 0; b < a; ++b) outer *= p.dims[b];
+        fsx::StepTwiddle none;
+        if (ga.direct) {
+            fsx::AxisGeom g{ga.n, inner, outer, ga.n * inner, inner};
+            FSX_CK(fsx::launch_axis_direct(Z, Z, g, sign, p.tables.get(ga.table), st));
+        } else if (!ga.n1) {
+            fsx::AxisGeom g{ga.n, inner, outer, ga.n * inner, inner};
+            FSX_CK(fsx::launch_axis_pow2(Z, Z, g, sign, none, dev.tw_all.as<double2>(), st));
+        } else {
+            // four-step split: [outer][n1][n2][inner]
+            fsx::AxisGeom g1{ga.n1, ga.n2 * inner, outer, ga.n * inner, ga.n2 * inner};
+            fsx::AxisGeom g2{ga.n2, inner, outer * ga.n1, ga.n2 * inner, inner};
+            fsx::StepTwiddle tw;
+            tw.col_div = inner;
+            tw.tab = p.tables.get(ga.table);
+            if (!inverse) {
+                tw.mode = 1;
+                FSX_CK(fsx::launch_axis_pow2(Z, Z, g1, sign, tw, dev.tw_all.as<double2>(), st));
+                FSX_CK(fsx::launch_axis_pow2(Z, Z, g2, sign, none, dev.tw_all.as<double2>(), st));
+            } else {
+                tw.mode = 2;
+                FSX_CK(fsx::launch_axis_pow2(Z, Z, g2, sign, none, dev.tw_all.as<double2>(), st));
+                FSX_CK(fsx::launch_axis_pow2(Z, Z, g1, sign, tw, dev.tw_all.as<double2>(), st));
+            }
+        }
+    };
+    if (!inverse)
+        for (int a = 0; a < r; ++a) run_axis(a);
+    else
+        for (int a = r - 1; a >= 0; --a) run_axis(a);
+}
+
+// ------------------------------------------------------------------ solve
+struct Stamps {
+    Device* dev;
+    bool on;
+    cudaStream_t st;
+    int n = 0;
+    void mark() {
+        if (on) FSX_CK(cudaEventRecord(dev->ev[n++], st));
+    }
+};
+
+// Runs one solve on device pointers; stage boundaries are stamped into
+// ev[0..3] when timings are requested.
+void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, const double* d_a0, double* d_out,
+              cudaStream_t st, Stamps& sp) {
+    fsx::Flags* flags = dev.flags.as<fsx::Flags>();
+    const double2* tw = dev.tw_all.as<double2>();
+    const int r = (int)p.dims.size();
+    sp.mark();
+    if (p.kind == kFusedR2C) {
+        double2* H = p.work.as<double2>();
+        FSX_CK(fsx::launch_r2c_rows(d_a0, H, p.rows, p.L, p.P, tw, st));
+        fsx::StepTwiddle none;
+        if (r == 3) FSX_CK(fsx::launch_axis_pow2(H, H, p.ax1, -1, none, tw, st));
+        sp.mark();
+        const fsx::FusedSymbol sym = fused_symbol(p, taps, T);
+        FSX_CK(fsx::launch_fused_r2c(H, p.ax0, sym, tw, st));
+        sp.mark();
+        if (r == 3) FSX_CK(fsx::launch_axis_pow2(H, H, p.ax1, +1, none, tw, st));
+        FSX_CK(fsx::launch_c2r_rows(H, d_out, p.rows, p.L, p.P, tw, flags, st));
+        sp.mark();
+    } else if (p.kind == kRowPair1D) {
+        if (d_out != d_a0)
+            FSX_CK(cudaMemcpyAsync(d_out, d_a0, (size_t)p.cells * p.m * 8, cudaMemcpyDeviceToDevice, st));
+        double2* z = reinterpret_cast<double2*>(d_out);
+        fsx::StepTwiddle tf;
+        tf.mode = 1;
+        tf.col_div = 1;
+        tf.tab = p.tables.get(p.t_M);
+        if (p.N1 > 1) FSX_CK(fsx::launch_axis_pow2(z, z, p.colg, -1, tf, tw, st));
+        sp.mark();
+        const fsx::RowPairArgs a = rowpair_args(p, taps, T, z, dev);
+        FSX_CK(fsx::launch_rowpair(a, st));
+        sp.mark();
+        fsx::StepTwiddle ti = tf;
+        ti.mode = 2;
+        if (p.N1 > 1) FSX_CK(fsx::launch_axis_pow2(z, z, p.colg, +1, ti, tw, st));
+        FSX_CK(fsx::launch_finite_check(d_out, p.cells * p.m, flags, st));
+        sp.mark();
+    } else {
+        double2* Z = p.work.as<double2>();
+        FSX_CK(fsx::launch_promote(d_a0, Z, p.cells * p.m, st));
+        general_axes(p, dev, Z, false, st);
+        sp.mark();
+        fsx::GeneralSymbol sym = general_symbol(p, taps, q, T, st);
+        if (q) {
+            FSX_CK(cudaMemsetAsync(const_cast<double*>(sym.qmax), 0, 8, st));
+            FSX_CK(fsx::launch_symbol_absmax(sym, const_cast<double*>(sym.qmax), st));
+        }
+        FSX_CK(fsx::launch_spectral_general(Z, sym, st));
+        sp.mark();
+        general_axes(p, dev, Z, true, st);
+        FSX_CK(fsx::launch_extract(Z, d_out, p.cells * p.m, flags, st));
+        sp.mark();
+    }
+}
+
+double bits_to_double(unsigned long long b) {
+    double d;
+    std::memcpy(&d, &b, 8);
+    return d;
+}
+
+// Decide NumericError from the device flags (realize_checked,
+// proj/src/periodic.cpp:53-63) and reset them.
+void check_flags(Device& dev, int kind, cudaStream_t st) {
+    fsx::Flags h;
+    FSX_CK(cudaMemcpyAsync(&h, dev.flags.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    FSX_CK(cudaStreamSynchronize(st));
+    FSX_CK(cudaMemsetAsync(dev.flags.p, 0, sizeof(fsx::Flags), st));
+    if (h.nonfinite) throw NumErr("solve_periodic: non-finite value after inverse FFT");
+    if (kind == kGeneral) {
+        const double mre = bits_to_double(h.max_re_bits), mim = bits_to_double(h.max_im_bits);
+        if (mim > 1e-6 * mre) {
+            char buf[256];
+            std::snprintf(buf, sizeof buf,
+                          "solve_periodic: imaginary residue %f exceeds 1e-6 * max |real| (%f); spectrum likely blew up",
+                          mim, mre);
+            throw NumErr(buf);
+        }
+    }
+}
+
+cudaStream_t stream_of(Device& dev, const fsx_options* opt) {
+    return (opt && opt->stream) ? reinterpret_cast<cudaStream_t>(opt->stream) : dev.stream;
+}
+
+struct SolveReq {
+    const fsx_shape* shape;
+    const double* a0;
+    const fsx_kernel* k;
+    const fsx_kernel* q;  // implicit: q (mass), k = s
+    u64 T;
+    double* out;
+    const fsx_options* opt;
+    fsx_stage_timings* st;
+    bool vector = false;
+    bool device_ptrs = false;
+};
+
+void solve(const SolveReq& rq) {
+    const Shape s = parse_shape(rq.shape);
+    Taps taps, qtaps;
+    if (rq.vector) {
+        // proj/src/periodic.cpp:103-104 checks the kernel's fields first
+        if (!rq.k || rq.k->fields < 2) throw SpecErr("solve_periodic_vector: kernel must carry m > 1 blocks");
+    }
+    if (rq.q) {
+        if (!rq.q || !rq.k || rq.q->fields != 1 || rq.k->fields != 1)
+            throw SpecErr("solve_periodic_implicit: scalar kernels only");
+        qtaps = parse_kernel(rq.q);
+        taps = parse_kernel(rq.k);
+        require_fits(qtaps, s);
+        require_fits(taps, s);
+    } else {
+        taps = parse_kernel(rq.k);
+        require_fits(taps, s);
+    }
+    if (!rq.a0 || !rq.out) throw SpecErr("fsx: null grid pointer");
+    const size_t bytes = (size_t)s.values() * 8;
+    const int ordinal = rq.opt ? rq.opt->device : 0;
+    if (rq.T == 0 && !rq.device_ptrs) {
+        // proj/src/periodic.cpp:79: the input, bit for bit (a copy, no arithmetic)
+        if (rq.out != rq.a0) std::memmove(rq.out, rq.a0, bytes);
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_mu);
+    Device& dev = device_for(ordinal);
+    cudaStream_t st = stream_of(dev, rq.opt);
+    if (rq.T == 0) {
+        if (rq.out != rq.a0) FSX_CK(cudaMemcpyAsync(rq.out, rq.a0, bytes, cudaMemcpyDeviceToDevice, st));
+        return;
+    }
+    const int force_general = (rq.opt && rq.opt->path == 1) || rq.q != nullptr;
+    Plan& p = get_plan(dev, s, taps, force_general);
+    Stamps sp{&dev, rq.st != nullptr, st};
+    if (rq.device_ptrs) {
+        run_plan(p, dev, taps, rq.q ? &qtaps : nullptr, rq.T, rq.a0, rq.out, st, sp);
+        return;
+    }
+    p.d_in.ensure(bytes);
+    p.d_out.ensure(bytes);
+    cudaEvent_t h0 = dev.ev[6], h1 = dev.ev[7];
+    if (sp.on) FSX_CK(cudaEventRecord(h0, st));
+    FSX_CK(cudaMemcpyAsync(p.d_in.p, rq.a0, bytes, cudaMemcpyHostToDevice, st));
+    run_plan(p, dev, taps, rq.q ? &qtaps : nullptr, rq.T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp);
+    FSX_CK(cudaMemcpyAsync(rq.out, p.d_out.p, bytes, cudaMemcpyDeviceToHost, st));
+    if (sp.on) FSX_CK(cudaEventRecord(h1, st));
+    check_flags(dev, p.kind, st);
+    if (sp.on) {
+        float t[4] = {0, 0, 0, 0}, pre = 0, post = 0;
+        for (int i = 0; i < 3; ++i) FSX_CK(cudaEventElapsedTime(&t[i], dev.ev[i], dev.ev[i + 1]));
+        FSX_CK(cudaEventElapsedTime(&pre, h0, dev.ev[0]));
+        FSX_CK(cudaEventElapsedTime(&post, dev.ev[3], h1));
+        // H2D counts toward forward_fft, D2H toward inverse_fft (the
+        // reference's stages cover the whole call, proj/src/periodic.cpp:27-86)
+        rq.st->forward_fft += (pre + t[0]) * 1e-3;
+        rq.st->squaring += t[1] * 1e-3;
+        rq.st->hadamard += 0.0;
+        rq.st->inverse_fft += (t[2] + post) * 1e-3;
+    }
+}
+
+template <class F>
+fsx_status guarded(F&& f) {
+    try {
+        f();
+        g_err.clear();
+        return FSX_OK;
+    } catch (const SpecErr& e) {
+        g_err = e.what();
+        return FSX_ERR_SPEC;
+    } catch (const NumErr& e) {
+        g_err = e.what();
+        return FSX_ERR_NUMERIC;
+    } catch (const CudaErr& e) {
+        g_err = e.what();
+        return e.code == cudaErrorMemoryAllocation ? FSX_ERR_OOM : FSX_ERR_CUDA;
+    } catch (const std::bad_alloc&) {
+        g_err = "fsx: host allocation failed";
+        return FSX_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return FSX_ERR_CUDA;
+    }
+}
+
+}  // namespace
+
+struct fsx_spectrum_cache {
+    std::mutex mu;
+    int used = 0;
+};
+
+extern "C" {
+
+const char* fsx_last_error(void) { return g_err.c_str(); }
+int32_t fsx_version(void) { return 100; }
+
+int32_t fsx_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+fsx_status fsx_solve_periodic(const fsx_shape* shape, const double* a0, const fsx_kernel* k, uint64_t T,
+                              double* out, const fsx_options* opt, fsx_stage_timings* st) {
+    return guarded([&] { solve({shape, a0, k, nullptr, T, out, opt, st}); });
+}
+
+fsx_status fsx_solve_periodic_vector(const fsx_shape* shape, const double* a0, const fsx_kernel* k, uint64_t T,
+                                     double* out, const fsx_options* opt, fsx_stage_timings* st) {
+    return guarded([&] {
+        SolveReq rq{shape, a0, k, nullptr, T, out, opt, st};
+        rq.vector = true;
+        solve(rq);
+    });
+}
+
+fsx_spectrum_cache* fsx_spectrum_cache_create(void) { return new (std::nothrow) fsx_spectrum_cache(); }
+void fsx_spectrum_cache_destroy(fsx_spectrum_cache* c) { delete c; }
+
+fsx_status fsx_solve_periodic_cached(const fsx_shape* shape, const double* a0, const fsx_kernel* k, uint64_t T,
+                                     fsx_spectrum_cache* cache, double* out, const fsx_options* opt,
+                                     fsx_stage_timings* st) {
+    return guarded([&] {
+        if (!cache) throw SpecErr("solve_periodic_cached: null cache");
+        std::lock_guard<std::mutex> lk(cache->mu);
+        ++cache->used;
+        solve({shape, a0, k, nullptr, T, out, opt, st});
+    });
+}
+
+fsx_status fsx_solve_periodic_implicit(const fsx_shape* shape, const double* a0, const fsx_kernel* q,
+                                       const fsx_kernel* s, uint64_t T, double* out, const fsx_options* opt,
+                                       fsx_stage_timings* st) {
+    return guarded([&] {
+        if (!q || !s) throw SpecErr("solve_periodic_implicit: null kernel");
+        SolveReq rq{shape, a0, s, q, T, out, opt, st};
+        solve(rq);
+    });
+}
+
+fsx_status fsx_solve_periodic_device(const fsx_shape* shape, const double* d_a0, const fsx_kernel* k, uint64_t T,
+                                     double* d_out, const fsx_options* opt) {
+    return guarded([&] {
+        SolveReq rq{shape, d_a0, k, nullptr, T, d_out, opt, nullptr};
+        rq.device_ptrs = true;
+        solve(rq);
+    });
+}
+
+fsx_status fsx_device_check(const fsx_options* opt) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(opt ? opt->device : 0);
+        check_flags(dev, kFusedR2C, stream_of(dev, opt));
+    });
+}
+
+fsx_status fsx_plan_describe(const fsx_shape* shape, const fsx_kernel* k, const fsx_options* opt,
+                             fsx_plan_info* info) {
+    return guarded([&] {
+        if (!info) throw SpecErr("fsx_plan_describe: null info");
+        const Shape s = parse_shape(shape);
+        const Taps taps = parse_kernel(k);
+        require_fits(taps, s);
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(opt ? opt->device : 0);
+        Plan& p = get_plan(dev, s, taps, opt && opt->path == 1);
+        info->path = p.kind;
+        info->launches = p.launches;
+        info->alg_bytes = p.alg_bytes;
+        info->fused_bytes = p.fused_bytes;
+        info->work_bytes = (int64_t)p.work.bytes;
+    });
+}
+
+// ---------------------------------------------------------------- building blocks
+fsx_status fsx_multi_fft(const fsx_shape* shape, const double* in, double* out, int32_t inverse) {
+    return guarded([&] {
+        const Shape s = parse_shape(shape);
+        if (!in || !out) throw SpecErr("multi_fft: null pointer");
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(0);
+        cudaStream_t st = dev.stream;
+        Taps dummy;
+        dummy.rank = s.rank();
+        dummy.m = s.fields;
+        dummy.map.emplace(std::vector<i64>(s.rank(), 0), std::vector<double>(s.fields * s.fields, 0.0));
+        Plan& p = get_plan(dev, s, dummy, 1);
+        const size_t bytes = (size_t)s.values() * 16;
+        double2* Z = p.work.as<double2>();
+        p.d_in.ensure(bytes);
+        FSX_CK(cudaMemcpyAsync(Z, in, bytes, cudaMemcpyHostToDevice, st));
+        const int r = (int)p.dims.size();
+        // split axes are stored [k1][k2] between the passes; present natural order
+        auto permute = [&](int to_natural) {
+            for (int a = 0; a < r; ++a) {
+                const GenAxis& ga = p.gax[a];
+                if (!ga.n1) continue;
+                i64 inner = p.m, outer = 1;
+                for (int b = a + 1; b < r; ++b) inner *= p.dims[b];
+                for (int b = 0; b < a; ++b) outer *= p.dims[b];
+                FSX_CK(fsx::launch_transpose_split(Z, p.d_in.as<double2>(), outer, ga.n1, ga.n2, inner, to_natural, st));
+                FSX_CK(cudaMemcpyAsync(Z, p.d_in.p, bytes, cudaMemcpyDeviceToDevice, st));
+            }
+        };
+        if (inverse) permute(0);
+        general_axes(p, dev, Z, inverse != 0, st);
+        if (!inverse) permute(1);
+        // inverse: 1/n per axis (proj/src/fft.cpp:151-154)
+        if (inverse) FSX_CK(fsx::launch_scale(Z, s.values(), 1.0 / (double)s.cells, st));
+        FSX_CK(cudaMemcpyAsync(out, Z, bytes, cudaMemcpyDeviceToHost, st));
+        FSX_CK(cudaStreamSynchronize(st));
+    });
+}
+
+fsx_status fsx_spectrum_from_kernel(const fsx_shape* shape, const fsx_kernel* k, double* out) {
+    return guarded([&] {
+        const Shape s = parse_shape(shape);
+        const Taps taps = parse_kernel(k);
+        require_fits(taps, s);
+        if (!out) throw SpecErr("spectrum_from_kernel: null output");
+        if (s.fields > 4) throw SpecErr("spectrum_from_kernel: fields > 4 not supported on the GPU path");
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(0);
+        cudaStream_t st = dev.stream;
+        Plan& p = get_plan(dev, s, taps, 1);
+        fsx::GeneralSymbol sym = general_symbol(p, taps, nullptr, 1, st);
+        for (int a = 0; a < sym.rank; ++a) sym.split[a] = 0;
+        const size_t bytes = (size_t)s.cells * s.fields * s.fields * 16;
+        DevBuf o;
+        o.ensure(bytes);
+        FSX_CK(fsx::launch_symbol_blocks(o.as<double2>(), sym, 0, st));
+        FSX_CK(cudaMemcpyAsync(out, o.p, bytes, cudaMemcpyDeviceToHost, st));
+        FSX_CK(cudaStreamSynchronize(st));
+    });
+}
+
+static void spectral_io(const fsx_shape* shape, Shape& s, size_t& bytes) {
+    s = parse_shape(shape);
+    if (s.fields > 4) throw SpecErr("spectrum: fields > 4 not supported on the GPU path");
+    bytes = (size_t)s.cells * s.fields * s.fields * 16;
+}
+
+fsx_status fsx_pow_spectrum(const fsx_shape* shape, const double* blocks, uint64_t T, double* out) {
+    return guarded([&] {
+        Shape s;
+        size_t bytes;
+        spectral_io(shape, s, bytes);
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(0);
+        cudaStream_t st = dev.stream;
+        DevBuf a, b;
+        a.ensure(bytes);
+        b.ensure(bytes);
+        FSX_CK(cudaMemcpyAsync(a.p, blocks, bytes, cudaMemcpyHostToDevice, st));
+        FSX_CK(fsx::launch_pow_blocks(a.as<double2>(), b.as<double2>(), s.cells, s.fields, T, st));
+        FSX_CK(cudaMemcpyAsync(out, b.p, bytes, cudaMemcpyDeviceToHost, st));
+        FSX_CK(cudaStreamSynchronize(st));
+    });
+}
+
+fsx_status fsx_pseudo_inverse_spectrum(const fsx_shape* shape, const double* blocks, double* out) {
+    return guarded([&] {
+        Shape s;
+        size_t bytes;
+        spectral_io(shape, s, bytes);
+        if (s.fields != 1) throw SpecErr("pseudo_inverse_spectrum: scalar spectra only");
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(0);
+        cudaStream_t st = dev.stream;
+        DevBuf a, b, mx;
+        a.ensure(bytes);
+        b.ensure(bytes);
+        mx.ensure(8);
+        FSX_CK(cudaMemcpyAsync(a.p, blocks, bytes, cudaMemcpyHostToDevice, st));
+        FSX_CK(cudaMemsetAsync(mx.p, 0, 8, st));
+        FSX_CK(fsx::launch_absmax(a.as<double2>(), s.cells, mx.as<double>(), st));
+        FSX_CK(fsx::launch_pinv(a.as<double2>(), b.as<double2>(), s.cells, mx.as<double>(), st));
+        FSX_CK(cudaMemcpyAsync(out, b.p, bytes, cudaMemcpyDeviceToHost, st));
+        FSX_CK(cudaStreamSynchronize(st));
+    });
+}
+
+fsx_status fsx_multiply_spectra(const fsx_shape* shape, const double* a, const double* b, double* out) {
+    return guarded([&] {
+        Shape s;
+        size_t bytes;
+        spectral_io(shape, s, bytes);
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(0);
+        cudaStream_t st = dev.stream;
+        DevBuf da, db, dc;
+        da.ensure(bytes);
+        db.ensure(bytes);
+        dc.ensure(bytes);
+        FSX_CK(cudaMemcpyAsync(da.p, a, bytes, cudaMemcpyHostToDevice, st));
+        FSX_CK(cudaMemcpyAsync(db.p, b, bytes, cudaMemcpyHostToDevice, st));
+        FSX_CK(fsx::launch_block_mul(da.as<double2>(), db.as<double2>(), dc.as<double2>(), s.cells, s.fields, st));
+        FSX_CK(cudaMemcpyAsync(out, dc.p, bytes, cudaMemcpyDeviceToHost, st));
+        FSX_CK(cudaStreamSynchronize(st));
+    });
+}
+
+fsx_status fsx_hadamard(const fsx_shape* shape, const double* lam, const double* x, double* y) {
+    return guarded([&] {
+        Shape s;
+        size_t bytes;
+        spectral_io(shape, s, bytes);
+        const size_t xb = (size_t)s.values() * 16;
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(0);
+        cudaStream_t st = dev.stream;
+        DevBuf dl, dx, dy;
+        dl.ensure(bytes);
+        dx.ensure(xb);
+        dy.ensure(xb);
+        FSX_CK(cudaMemcpyAsync(dl.p, lam, bytes, cudaMemcpyHostToDevice, st));
+        FSX_CK(cudaMemcpyAsync(dx.p, x, xb, cudaMemcpyHostToDevice, st));
+        FSX_CK(fsx::launch_block_matvec(dl.as<double2>(), dx.as<double2>(), dy.as<double2>(), s.cells, s.fields, st));
+        FSX_CK(cudaMemcpyAsync(y, dy.p, xb, cudaMemcpyDeviceToHost, st));
+        FSX_CK(cudaStreamSynchronize(st));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,234 @@
+// Device building blocks for the sm_100a StencilFFT-P path.
+//
+//   * fp64 complex helpers on double2 (re, im)
+//   * register-resident radix-2/4/8/16 DFT butterflies with folded constants
+//   * LineFFT<N, SIGN>: a Stockham autosort FFT of one pow2 line executed by
+//     N/R threads (R = min(16, N) elements per thread held in registers);
+//     the passes exchange through a bank-swizzled shared-memory line buffer.
+//
+// Conventions follow the reference FFT (proj/src/fft.cpp:143-155): forward is
+// X[k] = sum_n x[n] exp(-2 pi i n k / N), unnormalized; SIGN = -1 forward,
+// +1 inverse (normalization is folded into the spectral multiply by the
+// callers, see fsx_kernels.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fsx {
+
+using i64 = long long;
+using u64 = unsigned long long;
+
+__host__ __device__ constexpr int ilog2c(long long n) { return n <= 1 ? 0 : 1 + ilog2c(n >> 1); }
+
+// ------------------------------------------------------------------ complex
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// multiply by SIGN * i   (SIGN = -1: -i, +1: +i)
+template <int SIGN>
+__device__ __forceinline__ double2 cmul_si(double2 a) {
+    return SIGN < 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+}
+// a * w^SIGN-direction: forward uses the table value w, inverse its conjugate
+template <int SIGN>
+__device__ __forceinline__ double2 ctw(double2 a, double2 w) {
+    return SIGN < 0 ? cmul(a, w) : cmulc(a, w);
+}
+
+// ------------------------------------------------------------------ constant twiddles
+// cos(2 pi j / 16) for j = 0..4 (quarter wave); everything else by symmetry.
+__device__ __forceinline__ constexpr double cos16q(int j) {
+    return j == 0 ? 1.0
+         : j == 1 ? 0.92387953251128673848
+         : j == 2 ? 0.70710678118654752440
+         : j == 3 ? 0.38268343236508977173
+                  : 0.0;
+}
+
+// Multiply a by exp(SIGN * 2 pi i * J / R) with J, R compile-time; the
+// trivial angles are folded to swaps/negations.
+template <int J, int R, int SIGN>
+__device__ __forceinline__ double2 cmul_const(double2 a) {
+    constexpr int j16 = ((J * 16 / R) % 16 + 16) % 16;  // angle in sixteenths (R divides 16)
+    if constexpr (j16 == 0) return a;
+    else if constexpr (j16 == 8) return make_double2(-a.x, -a.y);
+    else if constexpr (j16 == 4) return cmul_si<SIGN>(a);
+    else if constexpr (j16 == 12) return cmul_si<-SIGN>(a);
+    else {
+        // exp(i theta) with theta = 2 pi j16 / 16 (then conj for SIGN = -1)
+        constexpr int q = j16 % 4, quad = j16 / 4;
+        constexpr double c0 = cos16q(q), s0 = cos16q(4 - q);  // cos, sin in the first quadrant
+        constexpr double c = quad == 0 ? c0 : quad == 1 ? -s0 : quad == 2 ? -c0 : s0;
+        constexpr double s = quad == 0 ? s0 : quad == 1 ? c0 : quad == 2 ? -s0 : -c0;
+        constexpr double ss = SIGN < 0 ? -s : s;
+        if constexpr (q == 2) {
+            // c, s = +-1/sqrt2
+            return make_double2(c * a.x - ss * a.y, c * a.y + ss * a.x);
+        } else {
+            return make_double2(fma(c, a.x, -ss * a.y), fma(c, a.y, ss * a.x));
+        }
+    }
+}
+
+// ------------------------------------------------------------------ DFT butterflies
+// In-place DFT of v[0..R) in natural order.  Written as Cooley-Tukey
+// R = R1 * R2 with the inner twiddles folded at compile time.
+template <int R, int SIGN>
+struct Dft;
+
+template <int SIGN>
+struct Dft<1, SIGN> {
+    __device__ __forceinline__ static void run(double2*) {}
+};
+
+template <int SIGN>
+struct Dft<2, SIGN> {
+    __device__ __forceinline__ static void run(double2* v) {
+        const double2 a = v[0], b = v[1];
+        v[0] = cadd(a, b);
+        v[1] = csub(a, b);
+    }
+};
+
+template <int SIGN>
+struct Dft<4, SIGN> {
+    __device__ __forceinline__ static void run(double2* v) {
+        const double2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+        const double2 t2 = cadd(v[1], v[3]), t3 = cmul_si<SIGN>(csub(v[1], v[3]));
+        v[0] = cadd(t0, t2);
+        v[2] = csub(t0, t2);
+        v[1] = cadd(t1, t3);
+        v[3] = csub(t1, t3);
+    }
+};
+
+// R = R1 * R2: X[k1 + R1 k2] = sum_n2 W_R2^(n2 k2) W_R^(n2 k1) sum_n1 x[R2 n1 + n2] W_R1^(n1 k1)
+template <int R1, int R2, int SIGN>
+struct DftCT {
+    static constexpr int R = R1 * R2;
+    template <int N2, int K1>
+    __device__ __forceinline__ static void tw(double2 (&y)[R2][R1]) {
+        if constexpr (N2 < R2) {
+            if constexpr (K1 < R1) {
+                y[N2][K1] = cmul_const<N2 * K1, R, SIGN>(y[N2][K1]);
+                tw<N2, K1 + 1>(y);
+            } else {
+                tw<N2 + 1, 0>(y);
+            }
+        }
+    }
+    __device__ __forceinline__ static void run(double2* v) {
+        double2 y[R2][R1];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) {
+#pragma unroll
+            for (int n1 = 0; n1 < R1; ++n1) y[n2][n1] = v[R2 * n1 + n2];
+            Dft<R1, SIGN>::run(y[n2]);
+        }
+        tw<0, 0>(y);
+#pragma unroll
+        for (int k1 = 0; k1 < R1; ++k1) {
+            double2 z[R2];
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) z[n2] = y[n2][k1];
+            Dft<R2, SIGN>::run(z);
+#pragma unroll
+            for (int k2 = 0; k2 < R2; ++k2) v[k1 + R1 * k2] = z[k2];
+        }
+    }
+};
+
+template <int SIGN>
+struct Dft<8, SIGN> {
+    __device__ __forceinline__ static void run(double2* v) { DftCT<2, 4, SIGN>::run(v); }
+};
+template <int SIGN>
+struct Dft<16, SIGN> {
+    __device__ __forceinline__ static void run(double2* v) { DftCT<4, 4, SIGN>::run(v); }
+};
+
+// ------------------------------------------------------------------ smem swizzle
+// 16-byte elements: 8 per 128-byte bank row.  XOR the low 3 bits with bits
+// 3..5 and 4..6 so the Stockham scatter strides 2, 4, 8, 16 and the unit
+// stride gathers are all conflict-free per quarter warp.
+__device__ __forceinline__ int swz(int p) { return p ^ (((p >> 3) ^ (p >> 4)) & 7); }
+
+// ------------------------------------------------------------------ line FFT
+// One pow2 line of N complex values, transformed by TPL = N/R threads.
+// Thread t holds v[q] = x[t + q * TPL] on entry and X[t + q * TPL] on exit.
+// `line` is this line's shared-memory buffer (N elements, swizzled index);
+// `tw` is the twiddle table for N: tw[x] = exp(-2 pi i x / N), x < N.
+// Every thread of the CTA must call run() together (it contains
+// __syncthreads); lines of one CTA are transformed concurrently.
+template <int N, int SIGN>
+struct LineFFT {
+    static constexpr int LOGN = ilog2c(N);
+    static constexpr int R = N < 16 ? N : 16;
+    static constexpr int TPL = N / R;
+    static constexpr int P16 = N < 16 ? 0 : LOGN / 4;
+    static constexpr int REM = N < 16 ? LOGN : LOGN % 4;
+    static constexpr int NPASS = P16 + (REM > 0 ? 1 : 0);
+    static constexpr int EXCHANGES = NPASS - 1;
+
+    template <int S>
+    __host__ __device__ static constexpr int radix() { return S < P16 ? 16 : (1 << REM); }
+    template <int S>
+    __host__ __device__ static constexpr int ns() {
+        if constexpr (S == 0) return 1;
+        else return ns<S - 1>() * radix<S - 1>();
+    }
+
+    template <int S>
+    __device__ __forceinline__ static void pass(double2 (&v)[R], int t, double2* line, const double2* __restrict__ tw) {
+        constexpr int r = radix<S>();
+        constexpr int Ns = ns<S>();
+        constexpr int C = R / r;
+        constexpr int STEP = N / (Ns * r);
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+            double2 a[r];
+#pragma unroll
+            for (int u = 0; u < r; ++u) a[u] = v[i + u * C];
+            if constexpr (Ns > 1) {
+                const int j = t + i * TPL;
+                const int k = j & (Ns - 1);
+#pragma unroll
+                for (int u = 1; u < r; ++u) a[u] = ctw<SIGN>(a[u], __ldg(tw + u * k * STEP));
+            }
+            Dft<r, SIGN>::run(a);
+#pragma unroll
+            for (int u = 0; u < r; ++u) v[i + u * C] = a[u];
+        }
+        if constexpr (S + 1 < NPASS) {
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < C; ++i) {
+                const int j = t + i * TPL;
+                const int k = j & (Ns - 1);
+                const int base = (j - k) * r + k;
+#pragma unroll
+                for (int u = 0; u < r; ++u) line[swz(base + u * Ns)] = v[i + u * C];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < R; ++q) v[q] = line[swz(t + q * TPL)];
+            pass<S + 1>(v, t, line, tw);
+        }
+    }
+
+    __device__ __forceinline__ static void run(double2 (&v)[R], int t, double2* line, const double2* __restrict__ tw) {
+        if constexpr (NPASS > 0) pass<0>(v, t, line, tw);
+    }
+};
+
+}  // namespace fsx

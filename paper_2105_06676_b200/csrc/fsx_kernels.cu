@@ -1,0 +1,985 @@
+// sm_100a kernels of the B200 StencilFFT-P path.
+//
+// Hot path (per BASELINE north_star; reference: proj/src/periodic.cpp:27-86,
+// proj/src/fft.cpp:143-192, proj/src/spectrum.cpp:21-134):
+//   k_r2c_rows      last-axis real -> half spectrum (packed pairs + split)
+//   k_strided       C2C along a non-contiguous axis (optionally four-step twiddled)
+//   k_fused_r2c     last forward axis pass + analytic symbol^T * x + first inverse pass
+//   k_c2r_rows      half spectrum -> real, non-finite scan (realize_checked)
+//   k_rowpair       1D four-step row stage fused with pairing + symbol^T + inverse rows
+// General path (any dims / fields / non-pow2; still on the GPU):
+//   k_contig / k_strided / k_direct_dft, k_spectral_general, k_promote, k_extract
+//
+// See DESIGN.md for the data layout and the roofline of each kernel.
+#include <cfloat>
+
+#include "fsx_device.cuh"
+#include "fsx_kernels.h"
+
+namespace fsx {
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ double2 phase_at(const PhaseTable& t, i64 x) {
+    if (t.shift == 0) return __ldg(t.lo + x);
+    return cmul(__ldg(t.hi + (x >> t.shift)), __ldg(t.lo + (x & t.mask)));
+}
+
+__device__ __forceinline__ i64 modp(i64 a, i64 n) {
+    const i64 r = a % n;
+    return r < 0 ? r + n : r;
+}
+
+// exp(+2 pi i x / n) for the pow2 tables: conj(tw_all[n + (x mod n)])
+__device__ __forceinline__ double2 eplus_pow2(const double2* tw_all, i64 n, i64 x) {
+    return cconj(__ldg(tw_all + n + (x & (n - 1))));
+}
+
+template <int N>
+struct Cfg {
+    static constexpr int R = N < 16 ? N : 16;
+    static constexpr int TPL = N / R;
+    // strided tiles: W adjacent columns x N (64 KB of fp64 complex for N >= 512)
+    static constexpr int W = N >= 4096 ? 1 : (4096 / N > 64 ? 64 : 4096 / N);
+    // contiguous tiles: LINES lines x N, 256 threads
+    static constexpr int LINES = N >= 4096 ? 1 : (256 / TPL);
+    static constexpr int GW = W < 8 ? W : 8;                 // columns per quarter warp
+    static constexpr int LSW = GW > 1 ? N + 8 / GW : N;      // smem line stride, strided tiles
+    static constexpr int GL = TPL >= 8 ? 1 : 8 / TPL;        // lines per quarter warp
+    static constexpr int LSL = GL > 1 ? N + 8 / GL : N;      // smem line stride, contiguous tiles
+};
+
+// Binary exponentiation of a scalar symbol, the reference loop shape
+// (proj/src/spectrum.cpp:53-64), with an exact-to-tolerance underflow
+// short cut: |lam|^T < 2^-1100 is below every representable contribution
+// (the reference's own product underflows to 0 / subnormal there).
+__device__ __forceinline__ double2 pow_scalar(double2 lam, u64 T) {
+    const double mag2 = fma(lam.x, lam.x, lam.y * lam.y);
+    if (mag2 < 1.0) {
+        int e;
+        const double mant = frexp(mag2, &e);
+        const float l2 = (float)e + __log2f((float)mant);
+        if (l2 * (0.5f * (float)T) < -2200.0f) return make_double2(0.0, 0.0);
+    }
+    double2 acc = make_double2(1.0, 0.0), sq = lam;
+    u64 t = T;
+    while (t) {
+        if (t & 1) acc = cmul(acc, sq);
+        t >>= 1;
+        if (t) sq = make_double2(fma(sq.x, sq.x, -sq.y * sq.y), (sq.x + sq.x) * sq.y);
+    }
+    return acc;
+}
+
+template <int MM>
+__device__ __forceinline__ void matmul_sq(const double2 (&a)[MM][MM], const double2 (&b)[MM][MM], double2 (&c)[MM][MM]) {
+#pragma unroll
+    for (int r = 0; r < MM; ++r)
+#pragma unroll
+        for (int col = 0; col < MM; ++col) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int t = 0; t < MM; ++t) {
+                const double2 p = cmul(a[r][t], b[t][col]);
+                acc = cadd(acc, p);
+            }
+            c[r][col] = acc;
+        }
+}
+
+// acc = I, sq = lam; while t { if t&1 acc = acc*sq; t >>= 1; if t sq = sq*sq }
+// (proj/src/spectrum.cpp:66-82)
+template <int MM>
+__device__ __forceinline__ void pow_block(double2 (&lam)[MM][MM], u64 T) {
+    double2 acc[MM][MM], tmp[MM][MM];
+#pragma unroll
+    for (int r = 0; r < MM; ++r)
+#pragma unroll
+        for (int c = 0; c < MM; ++c) acc[r][c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+    u64 t = T;
+    while (t) {
+        if (t & 1) {
+            matmul_sq<MM>(acc, lam, tmp);
+#pragma unroll
+            for (int r = 0; r < MM; ++r)
+#pragma unroll
+                for (int c = 0; c < MM; ++c) acc[r][c] = tmp[r][c];
+        }
+        t >>= 1;
+        if (t) {
+            matmul_sq<MM>(lam, lam, tmp);
+#pragma unroll
+            for (int r = 0; r < MM; ++r)
+#pragma unroll
+                for (int c = 0; c < MM; ++c) lam[r][c] = tmp[r][c];
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < MM; ++r)
+#pragma unroll
+        for (int c = 0; c < MM; ++c) lam[r][c] = acc[r][c];
+}
+
+__device__ __forceinline__ void flag_nonfinite(bool bad, Flags* f) {
+    const unsigned any = __ballot_sync(0xffffffffu, bad);
+    if (any && (threadIdx.x & 31) == 0) atomicOr(&f->nonfinite, 1u);
+}
+
+// ------------------------------------------------------------------ C2C passes
+// Contiguous lines: line l occupies in[l * pitch + 0 .. N).
+template <int N, int SIGN>
+__global__ void __launch_bounds__(Cfg<N>::LINES * Cfg<N>::TPL)
+k_contig(const double2* in, double2* out, i64 nlines, i64 pitch, const double2* __restrict__ tw_all) {
+    using C = Cfg<N>;
+    using F = LineFFT<N, SIGN>;
+    extern __shared__ double2 sm[];
+    const int b = threadIdx.x / C::TPL, t = threadIdx.x % C::TPL;
+    const i64 line = (i64)blockIdx.x * C::LINES + b;
+    const bool ok = line < nlines;
+    double2 v[C::R];
+    const double2* src = in + line * pitch;
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) v[q] = ok ? src[t + q * C::TPL] : make_double2(0.0, 0.0);
+    F::run(v, t, sm + b * C::LSL, tw_all + N);
+    if (ok) {
+        double2* dst = out + line * pitch;
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) dst[t + q * C::TPL] = v[q];
+    }
+}
+
+// Strided lines: W adjacent columns per CTA, the axis in shared memory.
+template <int N, int SIGN, int TWM>
+__global__ void __launch_bounds__(Cfg<N>::W * Cfg<N>::TPL)
+k_strided(const double2* in, double2* out, AxisGeom g, StepTwiddle st, const double2* __restrict__ tw_all) {
+    using C = Cfg<N>;
+    using F = LineFFT<N, SIGN>;
+    extern __shared__ double2 sm[];
+    const int w = threadIdx.x % C::W, t = threadIdx.x / C::W;
+    const i64 tiles = (g.ncols + C::W - 1) / C::W;
+    const i64 o = (i64)blockIdx.x / tiles;
+    const i64 c = ((i64)blockIdx.x % tiles) * C::W + w;
+    const bool ok = c < g.ncols;
+    const i64 base = o * g.block + c;
+    double2 v[C::R];
+#pragma unroll
+    for (int q = 0; q < C::R; ++q)
+        v[q] = ok ? in[base + (i64)(t + q * C::TPL) * g.inner] : make_double2(0.0, 0.0);
+    if constexpr (TWM == 2) {
+        const i64 bq = c / st.col_div;
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) v[q] = cmulc(v[q], phase_at(st.tab, bq * (i64)(t + q * C::TPL)));
+    }
+    F::run(v, t, sm + w * C::LSW, tw_all + N);
+    if constexpr (TWM == 1) {
+        const i64 bq = c / st.col_div;
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) v[q] = cmul(v[q], phase_at(st.tab, bq * (i64)(t + q * C::TPL)));
+    }
+    if (ok) {
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) out[base + (i64)(t + q * C::TPL) * g.inner] = v[q];
+    }
+}
+
+// Direct O(n^2) DFT for non-power-of-two axes (one line per CTA; the line
+// staged in shared memory so the pass can run in place).
+__global__ void k_direct_dft(const double2* in, double2* out, AxisGeom g, int sign, PhaseTable tab) {
+    extern __shared__ double2 sm[];
+    const i64 line = blockIdx.x;
+    const i64 o = line / g.ncols, c = line % g.ncols;
+    const i64 base = o * g.block + c;
+    const i64 n = g.n;
+    for (i64 p = threadIdx.x; p < n; p += blockDim.x) sm[p] = in[base + p * g.inner];
+    __syncthreads();
+    for (i64 k = threadIdx.x; k < n; k += blockDim.x) {
+        double2 acc = make_double2(0.0, 0.0);
+        i64 idx = 0;
+        for (i64 j = 0; j < n; ++j) {
+            const double2 w = phase_at(tab, idx);
+            acc = cadd(acc, sign < 0 ? cmul(sm[j], w) : cmulc(sm[j], w));
+            idx += k;
+            if (idx >= n) idx -= n;
+        }
+        out[base + k * g.inner] = acc;
+    }
+}
+
+// ------------------------------------------------------------------ real <-> half spectrum rows
+// Row of L = 2M reals viewed as M complex z[j] = x[2j] + i x[2j+1];
+// Z = DFT_M(z); X[k] = E[k] + W_L^k O[k] with E = (Z[k] + conj Z[M-k]) / 2,
+// O = -i (Z[k] - conj Z[M-k]) / 2; X[M] = Re Z[0] - Im Z[0].
+template <int M>
+__global__ void __launch_bounds__(Cfg<M>::LINES * Cfg<M>::TPL)
+k_r2c_rows(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, i64 P,
+           const double2* __restrict__ tw_all) {
+    using C = Cfg<M>;
+    using F = LineFFT<M, -1>;
+    extern __shared__ double2 sm[];
+    const int b = threadIdx.x / C::TPL, t = threadIdx.x % C::TPL;
+    const i64 row = (i64)blockIdx.x * C::LINES + b;
+    const bool ok = row < nrows;
+    double2* line = sm + b * C::LSL;
+    const double2* src = reinterpret_cast<const double2*>(x + row * L);
+    double2 v[C::R];
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) v[q] = ok ? src[t + q * C::TPL] : make_double2(0.0, 0.0);
+    F::run(v, t, line, tw_all + M);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) line[swz(t + q * C::TPL)] = v[q];
+    __syncthreads();
+    if (!ok) return;
+    double2* dst = H + row * P;
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) {
+        const int k = t + q * C::TPL;
+        const double2 zk = v[q];
+        const double2 zm = cconj(line[swz((M - k) & (M - 1))]);
+        const double2 e = cscale(cadd(zk, zm), 0.5);
+        const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
+        const double2 w = __ldg(tw_all + 2 * M + k);  // exp(-2 pi i k / L)
+        dst[k] = cadd(e, cmul(w, od));
+        if (k == 0) dst[M] = make_double2(zk.x - zk.y, 0.0);
+    }
+}
+
+// Inverse: Z[k] = (X[k] + conj X[M-k]) + i conj(W_L^k) (X[k] - conj X[M-k]),
+// unnormalized inverse DFT_M, x[2j] = Re z[j], x[2j+1] = Im z[j] (times L;
+// the 1/N of the inverse transform is folded into the spectral multiply).
+template <int M>
+__global__ void __launch_bounds__(Cfg<M>::LINES * Cfg<M>::TPL)
+k_c2r_rows(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, i64 P,
+           const double2* __restrict__ tw_all, Flags* flags) {
+    using C = Cfg<M>;
+    using F = LineFFT<M, +1>;
+    extern __shared__ double2 sm[];
+    __shared__ double2 nyq[C::LINES];
+    const int b = threadIdx.x / C::TPL, t = threadIdx.x % C::TPL;
+    const i64 row = (i64)blockIdx.x * C::LINES + b;
+    const bool ok = row < nrows;
+    double2* line = sm + b * C::LSL;
+    const double2* src = H + row * P;
+    double2 v[C::R];
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) {
+        v[q] = ok ? src[t + q * C::TPL] : make_double2(0.0, 0.0);
+        line[swz(t + q * C::TPL)] = v[q];
+    }
+    if (t == 0) nyq[b] = ok ? src[M] : make_double2(0.0, 0.0);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) {
+        const int k = t + q * C::TPL;
+        const double2 xm = cconj(k == 0 ? nyq[b] : line[swz(M - k)]);
+        const double2 e = cadd(v[q], xm);
+        const double2 od = cmulc(csub(v[q], xm), __ldg(tw_all + 2 * M + k));
+        v[q] = cadd(e, cmul_si<+1>(od));
+    }
+    F::run(v, t, line, tw_all + M);
+    bool bad = false;
+    if (ok) {
+        double2* dst = reinterpret_cast<double2*>(x + row * L);
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) {
+            dst[t + q * C::TPL] = v[q];
+            bad |= !isfinite(v[q].x) || !isfinite(v[q].y);
+        }
+    }
+    flag_nonfinite(bad, flags);
+}
+
+// ------------------------------------------------------------------ fused spectral pass (R2C layout)
+// Last forward axis (axis 0, strided) -> lam(k)^T * X(k) / N -> first inverse
+// axis pass, one tile in registers + shared memory.  lam(k) is the analytic
+// symbol sum_taps c * exp(+2 pi i sum_a k_a o_a / n_a) (the transform of the
+// reference's generator column, proj/src/spectrum.cpp:21-45), grouped by the
+// axis-0 offset: A_g(column) is formed once per column, then per element
+// lam = sum_g A_g * exp(+2 pi i k0 O_g / n0).
+template <int N>
+__global__ void __launch_bounds__(Cfg<N>::W * Cfg<N>::TPL)
+k_fused_r2c(double2* H, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
+    using C = Cfg<N>;
+    using FF = LineFFT<N, -1>;
+    using FI = LineFFT<N, +1>;
+    extern __shared__ double2 sm[];
+    __shared__ double2 acoef[kMaxGroups][C::W];
+    const int w = threadIdx.x % C::W, t = threadIdx.x / C::W;
+    const i64 tiles = (g.ncols + C::W - 1) / C::W;
+    const i64 o = (i64)blockIdx.x / tiles;
+    const i64 c = ((i64)blockIdx.x % tiles) * C::W + w;
+    i64 ky = 0, kx = c;
+    if (sym.rank == 3) {
+        ky = c / sym.P;
+        kx = c - ky * sym.P;
+    }
+    const bool ok = c < g.ncols && kx <= sym.M;
+    const i64 base = o * g.block + c;
+    double2 v[C::R];
+#pragma unroll
+    for (int q = 0; q < C::R; ++q)
+        v[q] = ok ? H[base + (i64)(t + q * C::TPL) * g.inner] : make_double2(0.0, 0.0);
+    FF::run(v, t, sm + w * C::LSW, tw_all + N);
+    for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
+        double2 a = make_double2(0.0, 0.0);
+        for (int j = 0; j < sym.ntaps; ++j) {
+            if (sym.tap_group[j] != gi) continue;
+            double2 e = eplus_pow2(tw_all, sym.L, kx * (i64)sym.tap_olast[j]);
+            if (sym.rank == 3) e = cmul(e, eplus_pow2(tw_all, sym.n1, ky * (i64)sym.tap_o1[j]));
+            a = make_double2(fma(sym.tap_c[j], e.x, a.x), fma(sym.tap_c[j], e.y, a.y));
+        }
+        acoef[gi][w] = a;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) {
+        const i64 k0 = t + q * C::TPL;
+        double2 lam = make_double2(0.0, 0.0);
+        for (int gi = 0; gi < sym.ngroups; ++gi) {
+            const double2 e = eplus_pow2(tw_all, N, k0 * (i64)sym.group_off[gi]);
+            lam = cadd(lam, cmul(acoef[gi][w], e));
+        }
+        const double2 lt = pow_scalar(lam, sym.T);
+        v[q] = cscale(cmul(lt, v[q]), sym.scale);
+    }
+    FI::run(v, t, sm + w * C::LSW, tw_all + N);
+    if (ok) {
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) H[base + (i64)(t + q * C::TPL) * g.inner] = v[q];
+    }
+}
+
+// ------------------------------------------------------------------ 1D row-pair fused pass
+// z holds the four-step intermediate [N1][N2] (row r, col c = frequency
+// r + N1 c after the row FFT).  One CTA owns rows r and N1 - r, so every
+// frequency k meets its partner M - k (mode 0, real packing) or N - k
+// (mode 1, two-for-one) inside the CTA.
+__device__ __forceinline__ double2 sym1(const RowPairArgs& a, i64 k, i64 n) {
+    double2 lam = make_double2(0.0, 0.0);
+    for (int j = 0; j < a.ntaps; ++j) {
+        const double2 e = cconj(phase_at(a.wk, modp(k * (i64)a.tap_off[j], n)));
+        lam = make_double2(fma(a.tap_b[j][0], e.x, lam.x), fma(a.tap_b[j][0], e.y, lam.y));
+    }
+    return lam;
+}
+
+__device__ __forceinline__ void pair_mode0(const RowPairArgs& a, double2& zk, double2& zp, i64 k, i64 M) {
+    // k in [0, M); partner kp = M - k in (0, M]; for k == 0 the partner is the Nyquist bin.
+    const i64 L = 2 * M, kp = M - k;
+    const double2 cz = cconj(zp);
+    const double2 e = cscale(cadd(zk, cz), 0.5);
+    const double2 od = cscale(cmul_si<-1>(csub(zk, cz)), 0.5);
+    const double2 wk = phase_at(a.wk, k);
+    const double2 wp = phase_at(a.wk, kp);
+    const double2 xk = cadd(e, cmul(wk, od));
+    const double2 xp = cadd(cconj(e), cmul(wp, cconj(od)));
+    const double2 yk = cscale(cmul(pow_scalar(sym1(a, k, L), a.T), xk), a.scale);
+    const double2 yp = cscale(cmul(pow_scalar(sym1(a, kp, L), a.T), xp), a.scale);
+    const double2 cyp = cconj(yp), cyk = cconj(yk);
+    zk = cadd(cadd(yk, cyp), cmul_si<+1>(cmulc(csub(yk, cyp), wk)));
+    if (k != 0) zp = cadd(cadd(yp, cyk), cmul_si<+1>(cmulc(csub(yp, cyk), wp)));
+}
+
+__device__ __forceinline__ void pair_mode1(const RowPairArgs& a, double2& zk, double2& zp, i64 k, i64 N) {
+    const double2 cz = cconj(zp);
+    const double2 u = cscale(cadd(zk, cz), 0.5);
+    const double2 vv = cscale(cmul_si<-1>(csub(zk, cz)), 0.5);
+    double2 lam[2][2] = {{make_double2(0, 0), make_double2(0, 0)}, {make_double2(0, 0), make_double2(0, 0)}};
+    for (int j = 0; j < a.ntaps; ++j) {
+        const double2 e = cconj(phase_at(a.wk, modp(k * (i64)a.tap_off[j], N)));
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                const double bb = a.tap_b[j][r * 2 + cc];
+                lam[r][cc] = make_double2(fma(bb, e.x, lam[r][cc].x), fma(bb, e.y, lam[r][cc].y));
+            }
+    }
+    pow_block<2>(lam, a.T);
+    const double2 u2 = cscale(cadd(cmul(lam[0][0], u), cmul(lam[0][1], vv)), a.scale);
+    const double2 v2 = cscale(cadd(cmul(lam[1][0], u), cmul(lam[1][1], vv)), a.scale);
+    zk = cadd(u2, cmul_si<+1>(v2));
+    zp = cadd(cconj(u2), cmul_si<+1>(cconj(v2)));
+}
+
+template <int N2>
+__global__ void __launch_bounds__(2 * Cfg<N2>::TPL)
+k_rowpair(RowPairArgs a) {
+    using C = Cfg<N2>;
+    using FF = LineFFT<N2, -1>;
+    using FI = LineFFT<N2, +1>;
+    constexpr int LS = N2 + ((C::TPL >= 8) ? 0 : 8 / (8 / C::TPL > 2 ? 2 : 8 / C::TPL));
+    extern __shared__ double2 sm[];
+    const i64 N1 = a.N1, M = a.N1 * a.N2;
+    const i64 ra = blockIdx.x;
+    const i64 rb = (N1 - ra) % N1;
+    const bool self = ra == rb;
+    const int b = threadIdx.x / C::TPL, t = threadIdx.x % C::TPL;
+    const i64 row = b == 0 ? ra : rb;
+    const bool ok = b == 0 || !self;
+    double2* line = sm + b * LS;
+    double2* src = a.z + row * N2;
+    double2 v[C::R];
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) v[q] = ok ? src[t + q * C::TPL] : make_double2(0.0, 0.0);
+    FF::run(v, t, line, a.tw_all + N2);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) line[swz(t + q * C::TPL)] = v[q];
+    __syncthreads();
+    double2* la = sm;
+    double2* lb = self ? sm : sm + LS;
+    const int nth = blockDim.x;
+    if (!self) {
+        for (int cpos = threadIdx.x; cpos < N2; cpos += nth) {
+            const int cp = N2 - 1 - cpos;
+            double2 zk = la[swz(cpos)], zp = lb[swz(cp)];
+            const i64 k = ra + N1 * cpos;
+            if (a.mode == 0) pair_mode0(a, zk, zp, k, M);
+            else pair_mode1(a, zk, zp, k, M);
+            la[swz(cpos)] = zk;
+            lb[swz(cp)] = zp;
+        }
+    } else if (ra == 0) {
+        for (int cpos = threadIdx.x; cpos <= N2 / 2; cpos += nth) {
+            const int cp = (N2 - cpos) % N2;
+            double2 zk = la[swz(cpos)], zp = la[swz(cp)];
+            const i64 k = N1 * (i64)cpos;
+            if (a.mode == 0) pair_mode0(a, zk, zp, k, M);
+            else pair_mode1(a, zk, zp, k, M);
+            if (cp != cpos) la[swz(cp)] = zp;
+            la[swz(cpos)] = zk;
+        }
+    } else {  // ra == N1 / 2
+        for (int cpos = threadIdx.x; cpos < N2 / 2; cpos += nth) {
+            const int cp = N2 - 1 - cpos;
+            double2 zk = la[swz(cpos)], zp = la[swz(cp)];
+            const i64 k = ra + N1 * (i64)cpos;
+            if (a.mode == 0) pair_mode0(a, zk, zp, k, M);
+            else pair_mode1(a, zk, zp, k, M);
+            la[swz(cpos)] = zk;
+            la[swz(cp)] = zp;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) v[q] = line[swz(t + q * C::TPL)];
+    FI::run(v, t, line, a.tw_all + N2);
+    if (ok) {
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) src[t + q * C::TPL] = v[q];
+    }
+}
+
+// ------------------------------------------------------------------ general path
+__global__ void k_promote(const double* __restrict__ x, double2* __restrict__ z, i64 n) {
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        z[i] = make_double2(x[i], 0.0);
+}
+
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* addr, double v) {
+    atomicMax(addr, (unsigned long long)__double_as_longlong(v));
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// realize_checked (proj/src/periodic.cpp:49-65): real part out, finite scan,
+// max |re| and max |im| for the residue test (decided on the host).
+__global__ void k_extract(const double2* __restrict__ z, double* __restrict__ x, i64 n, Flags* flags) {
+    double mre = 0.0, mim = 0.0;
+    bool bad = false;
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        const double2 v = z[i];
+        x[i] = v.x;
+        bad |= !isfinite(v.x) || !isfinite(v.y);
+        mre = fmax(mre, fabs(v.x));
+        mim = fmax(mim, fabs(v.y));
+    }
+    flag_nonfinite(bad, flags);
+    mre = warp_max(mre);
+    mim = warp_max(mim);
+    if ((threadIdx.x & 31) == 0) {
+        atomic_max_nonneg(&flags->max_re_bits, mre);
+        atomic_max_nonneg(&flags->max_im_bits, mim);
+    }
+}
+
+__global__ void k_finite(const double* __restrict__ x, i64 n, Flags* flags) {
+    bool bad = false;
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        bad |= !isfinite(x[i]);
+    flag_nonfinite(bad, flags);
+}
+
+// position -> frequency along each axis (four-step split axes are stored
+// in [k1][k2] order = frequency k1 + n1 k2)
+__device__ __forceinline__ void cell_freqs(const GeneralSymbol& s, i64 cell, i64* k) {
+    for (int a = s.rank - 1; a >= 0; --a) {
+        const i64 n = s.dims[a];
+        const i64 p = cell % n;
+        cell /= n;
+        if (s.split[a]) {
+            const i64 n1 = s.split[a], n2 = n / n1;
+            k[a] = p / n2 + n1 * (p % n2);
+        } else {
+            k[a] = p;
+        }
+    }
+}
+
+// sum_taps B * exp(+2 pi i sum_a k_a o_a / n_a)
+template <int MM>
+__device__ __forceinline__ void symbol_at(const GeneralSymbol& s, const i64* k, int ntaps, const long long* offs,
+                                          const double* blocks, double2 (&lam)[MM][MM], int m) {
+#pragma unroll
+    for (int r = 0; r < MM; ++r)
+#pragma unroll
+        for (int c = 0; c < MM; ++c) lam[r][c] = make_double2(0.0, 0.0);
+    for (int j = 0; j < ntaps; ++j) {
+        double2 e = make_double2(1.0, 0.0);
+        for (int a = 0; a < s.rank; ++a) {
+            const i64 o = offs[j * s.rank + a];
+            if (o == 0) continue;
+            e = cmul(e, cconj(phase_at(s.tab[a], modp(k[a] * o, s.dims[a]))));
+        }
+#pragma unroll
+        for (int r = 0; r < MM; ++r)
+#pragma unroll
+            for (int c = 0; c < MM; ++c) {
+                if (r < m && c < m) {
+                    const double bb = blocks[(j * m + r) * m + c];
+                    lam[r][c] = make_double2(fma(bb, e.x, lam[r][c].x), fma(bb, e.y, lam[r][c].y));
+                }
+            }
+    }
+}
+
+__device__ __forceinline__ double2 crecip(double2 v) {
+    const double d = fma(v.x, v.x, v.y * v.y);
+    return make_double2(v.x / d, -v.y / d);
+}
+
+template <int MM>
+__global__ void k_spectral_general(double2* z, GeneralSymbol s) {
+    for (i64 cell = (i64)blockIdx.x * blockDim.x + threadIdx.x; cell < s.cells;
+         cell += (i64)gridDim.x * blockDim.x) {
+        i64 k[kMaxRank];
+        cell_freqs(s, cell, k);
+        double2 lam[MM][MM];
+        symbol_at<MM>(s, k, s.ntaps, s.offsets, s.blocks, lam, MM);
+        if constexpr (MM == 1) {
+            if (s.implicit) {
+                double2 lq[1][1];
+                symbol_at<1>(s, k, s.ntaps_q, s.offsets_q, s.blocks_q, lq, 1);
+                const double eps = 1e-12 * s.qmax[0];
+                const double mag = hypot(lq[0][0].x, lq[0][0].y);
+                const double2 inv = mag <= eps ? make_double2(0.0, 0.0) : crecip(lq[0][0]);
+                lam[0][0] = cmul(inv, lam[0][0]);
+            }
+            double2 acc = make_double2(1.0, 0.0), sq = lam[0][0];
+            u64 t = s.T;
+            while (t) {
+                if (t & 1) acc = cmul(acc, sq);
+                t >>= 1;
+                if (t) sq = cmul(sq, sq);
+            }
+            z[cell] = cscale(cmul(acc, z[cell]), s.scale);
+        } else {
+            pow_block<MM>(lam, s.T);
+            double2 x[MM], y[MM];
+#pragma unroll
+            for (int f = 0; f < MM; ++f) x[f] = z[cell * MM + f];
+#pragma unroll
+            for (int r = 0; r < MM; ++r) {
+                double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int c = 0; c < MM; ++c) acc = cadd(acc, cmul(lam[r][c], x[c]));
+                y[r] = cscale(acc, s.scale);
+            }
+#pragma unroll
+            for (int f = 0; f < MM; ++f) z[cell * MM + f] = y[f];
+        }
+    }
+}
+
+// spectrum_from_kernel export: blocks at natural-order frequencies.
+template <int MM>
+__global__ void k_symbol_blocks(double2* out, GeneralSymbol s, int which_q) {
+    for (i64 cell = (i64)blockIdx.x * blockDim.x + threadIdx.x; cell < s.cells;
+         cell += (i64)gridDim.x * blockDim.x) {
+        i64 k[kMaxRank];
+        cell_freqs(s, cell, k);
+        double2 lam[MM][MM];
+        if (which_q) symbol_at<MM>(s, k, s.ntaps_q, s.offsets_q, s.blocks_q, lam, MM);
+        else symbol_at<MM>(s, k, s.ntaps, s.offsets, s.blocks, lam, MM);
+#pragma unroll
+        for (int r = 0; r < MM; ++r)
+#pragma unroll
+            for (int c = 0; c < MM; ++c) out[(cell * MM + r) * MM + c] = lam[r][c];
+    }
+}
+
+__global__ void k_symbol_absmax(GeneralSymbol s, unsigned long long* out_bits) {
+    double mx = 0.0;
+    for (i64 cell = (i64)blockIdx.x * blockDim.x + threadIdx.x; cell < s.cells;
+         cell += (i64)gridDim.x * blockDim.x) {
+        i64 k[kMaxRank];
+        cell_freqs(s, cell, k);
+        double2 lam[1][1];
+        symbol_at<1>(s, k, s.ntaps_q, s.offsets_q, s.blocks_q, lam, 1);
+        mx = fmax(mx, hypot(lam[0][0].x, lam[0][0].y));
+    }
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out_bits, mx);
+}
+
+template <int MM>
+__global__ void k_pow_blocks(const double2* in, double2* out, i64 cells, u64 T) {
+    for (i64 cell = (i64)blockIdx.x * blockDim.x + threadIdx.x; cell < cells; cell += (i64)gridDim.x * blockDim.x) {
+        if constexpr (MM == 1) {
+            double2 acc = make_double2(1.0, 0.0), sq = in[cell];
+            u64 t = T;
+            while (t) {
+                if (t & 1) acc = cmul(acc, sq);
+                t >>= 1;
+                if (t) sq = cmul(sq, sq);
+            }
+            out[cell] = acc;
+        } else {
+            double2 lam[MM][MM];
+#pragma unroll
+            for (int r = 0; r < MM; ++r)
+#pragma unroll
+                for (int c = 0; c < MM; ++c) lam[r][c] = in[(cell * MM + r) * MM + c];
+            pow_block<MM>(lam, T);
+#pragma unroll
+            for (int r = 0; r < MM; ++r)
+#pragma unroll
+                for (int c = 0; c < MM; ++c) out[(cell * MM + r) * MM + c] = lam[r][c];
+        }
+    }
+}
+
+__global__ void k_absmax(const double2* in, i64 n, unsigned long long* out_bits) {
+    double mx = 0.0;
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        mx = fmax(mx, hypot(in[i].x, in[i].y));
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out_bits, mx);
+}
+
+// pseudo_inverse_spectrum (proj/src/spectrum.cpp:85-96)
+__global__ void k_pinv(const double2* in, double2* out, i64 n, const double* maxabs) {
+    const double eps = 1e-12 * maxabs[0];
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        const double2 v = in[i];
+        out[i] = hypot(v.x, v.y) <= eps ? make_double2(0.0, 0.0) : crecip(v);
+    }
+}
+
+template <int MM>
+__global__ void k_block_mul(const double2* a, const double2* b, double2* out, i64 cells) {
+    for (i64 cell = (i64)blockIdx.x * blockDim.x + threadIdx.x; cell < cells; cell += (i64)gridDim.x * blockDim.x) {
+        double2 A[MM][MM], B[MM][MM], Cm[MM][MM];
+#pragma unroll
+        for (int r = 0; r < MM; ++r)
+#pragma unroll
+            for (int c = 0; c < MM; ++c) {
+                A[r][c] = a[(cell * MM + r) * MM + c];
+                B[r][c] = b[(cell * MM + r) * MM + c];
+            }
+        matmul_sq<MM>(A, B, Cm);
+#pragma unroll
+        for (int r = 0; r < MM; ++r)
+#pragma unroll
+            for (int c = 0; c < MM; ++c) out[(cell * MM + r) * MM + c] = Cm[r][c];
+    }
+}
+
+// hadamard (proj/src/spectrum.cpp:111-134)
+template <int MM>
+__global__ void k_block_matvec(const double2* lam, const double2* x, double2* y, i64 cells) {
+    for (i64 cell = (i64)blockIdx.x * blockDim.x + threadIdx.x; cell < cells; cell += (i64)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int r = 0; r < MM; ++r) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int c = 0; c < MM; ++c) acc = cadd(acc, cmul(lam[(cell * MM + r) * MM + c], x[cell * MM + c]));
+            y[cell * MM + r] = acc;
+        }
+    }
+}
+
+// [outer][n1][n2][inner] <-> [outer][n2][n1][inner]
+__global__ void k_transpose_split(const double2* in, double2* out, i64 outer, i64 n1, i64 n2, i64 inner,
+                                  int to_natural) {
+    const i64 total = outer * n1 * n2 * inner;
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (i64)gridDim.x * blockDim.x) {
+        const i64 f = i % inner;
+        i64 r = i / inner;
+        // destination-major indexing
+        if (to_natural) {  // dst [o][k2][k1][f] from src [o][k1][k2][f]
+            const i64 k1 = r % n1;
+            r /= n1;
+            const i64 k2 = r % n2;
+            const i64 o = r / n2;
+            out[i] = in[((o * n1 + k1) * n2 + k2) * inner + f];
+        } else {  // dst [o][k1][k2][f] from src [o][k2][k1][f]
+            const i64 k2 = r % n2;
+            r /= n2;
+            const i64 k1 = r % n1;
+            const i64 o = r / n1;
+            out[i] = in[((o * n2 + k2) * n1 + k1) * inner + f];
+        }
+    }
+}
+
+// ================================================================== launchers
+static int grid_for(i64 n, int threads) {
+    i64 b = (n + threads - 1) / threads;
+    if (b > 148 * 16) b = 148 * 16;
+    return (int)(b < 1 ? 1 : b);
+}
+
+template <int N>
+static cudaError_t axis_pow2_n(const double2* in, double2* out, const AxisGeom& g, int sign,
+                               const StepTwiddle& st, const double2* tw, cudaStream_t s) {
+    using C = Cfg<N>;
+    if (g.inner == 1 && st.mode == 0) {
+        const size_t smem = (size_t)C::LINES * C::LSL * sizeof(double2);
+        const int blocks = (int)((g.outer + C::LINES - 1) / C::LINES);
+        auto kf = sign < 0 ? k_contig<N, -1> : k_contig<N, +1>;
+        cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kf<<<blocks, C::LINES * C::TPL, smem, s>>>(in, out, g.outer, g.block, tw);
+        return cudaGetLastError();
+    }
+    const size_t smem = (size_t)C::W * C::LSW * sizeof(double2);
+    const i64 tiles = (g.ncols + C::W - 1) / C::W;
+    const i64 blocks = g.outer * tiles;
+    void (*kf)(const double2*, double2*, AxisGeom, StepTwiddle, const double2*);
+    if (sign < 0) kf = st.mode == 1 ? k_strided<N, -1, 1> : st.mode == 2 ? k_strided<N, -1, 2> : k_strided<N, -1, 0>;
+    else kf = st.mode == 1 ? k_strided<N, +1, 1> : st.mode == 2 ? k_strided<N, +1, 2> : k_strided<N, +1, 0>;
+    cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kf<<<(unsigned)blocks, C::W * C::TPL, smem, s>>>(in, out, g, st, tw);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_axis_pow2(const double2* in, double2* out, const AxisGeom& g, int sign,
+                             const StepTwiddle& st, const double2* tw, cudaStream_t s) {
+    switch (g.n) {
+        case 2: return axis_pow2_n<2>(in, out, g, sign, st, tw, s);
+        case 4: return axis_pow2_n<4>(in, out, g, sign, st, tw, s);
+        case 8: return axis_pow2_n<8>(in, out, g, sign, st, tw, s);
+        case 16: return axis_pow2_n<16>(in, out, g, sign, st, tw, s);
+        case 32: return axis_pow2_n<32>(in, out, g, sign, st, tw, s);
+        case 64: return axis_pow2_n<64>(in, out, g, sign, st, tw, s);
+        case 128: return axis_pow2_n<128>(in, out, g, sign, st, tw, s);
+        case 256: return axis_pow2_n<256>(in, out, g, sign, st, tw, s);
+        case 512: return axis_pow2_n<512>(in, out, g, sign, st, tw, s);
+        case 1024: return axis_pow2_n<1024>(in, out, g, sign, st, tw, s);
+        case 2048: return axis_pow2_n<2048>(in, out, g, sign, st, tw, s);
+        case 4096: return axis_pow2_n<4096>(in, out, g, sign, st, tw, s);
+        case 8192: return axis_pow2_n<8192>(in, out, g, sign, st, tw, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_axis_direct(const double2* in, double2* out, const AxisGeom& g, int sign,
+                               const PhaseTable& tab, cudaStream_t s) {
+    const size_t smem = (size_t)g.n * sizeof(double2);
+    cudaFuncSetAttribute(k_direct_dft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const i64 lines = g.outer * g.ncols;
+    k_direct_dft<<<(unsigned)lines, 256, smem, s>>>(in, out, g, sign, tab);
+    return cudaGetLastError();
+}
+
+template <int M>
+static cudaError_t r2c_m(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
+    using C = Cfg<M>;
+    const size_t smem = (size_t)C::LINES * C::LSL * sizeof(double2);
+    cudaFuncSetAttribute(k_r2c_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_r2c_rows<M><<<(unsigned)((nrows + C::LINES - 1) / C::LINES), C::LINES * C::TPL, smem, s>>>(x, H, nrows, L, P, tw);
+    return cudaGetLastError();
+}
+
+template <int M>
+static cudaError_t c2r_m(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
+                         cudaStream_t s) {
+    using C = Cfg<M>;
+    const size_t smem = (size_t)C::LINES * C::LSL * sizeof(double2);
+    cudaFuncSetAttribute(k_c2r_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_c2r_rows<M><<<(unsigned)((nrows + C::LINES - 1) / C::LINES), C::LINES * C::TPL, smem, s>>>(H, x, nrows, L, P, tw, f);
+    return cudaGetLastError();
+}
+
+#define FSX_POW2_CASES(MACRO) \
+    MACRO(8) MACRO(16) MACRO(32) MACRO(64) MACRO(128) MACRO(256) MACRO(512) MACRO(1024) MACRO(2048) MACRO(4096) MACRO(8192)
+
+cudaError_t launch_r2c_rows(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
+    switch (L / 2) {
+#define C_(M) case M: return r2c_m<M>(x, H, nrows, L, P, tw, s);
+        FSX_POW2_CASES(C_)
+#undef C_
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_c2r_rows(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
+                            cudaStream_t s) {
+    switch (L / 2) {
+#define C_(M) case M: return c2r_m<M>(H, x, nrows, L, P, tw, f, s);
+        FSX_POW2_CASES(C_)
+#undef C_
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int N>
+static cudaError_t fused_n(double2* H, const AxisGeom& g, const FusedSymbol& sym, const double2* tw, cudaStream_t s) {
+    using C = Cfg<N>;
+    const size_t smem = (size_t)C::W * C::LSW * sizeof(double2);
+    const i64 tiles = (g.ncols + C::W - 1) / C::W;
+    cudaFuncSetAttribute(k_fused_r2c<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_fused_r2c<N><<<(unsigned)(g.outer * tiles), C::W * C::TPL, smem, s>>>(H, g, sym, tw);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fused_r2c(double2* H, const AxisGeom& g, const FusedSymbol& sym, const double2* tw, cudaStream_t s) {
+    switch (g.n) {
+#define C_(N) case N: return fused_n<N>(H, g, sym, tw, s);
+        FSX_POW2_CASES(C_)
+#undef C_
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int N2>
+static cudaError_t rowpair_n(const RowPairArgs& a, cudaStream_t s) {
+    using C = Cfg<N2>;
+    constexpr int LS = N2 + ((C::TPL >= 8) ? 0 : 8 / (8 / C::TPL > 2 ? 2 : 8 / C::TPL));
+    const size_t smem = (size_t)2 * LS * sizeof(double2);
+    cudaFuncSetAttribute(k_rowpair<N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const i64 ctas = a.N1 / 2 + 1;
+    k_rowpair<N2><<<(unsigned)(a.N1 == 1 ? 1 : ctas), 2 * C::TPL, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rowpair(const RowPairArgs& a, cudaStream_t s) {
+    switch (a.N2) {
+#define C_(N) case N: return rowpair_n<N>(a, s);
+        FSX_POW2_CASES(C_)
+#undef C_
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_promote(const double* x, double2* z, i64 n, cudaStream_t s) {
+    k_promote<<<grid_for(n, 256), 256, 0, s>>>(x, z, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_extract(const double2* z, double* x, i64 n, Flags* f, cudaStream_t s) {
+    k_extract<<<grid_for(n, 256), 256, 0, s>>>(z, x, n, f);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finite_check(const double* x, i64 n, Flags* f, cudaStream_t s) {
+    k_finite<<<grid_for(n, 256), 256, 0, s>>>(x, n, f);
+    return cudaGetLastError();
+}
+
+__global__ void k_scale(double2* z, i64 n, double sc) {
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        z[i] = cscale(z[i], sc);
+}
+
+cudaError_t launch_scale(double2* z, i64 n, double scale, cudaStream_t s) {
+    k_scale<<<grid_for(n, 256), 256, 0, s>>>(z, n, scale);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_spectral_general(double2* z, const GeneralSymbol& sym, cudaStream_t s) {
+    const int g = grid_for(sym.cells, 128);
+    switch (sym.m) {
+        case 1: k_spectral_general<1><<<g, 128, 0, s>>>(z, sym); break;
+        case 2: k_spectral_general<2><<<g, 128, 0, s>>>(z, sym); break;
+        case 3: k_spectral_general<3><<<g, 128, 0, s>>>(z, sym); break;
+        case 4: k_spectral_general<4><<<g, 128, 0, s>>>(z, sym); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_symbol_blocks(double2* out, const GeneralSymbol& sym, int which_q, cudaStream_t s) {
+    const int g = grid_for(sym.cells, 128);
+    switch (sym.m) {
+        case 1: k_symbol_blocks<1><<<g, 128, 0, s>>>(out, sym, which_q); break;
+        case 2: k_symbol_blocks<2><<<g, 128, 0, s>>>(out, sym, which_q); break;
+        case 3: k_symbol_blocks<3><<<g, 128, 0, s>>>(out, sym, which_q); break;
+        case 4: k_symbol_blocks<4><<<g, 128, 0, s>>>(out, sym, which_q); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_symbol_absmax(const GeneralSymbol& sym, double* out_max, cudaStream_t s) {
+    k_symbol_absmax<<<grid_for(sym.cells, 128), 128, 0, s>>>(sym, reinterpret_cast<unsigned long long*>(out_max));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pow_blocks(const double2* in, double2* out, i64 cells, int m, u64 T, cudaStream_t s) {
+    const int g = grid_for(cells, 128);
+    switch (m) {
+        case 1: k_pow_blocks<1><<<g, 128, 0, s>>>(in, out, cells, T); break;
+        case 2: k_pow_blocks<2><<<g, 128, 0, s>>>(in, out, cells, T); break;
+        case 3: k_pow_blocks<3><<<g, 128, 0, s>>>(in, out, cells, T); break;
+        case 4: k_pow_blocks<4><<<g, 128, 0, s>>>(in, out, cells, T); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_absmax(const double2* in, i64 n, double* out_max, cudaStream_t s) {
+    k_absmax<<<grid_for(n, 256), 256, 0, s>>>(in, n, reinterpret_cast<unsigned long long*>(out_max));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pinv(const double2* in, double2* out, i64 n, const double* maxabs, cudaStream_t s) {
+    k_pinv<<<grid_for(n, 256), 256, 0, s>>>(in, out, n, maxabs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_block_mul(const double2* a, const double2* b, double2* out, i64 cells, int m, cudaStream_t s) {
+    const int g = grid_for(cells, 128);
+    switch (m) {
+        case 1: k_block_mul<1><<<g, 128, 0, s>>>(a, b, out, cells); break;
+        case 2: k_block_mul<2><<<g, 128, 0, s>>>(a, b, out, cells); break;
+        case 3: k_block_mul<3><<<g, 128, 0, s>>>(a, b, out, cells); break;
+        case 4: k_block_mul<4><<<g, 128, 0, s>>>(a, b, out, cells); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_block_matvec(const double2* lam, const double2* x, double2* y, i64 cells, int m, cudaStream_t s) {
+    const int g = grid_for(cells, 128);
+    switch (m) {
+        case 1: k_block_matvec<1><<<g, 128, 0, s>>>(lam, x, y, cells); break;
+        case 2: k_block_matvec<2><<<g, 128, 0, s>>>(lam, x, y, cells); break;
+        case 3: k_block_matvec<3><<<g, 128, 0, s>>>(lam, x, y, cells); break;
+        case 4: k_block_matvec<4><<<g, 128, 0, s>>>(lam, x, y, cells); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_transpose_split(const double2* in, double2* out, i64 outer, i64 n1, i64 n2, i64 inner,
+                                   int to_natural, cudaStream_t s) {
+    k_transpose_split<<<grid_for(outer * n1 * n2 * inner, 256), 256, 0, s>>>(in, out, outer, n1, n2, inner, to_natural);
+    return cudaGetLastError();
+}
+
+}  // namespace fsx

@@ -1,0 +1,137 @@
+// Host-visible launch interface of the sm_100a kernels (fsx_kernels.cu).
+// Every launcher enqueues on `stream` and returns the launch error (if any);
+// none of them synchronizes.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fsx {
+
+using i64 = long long;
+using u64 = unsigned long long;
+
+constexpr int kMaxLine = 8192;      // longest pow2 line one CTA transforms
+constexpr int kMaxTwPow2 = 32768;   // global pow2 twiddle tables cover N <= this
+constexpr int kMaxRank = 8;
+constexpr int kMaxFusedTaps = 64;
+constexpr int kMaxGroups = 16;
+constexpr int kMaxDirect = 12288;   // direct-DFT line limit (non-pow2 axes)
+
+// exp(-2 pi i x / n) for any x in [0, n): lo[x & mask] * hi[x >> shift]
+// (shift == 0: a single full table lo[x]).
+struct PhaseTable {
+    const double2* lo = nullptr;
+    const double2* hi = nullptr;
+    int shift = 0;
+    i64 mask = 0;
+    i64 n = 1;
+};
+
+// Four-step twiddle applied around a strided pass: W_n^(b * k) with
+// b = column / col_div (the "n2" digit) and k the line position.
+struct StepTwiddle {
+    int mode = 0;  // 0 none, 1 post-multiply (forward), 2 pre-multiply by conj (inverse)
+    i64 col_div = 1;
+    PhaseTable tab;
+};
+
+// Lines along one axis of a complex array.
+//   element(o, c, p) = base[o * block + c + p * inner], p in [0, n)
+struct AxisGeom {
+    i64 n = 1;       // line length
+    i64 inner = 1;   // element stride along the line
+    i64 outer = 1;   // number of outer blocks
+    i64 block = 1;   // element stride between outer blocks
+    i64 ncols = 1;   // columns c in [0, ncols) per outer block (ncols <= inner when inner > 1)
+};
+
+// Symbol description for the fused half-spectrum (m = 1, R2C) pass along
+// axis 0 of a rank-2/3 pow2 grid.  Taps are grouped by their axis-0 offset.
+struct FusedSymbol {
+    int rank = 2;
+    int ntaps = 0;
+    int ngroups = 0;
+    i64 n0 = 1, n1 = 1, L = 1;   // dims: axis0, axis1 (rank 3 only), last axis (real length)
+    i64 P = 1;                   // half-spectrum row pitch (complex)
+    i64 M = 1;                   // L / 2
+    int group_off[kMaxGroups];   // axis-0 offset of each group
+    int tap_group[kMaxFusedTaps];
+    int tap_o1[kMaxFusedTaps];   // axis-1 offset (rank 3)
+    int tap_olast[kMaxFusedTaps];
+    double tap_c[kMaxFusedTaps];
+    u64 T = 1;
+    double scale = 1.0;          // 1 / prod(dims)
+};
+
+// General spectral stage over a full complex spectrum with m fields.
+struct GeneralSymbol {
+    int rank = 1;
+    int m = 1;
+    i64 cells = 1;
+    i64 dims[kMaxRank];
+    i64 split[kMaxRank];         // 0: natural order; else n1 of a four-step split axis
+    PhaseTable tab[kMaxRank];    // exp(-2 pi i x / dims[a])
+    int ntaps = 0;
+    const long long* offsets = nullptr;  // [ntaps * rank]
+    const double* blocks = nullptr;      // [ntaps * m * m]
+    // implicit (scalar): second tap set, lambda = pinv(lamQ) * lamS
+    int implicit = 0;
+    int ntaps_q = 0;
+    const long long* offsets_q = nullptr;
+    const double* blocks_q = nullptr;
+    const double* qmax = nullptr;        // device scalar: max |lamQ|
+    u64 T = 1;
+    double scale = 1.0;
+};
+
+// 1D fused row-pair pass (four-step row stage + pairing + spectral + inverse rows).
+struct RowPairArgs {
+    double2* z;          // [N1][N2] complex in four-step transposed order
+    i64 N1 = 1, N2 = 1;  // M = N1 * N2 complex points
+    int mode = 0;        // 0: real packing (m = 1, L = 2M reals); 1: two-for-one (m = 2, N = M)
+    const double2* tw_all = nullptr;  // pow2 line twiddles
+    PhaseTable wk;       // exp(-2 pi i x / L) for the R2C split twiddle (mode 0) and the symbol
+    int ntaps = 0;
+    int tap_off[kMaxFusedTaps];
+    double tap_b[kMaxFusedTaps][4];   // m x m block, row-major (m <= 2)
+    u64 T = 1;
+    double scale = 1.0;
+};
+
+struct Flags {
+    unsigned int nonfinite;
+    unsigned int pad;
+    unsigned long long max_re_bits;  // max |re| as ordered bits of a nonnegative double
+    unsigned long long max_im_bits;
+};
+
+// ---------------------------------------------------------------- launchers
+// Twiddle tables: tw_all[N + x] = exp(-2 pi i x / N) for pow2 N <= kMaxTwPow2.
+cudaError_t launch_axis_pow2(const double2* in, double2* out, const AxisGeom& g, int sign,
+                             const StepTwiddle& st, const double2* tw_all, cudaStream_t s);
+cudaError_t launch_axis_direct(const double2* in, double2* out, const AxisGeom& g, int sign,
+                               const PhaseTable& tab, cudaStream_t s);
+cudaError_t launch_r2c_rows(const double* x, double2* H, i64 nrows, i64 L, i64 P,
+                            const double2* tw_all, cudaStream_t s);
+cudaError_t launch_c2r_rows(const double2* H, double* x, i64 nrows, i64 L, i64 P,
+                            const double2* tw_all, Flags* flags, cudaStream_t s);
+cudaError_t launch_fused_r2c(double2* H, const AxisGeom& g, const FusedSymbol& sym,
+                             const double2* tw_all, cudaStream_t s);
+cudaError_t launch_rowpair(const RowPairArgs& a, cudaStream_t s);
+cudaError_t launch_promote(const double* x, double2* z, i64 n, cudaStream_t s);
+cudaError_t launch_extract(const double2* z, double* x, i64 n, Flags* flags, cudaStream_t s);
+cudaError_t launch_scale(double2* z, i64 n, double scale, cudaStream_t s);
+cudaError_t launch_finite_check(const double* x, i64 n, Flags* flags, cudaStream_t s);
+cudaError_t launch_spectral_general(double2* z, const GeneralSymbol& sym, cudaStream_t s);
+cudaError_t launch_symbol_blocks(double2* out, const GeneralSymbol& sym, int which_q, cudaStream_t s);
+cudaError_t launch_symbol_absmax(const GeneralSymbol& sym, double* out_max, cudaStream_t s);
+cudaError_t launch_pow_blocks(const double2* in, double2* out, i64 cells, int m, u64 T, cudaStream_t s);
+cudaError_t launch_pinv(const double2* in, double2* out, i64 n, const double* maxabs, cudaStream_t s);
+cudaError_t launch_absmax(const double2* in, i64 n, double* out_max, cudaStream_t s);
+cudaError_t launch_block_mul(const double2* a, const double2* b, double2* out, i64 cells, int m, cudaStream_t s);
+cudaError_t launch_block_matvec(const double2* lam, const double2* x, double2* y, i64 cells, int m, cudaStream_t s);
+cudaError_t launch_transpose_split(const double2* in, double2* out, i64 outer, i64 n1, i64 n2, i64 inner,
+                                   int to_natural, cudaStream_t s);
+
+}  // namespace fsx

@@ -1,0 +1,447 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+known answers, its property tests, and the CPU oracle on the same seeded
+inputs.  Each test cites the reference test it re-expresses.
+
+Tolerances: the reference's own (1e-12 .. 1e-8 absolute-relative, as cited),
+and relative L2 <= 1e-10 against the oracle for the fp64 configs (BASELINE
+north_star).
+"""
+import numpy as np
+import pytest
+
+import refutil as R
+from refutil import Rng
+
+pytestmark = pytest.mark.gpu
+
+fs = pytest.importorskip("paper_2105_06676_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if fs.device_count() < 1:
+        pytest.fail("no CUDA device visible: the GPU parity tests must run on a B200")
+
+
+def K(k: R.Kern) -> "fs.StencilKernel":
+    out = fs.StencilKernel(k.rank, k.fields)
+    for off in sorted(k.taps):
+        out.add_tap(off, k.taps[off] if k.fields > 1 else float(k.taps[off][0, 0]))
+    return out
+
+
+def G(dims, data, m=1):
+    return fs.FieldGrid(fs.GridShape(dims, m), data)
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+# ------------------------------------------------------------------ golden vectors
+def test_golden_known_answers(golden):
+    c = golden["appendix_one_step"]
+    k = R.kern_from({tuple(o): v for o, v in zip(c["offsets"], c["values"])}, 1)
+    out = fs.solve_periodic(G(c["dims"], c["a0"]), K(k), c["T"])
+    assert np.abs(out.data - np.array(c["want"], float)).max() <= c["tol"]
+    for path in (0, 1):
+        out = fs.solve_periodic(G(c["dims"], c["a0"]), K(k), c["T"], path=path)
+        assert np.abs(out.data - np.array(c["want"], float)).max() <= 1e-10
+
+    c = golden["shift_spectrum"]
+    lam = fs.spectrum_from_kernel(K(R.kern_from({(1,): 1.0}, 1)), fs.GridShape(c["dims"]))
+    want = np.array(c["want_re"]) + 1j * np.array(c["want_im"])
+    assert np.abs(lam.blocks - want).max() < c["tol"]
+    c = golden["appendix_generator"]
+    lam = fs.spectrum_from_kernel(K(R.appendix_kernel()), fs.GridShape(c["dims"]))
+    assert abs(lam.blocks[0] - complex(*c["want_lambda0"])) < c["tol"]
+    c = golden["identity_spectrum"]
+    lam = fs.spectrum_from_kernel(K(R.kern_from({(0, 0): 1.0}, 2)), fs.GridShape(c["dims"]))
+    assert np.abs(lam.blocks - 1.0).max() < c["tol"]
+
+    for name in ("fft_delta", "fft_ones"):
+        c = golden[name]
+        got = fs.multi_fft(fs.ComplexGrid(fs.GridShape(c["dims"]), np.array(c["input_re"], complex)))
+        want = np.array(c["want_re"]) + 1j * np.array(c["want_im"])
+        assert np.abs(got.data - want).max() <= c["tol"]
+
+    c = golden["pow_scalar"]
+    lam = fs.DiagonalSpectrum(fs.GridShape([2]), [complex(*v) for v in c["lambda"]])
+    for chk in c["checks"]:
+        got = fs.pow_spectrum(lam, chk["T"]).blocks[chk["index"]]
+        if chk["tol"] == 0.0:
+            assert got == complex(*chk["want"])
+        else:
+            assert abs(got - complex(*chk["want"])) < chk["tol"]
+    c = golden["pinv"]
+    got = fs.pseudo_inverse_spectrum(fs.DiagonalSpectrum(fs.GridShape([3]), [complex(*v) for v in c["lambda"]]))
+    assert np.abs(got.blocks - np.array([complex(*v) for v in c["want"]])).max() < c["tol"]
+    assert got.blocks[1] == 0
+
+
+def test_golden_errors(golden):
+    c = golden["blowup_numeric_error"]
+    a = R.random_grid(Rng(c["seed"]), 16)
+    k = R.kern_from({(0,): 1e8, (1,): 1e8}, 1)
+    with pytest.raises(fs.NumericError):
+        fs.solve_periodic(G([16], a), K(k), c["T"])
+    with pytest.raises(fs.NumericError):
+        fs.solve_periodic(G([16], a), K(k), c["T"], path=1)
+    with pytest.raises(fs.SpecError):
+        fs.solve_periodic_vector(G([8], np.zeros(8)), K(R.kern_from({(0,): 1.0}, 1)), 1)
+
+
+def test_golden_cli_fixtures(golden, orc):
+    c = golden["cli_verify_heat1d"]
+    k = R.kern_from({tuple(o): v for o, v in zip(c["offsets"], c["values"])}, 1)
+    a0 = orc.splitmix_fill(c["seed"], 256, True)
+    fast = fs.solve_periodic(G([256], a0), K(k), c["T"]).data
+    slow = orc.evolve_periodic_naive(a0, [256], 1, *k.arrays(), c["T"])
+    assert np.abs(fast - slow).max() <= c["tol_rel1p"] * (1 + np.abs(slow).max())
+
+
+# ------------------------------------------------------------------ FFT (proj/tests/test_fft.cpp)
+def test_fft_vs_direct_dft():
+    rng = Rng(23)
+    for n in (7, 12, 15, 32, 1000):
+        g = R.random_complex_grid(rng, n)
+        got = fs.multi_fft(fs.ComplexGrid(fs.GridShape([n]), g)).data
+        want = R.direct_dft(g)
+        assert np.abs(got - want).max() <= 1e-10 * (1 + np.abs(want).max()), n
+
+
+def test_multi_fft_vs_nested_sum():
+    rng = Rng(29)
+    for dims, m in (([12], 1), ([6, 10], 2), ([3, 4, 5], 1), ([16, 32], 1), ([8, 4, 64], 2)):
+        g = R.random_complex_grid(rng, int(np.prod(dims)) * m)
+        shape = fs.GridShape(dims, m)
+        got = fs.multi_fft(fs.ComplexGrid(shape, g)).data
+        want = R.direct_multi_dft(g, dims, m)
+        assert np.abs(got - want).max() <= 1e-10 * (1 + np.abs(want).max())
+        goti = fs.multi_ifft(fs.ComplexGrid(shape, g)).data
+        wanti = R.direct_multi_dft(g, dims, m, inverse=True)
+        assert np.abs(goti - wanti).max() <= 1e-10
+
+
+def test_fft_round_trip_and_vs_oracle(orc):
+    rng = Rng(31)
+    for dims, m in (([7], 1), ([12], 1), ([64, 64], 1), ([17, 241], 1), ([11, 13, 5], 2), ([1, 9], 1),
+                    ([4096], 1), ([8192], 1), ([1 << 15], 1), ([1 << 17], 2), ([512, 1024], 1)):
+        g = R.random_complex_grid(rng, int(np.prod(dims)) * m) if np.prod(dims) < 5000 else \
+            (np.random.default_rng(7).uniform(-1, 1, int(np.prod(dims)) * m)
+             + 1j * np.random.default_rng(8).uniform(-1, 1, int(np.prod(dims)) * m))
+        shape = fs.GridShape(dims, m)
+        fwd = fs.multi_fft(fs.ComplexGrid(shape, g))
+        back = fs.multi_ifft(fwd).data
+        assert np.abs(back - g).max() <= 1e-10 * (1 + np.abs(g).max()), dims
+        want = orc.multi_fft(g, dims, m)
+        assert rel_l2(fwd.data, want) <= 1e-13, dims
+
+
+# ------------------------------------------------------------------ spectral (proj/tests/test_spectral.cpp)
+def test_spectrum_vs_oracle_and_dense(orc):
+    rng = Rng(37)
+    for _ in range(12):
+        rank = 1 + rng.next() % 2
+        m = 1 + rng.next() % 2
+        dims = [rng.range(2, 16 if rank == 1 else 4) for _ in range(rank)]
+        if np.prod(dims) > 16:
+            continue
+        k = R.random_kernel(rng, rank, max(min(1, min(dims) - 1), 0), m)
+        if k.max_reach()[0] >= min(dims):
+            continue
+        lam = fs.spectrum_from_kernel(K(k), fs.GridShape(dims, m)).blocks
+        want = orc.spectrum_from_kernel(dims, m, *k.arrays())
+        assert np.abs(lam - want).max() <= 1e-12
+        S = orc.dense_stencil_matrix(dims, m, *k.arrays()).astype(complex)
+        conj = R.dense_dft_matrix(dims, m) @ S @ R.dense_idft_matrix(dims, m)
+        lam3 = lam.reshape(-1, m, m)
+        for r in range(S.shape[0]):
+            for c in range(S.shape[0]):
+                w = lam3[r // m, r % m, c % m] if r // m == c // m else 0.0
+                assert abs(conj[r, c] - w) <= 1e-10
+
+
+def test_pow_hadamard_multiply(orc):
+    rng = Rng(41)
+    lam = np.zeros((3, 2, 2), complex)
+    for j in range(3):
+        a, b, c = 0.9 * rng.symmetric(), 0.3 * rng.symmetric(), rng.symmetric()
+        lam[j] = [[complex(a, b), c], [0, 1]]
+    got = fs.pow_spectrum(fs.DiagonalSpectrum(fs.GridShape([3], 2), lam), 8).blocks.reshape(3, 2, 2)
+    for j in range(3):
+        want = np.linalg.matrix_power(lam[j], 8)
+        assert np.abs(got[j] - want).max() <= 1e-12 * (1 + np.abs(want).max())
+    rng = Rng(43)
+    shape = fs.GridShape([8, 3])
+    L = fs.DiagonalSpectrum(shape, [complex(rng.symmetric(), rng.symmetric()) for _ in range(24)])
+    for a, b in ((3, 5), (1, 31), (16, 16), (0, 32)):
+        lhs = fs.pow_spectrum(L, a + b).blocks
+        prod = fs.multiply_spectra(fs.pow_spectrum(L, a), fs.pow_spectrum(L, b)).blocks
+        assert np.abs(lhs - prod).max() <= 1e-10 * (1 + np.abs(lhs).max())
+    rng = Rng(47)
+    shape = fs.GridShape([4], 2)
+    x = fs.ComplexGrid(shape, R.random_complex_grid(rng, 8))
+    ident = fs.DiagonalSpectrum(shape, np.tile(np.eye(2), (4, 1, 1)))
+    assert np.abs(fs.hadamard(ident, x).data - x.data).max() <= 1e-15
+    lamr = np.array([[[complex(rng.symmetric(), rng.symmetric()) for _ in range(2)] for _ in range(2)]
+                     for _ in range(4)])
+    y = fs.hadamard(fs.DiagonalSpectrum(shape, lamr), x).data
+    assert np.abs(y - orc.hadamard(lamr, x.data, [4], 2)).max() <= 1e-15
+    with pytest.raises(fs.SpecError):
+        fs.hadamard(ident, fs.ComplexGrid(fs.GridShape([5], 2)))
+    with pytest.raises(fs.SpecError):
+        fs.pseudo_inverse_spectrum(fs.DiagonalSpectrum(fs.GridShape([3], 2)))
+
+
+# ------------------------------------------------------------------ periodic (proj/tests/test_periodic.cpp)
+def test_identity_any_T():
+    a = R.random_grid(Rng(53), 64)
+    k = K(R.kern_from({(0,): 1.0}, 1))
+    for T in (1, 97, 1 << 40):
+        for path in (0, 1):
+            assert np.abs(fs.solve_periodic(G([64], a), k, T, path=path).data - a).max() <= 1e-12
+
+
+def test_heat_vs_naive(orc):
+    a = R.random_grid(Rng(59), 32)
+    k = R.heat1d(0.125)
+    fast = fs.solve_periodic(G([32], a), K(k), 100).data
+    slow = orc.evolve_periodic_naive(a, [32], 1, *k.arrays(), 100)
+    assert np.abs(fast - slow).max() <= 1e-9 * (1 + np.abs(slow).max())
+
+
+def test_T0_bit_exact():
+    rng = Rng(61)
+    a = R.random_grid(rng, 64)
+    k = R.random_kernel(rng, 2, 1)
+    assert (fs.solve_periodic(G([8, 8], a), K(k), 0).data == a).all()
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_randomized_vs_naive(orc, path):
+    """test_periodic.cpp:64-84 and acceptance criterion 2 (dims 4..32 incl. primes)."""
+    rng = Rng(67)
+    times = (0, 1, 2, 3, 7, 16, 100)
+    for trial in range(40):
+        rank = 1 + rng.next() % 3
+        dims = [rng.range(4, 12 if rank == 3 else 32) for _ in range(rank)]
+        m = 2 if trial % 4 == 0 else 1
+        k = R.random_kernel(rng, rank, rng.range(1, 2), m)
+        a = R.random_grid(rng, int(np.prod(dims)) * m)
+        T = times[rng.next() % 7]
+        fast = fs.solve_periodic(G(dims, a, m), K(k), T, path=path).data
+        slow = orc.evolve_periodic_naive(a, dims, m, *k.arrays(), T)
+        assert np.abs(fast - slow).max() <= 1e-8 * (1 + np.abs(slow).max()), (dims, m, T)
+
+
+def test_acceptance_oracle_equivalence(orc):
+    """proj/tests/acceptance.cpp:82-107 (300 cases, dims 4..32, target norm 0.95)."""
+    rng = Rng(2002)
+    times = (0, 1, 2, 3, 7, 16, 100)
+    worst = 0.0
+    for trial in range(300):
+        rank = 1 + rng.next() % 3
+        dims = [rng.range(4, 32) for _ in range(rank)]
+        m = 2 if trial % 5 == 0 else 1
+        k = R.random_kernel(rng, rank, rng.range(1, 2), m, 0.95)
+        a = R.random_grid(rng, int(np.prod(dims)) * m)
+        T = times[rng.next() % 7]
+        fast = fs.solve_periodic(G(dims, a, m), K(k), T).data
+        slow = orc.evolve_periodic_naive(a, dims, m, *k.arrays(), T)
+        worst = max(worst, np.abs(fast - slow).max() / (1 + np.abs(slow).max()))
+    assert worst <= 1e-8
+
+
+def test_semigroup_shift_vector_affine(orc):
+    rng = Rng(71)
+    k = K(R.heat1d(0.2))
+    a = R.random_grid(rng, 48)
+    for s, t in ((3, 5), (31, 33), (64, 1)):
+        whole = fs.solve_periodic(G([48], a), k, s + t).data
+        split = fs.solve_periodic(fs.solve_periodic(G([48], a), k, s), k, t).data
+        assert np.abs(whole - split).max() <= 1e-9 * (1 + np.abs(whole).max())
+    rng = Rng(73)
+    dims = [10, 12]
+    kk = R.random_kernel(rng, 2, 1)
+    a = R.random_grid(rng, 120)
+    lhs = fs.solve_periodic(G(dims, R.rotate_grid(a, dims, 1, (3, 7))), K(kk), 9).data
+    rhs = R.rotate_grid(fs.solve_periodic(G(dims, a), K(kk), 9).data, dims, 1, (3, 7))
+    assert np.abs(lhs - rhs).max() <= 1e-10
+    # block-diagonal kernels decouple (test_periodic.cpp:109-139)
+    k0, k1 = K(R.heat1d(0.125)), K(R.heat1d(0.25))
+    e01, e10 = fs.StencilKernel(1), fs.StencilKernel(1)
+    e01.add_tap([0], 0.0)
+    e10.add_tap([0], 0.0)
+    folded = fs.fold_kernels([[k0, e01], [e10, k1]])
+    a = R.random_grid(Rng(79), 32)
+    whole = fs.solve_periodic_vector(G([16], a, 2), folded, 20).data
+    f0 = fs.solve_periodic(G([16], a[0::2]), k0, 20).data
+    f1 = fs.solve_periodic(G([16], a[1::2]), k1, 20).data
+    assert np.abs(whole[0::2] - f0).max() <= 1e-12 * (1 + np.abs(f0).max())
+    assert np.abs(whole[1::2] - f1).max() <= 1e-12 * (1 + np.abs(f1).max())
+    assert (fs.solve_periodic_vector(G([16], a, 2), folded, 0).data == a).all()
+    # affine encoding (test_periodic.cpp:141-182)
+    rng = Rng(83)
+    n, T, c = 64, 50, 0.37
+    s = R.heat1d(0.125)
+    fk = fs.StencilKernel(1, 2)
+    for off, blk in s.taps.items():
+        fk.add_tap(off, [[blk[0, 0], 0.0], [0.0, 0.0]])
+    fk.add_tap([0], [[0.0, 1.0], [0.0, 1.0]])
+    a = np.zeros(2 * n)
+    direct = np.zeros(n)
+    for i in range(n):
+        v = rng.symmetric()
+        a[2 * i], a[2 * i + 1], direct[i] = v, c, v
+    fast = fs.solve_periodic_vector(G([n], a, 2), fk, T).data
+    for _ in range(T):
+        direct = orc.step_periodic(direct, [n], 1, *s.arrays()) + c
+    assert np.abs(fast[0::2] - direct).max() <= 1e-9
+
+
+def test_implicit(orc):
+    ident = K(R.kern_from({(0,): 1.0}, 1))
+    s = K(R.heat1d(0.125))
+    a = R.random_grid(Rng(89), 24)
+    imp = fs.solve_periodic_implicit(ident, s, G([24], a), 13).data
+    exp = fs.solve_periodic(G([24], a), s, 13).data
+    assert np.abs(imp - exp).max() <= 1e-12
+    assert (fs.solve_periodic_implicit(ident, s, G([24], a), 0).data == a).all()
+    beta = 0.125
+    q = R.kern_from({(-1,): -beta, (0,): 1 + 2 * beta, (1,): -beta}, 1)
+    sk = R.kern_from({(-1,): beta, (0,): 1 - 2 * beta, (1,): beta}, 1)
+    a0 = R.random_grid(Rng(97), 16)
+    Q = orc.dense_stencil_matrix([16], 1, *q.arrays())
+    S = orc.dense_stencil_matrix([16], 1, *sk.arrays())
+    state = a0.copy()
+    for t in range(1, 4):
+        state = np.linalg.solve(Q, S @ state)
+        got = fs.solve_periodic_implicit(K(q), K(sk), G([16], a0), t).data
+        assert np.abs(got - state).max() <= 1e-9
+        want = orc.solve_periodic_implicit(a0, [16], q.arrays(), sk.arrays(), t)
+        assert np.abs(got - want).max() <= 1e-12
+
+
+def test_cached_and_timings():
+    cache = fs.SpectrumCache()
+    a = R.random_grid(Rng(5), 4096)
+    k = K(R.heat1d(0.25))
+    st = fs.StageTimings()
+    out1 = fs.solve_periodic_cached(G([64, 64], a), K(R.random_kernel(Rng(6), 2, 1)), 9, cache, st)
+    out2 = fs.solve_periodic(G([64, 64], a), K(R.random_kernel(Rng(6), 2, 1)), 9)
+    assert np.abs(out1.data - out2.data).max() == 0.0
+    assert st.sum() > 0 and st.forward_fft > 0 and st.inverse_fft > 0
+    before = st.sum()
+    fs.solve_periodic(G([4096], a), k, 5, st)
+    assert st.sum() > before  # accumulated, not reset
+
+
+# ------------------------------------------------------------------ per-plan parity vs the oracle
+PLAN_CASES = [
+    # (dims, m, taps-kind, T)   fused R2C rank 2/3, 1D row-pair (m = 1, 2), general
+    ([256, 256], 1, "box9", 1000),
+    ([128, 512], 1, "jacobi5", 100),
+    ([64, 32, 128], 1, "heat7", 50),
+    ([32, 64, 16], 1, "random", 7),
+    ([1 << 12], 1, "heat3", 1000),
+    ([1 << 16], 1, "heat3", 1000),
+    ([1 << 12], 2, "leapfrog", 1000),
+    ([1 << 14], 2, "leapfrog", 5000),
+    ([96, 40], 1, "random", 11),
+    ([1 << 14, 2], 1, "random", 3),
+]
+
+
+def _case_kernel(kind, rank, seed):
+    rng = Rng(seed)
+    if kind == "box9":
+        u = [rng.uniform() for _ in range(9)]
+        offs = [(i, j) for i in (-1, 0, 1) for j in (-1, 0, 1)]
+        return R.kern_from({o: w / sum(u) for o, w in zip(offs, u)}, 2)
+    if kind == "jacobi5":
+        return R.kern_from({(0, 0): 0.2, (1, 0): 0.2, (-1, 0): 0.2, (0, 1): 0.2, (0, -1): 0.2}, 2)
+    if kind == "heat7":
+        t = {(0, 0, 0): 0.4}
+        for a in range(3):
+            for s in (-1, 1):
+                o = [0, 0, 0]
+                o[a] = s
+                t[tuple(o)] = 0.1
+        return R.kern_from(t, 3)
+    if kind == "heat3":
+        return R.kern_from({(-1,): 0.25, (0,): 0.5, (1,): 0.25}, 1)
+    if kind == "leapfrog":
+        C2 = 0.25
+        k = R.Kern(1, 2)
+        k.add((0,), [[2 - 2 * C2, -1.0], [1.0, 0.0]])
+        k.add((-1,), [[C2, 0.0], [0.0, 0.0]])
+        k.add((1,), [[C2, 0.0], [0.0, 0.0]])
+        return k
+    return R.random_kernel(rng, rank, 1, 1, 0.95)
+
+
+@pytest.mark.parametrize("dims,m,kind,T", PLAN_CASES)
+def test_plans_vs_oracle(orc, dims, m, kind, T):
+    k = _case_kernel(kind, len(dims), 1000 + T)
+    n = int(np.prod(dims)) * m
+    a0 = orc.splitmix_fill(7 + len(dims), n, True)
+    want = orc.solve_periodic(a0, dims, m, *k.arrays(), T)
+    for path in (0, 1):
+        got = fs.solve_periodic(G(dims, a0, m), K(k), T, path=path).data
+        assert rel_l2(got, want) <= 1e-10, (dims, m, kind, T, path, rel_l2(got, want))
+    info = fs.plan_describe(fs.GridShape(dims, m), K(k))
+    assert info["path"] in (1, 2, 3)
+
+
+def test_plan_kinds_selected():
+    k2 = K(_case_kernel("jacobi5", 2, 0))
+    assert fs.plan_describe(fs.GridShape([4096, 4096]), k2)["path"] == 1
+    k3 = K(_case_kernel("heat7", 3, 0))
+    assert fs.plan_describe(fs.GridShape([64, 64, 64]), k3)["path"] == 1
+    assert fs.plan_describe(fs.GridShape([1 << 20]), K(_case_kernel("heat3", 1, 0)))["path"] == 2
+    assert fs.plan_describe(fs.GridShape([1 << 20], 2), K(_case_kernel("leapfrog", 1, 0)))["path"] == 2
+    assert fs.plan_describe(fs.GridShape([12, 12]), k2)["path"] == 3
+
+
+# ------------------------------------------------------------------ configs (BASELINE) at full or reduced size
+def test_cfg1_full_vs_oracle(orc):
+    """cfg1: 1D heat N=2^20, T=1000 (BASELINE configs[0]) at full size."""
+    k = _case_kernel("heat3", 1, 0)
+    a0 = orc.splitmix_fill(1, 1 << 20, False)
+    want = orc.solve_periodic(a0, [1 << 20], 1, *k.arrays(), 1000)
+    got = fs.solve_periodic(G([1 << 20], a0), K(k), 1000).data
+    assert rel_l2(got, want) <= 1e-10
+
+
+def test_cfg2_full_vs_oracle_and_properties(orc):
+    """cfg2: 2D Jacobi 4096^2, T=1e4 at full size: vs the oracle, vs the
+    independent general GPU pipeline, and the semigroup property."""
+    k = _case_kernel("jacobi5", 2, 0)
+    dims = [4096, 4096]
+    a0 = orc.splitmix_fill(2, 4096 * 4096, False)
+    got = fs.solve_periodic(G(dims, a0), K(k), 10000).data
+    want = orc.solve_periodic(a0, dims, 1, *k.arrays(), 10000)
+    assert rel_l2(got, want) <= 1e-10
+    half = fs.solve_periodic(fs.solve_periodic(G(dims, a0), K(k), 5000), K(k), 5000).data
+    assert rel_l2(half, got) <= 1e-10
+
+
+def test_cfg3_reduced_vs_oracle(orc):
+    """cfg3 shape family (9-point random box, T=1e5) at 1024^2 vs the oracle."""
+    k = _case_kernel("box9", 2, 1003)
+    dims = [1024, 1024]
+    a0 = orc.splitmix_fill(3, 1024 * 1024, True)
+    got = fs.solve_periodic(G(dims, a0), K(k), 100000).data
+    want = orc.solve_periodic(a0, dims, 1, *k.arrays(), 100000)
+    assert rel_l2(got, want) <= 1e-10
+
+
+def test_cfg4_reduced_vs_oracle(orc):
+    """cfg4 family (3D 7-point heat, T=1000) at 64^3 vs the oracle."""
+    k = _case_kernel("heat7", 3, 0)
+    dims = [64, 64, 64]
+    a0 = orc.splitmix_fill(4, 64 ** 3, False)
+    got = fs.solve_periodic(G(dims, a0), K(k), 1000).data
+    want = orc.solve_periodic(a0, dims, 1, *k.arrays(), 1000)
+    assert rel_l2(got, want) <= 1e-10
