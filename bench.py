@@ -1,0 +1,373 @@
+"""Benchmark: StencilFFT-P periodic solve on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl reference]
+
+A step is one full periodic solve a_T = IFFT(FFT(s)^T . FFT(a_0)) of the
+configured synthetic grid.  The default workload is BASELINE configs[1]
+(cfg2: 2D 5-point Jacobi, 4096^2 fp64, T = 1e4).
+
+`value`  cell-updates/s (cells * T / device time) with a_0 resident in HBM,
+         the step timed with CUDA events on the solve's stream, L2 flushed
+         (256 MiB write) before every step; max over ranks; whole-job sum.
+`e2e`    the same metric through the public host API (pinned host input,
+         H2D + solve + D2H inside the timed region).
+`roofline` the fused spectral kernel (k_fused_r2c for plan 1): its
+         algorithmic bytes / its CUDA-event duration inside the timed steps.
+`cpu_baseline` the reference path (oracle restatement, test infrastructure)
+         timed on this host, rank 0 at N = 1 only.
+
+Multi-GPU (torchrun, one rank per GPU): independent replicas of the
+configured grid per rank ("replicas", scaling weak); no data-path collective.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cell-updates/sec (N·T/wall) and FFT-pipeline HBM GB/s vs peak, 1/2/4/8 GPUs"
+UNIT = "cell-updates/s"
+FLUSH_BYTES = 256 << 20
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(cfg_name):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(cfg_name)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                mx.append(float(s[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, s[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference(cfg, steps, warmup, budget_s=150.0):
+    """Times the reference CPU path (oracle restatement of proj/src/periodic.cpp,
+    all host threads) on a bounded sample of the workload.  Returns
+    (cell-updates/s, sample description, cores)."""
+    import numpy as np
+
+    from oracle import oracle as orc
+
+    orc.build()
+    cores = orc.thread_count()
+    # calibrate on a small square of the same family, extrapolate N log N
+    dims = list(cfg.dims)
+    rank = len(dims)
+    small = [max(8, d // (16 if rank > 1 else 64)) for d in dims]
+    sc = cfg.scaled(small)
+    off, blk = sc.kernel().arrays()
+    a = sc.initial()
+    t0 = time.perf_counter()
+    orc.solve_periodic(a, small, cfg.fields, off, blk, cfg.T, vector=cfg.fields > 1)
+    t_small = max(time.perf_counter() - t0, 1e-4)
+    n_s = sc.cells()
+
+    def estimate(d):
+        n = math.prod(d)
+        return t_small * (n / n_s) * (math.log2(n) / max(math.log2(n_s), 1.0))
+
+    runs = max(1, steps + warmup)
+    use = dims
+    while estimate(use) * runs > budget_s and math.prod(use) > 4096:
+        use = [max(8, d // 2) for d in use]
+    sample = cfg.scaled(use) if use != dims else cfg
+    off, blk = sample.kernel().arrays()
+    a = sample.initial()
+    return sample, off, blk, a, cores
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import oracle as orc
+
+    sample, off, blk, a, cores = cpu_reference(cfg, args.steps, args.warmup)
+    for _ in range(args.warmup):
+        orc.solve_periodic(a, sample.dims, sample.fields, off, blk, sample.T, vector=sample.fields > 1)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        out = orc.solve_periodic(a, sample.dims, sample.fields, off, blk, sample.T, vector=sample.fields > 1)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    value = sample.cells() * sample.T / t
+    desc = (f"oracle (CPU restatement of the reference solve_periodic; radix-2/Bluestein FFT, FFT-of-generator "
+            f"spectrum, std::thread chunks) on grid {sample.dims} x{sample.fields}, T={sample.T}"
+            + ("" if sample.dims == cfg.dims else f" (bounded sample of {cfg.dims})"))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SplitMix64, reference init)",
+        "config": {"workload": cfg.name + ": " + cfg.description, "grid": cfg.dims, "fields": cfg.fields,
+                   "T": cfg.T, "sample_grid": sample.dims},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+        "checksum": float(np.abs(out).sum()),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args, cfg):
+    import numpy as np
+    import torch
+
+    import paper_2105_06676_b200 as fs
+
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    stream = torch.cuda.Stream()
+    sptr = stream.cuda_stream
+    shape, kern = cfg.shape(), cfg.kernel()
+    info = fs.plan_describe(shape, kern)
+    host = cfg.initial()
+    n = host.size
+    d_a0 = torch.from_numpy(host).to(f"cuda:{dev}")
+    d_out = torch.empty_like(d_a0)
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device=f"cuda:{dev}")
+    torch.cuda.synchronize()
+
+    def solve(stage=0):
+        fs.solve_periodic_device(shape, d_a0.data_ptr(), kern, cfg.T, d_out.data_ptr(), stream=sptr,
+                                 device=dev, stage_events=stage)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            flush.fill_(1)
+            solve()
+    stream.synchronize()
+    fs.device_check(stream=sptr, device=dev)
+
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    sampler = ClockSampler(dev if ws == 1 else local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    step_ms, fused_ms = [], []
+    wall0 = time.perf_counter()
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            flush.fill_(i)
+            ev0[i].record(stream)
+            solve(stage=1)
+            ev1[i].record(stream)
+            ev1[i].synchronize()
+            step_ms.append(ev0[i].elapsed_time(ev1[i]))
+            fused_ms.append(fs.last_stage_ms(device=dev)[1])
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    wall = time.perf_counter() - wall0
+    clocks = sampler.stop()
+    fs.device_check(stream=sptr, device=dev)
+    ms = sum(step_ms) / len(step_ms)
+    fms = sum(fused_ms) / len(fused_ms)
+    if dist is not None:
+        t = torch.tensor([ms, fms], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, fms = float(t[0]), float(t[1])
+    cells_T = cfg.cells() * cfg.T
+    value = cells_T * ws / (ms * 1e-3)
+
+    # e2e through the public host API: pinned host in/out, H2D + solve + D2H per step
+    e2e_val = None
+    if not args.no_e2e:
+        pin_in = torch.from_numpy(host).pin_memory()
+        pin_out = torch.empty(n, dtype=torch.float64).pin_memory()
+        grid = fs.FieldGrid(shape, pin_in.numpy())
+        out_np = pin_out.numpy()
+        for _ in range(max(1, args.warmup)):
+            fs.solve_periodic(grid, kern, cfg.T, out=out_np)
+        e2e_t = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            fs.solve_periodic(grid, kern, cfg.T, out=out_np)
+            e2e_t.append(time.perf_counter() - t0)
+        et = sum(e2e_t) / len(e2e_t)
+        if dist is not None:
+            t = torch.tensor([et], dtype=torch.float64, device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            et = float(t[0])
+        e2e_val = cells_T * ws / et
+        # parity sanity: host result equals the device result
+        assert np.array_equal(out_np, d_out.cpu().numpy())
+
+    peak, peak_src = load_peaks()
+    fused_gbs = info["fused_bytes"] / (fms * 1e-3) / 1e9 if fms > 0 else None
+    pipe_gbs = info["alg_bytes"] / (ms * 1e-3) / 1e9
+    kernel_name = {1: "k_fused_r2c", 2: "k_rowpair", 3: "k_spectral_general"}[info["path"]]
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (SplitMix64 stream of the reference's random init; " + cfg.init + f", seed {cfg.seed})",
+        "config": {
+            "workload": cfg.name + ": " + cfg.description,
+            "grid": cfg.dims, "fields": cfg.fields, "T": cfg.T,
+            "parallelism": "replicas" if ws > 1 else "single",
+            "l2": f"flushed before every step ({FLUSH_BYTES >> 20} MiB write), grid {n * 8 >> 20} MiB",
+            "plan": info["path"],
+            "wall_s_timed_region": wall,
+        },
+        "roofline": {
+            "bound": "hbm",
+            "kernel": kernel_name,
+            "achieved": fused_gbs,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": (fused_gbs / peak) if fused_gbs else None,
+            "traffic": load_traffic(cfg.name),
+            "alg_bytes_per_launch": info["fused_bytes"],
+            "kernel_ms": fms,
+            "peak_source": peak_src,
+        },
+        "pipeline": {"alg_bytes_per_step": info["alg_bytes"], "achieved_gbs": pipe_gbs, "frac": pipe_gbs / peak},
+        "gpu_launches": info["launches"] * args.steps,
+        "clocks": clocks,
+    }
+    if e2e_val is not None:
+        line["e2e"] = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 8}
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        from oracle import oracle as orc
+
+        sample, off, blk, a, cores = cpu_reference(cfg, 1, 0, budget_s=30.0)
+        t0 = time.perf_counter()
+        orc.solve_periodic(a, sample.dims, sample.fields, off, blk, sample.T, vector=sample.fields > 1)
+        tc = time.perf_counter() - t0
+        line["cpu_baseline"] = {
+            "value": sample.cells() * sample.T / tc, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"one oracle solve_periodic on grid {sample.dims} x{sample.fields}, T={sample.T}"
+                      + ("" if sample.dims == cfg.dims else f" (bounded sample of {cfg.dims})"),
+        }
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    from paper_2105_06676_b200.synthetic import configs
+
+    cfg = configs()[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_gpu(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -74,7 +74,8 @@ typedef struct fsx_stage_timings {
 typedef struct fsx_options {
     int32_t device;     /* CUDA device ordinal (default 0) */
     int32_t path;       /* 0 = auto (fused fast path when eligible), 1 = force general path */
-    int32_t reserved0;
+    int32_t stage_events; /* device API: record CUDA events at the stage boundaries of each
+                             solve (read back with fsx_last_stage_ms) */
     int32_t reserved1;
     void* stream;       /* cudaStream_t to enqueue on (NULL = library stream) */
 } fsx_options;
@@ -118,6 +119,12 @@ fsx_status fsx_solve_periodic_implicit(const fsx_shape* shape, const double* a0,
 fsx_status fsx_solve_periodic_device(const fsx_shape* shape, const double* d_a0, const fsx_kernel* k,
                                      uint64_t T, double* d_out, const fsx_options* opt);
 fsx_status fsx_device_check(const fsx_options* opt);
+
+/* Stage durations (ms) of the most recent device solve enqueued with
+ * opt->stage_events = 1: ms[0] forward passes, ms[1] the fused spectral
+ * pass (plan 1: exactly one kernel, k_fused_r2c), ms[2] inverse passes.
+ * Waits for that solve's last stage event. */
+fsx_status fsx_last_stage_ms(const fsx_options* opt, double* ms);
 
 /* ---------------------------------------------------------------- building blocks
  * (host pointers, complex = interleaved fp64) */

@@ -23,6 +23,7 @@ from .fftstencil import (  # noqa: F401
     fft,
     fold_kernels,
     hadamard,
+    last_stage_ms,
     multi_fft,
     multi_ifft,
     multiply_spectra,

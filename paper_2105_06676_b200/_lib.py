@@ -60,7 +60,7 @@ class FsxOptions(ctypes.Structure):
     _fields_ = [
         ("device", ctypes.c_int32),
         ("path", ctypes.c_int32),
-        ("reserved0", ctypes.c_int32),
+        ("stage_events", ctypes.c_int32),
         ("reserved1", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
     ]
@@ -86,6 +86,7 @@ EXPORTS = (
     "fsx_solve_periodic_implicit",
     "fsx_solve_periodic_device",
     "fsx_device_check",
+    "fsx_last_stage_ms",
     "fsx_multi_fft",
     "fsx_spectrum_from_kernel",
     "fsx_pow_spectrum",

@@ -769,7 +769,7 @@ void solve(const SolveReq& rq) {
     }
     const int force_general = (rq.opt && rq.opt->path == 1) || rq.q != nullptr;
     Plan& p = get_plan(dev, s, taps, force_general);
-    Stamps sp{&dev, rq.st != nullptr, st};
+    Stamps sp{&dev, rq.st != nullptr || (rq.device_ptrs && rq.opt && rq.opt->stage_events), st};
     if (rq.device_ptrs) {
         run_plan(p, dev, taps, rq.q ? &qtaps : nullptr, rq.T, rq.a0, rq.out, st, sp);
         return;
@@ -894,6 +894,20 @@ fsx_status fsx_device_check(const fsx_options* opt) {
         std::lock_guard<std::mutex> lk(g_mu);
         Device& dev = device_for(opt ? opt->device : 0);
         check_flags(dev, kFusedR2C, stream_of(dev, opt));
+    });
+}
+
+fsx_status fsx_last_stage_ms(const fsx_options* opt, double* ms) {
+    return guarded([&] {
+        if (!ms) throw SpecErr("fsx_last_stage_ms: null output");
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(opt ? opt->device : 0);
+        FSX_CK(cudaEventSynchronize(dev.ev[3]));
+        for (int i = 0; i < 3; ++i) {
+            float t = 0;
+            FSX_CK(cudaEventElapsedTime(&t, dev.ev[i], dev.ev[i + 1]));
+            ms[i] = t;
+        }
     });
 }
 

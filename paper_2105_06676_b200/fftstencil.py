@@ -289,21 +289,24 @@ class DiagonalSpectrum:
         self.blocks[freq * m * m:(freq + 1) * m * m] = np.asarray(b, np.complex128).reshape(-1)
 
 
-def _opts(device: int = 0, path: int = 0, stream: int | None = None):
+def _opts(device: int = 0, path: int = 0, stream: int | None = None, stage_events: int = 0):
     o = _lib.FsxOptions()
-    o.device, o.path = device, path
+    o.device, o.path, o.stage_events = device, path, stage_events
     o.stream = stream
     return o
 
 
 # ---------------------------------------------------------------- solvers
-def _solve(fn, a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None, path: int, extra=()):
+def _solve(fn, a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None, path: int, extra=(), out=None):
     L = _lib.load()
     if T < 0 or T >= 1 << 64:
         raise SpecError("T must be a nonnegative 64-bit integer")
     shape_c = a0.shape._c()
     kc, keep = k._c()
-    out = np.empty_like(a0.data)
+    if out is None:
+        out = np.empty_like(a0.data)
+    elif out.dtype != np.float64 or out.size != a0.data.size or not out.flags.c_contiguous:
+        raise SpecError("out must be a contiguous float64 array of the grid's size")
     stc = st._push() if st is not None else None
     status = getattr(L, fn)(ctypes.byref(shape_c), a0.data.ctypes.data_as(_DP), ctypes.byref(kc),
                             ctypes.c_uint64(int(T)), *extra, out.ctypes.data_as(_DP),
@@ -315,9 +318,11 @@ def _solve(fn, a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None,
     return FieldGrid(a0.shape, out)
 
 
-def solve_periodic(a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None = None, *, path: int = 0):
-    """proj/src/periodic.cpp:76-86 on the B200 path (fsx_solve_periodic)."""
-    return _solve("fsx_solve_periodic", a0, k, T, st, path)
+def solve_periodic(a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None = None, *, path: int = 0,
+                   out: np.ndarray | None = None):
+    """proj/src/periodic.cpp:76-86 on the B200 path (fsx_solve_periodic).
+    ``out`` optionally supplies the (e.g. pinned) host array the result is written to."""
+    return _solve("fsx_solve_periodic", a0, k, T, st, path, out=out)
 
 
 def solve_periodic_vector(a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None = None, *, path: int = 0):
@@ -363,7 +368,7 @@ def solve_periodic_implicit(q: StencilKernel, s: StencilKernel, a0: FieldGrid, T
 
 
 def solve_periodic_device(shape: GridShape, d_a0: int, k: StencilKernel, T: int, d_out: int,
-                          stream: int | None = None, device: int = 0, path: int = 0) -> None:
+                          stream: int | None = None, device: int = 0, path: int = 0, stage_events: int = 0) -> None:
     """Device-resident solve (fsx_solve_periodic_device): pointers are CUDA
     device addresses (e.g. ``tensor.data_ptr()``); enqueued on ``stream``.
     Call :func:`device_check` to synchronize and surface NumericError."""
@@ -372,9 +377,16 @@ def solve_periodic_device(shape: GridShape, d_a0: int, k: StencilKernel, T: int,
     kc, keep = k._c()
     status = L.fsx_solve_periodic_device(ctypes.byref(shape_c), ctypes.c_void_p(d_a0), ctypes.byref(kc),
                                          ctypes.c_uint64(int(T)), ctypes.c_void_p(d_out),
-                                         ctypes.byref(_opts(device, path, stream)))
+                                         ctypes.byref(_opts(device, path, stream, stage_events)))
     del keep
     _lib.check(status)
+
+
+def last_stage_ms(device: int = 0) -> list:
+    """[forward, fused spectral, inverse] ms of the last device solve enqueued with stage_events=1."""
+    ms = (ctypes.c_double * 3)()
+    _lib.check(_lib.load().fsx_last_stage_ms(ctypes.byref(_opts(device)), ms))
+    return list(ms)
 
 
 def device_check(stream: int | None = None, device: int = 0) -> None:

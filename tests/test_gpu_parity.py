@@ -387,9 +387,18 @@ def test_plans_vs_oracle(orc, dims, m, kind, T):
     n = int(np.prod(dims)) * m
     a0 = orc.splitmix_fill(7 + len(dims), n, True)
     want = orc.solve_periodic(a0, dims, m, *k.arrays(), T)
+    truth = orc.solve_periodic_ld(a0, dims, m, *k.arrays(), T) if kind == "leapfrog" else None
     for path in (0, 1):
         got = fs.solve_periodic(G(dims, a0, m), K(k), T, path=path).data
-        assert rel_l2(got, want) <= 1e-10, (dims, m, kind, T, path, rel_l2(got, want))
+        if truth is None:
+            assert rel_l2(got, want) <= 1e-10, (dims, m, kind, T, path, rel_l2(got, want))
+        else:
+            # cfg5 family: the leapfrog symbol is a near-Jordan block at low
+            # frequency, so two fp64 pipelines legitimately differ by more than
+            # 1e-10.  Protocol: against the
+            # long-double truth, the GPU error must not exceed the oracle's.
+            e_gpu, e_orc = rel_l2(got, truth), rel_l2(want, truth)
+            assert e_gpu <= max(1e-12, 1.5 * e_orc), (dims, path, e_gpu, e_orc)
     info = fs.plan_describe(fs.GridShape(dims, m), K(k))
     assert info["path"] in (1, 2, 3)
 
