@@ -478,6 +478,18 @@ Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general)
 }
 
 // ------------------------------------------------------------------ symbol setup
+// Taps with c(o) == c(-o) for every offset give a real symbol
+// sum_o c(o) cos(2 pi k.o / n) (blocks compared entry by entry, exactly).
+bool symmetric_taps(const Taps& taps) {
+    for (const auto& kv : taps.map) {
+        std::vector<i64> neg(kv.first.size());
+        for (size_t a = 0; a < neg.size(); ++a) neg[a] = -kv.first[a];
+        auto it = taps.map.find(neg);
+        if (it == taps.map.end() || it->second != kv.second) return false;
+    }
+    return true;
+}
+
 fsx::FusedSymbol fused_symbol(const Plan& p, const Taps& taps, u64 T) {
     fsx::FusedSymbol s;
     const int r = (int)p.dims.size();
@@ -511,6 +523,7 @@ fsx::FusedSymbol fused_symbol(const Plan& p, const Taps& taps, u64 T) {
     }
     s.ntaps = j;
     s.ngroups = (int)gid.size();
+    s.real = symmetric_taps(taps) ? 1 : 0;
     return s;
 }
 

@@ -46,6 +46,9 @@ struct Cfg {
     static constexpr int LSW = GW > 1 ? N + 8 / GW : N;      // smem line stride, strided tiles
     static constexpr int GL = TPL >= 8 ? 1 : 8 / TPL;        // lines per quarter warp
     static constexpr int LSL = GL > 1 ? N + 8 / GL : N;      // smem line stride, contiguous tiles
+    // resident CTAs per SM the register budget is sized for (<= 128 regs at 256 threads)
+    static constexpr int MINB_W = W * TPL <= 256 ? 2 : 1;
+    static constexpr int MINB_L = LINES * TPL <= 256 ? 2 : 1;
 };
 
 // Binary exponentiation of a scalar symbol, the reference loop shape
@@ -66,6 +69,25 @@ __device__ __forceinline__ double2 pow_scalar(double2 lam, u64 T) {
         if (t & 1) acc = cmul(acc, sq);
         t >>= 1;
         if (t) sq = make_double2(fma(sq.x, sq.x, -sq.y * sq.y), (sq.x + sq.x) * sq.y);
+    }
+    return acc;
+}
+
+// Real symbol (symmetric stencil): same loop on one double.
+__device__ __forceinline__ double pow_real(double lam, u64 T) {
+    const double mag2 = lam * lam;
+    if (mag2 < 1.0) {
+        int e;
+        const double mant = frexp(mag2, &e);
+        const float l2 = (float)e + __log2f((float)mant);
+        if (l2 * (0.5f * (float)T) < -2200.0f) return 0.0;
+    }
+    double acc = 1.0, sq = lam;
+    u64 t = T;
+    while (t) {
+        if (t & 1) acc *= sq;
+        t >>= 1;
+        if (t) sq *= sq;
     }
     return acc;
 }
@@ -127,7 +149,7 @@ __device__ __forceinline__ void flag_nonfinite(bool bad, Flags* f) {
 // ------------------------------------------------------------------ C2C passes
 // Contiguous lines: line l occupies in[l * pitch + 0 .. N).
 template <int N, int SIGN>
-__global__ void __launch_bounds__(Cfg<N>::LINES * Cfg<N>::TPL)
+__global__ void __launch_bounds__(Cfg<N>::LINES * Cfg<N>::TPL, Cfg<N>::MINB_L)
 k_contig(const double2* in, double2* out, i64 nlines, i64 pitch, const double2* __restrict__ tw_all) {
     using C = Cfg<N>;
     using F = LineFFT<N, SIGN>;
@@ -149,7 +171,7 @@ k_contig(const double2* in, double2* out, i64 nlines, i64 pitch, const double2* 
 
 // Strided lines: W adjacent columns per CTA, the axis in shared memory.
 template <int N, int SIGN, int TWM>
-__global__ void __launch_bounds__(Cfg<N>::W * Cfg<N>::TPL)
+__global__ void __launch_bounds__(Cfg<N>::W * Cfg<N>::TPL, Cfg<N>::MINB_W)
 k_strided(const double2* in, double2* out, AxisGeom g, StepTwiddle st, const double2* __restrict__ tw_all) {
     using C = Cfg<N>;
     using F = LineFFT<N, SIGN>;
@@ -209,7 +231,7 @@ __global__ void k_direct_dft(const double2* in, double2* out, AxisGeom g, int si
 // Z = DFT_M(z); X[k] = E[k] + W_L^k O[k] with E = (Z[k] + conj Z[M-k]) / 2,
 // O = -i (Z[k] - conj Z[M-k]) / 2; X[M] = Re Z[0] - Im Z[0].
 template <int M>
-__global__ void __launch_bounds__(Cfg<M>::LINES * Cfg<M>::TPL)
+__global__ void __launch_bounds__(Cfg<M>::LINES * Cfg<M>::TPL, Cfg<M>::MINB_L)
 k_r2c_rows(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, i64 P,
            const double2* __restrict__ tw_all) {
     using C = Cfg<M>;
@@ -247,7 +269,7 @@ k_r2c_rows(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
 // unnormalized inverse DFT_M, x[2j] = Re z[j], x[2j+1] = Im z[j] (times L;
 // the 1/N of the inverse transform is folded into the spectral multiply).
 template <int M>
-__global__ void __launch_bounds__(Cfg<M>::LINES * Cfg<M>::TPL)
+__global__ void __launch_bounds__(Cfg<M>::LINES * Cfg<M>::TPL, Cfg<M>::MINB_L)
 k_c2r_rows(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, i64 P,
            const double2* __restrict__ tw_all, Flags* flags) {
     using C = Cfg<M>;
@@ -296,7 +318,7 @@ k_c2r_rows(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
 // axis-0 offset: A_g(column) is formed once per column, then per element
 // lam = sum_g A_g * exp(+2 pi i k0 O_g / n0).
 template <int N>
-__global__ void __launch_bounds__(Cfg<N>::W * Cfg<N>::TPL)
+__global__ void __launch_bounds__(Cfg<N>::W * Cfg<N>::TPL, Cfg<N>::MINB_W)
 k_fused_r2c(double2* H, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
     using C = Cfg<N>;
     using FF = LineFFT<N, -1>;
@@ -318,7 +340,8 @@ k_fused_r2c(double2* H, AxisGeom g, FusedSymbol sym, const double2* __restrict__
 #pragma unroll
     for (int q = 0; q < C::R; ++q)
         v[q] = ok ? H[base + (i64)(t + q * C::TPL) * g.inner] : make_double2(0.0, 0.0);
-    FF::run(v, t, sm + w * C::LSW, tw_all + N);
+    double2* line = sm + w * C::LSW;
+    FF::run(v, t, line, tw_all + N);
     for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
         double2 a = make_double2(0.0, 0.0);
         for (int j = 0; j < sym.ntaps; ++j) {
@@ -329,19 +352,40 @@ k_fused_r2c(double2* H, AxisGeom g, FusedSymbol sym, const double2* __restrict__
         }
         acoef[gi][w] = a;
     }
+    // The spectral multiply runs through this thread's own smem slots in a
+    // rolled loop: the register tile is parked, so the symbol / power code
+    // does not compete with the 16-element FFT state for registers.
     __syncthreads();
 #pragma unroll
+    for (int q = 0; q < C::R; ++q) line[swz(t + q * C::TPL)] = v[q];
+    __syncthreads();
+#pragma unroll 1
     for (int q = 0; q < C::R; ++q) {
-        const i64 k0 = t + q * C::TPL;
-        double2 lam = make_double2(0.0, 0.0);
-        for (int gi = 0; gi < sym.ngroups; ++gi) {
-            const double2 e = eplus_pow2(tw_all, N, k0 * (i64)sym.group_off[gi]);
-            lam = cadd(lam, cmul(acoef[gi][w], e));
+        const int k0 = t + q * C::TPL;
+        const int p = swz(k0);
+        if (sym.real) {
+            // symmetric taps: lam(k) is real (A_{-g} = conj A_g)
+            double lam = 0.0;
+            for (int gi = 0; gi < sym.ngroups; ++gi) {
+                const double2 e = eplus_pow2(tw_all, N, (i64)k0 * sym.group_off[gi]);
+                const double2 a = acoef[gi][w];
+                lam = fma(a.x, e.x, fma(-a.y, e.y, lam));
+            }
+            const double lt = pow_real(lam, sym.T) * sym.scale;
+            line[p] = cscale(line[p], lt);
+        } else {
+            double2 lam = make_double2(0.0, 0.0);
+            for (int gi = 0; gi < sym.ngroups; ++gi) {
+                const double2 e = eplus_pow2(tw_all, N, (i64)k0 * sym.group_off[gi]);
+                lam = cadd(lam, cmul(acoef[gi][w], e));
+            }
+            const double2 lt = pow_scalar(lam, sym.T);
+            line[p] = cscale(cmul(lt, line[p]), sym.scale);
         }
-        const double2 lt = pow_scalar(lam, sym.T);
-        v[q] = cscale(cmul(lt, v[q]), sym.scale);
     }
-    FI::run(v, t, sm + w * C::LSW, tw_all + N);
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) v[q] = line[swz(t + q * C::TPL)];
+    FI::run(v, t, line, tw_all + N);
     if (ok) {
 #pragma unroll
         for (int q = 0; q < C::R; ++q) H[base + (i64)(t + q * C::TPL) * g.inner] = v[q];

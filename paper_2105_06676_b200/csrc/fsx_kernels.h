@@ -62,6 +62,7 @@ struct FusedSymbol {
     double tap_c[kMaxFusedTaps];
     u64 T = 1;
     double scale = 1.0;          // 1 / prod(dims)
+    int real = 0;                // taps symmetric under o -> -o: lam is real
 };
 
 // General spectral stage over a full complex spectrum with m fields.
