@@ -259,6 +259,8 @@ struct Plan {
     // kind 1
     i64 L = 0, M = 0, P = 0, rows = 0;
     fsx::AxisGeom ax1, ax0;
+    alignas(64) unsigned char map0[128], map1[128];  // CUtensorMaps for TMA column passes
+    bool tma0 = false, tma1 = false;
     // kind 2
     i64 N1 = 1, N2 = 1, Mc = 0;
     int t_M = -1, t_wk = -1;
@@ -319,6 +321,12 @@ Device& device_for(int ordinal) {
     auto& ref = *d;
     g_devices.emplace(ordinal, std::move(d));
     return ref;
+}
+
+// FSX_TMA=0 keeps the strided passes on per-thread LDG/STG (A/B measurements).
+bool tma_enabled() {
+    const char* e = getenv("FSX_TMA");
+    return !(e && e[0] == '0');
 }
 
 // Splits a pow2 length into n1 * n2 with both <= kMaxLine.
@@ -414,6 +422,10 @@ Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general)
         p->ax0.outer = 1;
         p->ax0.block = p->dims[0] * plane;
         p->ax0.ncols = (r == 3) ? plane : p->M + 1;
+        if (tma_enabled()) {
+            p->tma0 = fsx::tma_cols_ok(p->ax0.n) && fsx::make_cols_tensor_map(p->map0, p->work.p, p->ax0) == 0;
+            p->tma1 = r == 3 && fsx::tma_cols_ok(p->ax1.n) && fsx::make_cols_tensor_map(p->map1, p->work.p, p->ax1) == 0;
+        }
         const i64 H = p->rows * (p->M + 1) * 16;
         p->fused_bytes = 2 * H;
         p->alg_bytes = 2 * R + (r == 3 ? 8 : 4) * H;
@@ -660,12 +672,20 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
         double2* H = p.work.as<double2>();
         FSX_CK(fsx::launch_r2c_rows(d_a0, H, p.rows, p.L, p.P, tw, st));
         fsx::StepTwiddle none;
-        if (r == 3) FSX_CK(fsx::launch_axis_pow2(H, H, p.ax1, -1, none, tw, st));
-        sp.mark();
         const fsx::FusedSymbol sym = fused_symbol(p, taps, T);
-        FSX_CK(fsx::launch_fused_r2c(H, p.ax0, sym, tw, st));
+        fsx::FusedSymbol nosym;
+        if (r == 3) {
+            if (p.tma1) FSX_CK(fsx::launch_cols_tma(p.map1, p.ax1, 0, nosym, tw, st));
+            else FSX_CK(fsx::launch_axis_pow2(H, H, p.ax1, -1, none, tw, st));
+        }
         sp.mark();
-        if (r == 3) FSX_CK(fsx::launch_axis_pow2(H, H, p.ax1, +1, none, tw, st));
+        if (p.tma0) FSX_CK(fsx::launch_cols_tma(p.map0, p.ax0, 2, sym, tw, st));
+        else FSX_CK(fsx::launch_fused_r2c(H, p.ax0, sym, tw, st));
+        sp.mark();
+        if (r == 3) {
+            if (p.tma1) FSX_CK(fsx::launch_cols_tma(p.map1, p.ax1, 1, nosym, tw, st));
+            else FSX_CK(fsx::launch_axis_pow2(H, H, p.ax1, +1, none, tw, st));
+        }
         FSX_CK(fsx::launch_c2r_rows(H, d_out, p.rows, p.L, p.P, tw, flags, st));
         sp.mark();
     } else if (p.kind == kRowPair1D) {

@@ -170,7 +170,12 @@ __device__ __forceinline__ int swz(int p) { return p ^ (((p >> 3) ^ (p >> 4)) & 
 // `tw` is the twiddle table for N: tw[x] = exp(-2 pi i x / N), x < N.
 // Every thread of the CTA must call run() together (it contains
 // __syncthreads); lines of one CTA are transformed concurrently.
-template <int N, int SIGN>
+//
+// PF = true hoists the next pass's twiddle loads above the exchange barrier
+// (their L1/L2 latency then overlaps the barrier wait and the shared-memory
+// round trip); it costs R-1 extra live double2 registers, so it is used by
+// the persistent kernels that run 8 warps per SM with the full register file.
+template <int N, int SIGN, bool PF = false>
 struct LineFFT {
     static constexpr int LOGN = ilog2c(N);
     static constexpr int R = N < 16 ? N : 16;
@@ -188,28 +193,59 @@ struct LineFFT {
         else return ns<S - 1>() * radix<S - 1>();
     }
 
+    // twiddles of pass S for this thread: w[i * r + u] = W_{Ns r}^{u k(i)}, u >= 1.
+    // Only the power-of-two exponents u = 1, 2, 4, 8 are read from the exact
+    // table; the others are products of at most two loaded/derived values
+    // (<= 3 roundings), which cuts the L1 traffic of the twiddles ~4x.
     template <int S>
-    __device__ __forceinline__ static void pass(double2 (&v)[R], int t, double2* line, const double2* __restrict__ tw) {
+    __device__ __forceinline__ static void load_tw(int t, const double2* __restrict__ tw, double2 (&w)[R]) {
         constexpr int r = radix<S>();
         constexpr int Ns = ns<S>();
         constexpr int C = R / r;
         constexpr int STEP = N / (Ns * r);
+        if constexpr (Ns > 1) {
+#pragma unroll
+            for (int i = 0; i < C; ++i) {
+                const int k = (t + i * TPL) & (Ns - 1);
+                double2* wi = w + i * r;
+#pragma unroll
+                for (int u = 1; u < r; u <<= 1) wi[u] = __ldg(tw + u * k * STEP);
+                if constexpr (r >= 4) wi[3] = cmul(wi[1], wi[2]);
+                if constexpr (r >= 8) {
+                    wi[5] = cmul(wi[1], wi[4]);
+                    wi[6] = cmul(wi[2], wi[4]);
+                    wi[7] = cmul(wi[3], wi[4]);
+                }
+                if constexpr (r >= 16) {
+#pragma unroll
+                    for (int u = 9; u < 16; ++u) wi[u] = cmul(wi[u - 8], wi[8]);
+                }
+            }
+        }
+    }
+
+    template <int S>
+    __device__ __forceinline__ static void pass(double2 (&v)[R], int t, double2* line, const double2* __restrict__ tw,
+                                                double2 (&w)[R]) {
+        constexpr int r = radix<S>();
+        constexpr int Ns = ns<S>();
+        constexpr int C = R / r;
+        if constexpr (!PF) load_tw<S>(t, tw, w);
 #pragma unroll
         for (int i = 0; i < C; ++i) {
             double2 a[r];
 #pragma unroll
             for (int u = 0; u < r; ++u) a[u] = v[i + u * C];
             if constexpr (Ns > 1) {
-                const int j = t + i * TPL;
-                const int k = j & (Ns - 1);
 #pragma unroll
-                for (int u = 1; u < r; ++u) a[u] = ctw<SIGN>(a[u], __ldg(tw + u * k * STEP));
+                for (int u = 1; u < r; ++u) a[u] = ctw<SIGN>(a[u], w[i * r + u]);
             }
             Dft<r, SIGN>::run(a);
 #pragma unroll
             for (int u = 0; u < r; ++u) v[i + u * C] = a[u];
         }
         if constexpr (S + 1 < NPASS) {
+            if constexpr (PF) load_tw<S + 1>(t, tw, w);
             __syncthreads();
 #pragma unroll
             for (int i = 0; i < C; ++i) {
@@ -222,12 +258,13 @@ struct LineFFT {
             __syncthreads();
 #pragma unroll
             for (int q = 0; q < R; ++q) v[q] = line[swz(t + q * TPL)];
-            pass<S + 1>(v, t, line, tw);
+            pass<S + 1>(v, t, line, tw, w);
         }
     }
 
     __device__ __forceinline__ static void run(double2 (&v)[R], int t, double2* line, const double2* __restrict__ tw) {
-        if constexpr (NPASS > 0) pass<0>(v, t, line, tw);
+        double2 w[R];
+        if constexpr (NPASS > 0) pass<0>(v, t, line, tw, w);
     }
 };
 

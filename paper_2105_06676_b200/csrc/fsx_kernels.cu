@@ -15,6 +15,7 @@
 
 #include "fsx_device.cuh"
 #include "fsx_kernels.h"
+#include "fsx_spectral.cuh"
 
 namespace fsx {
 
@@ -317,18 +318,22 @@ k_c2r_rows(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
 // reference's generator column, proj/src/spectrum.cpp:21-45), grouped by the
 // axis-0 offset: A_g(column) is formed once per column, then per element
 // lam = sum_g A_g * exp(+2 pi i k0 O_g / n0).
-template <int N>
-__global__ void __launch_bounds__(Cfg<N>::W * Cfg<N>::TPL, Cfg<N>::MINB_W)
+template <int N, int W, int MINB>
+__global__ void __launch_bounds__(W * Cfg<N>::TPL, MINB)
 k_fused_r2c(double2* H, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
     using C = Cfg<N>;
     using FF = LineFFT<N, -1>;
     using FI = LineFFT<N, +1>;
+    constexpr int GW = W < 8 ? W : 8;
+    constexpr int LSW = GW > 1 ? N + 8 / GW : N;
+    constexpr bool PAR = W <= 8;  // per-tap terms in parallel (smem for ntaps x W terms)
     extern __shared__ double2 sm[];
-    __shared__ double2 acoef[kMaxGroups][C::W];
-    const int w = threadIdx.x % C::W, t = threadIdx.x / C::W;
-    const i64 tiles = (g.ncols + C::W - 1) / C::W;
+    __shared__ double2 acoef[kMaxGroups][W];
+    __shared__ double2 tapterm[PAR ? kMaxFusedTaps : 1][PAR ? W : 1];
+    const int w = threadIdx.x % W, t = threadIdx.x / W;
+    const i64 tiles = (g.ncols + W - 1) / W;
     const i64 o = (i64)blockIdx.x / tiles;
-    const i64 c = ((i64)blockIdx.x % tiles) * C::W + w;
+    const i64 c = ((i64)blockIdx.x % tiles) * W + w;
     i64 ky = 0, kx = c;
     if (sym.rank == 3) {
         ky = c / sym.P;
@@ -340,51 +345,22 @@ k_fused_r2c(double2* H, AxisGeom g, FusedSymbol sym, const double2* __restrict__
 #pragma unroll
     for (int q = 0; q < C::R; ++q)
         v[q] = ok ? H[base + (i64)(t + q * C::TPL) * g.inner] : make_double2(0.0, 0.0);
-    double2* line = sm + w * C::LSW;
+    // per-column symbol coefficients: tap terms issued before the FFT so
+    // their table reads overlap it
+    if constexpr (PAR) {
+        for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
+    }
+    double2* line = sm + w * LSW;
     FF::run(v, t, line, tw_all + N);
+    __syncthreads();
     for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
         double2 a = make_double2(0.0, 0.0);
-        for (int j = 0; j < sym.ntaps; ++j) {
-            if (sym.tap_group[j] != gi) continue;
-            double2 e = eplus_pow2(tw_all, sym.L, kx * (i64)sym.tap_olast[j]);
-            if (sym.rank == 3) e = cmul(e, eplus_pow2(tw_all, sym.n1, ky * (i64)sym.tap_o1[j]));
-            a = make_double2(fma(sym.tap_c[j], e.x, a.x), fma(sym.tap_c[j], e.y, a.y));
-        }
+        for (int j = 0; j < sym.ntaps; ++j)
+            if (sym.tap_group[j] == gi) a = cadd(a, PAR ? tapterm[PAR ? j : 0][PAR ? w : 0] : tap_term(sym, tw_all, j, kx, ky));
         acoef[gi][w] = a;
     }
-    // The spectral multiply runs through this thread's own smem slots in a
-    // rolled loop: the register tile is parked, so the symbol / power code
-    // does not compete with the 16-element FFT state for registers.
     __syncthreads();
-#pragma unroll
-    for (int q = 0; q < C::R; ++q) line[swz(t + q * C::TPL)] = v[q];
-    __syncthreads();
-#pragma unroll 1
-    for (int q = 0; q < C::R; ++q) {
-        const int k0 = t + q * C::TPL;
-        const int p = swz(k0);
-        if (sym.real) {
-            // symmetric taps: lam(k) is real (A_{-g} = conj A_g)
-            double lam = 0.0;
-            for (int gi = 0; gi < sym.ngroups; ++gi) {
-                const double2 e = eplus_pow2(tw_all, N, (i64)k0 * sym.group_off[gi]);
-                const double2 a = acoef[gi][w];
-                lam = fma(a.x, e.x, fma(-a.y, e.y, lam));
-            }
-            const double lt = pow_real(lam, sym.T) * sym.scale;
-            line[p] = cscale(line[p], lt);
-        } else {
-            double2 lam = make_double2(0.0, 0.0);
-            for (int gi = 0; gi < sym.ngroups; ++gi) {
-                const double2 e = eplus_pow2(tw_all, N, (i64)k0 * sym.group_off[gi]);
-                lam = cadd(lam, cmul(acoef[gi][w], e));
-            }
-            const double2 lt = pow_scalar(lam, sym.T);
-            line[p] = cscale(cmul(lt, line[p]), sym.scale);
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < C::R; ++q) v[q] = line[swz(t + q * C::TPL)];
+    spectral_regs<N, C::R, C::TPL>(v, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
     FI::run(v, t, line, tw_all + N);
     if (ok) {
 #pragma unroll
@@ -813,6 +789,10 @@ static cudaError_t axis_pow2_n(const double2* in, double2* out, const AxisGeom& 
 
 cudaError_t launch_axis_pow2(const double2* in, double2* out, const AxisGeom& g, int sign,
                              const StepTwiddle& st, const double2* tw, cudaStream_t s) {
+    if (pipe_enabled() && pipe_cols_ok(g.n) && g.inner > 1 && st.mode == 0 && in == out) {
+        FusedSymbol none;
+        return launch_cols_pipe(out, g, sign < 0 ? 0 : 1, none, tw, s);
+    }
     switch (g.n) {
         case 2: return axis_pow2_n<2>(in, out, g, sign, st, tw, s);
         case 4: return axis_pow2_n<4>(in, out, g, sign, st, tw, s);
@@ -863,6 +843,7 @@ static cudaError_t c2r_m(const double2* H, double* x, i64 nrows, i64 L, i64 P, c
     MACRO(8) MACRO(16) MACRO(32) MACRO(64) MACRO(128) MACRO(256) MACRO(512) MACRO(1024) MACRO(2048) MACRO(4096) MACRO(8192)
 
 cudaError_t launch_r2c_rows(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
+    if (pipe_enabled() && pipe_rows_ok(L / 2)) return launch_r2c_pipe(x, H, nrows, L, P, tw, s);
     switch (L / 2) {
 #define C_(M) case M: return r2c_m<M>(x, H, nrows, L, P, tw, s);
         FSX_POW2_CASES(C_)
@@ -873,6 +854,7 @@ cudaError_t launch_r2c_rows(const double* x, double2* H, i64 nrows, i64 L, i64 P
 
 cudaError_t launch_c2r_rows(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
                             cudaStream_t s) {
+    if (pipe_enabled() && pipe_rows_ok(L / 2)) return launch_c2r_pipe(H, x, nrows, L, P, tw, f, s);
     switch (L / 2) {
 #define C_(M) case M: return c2r_m<M>(H, x, nrows, L, P, tw, f, s);
         FSX_POW2_CASES(C_)
@@ -881,17 +863,41 @@ cudaError_t launch_c2r_rows(const double2* H, double* x, i64 nrows, i64 L, i64 P
     }
 }
 
-template <int N>
-static cudaError_t fused_n(double2* H, const AxisGeom& g, const FusedSymbol& sym, const double2* tw, cudaStream_t s) {
-    using C = Cfg<N>;
-    const size_t smem = (size_t)C::W * C::LSW * sizeof(double2);
-    const i64 tiles = (g.ncols + C::W - 1) / C::W;
-    cudaFuncSetAttribute(k_fused_r2c<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_fused_r2c<N><<<(unsigned)(g.outer * tiles), C::W * C::TPL, smem, s>>>(H, g, sym, tw);
+template <int N, int W, int MINB>
+static cudaError_t fused_nw(double2* H, const AxisGeom& g, const FusedSymbol& sym, const double2* tw, cudaStream_t s) {
+    constexpr int GW = W < 8 ? W : 8;
+    constexpr int LSW = GW > 1 ? N + 8 / GW : N;
+    const size_t smem = (size_t)W * LSW * sizeof(double2);
+    const i64 tiles = (g.ncols + W - 1) / W;
+    cudaFuncSetAttribute(k_fused_r2c<N, W, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_fused_r2c<N, W, MINB><<<(unsigned)(g.outer * tiles), W * Cfg<N>::TPL, smem, s>>>(H, g, sym, tw);
     return cudaGetLastError();
 }
 
+// FSX_FUSED_VARIANT (A/B measurements, N = 4096 only): 0 = W1 x 2 CTAs/SM
+// (default), 1 = W1 x 1 CTA/SM (full register file), 2 = W2 x 1 CTA/SM.
+static int fused_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_FUSED_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
+template <int N>
+static cudaError_t fused_n(double2* H, const AxisGeom& g, const FusedSymbol& sym, const double2* tw, cudaStream_t s) {
+    using C = Cfg<N>;
+    if constexpr (N == 4096) {
+        const int var = fused_variant();
+        if (var == 1) return fused_nw<N, 1, 1>(H, g, sym, tw, s);
+        if (var == 2) return fused_nw<N, 2, 1>(H, g, sym, tw, s);
+    }
+    return fused_nw<N, C::W, C::MINB_W>(H, g, sym, tw, s);
+}
+
 cudaError_t launch_fused_r2c(double2* H, const AxisGeom& g, const FusedSymbol& sym, const double2* tw, cudaStream_t s) {
+    if (pipe_enabled() && pipe_cols_ok(g.n)) return launch_cols_pipe(H, g, 2, sym, tw, s);
     switch (g.n) {
 #define C_(N) case N: return fused_n<N>(H, g, sym, tw, s);
         FSX_POW2_CASES(C_)

@@ -132,6 +132,21 @@ cudaError_t launch_pinv(const double2* in, double2* out, i64 n, const double* ma
 cudaError_t launch_absmax(const double2* in, i64 n, double* out_max, cudaStream_t s);
 cudaError_t launch_block_mul(const double2* a, const double2* b, double2* out, i64 cells, int m, cudaStream_t s);
 cudaError_t launch_block_matvec(const double2* lam, const double2* x, double2* y, i64 cells, int m, cudaStream_t s);
+// persistent cp.async-pipelined passes (fsx_pipe.cu)
+bool pipe_rows_ok(i64 M);
+bool pipe_cols_ok(i64 N);
+bool pipe_enabled();
+cudaError_t launch_r2c_pipe(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw_all,
+                            cudaStream_t s);
+cudaError_t launch_c2r_pipe(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw_all,
+                            Flags* flags, cudaStream_t s);
+cudaError_t launch_cols_pipe(double2* H, const AxisGeom& g, int mode, const FusedSymbol& sym,
+                             const double2* tw_all, cudaStream_t s);
+// TMA column passes (fsx_tma.cu); tensor_map points at a 64-byte aligned CUtensorMap
+bool tma_cols_ok(i64 N);
+int make_cols_tensor_map(void* out_map, void* base, const AxisGeom& g);
+cudaError_t launch_cols_tma(const void* tensor_map, const AxisGeom& g, int mode, const FusedSymbol& sym,
+                            const double2* tw_all, cudaStream_t s);
 cudaError_t launch_transpose_split(const double2* in, double2* out, i64 outer, i64 n1, i64 n2, i64 inner,
                                    int to_natural, cudaStream_t s);
 

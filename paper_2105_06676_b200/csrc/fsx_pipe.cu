@@ -1,0 +1,331 @@
+// Persistent, software-pipelined versions of the hot-path passes.
+//
+// One CTA per (SM x occupancy slot) walks the tiles of its pass with a
+// two-stage cp.async pipeline: while tile i is transformed, tile i+1 is
+// already streaming into the other shared-memory stage, so HBM reads
+// overlap the FFT arithmetic instead of alternating with it (the round-1
+// ncu capture of the one-tile-per-CTA kernels showed long-scoreboard stalls
+// on the tile loads as the dominant stall at 8-16 warps/SM).
+// The stage that holds tile i doubles as that tile's FFT exchange buffer,
+// so a CTA needs 2 x tile bytes of shared memory.  Stores are plain
+// st.global from registers (fire-and-forget).
+//
+// Tiles: rows = one line of the contiguous axis (32 / 64 KB); columns =
+// W adjacent columns x N of a strided axis (64 KB).  Lines longer than 4096
+// complex (128 KB tiles) stay on the one-tile kernels in fsx_kernels.cu.
+#include <cstdlib>
+
+#include "fsx_device.cuh"
+#include "fsx_kernels.h"
+#include "fsx_spectral.cuh"
+
+namespace fsx {
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory");
+}
+
+template <int N>
+struct PCfg {
+    static constexpr int R = 16;
+    static constexpr int TPL = N / R;
+    static constexpr int W = N >= 4096 ? 1 : 4096 / N;   // columns per strided tile (64 KB)
+    static constexpr int GW = W < 8 ? W : 8;
+    static constexpr int LSW = GW > 1 ? N + 8 / GW : N;
+    static constexpr int TILE_W = W * LSW;               // strided tile, elements
+    static constexpr int NT_W = W * TPL;                 // strided threads
+    static constexpr int MINB_ROW = (N * 32 <= 64 * 1024) ? 3 : 1;  // rows: 2 x 32 KB stages -> 3 CTAs/SM
+};
+
+// ------------------------------------------------------------------ rows: R2C
+template <int M>
+__global__ void __launch_bounds__(PCfg<M>::TPL, PCfg<M>::MINB_ROW)
+k_r2c_pipe(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, i64 P,
+           const double2* __restrict__ tw_all) {
+    using C = PCfg<M>;
+    using F = LineFFT<M, -1, true>;
+    extern __shared__ double2 sm[];
+    const int t = threadIdx.x;
+    auto issue = [&](i64 row, int s) {
+        const double2* src = reinterpret_cast<const double2*>(x + row * L);
+        double2* dst = sm + s * M;
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) cp_async16(dst + swz(t + q * C::TPL), src + t + q * C::TPL);
+    };
+    i64 row = blockIdx.x;
+    if (row < nrows) issue(row, 0);
+    cp_commit();
+    for (int s = 0; row < nrows; row += gridDim.x, s ^= 1) {
+        const i64 nxt = row + gridDim.x;
+        if (nxt < nrows) issue(nxt, s ^ 1);
+        cp_commit();
+        cp_wait<1>();
+        double2* line = sm + s * M;
+        double2 v[C::R];
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) v[q] = line[swz(t + q * C::TPL)];
+        F::run(v, t, line, tw_all + M);
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) line[swz(t + q * C::TPL)] = v[q];
+        __syncthreads();
+        double2* dst = H + row * P;
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) {
+            const int k = t + q * C::TPL;
+            const double2 zk = v[q];
+            const double2 zm = cconj(line[swz((M - k) & (M - 1))]);
+            const double2 e = cscale(cadd(zk, zm), 0.5);
+            const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
+            const double2 w = __ldg(tw_all + 2 * M + k);
+            dst[k] = cadd(e, cmul(w, od));
+            if (k == 0) dst[M] = make_double2(zk.x - zk.y, 0.0);
+        }
+        __syncthreads();
+    }
+    cp_wait<0>();
+}
+
+// ------------------------------------------------------------------ rows: C2R
+template <int M>
+__global__ void __launch_bounds__(PCfg<M>::TPL, PCfg<M>::MINB_ROW)
+k_c2r_pipe(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, i64 P,
+           const double2* __restrict__ tw_all, Flags* flags) {
+    using C = PCfg<M>;
+    using F = LineFFT<M, +1, true>;
+    extern __shared__ double2 sm[];
+    __shared__ double2 nyq[2];
+    const int t = threadIdx.x;
+    auto issue = [&](i64 row, int s) {
+        const double2* src = H + row * P;
+        double2* dst = sm + s * M;
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) cp_async16(dst + swz(t + q * C::TPL), src + t + q * C::TPL);
+        if (t == 0) cp_async16(&nyq[s], src + M);
+    };
+    bool bad = false;
+    i64 row = blockIdx.x;
+    if (row < nrows) issue(row, 0);
+    cp_commit();
+    for (int s = 0; row < nrows; row += gridDim.x, s ^= 1) {
+        const i64 nxt = row + gridDim.x;
+        if (nxt < nrows) issue(nxt, s ^ 1);
+        cp_commit();
+        cp_wait<1>();
+        __syncthreads();
+        double2* line = sm + s * M;
+        double2 v[C::R];
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) {
+            const int k = t + q * C::TPL;
+            const double2 xk = line[swz(k)];
+            const double2 xm = cconj(k == 0 ? nyq[s] : line[swz(M - k)]);
+            const double2 e = cadd(xk, xm);
+            const double2 od = cmulc(csub(xk, xm), __ldg(tw_all + 2 * M + k));
+            v[q] = cadd(e, cmul_si<+1>(od));
+        }
+        F::run(v, t, line, tw_all + M);
+        double2* dst = reinterpret_cast<double2*>(x + row * L);
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) {
+            dst[t + q * C::TPL] = v[q];
+            bad |= !isfinite(v[q].x) || !isfinite(v[q].y);
+        }
+        __syncthreads();
+    }
+    cp_wait<0>();
+    const unsigned any = __ballot_sync(0xffffffffu, bad);
+    if (any && (threadIdx.x & 31) == 0) atomicOr(&flags->nonfinite, 1u);
+}
+
+// ------------------------------------------------------------------ columns
+// Tile = W adjacent columns x N of a strided axis.  MODE 0: forward C2C,
+// 1: inverse C2C, 2: fused R2C spectral pass (forward, lam^T x / N, inverse).
+template <int N, int MODE>
+__global__ void __launch_bounds__(PCfg<N>::NT_W, 1)
+k_cols_pipe(double2* H, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
+    using C = PCfg<N>;
+    using FF = LineFFT<N, -1, true>;
+    using FI = LineFFT<N, +1, true>;
+    extern __shared__ double2 sm[];
+    __shared__ double2 acoef[kMaxGroups][C::W];
+    __shared__ double2 tapterm[MODE == 2 ? kMaxFusedTaps : 1][C::W];
+    const int w = threadIdx.x % C::W, t = threadIdx.x / C::W;
+    const i64 tiles_per_outer = (g.ncols + C::W - 1) / C::W;
+    const i64 ntiles = g.outer * tiles_per_outer;
+    auto colof = [&](i64 tile, i64& base, i64& c) {
+        const i64 o = tile / tiles_per_outer;
+        c = (tile - o * tiles_per_outer) * C::W + w;
+        base = o * g.block + c;
+    };
+    auto valid = [&](i64 c) {
+        if (c >= g.ncols) return false;
+        if (MODE == 2 && sym.rank == 3) return c - (c / sym.P) * sym.P <= sym.M;
+        if (MODE == 2) return c <= sym.M;
+        return true;
+    };
+    auto issue = [&](i64 tile, int s) {
+        i64 base, c;
+        colof(tile, base, c);
+        if (!valid(c)) return;
+        double2* dst = sm + s * C::TILE_W + w * C::LSW;
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) cp_async16(dst + swz(t + q * C::TPL), H + base + (i64)(t + q * C::TPL) * g.inner);
+    };
+    i64 tile = blockIdx.x;
+    if (tile < ntiles) issue(tile, 0);
+    cp_commit();
+    for (int s = 0; tile < ntiles; tile += gridDim.x, s ^= 1) {
+        const i64 nxt = tile + gridDim.x;
+        if (nxt < ntiles) issue(nxt, s ^ 1);
+        cp_commit();
+        i64 base, c;
+        colof(tile, base, c);
+        const bool ok = valid(c);
+        if constexpr (MODE == 2) {
+            i64 ky = 0, kx = c;
+            if (sym.rank == 3) {
+                ky = c / sym.P;
+                kx = c - ky * sym.P;
+            }
+            for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
+        }
+        cp_wait<1>();
+        double2* line = sm + s * C::TILE_W + w * C::LSW;
+        double2 v[C::R];
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) v[q] = line[swz(t + q * C::TPL)];
+        if constexpr (MODE == 1) {
+            FI::run(v, t, line, tw_all + N);
+        } else {
+            FF::run(v, t, line, tw_all + N);
+        }
+        if constexpr (MODE == 2) {
+            __syncthreads();
+            for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
+                double2 a = make_double2(0.0, 0.0);
+                for (int j = 0; j < sym.ntaps; ++j)
+                    if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j][w]);
+                acoef[gi][w] = a;
+            }
+            __syncthreads();
+            spectral_regs<N, C::R, C::TPL>(v, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
+            FI::run(v, t, line, tw_all + N);
+        }
+        if (ok) {
+#pragma unroll
+            for (int q = 0; q < C::R; ++q) H[base + (i64)(t + q * C::TPL) * g.inner] = v[q];
+        }
+        __syncthreads();
+    }
+    cp_wait<0>();
+}
+
+// ================================================================== launchers
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <class K>
+static int persistent_grid(K kernel, int threads, size_t smem, i64 ntiles) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    const i64 g = (i64)per_sm * sm_count();
+    return (int)(ntiles < g ? ntiles : g);
+}
+
+template <int M>
+static cudaError_t r2c_pipe_m(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
+    const size_t smem = (size_t)2 * M * sizeof(double2);
+    cudaFuncSetAttribute(k_r2c_pipe<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = persistent_grid(k_r2c_pipe<M>, PCfg<M>::TPL, smem, nrows);
+    k_r2c_pipe<M><<<grid, PCfg<M>::TPL, smem, s>>>(x, H, nrows, L, P, tw);
+    return cudaGetLastError();
+}
+
+template <int M>
+static cudaError_t c2r_pipe_m(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
+                              cudaStream_t s) {
+    const size_t smem = (size_t)2 * M * sizeof(double2);
+    cudaFuncSetAttribute(k_c2r_pipe<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = persistent_grid(k_c2r_pipe<M>, PCfg<M>::TPL, smem, nrows);
+    k_c2r_pipe<M><<<grid, PCfg<M>::TPL, smem, s>>>(H, x, nrows, L, P, tw, f);
+    return cudaGetLastError();
+}
+
+template <int N, int MODE>
+static cudaError_t cols_pipe_n(double2* H, const AxisGeom& g, const FusedSymbol& sym, const double2* tw, cudaStream_t s) {
+    using C = PCfg<N>;
+    const size_t smem = (size_t)2 * C::TILE_W * sizeof(double2);
+    cudaFuncSetAttribute(k_cols_pipe<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const i64 ntiles = g.outer * ((g.ncols + C::W - 1) / C::W);
+    const int grid = persistent_grid(k_cols_pipe<N, MODE>, C::NT_W, smem, ntiles);
+    k_cols_pipe<N, MODE><<<grid, C::NT_W, smem, s>>>(H, g, sym, tw);
+    return cudaGetLastError();
+}
+
+// FSX_PIPE=0 selects the one-tile-per-CTA kernels (A/B measurements).
+bool pipe_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("FSX_PIPE");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+bool pipe_rows_ok(i64 M) { return M >= 512 && M <= 4096; }
+bool pipe_cols_ok(i64 N) { return N >= 1024 && N <= 4096; }
+
+cudaError_t launch_r2c_pipe(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
+    switch (L / 2) {
+        case 512: return r2c_pipe_m<512>(x, H, nrows, L, P, tw, s);
+        case 1024: return r2c_pipe_m<1024>(x, H, nrows, L, P, tw, s);
+        case 2048: return r2c_pipe_m<2048>(x, H, nrows, L, P, tw, s);
+        case 4096: return r2c_pipe_m<4096>(x, H, nrows, L, P, tw, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_c2r_pipe(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
+                            cudaStream_t s) {
+    switch (L / 2) {
+        case 512: return c2r_pipe_m<512>(H, x, nrows, L, P, tw, f, s);
+        case 1024: return c2r_pipe_m<1024>(H, x, nrows, L, P, tw, f, s);
+        case 2048: return c2r_pipe_m<2048>(H, x, nrows, L, P, tw, f, s);
+        case 4096: return c2r_pipe_m<4096>(H, x, nrows, L, P, tw, f, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_cols_pipe(double2* H, const AxisGeom& g, int mode, const FusedSymbol& sym, const double2* tw,
+                             cudaStream_t s) {
+#define FSX_COLS(N)                                                          \
+    case N:                                                                  \
+        return mode == 0 ? cols_pipe_n<N, 0>(H, g, sym, tw, s)               \
+             : mode == 1 ? cols_pipe_n<N, 1>(H, g, sym, tw, s)               \
+                         : cols_pipe_n<N, 2>(H, g, sym, tw, s);
+    switch (g.n) {
+        FSX_COLS(1024)
+        FSX_COLS(2048)
+        FSX_COLS(4096)
+        default: return cudaErrorInvalidValue;
+    }
+#undef FSX_COLS
+}
+
+}  // namespace fsx

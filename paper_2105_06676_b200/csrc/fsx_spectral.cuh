@@ -1,0 +1,101 @@
+// Device-side symbol / power helpers shared by the fused spectral passes.
+//
+// lam(k) = sum_taps c * exp(+2 pi i sum_a k_a o_a / n_a) is the transform of
+// the reference's generator column (proj/src/spectrum.cpp:21-45) evaluated
+// analytically with exact integer phase reduction; the power is the
+// reference's binary exponentiation loop (proj/src/spectrum.cpp:53-64).
+#pragma once
+
+#include "fsx_device.cuh"
+#include "fsx_kernels.h"
+
+namespace fsx {
+
+// exp(+2 pi i x / n) for pow2 n from the exact table: conj(tw_all[n + (x mod n)])
+__device__ __forceinline__ double2 eplus_tab(const double2* tw_all, i64 n, i64 x) {
+    return cconj(__ldg(tw_all + n + (x & (n - 1))));
+}
+
+// |lam|^T < 2^-1100 short cut: below every representable contribution (the
+// reference's own repeated squaring underflows to 0 / subnormal there).
+__device__ __forceinline__ bool negligible_power(double mag2, u64 T) {
+    if (!(mag2 < 1.0)) return false;
+    int e;
+    const double mant = frexp(mag2, &e);
+    const float l2 = (float)e + __log2f((float)mant);
+    return l2 * (0.5f * (float)T) < -2200.0f;
+}
+
+__device__ __forceinline__ double2 pow_complex(double2 lam, u64 T) {
+    if (negligible_power(fma(lam.x, lam.x, lam.y * lam.y), T)) return make_double2(0.0, 0.0);
+    double2 acc = make_double2(1.0, 0.0), sq = lam;
+    u64 t = T;
+    while (t) {
+        if (t & 1) acc = cmul(acc, sq);
+        t >>= 1;
+        if (t) sq = make_double2(fma(sq.x, sq.x, -sq.y * sq.y), (sq.x + sq.x) * sq.y);
+    }
+    return acc;
+}
+
+__device__ __forceinline__ double pow_realv(double lam, u64 T) {
+    if (negligible_power(lam * lam, T)) return 0.0;
+    double acc = 1.0, sq = lam;
+    u64 t = T;
+    while (t) {
+        if (t & 1) acc *= sq;
+        t >>= 1;
+        if (t) sq *= sq;
+    }
+    return acc;
+}
+
+// One tap's contribution to the per-column group coefficient:
+// c * exp(+2 pi i (kx o_last / L + ky o1 / n1)).
+__device__ __forceinline__ double2 tap_term(const FusedSymbol& sym, const double2* tw_all, int j, i64 kx, i64 ky) {
+    double2 e = eplus_tab(tw_all, sym.L, kx * (i64)sym.tap_olast[j]);
+    if (sym.rank == 3) e = cmul(e, eplus_tab(tw_all, sym.n1, ky * (i64)sym.tap_o1[j]));
+    return cscale(e, sym.tap_c[j]);
+}
+
+// v[q] (frequency k0 = t + q * TPL along axis 0) *= lam(k0)^T * scale, with
+// lam = sum_g A_g exp(+2 pi i k0 O_g / N); A_g read from `acoef(g)`.
+// Groups outer / elements inner so the 16 table reads of a group are
+// independent (memory-level parallelism instead of a latency chain).
+template <int N, int R, int TPL, class AC>
+__device__ __forceinline__ void spectral_regs(double2 (&v)[R], int t, const FusedSymbol& sym,
+                                              const double2* __restrict__ tw_all, AC acoef) {
+    if (sym.real) {
+        double lam[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) lam[q] = 0.0;
+        for (int gi = 0; gi < sym.ngroups; ++gi) {
+            const double2 a = acoef(gi);
+            const i64 og = sym.group_off[gi];
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const double2 e = eplus_tab(tw_all, N, (i64)(t + q * TPL) * og);
+                lam[q] = fma(a.x, e.x, fma(-a.y, e.y, lam[q]));
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = cscale(v[q], pow_realv(lam[q], sym.T) * sym.scale);
+    } else {
+        double2 lam[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) lam[q] = make_double2(0.0, 0.0);
+        for (int gi = 0; gi < sym.ngroups; ++gi) {
+            const double2 a = acoef(gi);
+            const i64 og = sym.group_off[gi];
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const double2 e = eplus_tab(tw_all, N, (i64)(t + q * TPL) * og);
+                lam[q] = cadd(lam[q], cmul(a, e));
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = cscale(cmul(pow_complex(lam[q], sym.T), v[q]), sym.scale);
+    }
+}
+
+}  // namespace fsx

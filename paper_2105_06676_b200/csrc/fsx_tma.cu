@@ -1,0 +1,211 @@
+// Strided-axis passes with TMA (cp.async.bulk.tensor) column I/O.
+//
+// A column of the half spectrum is N complex values 16 B apart at a stride
+// of a full row (P * 16 B).  Loaded with per-thread LDG/STG, every warp
+// instruction touches 16-32 different rows, and the round-1 profile of the
+// fused pass showed the LSU queue saturating (stall_lg + drain ~35 % of
+// samples).  Here one elected thread moves the whole column with
+// N / 256 TMA box copies ({2 doubles} x {256 rows}) into a linear
+// shared-memory tile (mbarrier completion), the CTA transforms it, and the
+// result leaves the same way (bulk store from shared memory).  The tile
+// doubles as the FFT exchange buffer, so a CTA needs N * 16 B of shared
+// memory and two CTAs share an SM (one loads while the other computes).
+//
+// Tensor map: the complex array viewed as fp64 [outer][n][2 * inner]
+// (dims {2 * inner, n, outer}), box {2, min(n, 256), 1}; built on the host
+// (fsx_api.cpp) with cuTensorMapEncodeTiled.
+#include <cuda.h>
+
+#include "fsx_device.cuh"
+#include "fsx_kernels.h"
+#include "fsx_spectral.cuh"
+
+namespace fsx {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y, int z) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(map), "r"(x),
+                 "r"(y), "r"(z), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+template <int N>
+struct TCfg {
+    static constexpr int R = N < 16 ? N : 16;
+    static constexpr int TPL = N / R;
+    static constexpr int W = N >= 4096 ? 1 : 4096 / N;   // adjacent columns per CTA (64 KB tile)
+    static constexpr int BOX = N < 256 ? N : 256;        // rows per TMA box
+    static constexpr int NBOX = N / BOX;
+    static constexpr int GW = W < 8 ? W : 8;
+    static constexpr int LSW = GW > 1 ? N + 8 / GW : N;  // exchange line stride (bank padding)
+    static constexpr int NT = W * TPL;
+    static constexpr int MINB = NT <= 256 ? 2 : 1;
+};
+
+// MODE 0: forward C2C, 1: inverse C2C, 2: fused R2C spectral pass.
+// The TMA tile is [N rows][W columns] (row-major, as the boxes land); the
+// FFT exchanges reuse the same buffer as W line-major rows of LSW.
+template <int N, int MODE>
+__global__ void __launch_bounds__(TCfg<N>::NT, TCfg<N>::MINB)
+k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
+    using C = TCfg<N>;
+    constexpr int W = C::W;
+    using FF = LineFFT<N, -1>;
+    using FI = LineFFT<N, +1>;
+    extern __shared__ __align__(128) double2 tile[];
+    __shared__ __align__(8) unsigned long long bar;
+    __shared__ double2 acoef[kMaxGroups][W];
+    __shared__ double2 tapterm[MODE == 2 ? kMaxFusedTaps : 1][W];
+    const int w = threadIdx.x % W, t = threadIdx.x / W;
+    const i64 tiles = (g.ncols + W - 1) / W;
+    const i64 o = (i64)blockIdx.x / tiles;
+    const i64 c0 = ((i64)blockIdx.x - o * tiles) * W;
+    const i64 c = c0 + w;
+    i64 ky = 0, kx = c;
+    if constexpr (MODE == 2) {
+        if (sym.rank == 3) {
+            ky = c / sym.P;
+            kx = c - ky * sym.P;
+        }
+        // pitch-padding tiles of a 3D plane (W divides P, so a tile is all-padding or none)
+        if (c0 - (c0 / sym.P) * sym.P > sym.M && sym.rank == 3) return;
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        mbar_expect_tx(&bar, (unsigned)(N * W * sizeof(double2)));
+#pragma unroll 1
+        for (int b = 0; b < C::NBOX; ++b)
+            tma_load_3d(tile + b * C::BOX * W, &map, (int)(2 * c0), b * C::BOX, (int)o, &bar);
+    }
+    if constexpr (MODE == 2) {
+        for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
+    }
+    __syncthreads();  // barrier initialised before anyone waits on it
+    mbar_wait(&bar, 0);
+    double2 v[C::R];
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) v[q] = tile[(t + q * C::TPL) * W + w];
+    double2* line = tile + w * C::LSW;
+    if constexpr (MODE == 1) {
+        FI::run(v, t, line, tw_all + N);
+    } else {
+        FF::run(v, t, line, tw_all + N);
+    }
+    if constexpr (MODE == 2) {
+        __syncthreads();
+        for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
+            double2 a = make_double2(0.0, 0.0);
+            for (int j = 0; j < sym.ntaps; ++j)
+                if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j][w]);
+            acoef[gi][w] = a;
+        }
+        __syncthreads();
+        spectral_regs<N, C::R, C::TPL>(v, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
+        FI::run(v, t, line, tw_all + N);
+    }
+    __syncthreads();  // last exchange reads done before the tile is overwritten
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) tile[(t + q * C::TPL) * W + w] = v[q];
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll 1
+        for (int b = 0; b < C::NBOX; ++b) tma_store_3d(&map, tile + b * C::BOX * W, (int)(2 * c0), b * C::BOX, (int)o);
+        bulk_commit();
+        bulk_wait_read0();
+    }
+}
+
+template <int N, int MODE>
+static cudaError_t cols_tma_n(const CUtensorMap& map, const AxisGeom& g, const FusedSymbol& sym, const double2* tw,
+                              cudaStream_t s) {
+    using C = TCfg<N>;
+    const size_t smem = (size_t)C::W * C::LSW * sizeof(double2);
+    const i64 tiles = (g.ncols + C::W - 1) / C::W;
+    cudaFuncSetAttribute(k_cols_tma<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_cols_tma<N, MODE><<<(unsigned)(g.outer * tiles), C::NT, smem, s>>>(map, g, sym, tw);
+    return cudaGetLastError();
+}
+
+// columns per TMA tile for a line length (the host builds the box to match)
+int tma_cols_width(i64 N) { return N >= 4096 ? 1 : (int)(4096 / N); }
+
+bool tma_cols_ok(i64 N) { return N >= 512 && N <= 8192; }
+
+cudaError_t launch_cols_tma(const void* tensor_map, const AxisGeom& g, int mode, const FusedSymbol& sym,
+                            const double2* tw, cudaStream_t s) {
+    const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(tensor_map);
+#define FSX_TMA(N)                                                     \
+    case N:                                                            \
+        return mode == 0 ? cols_tma_n<N, 0>(map, g, sym, tw, s)        \
+             : mode == 1 ? cols_tma_n<N, 1>(map, g, sym, tw, s)        \
+                         : cols_tma_n<N, 2>(map, g, sym, tw, s);
+    switch (g.n) {
+        FSX_TMA(512)
+        FSX_TMA(1024)
+        FSX_TMA(2048)
+        FSX_TMA(4096)
+        FSX_TMA(8192)
+        default: return cudaErrorInvalidValue;
+    }
+#undef FSX_TMA
+}
+
+// Host: tensor map over a complex array viewed as fp64 [outer][n][2*inner].
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int make_cols_tensor_map(void* out_map, void* base, const AxisGeom& g) {
+    static EncodeTiledFn encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return -1;
+        encode = reinterpret_cast<EncodeTiledFn>(fn);
+    }
+    if (g.outer > 1 && g.block != g.n * g.inner) return -2;  // contiguous outer blocks only
+    const cuuint64_t dims[3] = {(cuuint64_t)(2 * g.inner), (cuuint64_t)g.n, (cuuint64_t)g.outer};
+    const cuuint64_t strides[2] = {(cuuint64_t)(g.inner * 16), (cuuint64_t)(g.block * 16)};
+    const cuuint32_t box[3] = {(cuuint32_t)(2 * tma_cols_width(g.n)), (cuuint32_t)(g.n < 256 ? g.n : 256), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode(reinterpret_cast<CUtensorMap*>(out_map), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : (int)r;
+}
+
+}  // namespace fsx
