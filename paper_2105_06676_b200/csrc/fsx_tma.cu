@@ -16,6 +16,8 @@
 // (fsx_api.cpp) with cuTensorMapEncodeTiled.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "fsx_device.cuh"
 #include "fsx_kernels.h"
 #include "fsx_spectral.cuh"
@@ -147,9 +149,142 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
     }
 }
 
+// Persistent variant: one CTA per SM walks the tiles with two shared-memory
+// stages; the TMA load of tile i+1 is in flight while tile i is transformed,
+// and a stage is refilled only after the bulk store that drained it has
+// finished reading shared memory (cp.async.bulk.wait_group.read).
+template <int N, int MODE>
+__global__ void __launch_bounds__(TCfg<N>::NT, 1)
+k_cols_tma_pers(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
+                const double2* __restrict__ tw_all) {
+    using C = TCfg<N>;
+    constexpr int W = C::W;
+    constexpr int STAGE = W * C::LSW;
+    using FF = LineFFT<N, -1, true>;
+    using FI = LineFFT<N, +1, true>;
+    extern __shared__ __align__(128) double2 tile[];
+    __shared__ __align__(8) unsigned long long bar[2];
+    __shared__ double2 acoef[kMaxGroups][W];
+    __shared__ double2 tapterm[MODE == 2 ? kMaxFusedTaps : 1][W];
+    const int w = threadIdx.x % W, t = threadIdx.x / W;
+    const i64 tiles = (g.ncols + W - 1) / W;
+    const i64 ntiles = g.outer * tiles;
+    auto pos = [&](i64 tl, i64& o, i64& c0) {
+        o = tl / tiles;
+        c0 = (tl - o * tiles) * W;
+    };
+    auto live = [&](i64 c0) {
+        if constexpr (MODE == 2) {
+            if (sym.rank == 3) return c0 - (c0 / sym.P) * sym.P <= sym.M;
+        }
+        return true;
+    };
+    auto issue = [&](i64 tl, int s) {  // thread 0 only
+        i64 o, c0;
+        pos(tl, o, c0);
+        if (!live(c0)) {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&bar[s])) : "memory");
+            return;
+        }
+        mbar_expect_tx(&bar[s], (unsigned)(N * W * sizeof(double2)));
+#pragma unroll 1
+        for (int b = 0; b < C::NBOX; ++b)
+            tma_load_3d(tile + s * STAGE + b * C::BOX * W, &map, (int)(2 * c0), b * C::BOX, (int)o, &bar[s]);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        if ((i64)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    }
+    __syncthreads();
+    unsigned phase[2] = {0u, 0u};
+    int s = 0;
+    for (i64 tl = blockIdx.x; tl < ntiles; tl += gridDim.x, s ^= 1) {
+        const i64 nxt = tl + gridDim.x;
+        if (threadIdx.x == 0 && nxt < ntiles) {
+            bulk_wait_read0();  // the store of the tile that last used stage s^1 has read its smem
+            issue(nxt, s ^ 1);
+        }
+        i64 o, c0;
+        pos(tl, o, c0);
+        const i64 c = c0 + w;
+        double2* stg = tile + s * STAGE;
+        if (live(c0)) {
+            i64 ky = 0, kx = c;
+            if constexpr (MODE == 2) {
+                if (sym.rank == 3) {
+                    ky = c / sym.P;
+                    kx = c - ky * sym.P;
+                }
+                for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
+            }
+            mbar_wait(&bar[s], phase[s]);
+            double2 v[C::R];
+#pragma unroll
+            for (int q = 0; q < C::R; ++q) v[q] = stg[(t + q * C::TPL) * W + w];
+            double2* line = stg + w * C::LSW;
+            if constexpr (MODE == 1) {
+                FI::run(v, t, line, tw_all + N);
+            } else {
+                FF::run(v, t, line, tw_all + N);
+            }
+            if constexpr (MODE == 2) {
+                __syncthreads();
+                for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
+                    double2 a = make_double2(0.0, 0.0);
+                    for (int j = 0; j < sym.ntaps; ++j)
+                        if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j][w]);
+                    acoef[gi][w] = a;
+                }
+                __syncthreads();
+                spectral_regs<N, C::R, C::TPL>(v, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
+                FI::run(v, t, line, tw_all + N);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < C::R; ++q) stg[(t + q * C::TPL) * W + w] = v[q];
+            fence_proxy_async();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+#pragma unroll 1
+                for (int b = 0; b < C::NBOX; ++b)
+                    tma_store_3d(&map, stg + b * C::BOX * W, (int)(2 * c0), b * C::BOX, (int)o);
+                bulk_commit();
+            }
+        } else {
+            mbar_wait(&bar[s], phase[s]);
+        }
+        phase[s] ^= 1u;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) bulk_wait_read0();
+}
+
+static int tma_persistent() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_TMA_PERSIST");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
 template <int N, int MODE>
 static cudaError_t cols_tma_n(const CUtensorMap& map, const AxisGeom& g, const FusedSymbol& sym, const double2* tw,
                               cudaStream_t s) {
+    if (tma_persistent() && 2 * TCfg<N>::W * TCfg<N>::LSW * 16 <= 220 * 1024) {
+        using C = TCfg<N>;
+        const size_t smem = (size_t)2 * C::W * C::LSW * sizeof(double2);
+        const i64 ntiles = g.outer * ((g.ncols + C::W - 1) / C::W);
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_cols_tma_pers<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int grid = (int)(ntiles < sms ? ntiles : sms);
+        k_cols_tma_pers<N, MODE><<<grid, C::NT, smem, s>>>(map, g, sym, tw);
+        return cudaGetLastError();
+    }
     using C = TCfg<N>;
     const size_t smem = (size_t)C::W * C::LSW * sizeof(double2);
     const i64 tiles = (g.ncols + C::W - 1) / C::W;
