@@ -126,6 +126,37 @@ fsx_status fsx_device_check(const fsx_options* opt);
  * Waits for that solve's last stage event. */
 fsx_status fsx_last_stage_ms(const fsx_options* opt, double* ms);
 
+/* ---------------------------------------------------------------- slab decomposition
+ * Multi-GPU StencilFFT-P for rank-2/3 scalar pow2 grids (plan 1 eligible):
+ * rank r of P owns planes [r n0/P, (r+1) n0/P) of axis 0 of the real grid.
+ * One solve is
+ *     fsx_slab_forward(local a0 -> send)
+ *     all_to_all(recv <- send)      equal split: P chunks of xbuf_bytes / P
+ *     fsx_slab_spectral(recv, in place)
+ *     all_to_all(send <- recv)
+ *     fsx_slab_inverse(send -> local out)
+ * with the all-to-alls done by the caller (NCCL over NVLink).  The exchange
+ * layout needs no pack/unpack in 2D: the R2C rows are written directly as
+ * P column blocks, and the received buffer is already the [n0][block] column
+ * tile the fused pass transforms (3D packs with 2D copies after the local
+ * y pass).  All calls are asynchronous on opt->stream; device pointers; the
+ * non-finite check is deferred to fsx_device_check(). */
+typedef struct fsx_slab_info {
+    int32_t nranks;
+    int32_t rank;
+    int64_t local_dims[FSX_MAX_RANK]; /* this rank's slab of the real grid */
+    int64_t plane_offset;             /* first global index along axis 0 */
+    int64_t col_block;                /* 2D: kx columns per rank; 3D: ky rows per rank */
+    int64_t xbuf_bytes;               /* size of each exchange buffer (send and receive) */
+} fsx_slab_info;
+fsx_status fsx_slab_describe(const fsx_shape* global, int32_t nranks, int32_t rank, fsx_slab_info* info);
+fsx_status fsx_slab_forward(const fsx_shape* global, int32_t nranks, int32_t rank, const double* d_local_in,
+                            double* d_send, const fsx_options* opt);
+fsx_status fsx_slab_spectral(const fsx_shape* global, const fsx_kernel* k, uint64_t T, int32_t nranks,
+                             int32_t rank, double* d_recv, const fsx_options* opt);
+fsx_status fsx_slab_inverse(const fsx_shape* global, int32_t nranks, int32_t rank, const double* d_send,
+                            double* d_local_out, const fsx_options* opt);
+
 /* ---------------------------------------------------------------- building blocks
  * (host pointers, complex = interleaved fp64) */
 

@@ -87,6 +87,10 @@ EXPORTS = (
     "fsx_solve_periodic_device",
     "fsx_device_check",
     "fsx_last_stage_ms",
+    "fsx_slab_describe",
+    "fsx_slab_forward",
+    "fsx_slab_spectral",
+    "fsx_slab_inverse",
     "fsx_multi_fft",
     "fsx_spectrum_from_kernel",
     "fsx_pow_spectrum",

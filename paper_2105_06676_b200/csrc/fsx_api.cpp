@@ -670,7 +670,8 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
     sp.mark();
     if (p.kind == kFusedR2C) {
         double2* H = p.work.as<double2>();
-        FSX_CK(fsx::launch_r2c_rows(d_a0, H, p.rows, p.L, p.P, tw, st));
+        const fsx::RowLayout lay{p.P, 0, p.rows};
+        FSX_CK(fsx::launch_r2c_rows(d_a0, H, p.rows, p.L, lay, tw, st));
         fsx::StepTwiddle none;
         const fsx::FusedSymbol sym = fused_symbol(p, taps, T);
         fsx::FusedSymbol nosym;
@@ -686,7 +687,7 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
             if (p.tma1) FSX_CK(fsx::launch_cols_tma(p.map1, p.ax1, 1, nosym, tw, st));
             else FSX_CK(fsx::launch_axis_pow2(H, H, p.ax1, +1, none, tw, st));
         }
-        FSX_CK(fsx::launch_c2r_rows(H, d_out, p.rows, p.L, p.P, tw, flags, st));
+        FSX_CK(fsx::launch_c2r_rows(H, d_out, p.rows, p.L, lay, tw, flags, st));
         sp.mark();
     } else if (p.kind == kRowPair1D) {
         if (d_out != d_a0)
@@ -722,6 +723,138 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
         FSX_CK(fsx::launch_extract(Z, d_out, p.cells * p.m, flags, st));
         sp.mark();
     }
+}
+
+// ------------------------------------------------------------------ slab decomposition
+struct SlabPlan {
+    std::vector<i64> dims;
+    int P = 1, r = 0;
+    i64 n0l = 0, L = 0, M = 0, Pp = 0, n1 = 1, n1b = 0, CB = 0;
+    i64 xcount = 0;  // complex elements per exchange buffer
+    DevBuf H;        // 3D: local half spectrum [n0l][n1][Pp]
+    alignas(64) unsigned char mapH[128];
+    bool tmaH = false;
+    fsx::AxisGeom axy;  // 3D local y pass
+};
+
+std::map<std::string, std::unique_ptr<SlabPlan>> g_slabs;
+
+// Geometry only (no device work): validates and fills the sizes.
+void slab_geom(const fsx_shape* global, int P, int r, SlabPlan& sp) {
+    const Shape s = parse_shape(global);
+    const int rk = s.rank();
+    if (rk != 2 && rk != 3) throw SpecErr("slab: rank-2 or rank-3 grids only");
+    if (s.fields != 1) throw SpecErr("slab: scalar fields only");
+    if (P < 1 || r < 0 || r >= P) throw SpecErr("slab: bad rank / world size");
+    for (i64 d : s.dims)
+        if (!is_pow2(d)) throw SpecErr("slab: power-of-two dims only");
+    const i64 L = s.dims[rk - 1];
+    if (L < 16 || L > 2 * fsx::kMaxLine || s.dims[0] > fsx::kMaxLine || s.dims[0] % P)
+        throw SpecErr("slab: axis 0 must divide by the world size; line lengths as plan 1");
+    if (rk == 3 && (s.dims[1] % P || s.dims[1] > fsx::kMaxLine))
+        throw SpecErr("slab: axis 1 must divide by the world size");
+    sp.dims = s.dims;
+    sp.P = P;
+    sp.r = r;
+    sp.n0l = s.dims[0] / P;
+    sp.L = L;
+    sp.M = L / 2;
+    sp.Pp = sp.M + 8;
+    if (rk == 2) {
+        sp.CB = ((sp.M + 1 + P - 1) / P + 7) / 8 * 8;
+        sp.xcount = s.dims[0] * sp.CB;
+    } else {
+        sp.n1 = s.dims[1];
+        sp.n1b = sp.n1 / P;
+        sp.CB = sp.n1b;
+        sp.xcount = s.dims[0] * sp.n1b * sp.Pp;
+        sp.axy = fsx::AxisGeom{sp.n1, sp.Pp, sp.n0l, sp.n1 * sp.Pp, sp.M + 1};
+    }
+}
+
+// Device plan (call with g_mu held and the device selected).
+SlabPlan& slab_plan(const fsx_shape* global, int P, int r) {
+    const Shape s = parse_shape(global);
+    std::string key = std::to_string(P) + "/" + std::to_string(r);
+    for (i64 d : s.dims) key += ":" + std::to_string(d);
+    auto it = g_slabs.find(key);
+    if (it != g_slabs.end()) return *it->second;
+    if (g_slabs.size() >= 16) g_slabs.clear();
+    auto sp = std::make_unique<SlabPlan>();
+    slab_geom(global, P, r, *sp);
+    if (sp->dims.size() == 3) {
+        sp->H.ensure((size_t)sp->n0l * sp->n1 * sp->Pp * 16);
+        sp->tmaH = tma_enabled() && fsx::tma_cols_ok(sp->n1) &&
+                   fsx::make_cols_tensor_map(sp->mapH, sp->H.p, sp->axy) == 0;
+    }
+    auto& ref = *sp;
+    g_slabs.emplace(key, std::move(sp));
+    return ref;
+}
+
+void slab_forward(SlabPlan& sp, Device& dev, const double* in, double2* send, cudaStream_t st) {
+    const double2* tw = dev.tw_all.as<double2>();
+    if (sp.dims.size() == 2) {
+        const fsx::RowLayout lay{0, sp.CB, sp.n0l};
+        FSX_CK(fsx::launch_r2c_rows(in, send, sp.n0l, sp.L, lay, tw, st));
+        return;
+    }
+    double2* H = sp.H.as<double2>();
+    const fsx::RowLayout lay{sp.Pp, 0, sp.n0l * sp.n1};
+    FSX_CK(fsx::launch_r2c_rows(in, H, sp.n0l * sp.n1, sp.L, lay, tw, st));
+    fsx::FusedSymbol none;
+    fsx::StepTwiddle nt;
+    if (sp.tmaH) FSX_CK(fsx::launch_cols_tma(sp.mapH, sp.axy, 0, none, tw, st));
+    else FSX_CK(fsx::launch_axis_pow2(H, H, sp.axy, -1, nt, tw, st));
+    const size_t w = (size_t)sp.n1b * sp.Pp * 16;
+    for (int d = 0; d < sp.P; ++d)
+        FSX_CK(cudaMemcpy2DAsync(send + (i64)d * sp.n0l * sp.n1b * sp.Pp, w, H + (i64)d * sp.n1b * sp.Pp,
+                                 (size_t)sp.n1 * sp.Pp * 16, w, (size_t)sp.n0l, cudaMemcpyDeviceToDevice, st));
+}
+
+void slab_inverse(SlabPlan& sp, Device& dev, const double2* send, double* out, cudaStream_t st) {
+    const double2* tw = dev.tw_all.as<double2>();
+    fsx::Flags* flags = dev.flags.as<fsx::Flags>();
+    if (sp.dims.size() == 2) {
+        const fsx::RowLayout lay{0, sp.CB, sp.n0l};
+        FSX_CK(fsx::launch_c2r_rows(send, out, sp.n0l, sp.L, lay, tw, flags, st));
+        return;
+    }
+    double2* H = sp.H.as<double2>();
+    const size_t w = (size_t)sp.n1b * sp.Pp * 16;
+    for (int d = 0; d < sp.P; ++d)
+        FSX_CK(cudaMemcpy2DAsync(H + (i64)d * sp.n1b * sp.Pp, (size_t)sp.n1 * sp.Pp * 16,
+                                 send + (i64)d * sp.n0l * sp.n1b * sp.Pp, w, w, (size_t)sp.n0l,
+                                 cudaMemcpyDeviceToDevice, st));
+    fsx::FusedSymbol none;
+    fsx::StepTwiddle nt;
+    if (sp.tmaH) FSX_CK(fsx::launch_cols_tma(sp.mapH, sp.axy, 1, none, tw, st));
+    else FSX_CK(fsx::launch_axis_pow2(H, H, sp.axy, +1, nt, tw, st));
+    const fsx::RowLayout lay{sp.Pp, 0, sp.n0l * sp.n1};
+    FSX_CK(fsx::launch_c2r_rows(H, out, sp.n0l * sp.n1, sp.L, lay, tw, flags, st));
+}
+
+void slab_spectral(SlabPlan& sp, Device& dev, const Taps& taps, u64 T, double2* recv, cudaStream_t st) {
+    const double2* tw = dev.tw_all.as<double2>();
+    const int rk = (int)sp.dims.size();
+    // a plan-1 view of the global grid for the symbol fields
+    Plan view;
+    view.dims = sp.dims;
+    for (int a = 0; a < rk; ++a) view.axes.push_back(a);
+    view.L = sp.L;
+    view.M = sp.M;
+    view.P = rk == 3 ? sp.Pp : sp.CB;
+    view.cells = 1;
+    for (i64 d : sp.dims) view.cells *= d;
+    fsx::FusedSymbol sym = fused_symbol(view, taps, T);
+    sym.c_off = (i64)sp.r * sp.CB;
+    const i64 inner = rk == 3 ? sp.n1b * sp.Pp : sp.CB;
+    const fsx::AxisGeom g{sp.dims[0], inner, 1, sp.dims[0] * inner, inner};
+    alignas(64) unsigned char map[128];
+    if (tma_enabled() && fsx::tma_cols_ok(g.n) && fsx::make_cols_tensor_map(map, recv, g) == 0)
+        FSX_CK(fsx::launch_cols_tma(map, g, 2, sym, tw, st));
+    else
+        FSX_CK(fsx::launch_fused_r2c(recv, g, sym, tw, st));
 }
 
 double bits_to_double(unsigned long long b) {
@@ -941,6 +1074,59 @@ fsx_status fsx_last_stage_ms(const fsx_options* opt, double* ms) {
             FSX_CK(cudaEventElapsedTime(&t, dev.ev[i], dev.ev[i + 1]));
             ms[i] = t;
         }
+    });
+}
+
+fsx_status fsx_slab_describe(const fsx_shape* global, int32_t nranks, int32_t rank, fsx_slab_info* info) {
+    return guarded([&] {
+        if (!info) throw SpecErr("fsx_slab_describe: null info");
+        SlabPlan sp;
+        slab_geom(global, nranks, rank, sp);
+        std::memset(info, 0, sizeof(*info));
+        info->nranks = nranks;
+        info->rank = rank;
+        for (size_t a = 0; a < sp.dims.size(); ++a) info->local_dims[a] = sp.dims[a];
+        info->local_dims[0] = sp.n0l;
+        info->plane_offset = (int64_t)rank * sp.n0l;
+        info->col_block = sp.CB;
+        info->xbuf_bytes = sp.xcount * 16;
+    });
+}
+
+fsx_status fsx_slab_forward(const fsx_shape* global, int32_t nranks, int32_t rank, const double* d_local_in,
+                            double* d_send, const fsx_options* opt) {
+    return guarded([&] {
+        if (!d_local_in || !d_send) throw SpecErr("fsx_slab_forward: null pointer");
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(opt ? opt->device : 0);
+        SlabPlan& sp = slab_plan(global, nranks, rank);
+        slab_forward(sp, dev, d_local_in, reinterpret_cast<double2*>(d_send), stream_of(dev, opt));
+    });
+}
+
+fsx_status fsx_slab_spectral(const fsx_shape* global, const fsx_kernel* k, uint64_t T, int32_t nranks, int32_t rank,
+                             double* d_recv, const fsx_options* opt) {
+    return guarded([&] {
+        if (!d_recv) throw SpecErr("fsx_slab_spectral: null pointer");
+        const Shape s = parse_shape(global);
+        const Taps taps = parse_kernel(k);
+        require_fits(taps, s);
+        if ((i64)taps.map.size() > fsx::kMaxFusedTaps) throw SpecErr("slab: at most 64 taps");
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(opt ? opt->device : 0);
+        SlabPlan& sp = slab_plan(global, nranks, rank);
+        slab_spectral(sp, dev, taps, T, reinterpret_cast<double2*>(d_recv), stream_of(dev, opt));
+    });
+}
+
+fsx_status fsx_slab_inverse(const fsx_shape* global, int32_t nranks, int32_t rank, const double* d_send,
+                            double* d_local_out, const fsx_options* opt) {
+    return guarded([&] {
+        if (!d_send || !d_local_out) throw SpecErr("fsx_slab_inverse: null pointer");
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(opt ? opt->device : 0);
+        SlabPlan& sp = slab_plan(global, nranks, rank);
+        slab_inverse(sp, dev, reinterpret_cast<const double2*>(d_send), d_local_out, stream_of(dev, opt));
     });
 }
 

@@ -233,7 +233,7 @@ __global__ void k_direct_dft(const double2* in, double2* out, AxisGeom g, int si
 // O = -i (Z[k] - conj Z[M-k]) / 2; X[M] = Re Z[0] - Im Z[0].
 template <int M>
 __global__ void __launch_bounds__(Cfg<M>::LINES * Cfg<M>::TPL, Cfg<M>::MINB_L)
-k_r2c_rows(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, i64 P,
+k_r2c_rows(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, RowLayout lay,
            const double2* __restrict__ tw_all) {
     using C = Cfg<M>;
     using F = LineFFT<M, -1>;
@@ -252,7 +252,6 @@ k_r2c_rows(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
     for (int q = 0; q < C::R; ++q) line[swz(t + q * C::TPL)] = v[q];
     __syncthreads();
     if (!ok) return;
-    double2* dst = H + row * P;
 #pragma unroll
     for (int q = 0; q < C::R; ++q) {
         const int k = t + q * C::TPL;
@@ -261,8 +260,8 @@ k_r2c_rows(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
         const double2 e = cscale(cadd(zk, zm), 0.5);
         const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
         const double2 w = __ldg(tw_all + 2 * M + k);  // exp(-2 pi i k / L)
-        dst[k] = cadd(e, cmul(w, od));
-        if (k == 0) dst[M] = make_double2(zk.x - zk.y, 0.0);
+        H[lay.at(row, k)] = cadd(e, cmul(w, od));
+        if (k == 0) H[lay.at(row, M)] = make_double2(zk.x - zk.y, 0.0);
     }
 }
 
@@ -271,7 +270,7 @@ k_r2c_rows(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
 // the 1/N of the inverse transform is folded into the spectral multiply).
 template <int M>
 __global__ void __launch_bounds__(Cfg<M>::LINES * Cfg<M>::TPL, Cfg<M>::MINB_L)
-k_c2r_rows(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, i64 P,
+k_c2r_rows(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, RowLayout lay,
            const double2* __restrict__ tw_all, Flags* flags) {
     using C = Cfg<M>;
     using F = LineFFT<M, +1>;
@@ -281,14 +280,13 @@ k_c2r_rows(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
     const i64 row = (i64)blockIdx.x * C::LINES + b;
     const bool ok = row < nrows;
     double2* line = sm + b * C::LSL;
-    const double2* src = H + row * P;
     double2 v[C::R];
 #pragma unroll
     for (int q = 0; q < C::R; ++q) {
-        v[q] = ok ? src[t + q * C::TPL] : make_double2(0.0, 0.0);
+        v[q] = ok ? H[lay.at(row, t + q * C::TPL)] : make_double2(0.0, 0.0);
         line[swz(t + q * C::TPL)] = v[q];
     }
-    if (t == 0) nyq[b] = ok ? src[M] : make_double2(0.0, 0.0);
+    if (t == 0) nyq[b] = ok ? H[lay.at(row, M)] : make_double2(0.0, 0.0);
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < C::R; ++q) {
@@ -334,11 +332,8 @@ k_fused_r2c(double2* H, AxisGeom g, FusedSymbol sym, const double2* __restrict__
     const i64 tiles = (g.ncols + W - 1) / W;
     const i64 o = (i64)blockIdx.x / tiles;
     const i64 c = ((i64)blockIdx.x % tiles) * W + w;
-    i64 ky = 0, kx = c;
-    if (sym.rank == 3) {
-        ky = c / sym.P;
-        kx = c - ky * sym.P;
-    }
+    i64 kx, ky;
+    fused_col_freqs(sym, c, kx, ky);
     const bool ok = c < g.ncols && kx <= sym.M;
     const i64 base = o * g.block + c;
     double2 v[C::R];
@@ -821,7 +816,8 @@ cudaError_t launch_axis_direct(const double2* in, double2* out, const AxisGeom& 
 }
 
 template <int M>
-static cudaError_t r2c_m(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
+static cudaError_t r2c_m(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw,
+                         cudaStream_t s) {
     using C = Cfg<M>;
     const size_t smem = (size_t)C::LINES * C::LSL * sizeof(double2);
     cudaFuncSetAttribute(k_r2c_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -830,7 +826,7 @@ static cudaError_t r2c_m(const double* x, double2* H, i64 nrows, i64 L, i64 P, c
 }
 
 template <int M>
-static cudaError_t c2r_m(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
+static cudaError_t c2r_m(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw, Flags* f,
                          cudaStream_t s) {
     using C = Cfg<M>;
     const size_t smem = (size_t)C::LINES * C::LSL * sizeof(double2);
@@ -842,7 +838,8 @@ static cudaError_t c2r_m(const double2* H, double* x, i64 nrows, i64 L, i64 P, c
 #define FSX_POW2_CASES(MACRO) \
     MACRO(8) MACRO(16) MACRO(32) MACRO(64) MACRO(128) MACRO(256) MACRO(512) MACRO(1024) MACRO(2048) MACRO(4096) MACRO(8192)
 
-cudaError_t launch_r2c_rows(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
+cudaError_t launch_r2c_rows(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw,
+                            cudaStream_t s) {
     if (pipe_enabled() && pipe_rows_ok(L / 2)) return launch_r2c_pipe(x, H, nrows, L, P, tw, s);
     switch (L / 2) {
 #define C_(M) case M: return r2c_m<M>(x, H, nrows, L, P, tw, s);
@@ -852,7 +849,7 @@ cudaError_t launch_r2c_rows(const double* x, double2* H, i64 nrows, i64 L, i64 P
     }
 }
 
-cudaError_t launch_c2r_rows(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
+cudaError_t launch_c2r_rows(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw, Flags* f,
                             cudaStream_t s) {
     if (pipe_enabled() && pipe_rows_ok(L / 2)) return launch_c2r_pipe(H, x, nrows, L, P, tw, f, s);
     switch (L / 2) {

@@ -63,6 +63,34 @@ struct FusedSymbol {
     u64 T = 1;
     double scale = 1.0;          // 1 / prod(dims)
     int real = 0;                // taps symmetric under o -> -o: lam is real
+    i64 c_off = 0;               // slab decomposition: global frequency of local column block start
+                                 // (rank 2: kx offset; rank 3: ky offset)
+};
+
+// Local column c of a fused-pass tile -> global (kx, ky); valid iff kx <= M.
+__host__ __device__ inline void fused_col_freqs(const FusedSymbol& s, i64 c, i64& kx, i64& ky) {
+    if (s.rank == 3) {
+        ky = c / s.P;
+        kx = c - ky * s.P;
+        ky += s.c_off;
+    } else {
+        ky = 0;
+        kx = c + s.c_off;
+    }
+}
+
+// Row-kernel output/input layout: pitch rows (blk == 0: element (row, k) at
+// row * P + k) or the slab all-to-all layout (blk > 0: column block
+// d = k / blk of all rows is contiguous: d * nrows * blk + row * blk + k % blk).
+struct RowLayout {
+    i64 P = 0;
+    i64 blk = 0;
+    i64 nrows = 0;
+    __host__ __device__ i64 at(i64 row, i64 k) const {
+        if (blk == 0) return row * P + k;
+        const i64 d = k / blk;
+        return d * nrows * blk + row * blk + (k - d * blk);
+    }
 };
 
 // General spectral stage over a full complex spectrum with m fields.
@@ -113,9 +141,9 @@ cudaError_t launch_axis_pow2(const double2* in, double2* out, const AxisGeom& g,
                              const StepTwiddle& st, const double2* tw_all, cudaStream_t s);
 cudaError_t launch_axis_direct(const double2* in, double2* out, const AxisGeom& g, int sign,
                                const PhaseTable& tab, cudaStream_t s);
-cudaError_t launch_r2c_rows(const double* x, double2* H, i64 nrows, i64 L, i64 P,
+cudaError_t launch_r2c_rows(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P,
                             const double2* tw_all, cudaStream_t s);
-cudaError_t launch_c2r_rows(const double2* H, double* x, i64 nrows, i64 L, i64 P,
+cudaError_t launch_c2r_rows(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P,
                             const double2* tw_all, Flags* flags, cudaStream_t s);
 cudaError_t launch_fused_r2c(double2* H, const AxisGeom& g, const FusedSymbol& sym,
                              const double2* tw_all, cudaStream_t s);
@@ -136,9 +164,9 @@ cudaError_t launch_block_matvec(const double2* lam, const double2* x, double2* y
 bool pipe_rows_ok(i64 M);
 bool pipe_cols_ok(i64 N);
 bool pipe_enabled();
-cudaError_t launch_r2c_pipe(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw_all,
+cudaError_t launch_r2c_pipe(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw_all,
                             cudaStream_t s);
-cudaError_t launch_c2r_pipe(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw_all,
+cudaError_t launch_c2r_pipe(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw_all,
                             Flags* flags, cudaStream_t s);
 cudaError_t launch_cols_pipe(double2* H, const AxisGeom& g, int mode, const FusedSymbol& sym,
                              const double2* tw_all, cudaStream_t s);

@@ -46,7 +46,7 @@ struct PCfg {
 // ------------------------------------------------------------------ rows: R2C
 template <int M>
 __global__ void __launch_bounds__(PCfg<M>::TPL, PCfg<M>::MINB_ROW)
-k_r2c_pipe(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, i64 P,
+k_r2c_pipe(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, RowLayout lay,
            const double2* __restrict__ tw_all) {
     using C = PCfg<M>;
     using F = LineFFT<M, -1, true>;
@@ -75,7 +75,6 @@ k_r2c_pipe(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
 #pragma unroll
         for (int q = 0; q < C::R; ++q) line[swz(t + q * C::TPL)] = v[q];
         __syncthreads();
-        double2* dst = H + row * P;
 #pragma unroll
         for (int q = 0; q < C::R; ++q) {
             const int k = t + q * C::TPL;
@@ -84,8 +83,8 @@ k_r2c_pipe(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
             const double2 e = cscale(cadd(zk, zm), 0.5);
             const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
             const double2 w = __ldg(tw_all + 2 * M + k);
-            dst[k] = cadd(e, cmul(w, od));
-            if (k == 0) dst[M] = make_double2(zk.x - zk.y, 0.0);
+            H[lay.at(row, k)] = cadd(e, cmul(w, od));
+            if (k == 0) H[lay.at(row, M)] = make_double2(zk.x - zk.y, 0.0);
         }
         __syncthreads();
     }
@@ -95,7 +94,7 @@ k_r2c_pipe(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
 // ------------------------------------------------------------------ rows: C2R
 template <int M>
 __global__ void __launch_bounds__(PCfg<M>::TPL, PCfg<M>::MINB_ROW)
-k_c2r_pipe(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, i64 P,
+k_c2r_pipe(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, RowLayout lay,
            const double2* __restrict__ tw_all, Flags* flags) {
     using C = PCfg<M>;
     using F = LineFFT<M, +1, true>;
@@ -103,11 +102,10 @@ k_c2r_pipe(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
     __shared__ double2 nyq[2];
     const int t = threadIdx.x;
     auto issue = [&](i64 row, int s) {
-        const double2* src = H + row * P;
         double2* dst = sm + s * M;
 #pragma unroll
-        for (int q = 0; q < C::R; ++q) cp_async16(dst + swz(t + q * C::TPL), src + t + q * C::TPL);
-        if (t == 0) cp_async16(&nyq[s], src + M);
+        for (int q = 0; q < C::R; ++q) cp_async16(dst + swz(t + q * C::TPL), H + lay.at(row, t + q * C::TPL));
+        if (t == 0) cp_async16(&nyq[s], H + lay.at(row, M));
     };
     bool bad = false;
     i64 row = blockIdx.x;
@@ -166,8 +164,11 @@ k_cols_pipe(double2* H, AxisGeom g, FusedSymbol sym, const double2* __restrict__
     };
     auto valid = [&](i64 c) {
         if (c >= g.ncols) return false;
-        if (MODE == 2 && sym.rank == 3) return c - (c / sym.P) * sym.P <= sym.M;
-        if (MODE == 2) return c <= sym.M;
+        if (MODE == 2) {
+            i64 kx, ky;
+            fused_col_freqs(sym, c, kx, ky);
+            return kx <= sym.M;
+        }
         return true;
     };
     auto issue = [&](i64 tile, int s) {
@@ -189,11 +190,8 @@ k_cols_pipe(double2* H, AxisGeom g, FusedSymbol sym, const double2* __restrict__
         colof(tile, base, c);
         const bool ok = valid(c);
         if constexpr (MODE == 2) {
-            i64 ky = 0, kx = c;
-            if (sym.rank == 3) {
-                ky = c / sym.P;
-                kx = c - ky * sym.P;
-            }
+            i64 kx, ky;
+            fused_col_freqs(sym, c, kx, ky);
             for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
         }
         cp_wait<1>();
@@ -249,7 +247,7 @@ static int persistent_grid(K kernel, int threads, size_t smem, i64 ntiles) {
 }
 
 template <int M>
-static cudaError_t r2c_pipe_m(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
+static cudaError_t r2c_pipe_m(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw, cudaStream_t s) {
     const size_t smem = (size_t)2 * M * sizeof(double2);
     cudaFuncSetAttribute(k_r2c_pipe<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = persistent_grid(k_r2c_pipe<M>, PCfg<M>::TPL, smem, nrows);
@@ -258,7 +256,7 @@ static cudaError_t r2c_pipe_m(const double* x, double2* H, i64 nrows, i64 L, i64
 }
 
 template <int M>
-static cudaError_t c2r_pipe_m(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
+static cudaError_t c2r_pipe_m(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw, Flags* f,
                               cudaStream_t s) {
     const size_t smem = (size_t)2 * M * sizeof(double2);
     cudaFuncSetAttribute(k_c2r_pipe<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -291,7 +289,7 @@ bool pipe_enabled() {
 bool pipe_rows_ok(i64 M) { return M >= 512 && M <= 4096; }
 bool pipe_cols_ok(i64 N) { return N >= 1024 && N <= 4096; }
 
-cudaError_t launch_r2c_pipe(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
+cudaError_t launch_r2c_pipe(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw, cudaStream_t s) {
     switch (L / 2) {
         case 512: return r2c_pipe_m<512>(x, H, nrows, L, P, tw, s);
         case 1024: return r2c_pipe_m<1024>(x, H, nrows, L, P, tw, s);
@@ -301,7 +299,7 @@ cudaError_t launch_r2c_pipe(const double* x, double2* H, i64 nrows, i64 L, i64 P
     }
 }
 
-cudaError_t launch_c2r_pipe(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
+cudaError_t launch_c2r_pipe(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw, Flags* f,
                             cudaStream_t s) {
     switch (L / 2) {
         case 512: return c2r_pipe_m<512>(H, x, nrows, L, P, tw, f, s);

@@ -93,12 +93,9 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
     const i64 o = (i64)blockIdx.x / tiles;
     const i64 c0 = ((i64)blockIdx.x - o * tiles) * W;
     const i64 c = c0 + w;
-    i64 ky = 0, kx = c;
+    i64 kx = c, ky = 0;
     if constexpr (MODE == 2) {
-        if (sym.rank == 3) {
-            ky = c / sym.P;
-            kx = c - ky * sym.P;
-        }
+        fused_col_freqs(sym, c, kx, ky);
         // pitch-padding tiles of a 3D plane (W divides P, so a tile is all-padding or none)
         if (c0 - (c0 / sym.P) * sym.P > sym.M && sym.rank == 3) return;
     }
@@ -211,12 +208,9 @@ k_cols_tma_pers(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol
         const i64 c = c0 + w;
         double2* stg = tile + s * STAGE;
         if (live(c0)) {
-            i64 ky = 0, kx = c;
+            i64 kx = c, ky = 0;
             if constexpr (MODE == 2) {
-                if (sym.rank == 3) {
-                    ky = c / sym.P;
-                    kx = c - ky * sym.P;
-                }
+                fused_col_freqs(sym, c, kx, ky);
                 for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
             }
             mbar_wait(&bar[s], phase[s]);

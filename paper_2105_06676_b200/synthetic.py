@@ -18,9 +18,11 @@ from .fftstencil import GridShape, StencilKernel
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
 
 
-def splitmix64(seed: int, n: int) -> np.ndarray:
-    """n consecutive SplitMix64 outputs (vectorised; same stream as the reference)."""
-    i = np.arange(1, n + 1, dtype=np.uint64)
+def splitmix64(seed: int, n: int, start: int = 0) -> np.ndarray:
+    """SplitMix64 outputs start .. start+n-1 of the stream seeded with `seed`
+    (counter based: output i uses state seed + (i+1) * gamma), vectorised;
+    the same stream as the reference's sequential generator."""
+    i = np.arange(start + 1, start + n + 1, dtype=np.uint64)
     with np.errstate(over="ignore"):
         z = np.uint64(seed) + i * np.uint64(0x9E3779B97F4A7C15)
         z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
@@ -29,12 +31,12 @@ def splitmix64(seed: int, n: int) -> np.ndarray:
     return z
 
 
-def uniform01(seed: int, n: int) -> np.ndarray:
-    return (splitmix64(seed, n) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+def uniform01(seed: int, n: int, start: int = 0) -> np.ndarray:
+    return (splitmix64(seed, n, start) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
 
 
-def uniform_sym(seed: int, n: int) -> np.ndarray:
-    return 2.0 * uniform01(seed, n) - 1.0
+def uniform_sym(seed: int, n: int, start: int = 0) -> np.ndarray:
+    return 2.0 * uniform01(seed, n, start) - 1.0
 
 
 @dataclass
@@ -60,14 +62,15 @@ class Config:
     def cells(self) -> int:
         return int(np.prod(self.dims))
 
-    def initial(self) -> np.ndarray:
-        n = self.cells() * self.fields
+    def initial(self, start: int = 0, count: int | None = None) -> np.ndarray:
+        """Values start .. start+count-1 of the initial grid (storage order)."""
+        n = self.cells() * self.fields if count is None else count
         if self.init == "u01":
-            return uniform01(self.seed, n)
+            return uniform01(self.seed, n, start)
         if self.init == "sym":
-            return uniform_sym(self.seed, n)
+            return uniform_sym(self.seed, n, start)
         if self.init == "bumps":
-            return leapfrog_bumps(self.dims[0], self.seed + 1000)
+            return leapfrog_bumps(self.dims[0], self.seed + 1000)[start:start + n]
         raise ValueError(self.init)
 
     def scaled(self, dims) -> "Config":
