@@ -289,10 +289,16 @@ class DiagonalSpectrum:
         self.blocks[freq * m * m:(freq + 1) * m * m] = np.asarray(b, np.complex128).reshape(-1)
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the NULL stream's explicit handle
+
+
 def _opts(device: int = 0, path: int = 0, stream: int | None = None, stage_events: int = 0):
+    """fsx_options.  stream None -> the library's own stream; a handle of 0
+    (torch's default stream) is passed as cudaStreamLegacy so the work is
+    ordered with the caller's NULL-stream work instead of the library stream."""
     o = _lib.FsxOptions()
     o.device, o.path, o.stage_events = device, path, stage_events
-    o.stream = stream
+    o.stream = None if stream is None else (stream or CUDA_STREAM_LEGACY)
     return o
 
 
