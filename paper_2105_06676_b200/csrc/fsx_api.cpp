@@ -263,7 +263,8 @@ struct Plan {
     bool tma0 = false, tma1 = false;
     // kind 2
     i64 N1 = 1, N2 = 1, Mc = 0;
-    int t_M = -1, t_wk = -1;
+    i64 N1a = 0, N1b = 0;  // split column FFT (N1 > kMaxLine)
+    int t_M = -1, t_wk = -1, t_N1 = -1;
     fsx::AxisGeom colg;
     // kind 3
     std::vector<GenAxis> gax;
@@ -362,7 +363,8 @@ int choose_kind(const Plan& p, const Taps& taps, int force_general) {
         if (Mc <= 256) return kRowPair1D;
         const int b = ilog2(Mc);
         const int b2 = std::min(12, (b + 1) / 2);
-        if (b - b2 > ilog2(fsx::kMaxLine)) return kGeneral;
+        // column FFT of N1 = 2^(b-b2): one CTA up to 8192, a 2-level split up to 8192^2
+        if (b - b2 > 2 * ilog2(fsx::kMaxLine)) return kGeneral;
         return kRowPair1D;
     }
     return kGeneral;
@@ -444,15 +446,27 @@ Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general)
         }
         p->t_M = p->tables.add(make_phase(p->Mc));
         p->t_wk = p->tables.add(make_phase(p->m == 1 ? n : p->Mc));
-        p->tables.upload();
         p->colg.n = p->N1;
         p->colg.inner = p->N2;
         p->colg.outer = 1;
         p->colg.block = p->Mc;
         p->colg.ncols = p->N2;
+        int col_passes = p->N1 > 1 ? 1 : 0;
+        // FSX_COLSPLIT lowers the split threshold (tests exercise the 2^26 path small)
+        const char* cs = getenv("FSX_COLSPLIT");
+        const i64 max_col = cs ? std::max<i64>(4, atoll(cs)) : fsx::kMaxLine;
+        if (p->N1 > max_col) {
+            // the column FFT itself as a four-step split N1 = N1a x N1b
+            const int b1 = ilog2(p->N1);
+            p->N1b = i64(1) << ((b1 + 1) / 2);
+            p->N1a = p->N1 / p->N1b;
+            p->t_N1 = p->tables.add(make_phase(p->N1));
+            col_passes = 2;
+        }
+        p->tables.upload();
         p->fused_bytes = 2 * R;
-        p->alg_bytes = (p->N1 > 1 ? 6 : 2) * R + R;
-        p->launches = (p->N1 > 1 ? 3 : 1) + 1;
+        p->alg_bytes = (2 + 4 * col_passes) * R + R;
+        p->launches = 2 * col_passes + 1 + 1;
     } else {
         // general: complex Z of cells * m
         p->work.ensure((size_t)s.values() * sizeof(double2));
@@ -556,6 +570,8 @@ fsx::RowPairArgs rowpair_args(const Plan& p, const Taps& taps, u64 T, double2* z
         ++j;
     }
     a.ntaps = j;
+    a.real = symmetric_taps(taps) ? 1 : 0;
+    a.row_split = p.N1b;
     return a;
 }
 
@@ -697,14 +713,38 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
         tf.mode = 1;
         tf.col_div = 1;
         tf.tab = p.tables.get(p.t_M);
-        if (p.N1 > 1) FSX_CK(fsx::launch_axis_pow2(z, z, p.colg, -1, tf, tw, st));
+        // split column FFT: A over a (stride N1b N2) x W_N1^(b ka), then B over b
+        // (stride N2) x W_M^(n2 (ka + N1a kb)); rows end digit-reversed
+        const fsx::AxisGeom gA{p.N1a, p.N1b * p.N2, 1, p.Mc, p.N1b * p.N2};
+        const fsx::AxisGeom gB{p.N1b, p.N2, p.N1a, p.N1b * p.N2, p.N2};
+        fsx::StepTwiddle tA, tB;
+        if (p.N1a) {
+            tA.mode = 1;
+            tA.col_div = p.N2;
+            tA.tab = p.tables.get(p.t_N1);
+            tB.mode = 1;
+            tB.kmul = p.N1a;
+            tB.omul = 1;
+            tB.tab = p.tables.get(p.t_M);
+            FSX_CK(fsx::launch_axis_pow2(z, z, gA, -1, tA, tw, st));
+            FSX_CK(fsx::launch_axis_pow2(z, z, gB, -1, tB, tw, st));
+        } else if (p.N1 > 1) {
+            FSX_CK(fsx::launch_axis_pow2(z, z, p.colg, -1, tf, tw, st));
+        }
         sp.mark();
         const fsx::RowPairArgs a = rowpair_args(p, taps, T, z, dev);
         FSX_CK(fsx::launch_rowpair(a, st));
         sp.mark();
         fsx::StepTwiddle ti = tf;
         ti.mode = 2;
-        if (p.N1 > 1) FSX_CK(fsx::launch_axis_pow2(z, z, p.colg, +1, ti, tw, st));
+        if (p.N1a) {
+            tA.mode = 2;
+            tB.mode = 2;
+            FSX_CK(fsx::launch_axis_pow2(z, z, gB, +1, tB, tw, st));
+            FSX_CK(fsx::launch_axis_pow2(z, z, gA, +1, tA, tw, st));
+        } else if (p.N1 > 1) {
+            FSX_CK(fsx::launch_axis_pow2(z, z, p.colg, +1, ti, tw, st));
+        }
         FSX_CK(fsx::launch_finite_check(d_out, p.cells * p.m, flags, st));
         sp.mark();
     } else {

@@ -190,13 +190,15 @@ k_strided(const double2* in, double2* out, AxisGeom g, StepTwiddle st, const dou
     if constexpr (TWM == 2) {
         const i64 bq = c / st.col_div;
 #pragma unroll
-        for (int q = 0; q < C::R; ++q) v[q] = cmulc(v[q], phase_at(st.tab, bq * (i64)(t + q * C::TPL)));
+        for (int q = 0; q < C::R; ++q)
+            v[q] = cmulc(v[q], phase_at(st.tab, bq * ((i64)(t + q * C::TPL) * st.kmul + o * st.omul)));
     }
     F::run(v, t, sm + w * C::LSW, tw_all + N);
     if constexpr (TWM == 1) {
         const i64 bq = c / st.col_div;
 #pragma unroll
-        for (int q = 0; q < C::R; ++q) v[q] = cmul(v[q], phase_at(st.tab, bq * (i64)(t + q * C::TPL)));
+        for (int q = 0; q < C::R; ++q)
+            v[q] = cmul(v[q], phase_at(st.tab, bq * ((i64)(t + q * C::TPL) * st.kmul + o * st.omul)));
     }
     if (ok) {
 #pragma unroll
@@ -387,8 +389,14 @@ __device__ __forceinline__ void pair_mode0(const RowPairArgs& a, double2& zk, do
     const double2 wp = phase_at(a.wk, kp);
     const double2 xk = cadd(e, cmul(wk, od));
     const double2 xp = cadd(cconj(e), cmul(wp, cconj(od)));
-    const double2 yk = cscale(cmul(pow_scalar(sym1(a, k, L), a.T), xk), a.scale);
-    const double2 yp = cscale(cmul(pow_scalar(sym1(a, kp, L), a.T), xp), a.scale);
+    double2 yk, yp;
+    if (a.real) {
+        yk = cscale(xk, pow_realv(sym1(a, k, L).x, a.T) * a.scale);
+        yp = cscale(xp, pow_realv(sym1(a, kp, L).x, a.T) * a.scale);
+    } else {
+        yk = cscale(cmul(pow_scalar(sym1(a, k, L), a.T), xk), a.scale);
+        yp = cscale(cmul(pow_scalar(sym1(a, kp, L), a.T), xp), a.scale);
+    }
     const double2 cyp = cconj(yp), cyk = cconj(yk);
     zk = cadd(cadd(yk, cyp), cmul_si<+1>(cmulc(csub(yk, cyp), wk)));
     if (k != 0) zp = cadd(cadd(yp, cyk), cmul_si<+1>(cmulc(csub(yp, cyk), wp)));
@@ -398,6 +406,45 @@ __device__ __forceinline__ void pair_mode1(const RowPairArgs& a, double2& zk, do
     const double2 cz = cconj(zp);
     const double2 u = cscale(cadd(zk, cz), 0.5);
     const double2 vv = cscale(cmul_si<-1>(csub(zk, cz)), 0.5);
+    if (a.real) {
+        // symmetric block stencil: lam(k) = sum B cos(2 pi k o / N) is a real 2x2
+        // matrix; same binary-exponentiation loop in real arithmetic
+        double l00 = 0, l01 = 0, l10 = 0, l11 = 0;
+        for (int j = 0; j < a.ntaps; ++j) {
+            const double c = phase_at(a.wk, modp(k * (i64)a.tap_off[j], N)).x;
+            l00 = fma(a.tap_b[j][0], c, l00);
+            l01 = fma(a.tap_b[j][1], c, l01);
+            l10 = fma(a.tap_b[j][2], c, l10);
+            l11 = fma(a.tap_b[j][3], c, l11);
+        }
+        double a00 = 1, a01 = 0, a10 = 0, a11 = 1;
+        u64 t = a.T;
+        while (t) {
+            if (t & 1) {
+                const double b00 = fma(a00, l00, a01 * l10), b01 = fma(a00, l01, a01 * l11);
+                const double b10 = fma(a10, l00, a11 * l10), b11 = fma(a10, l01, a11 * l11);
+                a00 = b00;
+                a01 = b01;
+                a10 = b10;
+                a11 = b11;
+            }
+            t >>= 1;
+            if (t) {
+                const double s00 = fma(l00, l00, l01 * l10), s01 = fma(l00, l01, l01 * l11);
+                const double s10 = fma(l10, l00, l11 * l10), s11 = fma(l10, l01, l11 * l11);
+                l00 = s00;
+                l01 = s01;
+                l10 = s10;
+                l11 = s11;
+            }
+        }
+        const double sc = a.scale;
+        const double2 u2 = make_double2(sc * fma(a00, u.x, a01 * vv.x), sc * fma(a00, u.y, a01 * vv.y));
+        const double2 v2 = make_double2(sc * fma(a10, u.x, a11 * vv.x), sc * fma(a10, u.y, a11 * vv.y));
+        zk = cadd(u2, cmul_si<+1>(v2));
+        zp = cadd(cconj(u2), cmul_si<+1>(cconj(v2)));
+        return;
+    }
     double2 lam[2][2] = {{make_double2(0, 0), make_double2(0, 0)}, {make_double2(0, 0), make_double2(0, 0)}};
     for (int j = 0; j < a.ntaps; ++j) {
         const double2 e = cconj(phase_at(a.wk, modp(k * (i64)a.tap_off[j], N)));
@@ -429,7 +476,9 @@ k_rowpair(RowPairArgs a) {
     const i64 rb = (N1 - ra) % N1;
     const bool self = ra == rb;
     const int b = threadIdx.x / C::TPL, t = threadIdx.x % C::TPL;
-    const i64 row = b == 0 ? ra : rb;
+    const i64 fr = b == 0 ? ra : rb;  // frequency row k1
+    // storage row: k1 itself, or its digit-reversed position after a split column FFT
+    const i64 row = a.row_split ? (fr % (N1 / a.row_split)) * a.row_split + fr / (N1 / a.row_split) : fr;
     const bool ok = b == 0 || !self;
     double2* line = sm + b * LS;
     double2* src = a.z + row * N2;

@@ -30,9 +30,12 @@ struct PhaseTable {
 
 // Four-step twiddle applied around a strided pass: W_n^(b * k) with
 // b = column / col_div (the "n2" digit) and k the line position.
+// Exponent = (c / col_div) * (k * kmul + o * omul) for column c of outer
+// block o at line position k (kmul = 1, omul = 0: the plain four-step case).
 struct StepTwiddle {
     int mode = 0;  // 0 none, 1 post-multiply (forward), 2 pre-multiply by conj (inverse)
     i64 col_div = 1;
+    i64 kmul = 1, omul = 0;
     PhaseTable tab;
 };
 
@@ -126,6 +129,8 @@ struct RowPairArgs {
     double tap_b[kMaxFusedTaps][4];   // m x m block, row-major (m <= 2)
     u64 T = 1;
     double scale = 1.0;
+    int real = 0;        // symmetric taps: the (block) symbol is real
+    i64 row_split = 0;   // rows stored digit-reversed by a four-step split of N1 (= N1b), 0: natural
 };
 
 struct Flags {
