@@ -96,6 +96,13 @@ struct RowLayout {
     }
 };
 
+// compile-time layout selection for the hot row kernels (pitch: row * P + k)
+template <bool BLK>
+__host__ __device__ inline i64 row_at(const RowLayout& l, i64 row, i64 k) {
+    if constexpr (BLK) return l.at(row, k);
+    else return row * l.P + k;
+}
+
 // General spectral stage over a full complex spectrum with m fields.
 struct GeneralSymbol {
     int rank = 1;
@@ -175,6 +182,11 @@ cudaError_t launch_c2r_pipe(const double2* H, double* x, i64 nrows, i64 L, const
                             Flags* flags, cudaStream_t s);
 cudaError_t launch_cols_pipe(double2* H, const AxisGeom& g, int mode, const FusedSymbol& sym,
                              const double2* tw_all, cudaStream_t s);
+int rows_variant();
+cudaError_t launch_r2c_reg(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw_all,
+                           cudaStream_t s);
+cudaError_t launch_c2r_reg(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw_all,
+                           Flags* flags, cudaStream_t s);
 // TMA column passes (fsx_tma.cu); tensor_map points at a 64-byte aligned CUtensorMap
 bool tma_cols_ok(i64 N);
 int make_cols_tensor_map(void* out_map, void* base, const AxisGeom& g);

@@ -44,7 +44,7 @@ struct PCfg {
 };
 
 // ------------------------------------------------------------------ rows: R2C
-template <int M>
+template <int M, bool BLK>
 __global__ void __launch_bounds__(PCfg<M>::TPL, PCfg<M>::MINB_ROW)
 k_r2c_pipe(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, RowLayout lay,
            const double2* __restrict__ tw_all) {
@@ -83,8 +83,8 @@ k_r2c_pipe(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
             const double2 e = cscale(cadd(zk, zm), 0.5);
             const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
             const double2 w = __ldg(tw_all + 2 * M + k);
-            H[lay.at(row, k)] = cadd(e, cmul(w, od));
-            if (k == 0) H[lay.at(row, M)] = make_double2(zk.x - zk.y, 0.0);
+            H[row_at<BLK>(lay, row, k)] = cadd(e, cmul(w, od));
+            if (k == 0) H[row_at<BLK>(lay, row, M)] = make_double2(zk.x - zk.y, 0.0);
         }
         __syncthreads();
     }
@@ -92,7 +92,7 @@ k_r2c_pipe(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
 }
 
 // ------------------------------------------------------------------ rows: C2R
-template <int M>
+template <int M, bool BLK>
 __global__ void __launch_bounds__(PCfg<M>::TPL, PCfg<M>::MINB_ROW)
 k_c2r_pipe(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, RowLayout lay,
            const double2* __restrict__ tw_all, Flags* flags) {
@@ -104,8 +104,8 @@ k_c2r_pipe(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
     auto issue = [&](i64 row, int s) {
         double2* dst = sm + s * M;
 #pragma unroll
-        for (int q = 0; q < C::R; ++q) cp_async16(dst + swz(t + q * C::TPL), H + lay.at(row, t + q * C::TPL));
-        if (t == 0) cp_async16(&nyq[s], H + lay.at(row, M));
+        for (int q = 0; q < C::R; ++q) cp_async16(dst + swz(t + q * C::TPL), H + row_at<BLK>(lay, row, t + q * C::TPL));
+        if (t == 0) cp_async16(&nyq[s], H + row_at<BLK>(lay, row, M));
     };
     bool bad = false;
     i64 row = blockIdx.x;
@@ -140,6 +140,201 @@ k_c2r_pipe(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
     cp_wait<0>();
     const unsigned any = __ballot_sync(0xffffffffu, bad);
     if (any && (threadIdx.x & 31) == 0) atomicOr(&flags->nonfinite, 1u);
+}
+
+// ------------------------------------------------------------------ rows, register double buffer
+// Persistent row kernels that prefetch the NEXT row straight into a second
+// register array (plain LDG, no shared-memory staging): the row loads
+// overlap the current row's FFT, and the only shared-memory traffic left is
+// the FFT exchanges (the row passes were L1TEX-bound at ~1.5 wavefronts per
+// element with cp.async staging and a post-processing exchange).
+template <int M>
+struct RCfg {
+    static constexpr int TPL = M / 16;
+    static constexpr int MINB = TPL <= 128 ? 3 : 1;
+};
+
+// R2C split of pair (Zk, Zp) where Zp = Z[M - k] (k > 0); returns X[k].
+__device__ __forceinline__ double2 r2c_split(double2 zk, double2 zp, double2 wk) {
+    const double2 zm = cconj(zp);
+    const double2 e = cscale(cadd(zk, zm), 0.5);
+    const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
+    return cadd(e, cmul(wk, od));
+}
+
+template <int M>
+__global__ void __launch_bounds__(RCfg<M>::TPL, RCfg<M>::MINB)
+k_r2c_reg(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, RowLayout lay,
+          const double2* __restrict__ tw_all) {
+    using F = LineFFT<M, -1, false, true>;
+    constexpr int TPL = RCfg<M>::TPL, R = 16;
+    extern __shared__ double2 sm[];
+    const int t = threadIdx.x;
+    auto load = [&](i64 row, double2 (&v)[R]) {
+        const double2* src = reinterpret_cast<const double2*>(x + row * L);
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = src[t + q * TPL];
+    };
+    auto process = [&](i64 row, double2 (&v)[R]) {
+        F::run(v, t, sm, tw_all + M);
+        if constexpr (F::PAIRED) {
+            // v[i + 2u] = Z[item(i) + u M/8]; mirror M - k lives in this thread
+            const int j0 = t, j1 = t == 0 ? TPL : 2 * TPL - t;
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = (i == 0 ? j0 : j1) + u * (M / 8);
+                    const int qp = (1 - i) + 2 * (7 - u);                        // partner slot, t != 0
+                    const int qz = i == 0 ? 2 * ((8 - u) & 7) : 1 + 2 * (7 - u);  // partner slot, t == 0
+                    const double2 zk = v[i + 2 * u];
+                    const double2 zp = t == 0 ? v[qz] : v[qp];
+                    const double2 xk = r2c_split(zk, zp, __ldg(tw_all + 2 * M + k));
+                    H[lay.at(row, k)] = xk;
+                    if (i == 0 && u == 0 && t == 0) {
+                        H[lay.at(row, 0)] = make_double2(zk.x + zk.y, 0.0);
+                        H[lay.at(row, M)] = make_double2(zk.x - zk.y, 0.0);
+                    }
+                }
+        } else {
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < R; ++q) sm[swz(t + q * TPL)] = v[q];
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int k = t + q * TPL;
+                const double2 zk = v[q];
+                const double2 xk = r2c_split(zk, sm[swz((M - k) & (M - 1))], __ldg(tw_all + 2 * M + k));
+                H[lay.at(row, k)] = xk;
+                if (k == 0) H[lay.at(row, M)] = make_double2(zk.x - zk.y, 0.0);
+            }
+        }
+    };
+    double2 va[R], vb[R];
+    i64 row = blockIdx.x;
+    const i64 G = gridDim.x;
+    if (row < nrows) load(row, va);
+    for (; row < nrows; row += 2 * G) {
+        const i64 r1 = row + G;
+        if (r1 < nrows) load(r1, vb);
+        process(row, va);
+        if (r1 < nrows) {
+            if (r1 + G < nrows) load(r1 + G, va);
+            process(r1, vb);
+        }
+    }
+}
+
+template <int M>
+__global__ void __launch_bounds__(RCfg<M>::TPL, RCfg<M>::MINB)
+k_c2r_reg(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, RowLayout lay,
+          const double2* __restrict__ tw_all, Flags* flags) {
+    using F = LineFFT<M, +1>;
+    constexpr int TPL = RCfg<M>::TPL, R = 16;
+    extern __shared__ double2 sm[];
+    const int t = threadIdx.x;
+    bool bad = false;
+    auto load = [&](i64 row, double2 (&v)[R]) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = H[lay.at(row, t + q * TPL)];
+    };
+    auto process = [&](i64 row, double2 (&v)[R]) {
+        // mirror X[M - k] re-read through L1 (this CTA just streamed the row)
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int k = t + q * TPL;
+            const double2 xm = cconj(__ldg(H + lay.at(row, M - k)));
+            const double2 e = cadd(v[q], xm);
+            const double2 od = cmulc(csub(v[q], xm), __ldg(tw_all + 2 * M + k));
+            v[q] = cadd(e, cmul_si<+1>(od));
+        }
+        F::run(v, t, sm, tw_all + M);
+        double2* dst = reinterpret_cast<double2*>(x + row * L);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            dst[t + q * TPL] = v[q];
+            bad |= !isfinite(v[q].x) || !isfinite(v[q].y);
+        }
+    };
+    double2 va[R], vb[R];
+    i64 row = blockIdx.x;
+    const i64 G = gridDim.x;
+    if (row < nrows) load(row, va);
+    for (; row < nrows; row += 2 * G) {
+        const i64 r1 = row + G;
+        if (r1 < nrows) load(r1, vb);
+        process(row, va);
+        if (r1 < nrows) {
+            if (r1 + G < nrows) load(r1 + G, va);
+            process(r1, vb);
+        }
+    }
+    const unsigned any = __ballot_sync(0xffffffffu, bad);
+    if (any && (threadIdx.x & 31) == 0) atomicOr(&flags->nonfinite, 1u);
+}
+
+// FSX_ROWS: 0 = one-row-per-CTA kernels, 1 = cp.async staged (default, measured
+// fastest: cfg2 r2c 70 us / c2r 67 us), 2 = register double buffer (86 / 109 us)
+int rows_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_ROWS");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
+template <int M>
+static cudaError_t r2c_reg_m(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw,
+                             cudaStream_t s) {
+    const size_t smem = (size_t)M * sizeof(double2);
+    cudaFuncSetAttribute(k_r2c_reg<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_r2c_reg<M>, RCfg<M>::TPL, smem);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const i64 g = (i64)(per_sm < 1 ? 1 : per_sm) * sms;
+    k_r2c_reg<M><<<(int)(nrows < g ? nrows : g), RCfg<M>::TPL, smem, s>>>(x, H, nrows, L, P, tw);
+    return cudaGetLastError();
+}
+
+template <int M>
+static cudaError_t c2r_reg_m(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw,
+                             Flags* f, cudaStream_t s) {
+    const size_t smem = (size_t)M * sizeof(double2);
+    cudaFuncSetAttribute(k_c2r_reg<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_c2r_reg<M>, RCfg<M>::TPL, smem);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const i64 g = (i64)(per_sm < 1 ? 1 : per_sm) * sms;
+    k_c2r_reg<M><<<(int)(nrows < g ? nrows : g), RCfg<M>::TPL, smem, s>>>(H, x, nrows, L, P, tw, f);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_r2c_reg(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw,
+                           cudaStream_t s) {
+    switch (L / 2) {
+        case 512: return r2c_reg_m<512>(x, H, nrows, L, P, tw, s);
+        case 1024: return r2c_reg_m<1024>(x, H, nrows, L, P, tw, s);
+        case 2048: return r2c_reg_m<2048>(x, H, nrows, L, P, tw, s);
+        case 4096: return r2c_reg_m<4096>(x, H, nrows, L, P, tw, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_c2r_reg(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw,
+                           Flags* f, cudaStream_t s) {
+    switch (L / 2) {
+        case 512: return c2r_reg_m<512>(H, x, nrows, L, P, tw, f, s);
+        case 1024: return c2r_reg_m<1024>(H, x, nrows, L, P, tw, f, s);
+        case 2048: return c2r_reg_m<2048>(H, x, nrows, L, P, tw, f, s);
+        case 4096: return c2r_reg_m<4096>(H, x, nrows, L, P, tw, f, s);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 // ------------------------------------------------------------------ columns
@@ -249,9 +444,10 @@ static int persistent_grid(K kernel, int threads, size_t smem, i64 ntiles) {
 template <int M>
 static cudaError_t r2c_pipe_m(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw, cudaStream_t s) {
     const size_t smem = (size_t)2 * M * sizeof(double2);
-    cudaFuncSetAttribute(k_r2c_pipe<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int grid = persistent_grid(k_r2c_pipe<M>, PCfg<M>::TPL, smem, nrows);
-    k_r2c_pipe<M><<<grid, PCfg<M>::TPL, smem, s>>>(x, H, nrows, L, P, tw);
+    auto kf = P.blk ? k_r2c_pipe<M, true> : k_r2c_pipe<M, false>;
+    cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = persistent_grid(kf, PCfg<M>::TPL, smem, nrows);
+    kf<<<grid, PCfg<M>::TPL, smem, s>>>(x, H, nrows, L, P, tw);
     return cudaGetLastError();
 }
 
@@ -259,9 +455,10 @@ template <int M>
 static cudaError_t c2r_pipe_m(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw, Flags* f,
                               cudaStream_t s) {
     const size_t smem = (size_t)2 * M * sizeof(double2);
-    cudaFuncSetAttribute(k_c2r_pipe<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int grid = persistent_grid(k_c2r_pipe<M>, PCfg<M>::TPL, smem, nrows);
-    k_c2r_pipe<M><<<grid, PCfg<M>::TPL, smem, s>>>(H, x, nrows, L, P, tw, f);
+    auto kf = P.blk ? k_c2r_pipe<M, true> : k_c2r_pipe<M, false>;
+    cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = persistent_grid(kf, PCfg<M>::TPL, smem, nrows);
+    kf<<<grid, PCfg<M>::TPL, smem, s>>>(H, x, nrows, L, P, tw, f);
     return cudaGetLastError();
 }
 

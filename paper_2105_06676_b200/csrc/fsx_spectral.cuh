@@ -64,6 +64,52 @@ __device__ __forceinline__ double2 tap_term(const FusedSymbol& sym, const double
 // independent (memory-level parallelism instead of a latency chain).
 template <int N, int R, int TPL, class AC>
 __device__ __forceinline__ void spectral_regs(double2 (&v)[R], int t, const FusedSymbol& sym,
+                                              const double2* __restrict__ tw_all, AC acoef);
+
+// Element q of this thread is frequency k0 = kbase + q * kstride.
+template <int N, int R, class AC>
+__device__ __forceinline__ void spectral_regs_at(double2 (&v)[R], int kbase, int kstride, const FusedSymbol& sym,
+                                                 const double2* __restrict__ tw_all, AC acoef) {
+    if (sym.real) {
+        double lam[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) lam[q] = 0.0;
+        for (int gi = 0; gi < sym.ngroups; ++gi) {
+            const double2 a = acoef(gi);
+            const i64 og = sym.group_off[gi];
+            if (og == 0) {  // exp(0) = 1: no table read
+#pragma unroll
+                for (int q = 0; q < R; ++q) lam[q] += a.x;
+                continue;
+            }
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const double2 e = eplus_tab(tw_all, N, (i64)(kbase + q * kstride) * og);
+                lam[q] = fma(a.x, e.x, fma(-a.y, e.y, lam[q]));
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = cscale(v[q], pow_realv(lam[q], sym.T) * sym.scale);
+    } else {
+        double2 lam[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) lam[q] = make_double2(0.0, 0.0);
+        for (int gi = 0; gi < sym.ngroups; ++gi) {
+            const double2 a = acoef(gi);
+            const i64 og = sym.group_off[gi];
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const double2 e = eplus_tab(tw_all, N, (i64)(kbase + q * kstride) * og);
+                lam[q] = cadd(lam[q], cmul(a, e));
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = cscale(cmul(pow_complex(lam[q], sym.T), v[q]), sym.scale);
+    }
+}
+
+template <int N, int R, int TPL, class AC>
+__device__ __forceinline__ void spectral_regs(double2 (&v)[R], int t, const FusedSymbol& sym,
                                               const double2* __restrict__ tw_all, AC acoef) {
     if (sym.real) {
         double lam[R];
@@ -72,6 +118,11 @@ __device__ __forceinline__ void spectral_regs(double2 (&v)[R], int t, const Fuse
         for (int gi = 0; gi < sym.ngroups; ++gi) {
             const double2 a = acoef(gi);
             const i64 og = sym.group_off[gi];
+            if (og == 0) {
+#pragma unroll
+                for (int q = 0; q < R; ++q) lam[q] += a.x;
+                continue;
+            }
 #pragma unroll
             for (int q = 0; q < R; ++q) {
                 const double2 e = eplus_tab(tw_all, N, (i64)(t + q * TPL) * og);

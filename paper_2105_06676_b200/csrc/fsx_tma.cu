@@ -61,11 +61,11 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
-template <int N>
+template <int N, int WW = 0>
 struct TCfg {
     static constexpr int R = N < 16 ? N : 16;
     static constexpr int TPL = N / R;
-    static constexpr int W = N >= 4096 ? 1 : 4096 / N;   // adjacent columns per CTA (64 KB tile)
+    static constexpr int W = WW ? WW : (N >= 4096 ? 1 : 4096 / N);   // adjacent columns per CTA (64 KB tile)
     static constexpr int BOX = N < 256 ? N : 256;        // rows per TMA box
     static constexpr int NBOX = N / BOX;
     static constexpr int GW = W < 8 ? W : 8;
@@ -74,13 +74,15 @@ struct TCfg {
     static constexpr int MINB = NT <= 256 ? 2 : 1;
 };
 
+static int tma_w2();
+
 // MODE 0: forward C2C, 1: inverse C2C, 2: fused R2C spectral pass.
 // The TMA tile is [N rows][W columns] (row-major, as the boxes land); the
 // FFT exchanges reuse the same buffer as W line-major rows of LSW.
-template <int N, int MODE>
-__global__ void __launch_bounds__(TCfg<N>::NT, TCfg<N>::MINB)
+template <int N, int MODE, int WW = 0>
+__global__ void __launch_bounds__(TCfg<N, WW>::NT, TCfg<N, WW>::MINB)
 k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
-    using C = TCfg<N>;
+    using C = TCfg<N, WW>;
     constexpr int W = C::W;
     using FF = LineFFT<N, -1>;
     using FI = LineFFT<N, +1>;
@@ -116,7 +118,9 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
 #pragma unroll
     for (int q = 0; q < C::R; ++q) v[q] = tile[(t + q * C::TPL) * W + w];
     double2* line = tile + w * C::LSW;
-    if constexpr (MODE == 1) {
+    if constexpr (MODE == 3) {
+        // copy-only (measurement of the TMA column I/O alone)
+    } else if constexpr (MODE == 1) {
         FI::run(v, t, line, tw_all + N);
     } else {
         FF::run(v, t, line, tw_all + N);
@@ -146,6 +150,70 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
     }
 }
 
+// Fused spectral pass for 4096-point columns on the transposed four-step FFT
+// (Fft4096T): forward leaves the column in digit-transposed frequency order,
+// the symbol is evaluated in that order, and the inverse returns to natural
+// order -- one CTA-wide exchange per direction instead of two.
+__global__ void __launch_bounds__(256, 2)
+k_fused_tma4(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
+    constexpr int N = 4096;
+    extern __shared__ __align__(128) double2 tile[];
+    __shared__ __align__(8) unsigned long long bar;
+    __shared__ double2 acoef[kMaxGroups];
+    __shared__ double2 tapterm[kMaxFusedTaps];
+    const int t = threadIdx.x;
+    const i64 c = blockIdx.x;
+    i64 kx, ky;
+    fused_col_freqs(sym, c, kx, ky);
+    if (sym.rank == 3 && c - (c / sym.P) * sym.P > sym.M) return;
+    if (t == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        mbar_expect_tx(&bar, (unsigned)(N * sizeof(double2)));
+#pragma unroll 1
+        for (int b = 0; b < N / 256; ++b) tma_load_3d(tile + b * 256, &map, (int)(2 * c), b * 256, 0, &bar);
+    }
+    for (int j = t; j < sym.ntaps; j += 256) tapterm[j] = tap_term(sym, tw_all, j, kx, ky);
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    double2 v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = tile[t + 256 * q];
+    __syncthreads();  // tile consumed before the exchange overwrites it
+    Fft4096T::forward(v, t, tile, tw_all);
+    for (int gi = t; gi < sym.ngroups; gi += 256) {
+        double2 a = make_double2(0.0, 0.0);
+        for (int j = 0; j < sym.ntaps; ++j)
+            if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j]);
+        acoef[gi] = a;
+    }
+    __syncthreads();
+    spectral_regs_at<N, 16>(v, (t >> 4) + 16 * (t & 15), 256, sym, tw_all, [&](int gi) { return acoef[gi]; });
+    Fft4096T::inverse(v, t, tile, tw_all);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) tile[t + 256 * q] = v[q];
+    fence_proxy_async();
+    __syncthreads();
+    if (t == 0) {
+#pragma unroll 1
+        for (int b = 0; b < N / 256; ++b) tma_store_3d(&map, tile + b * 256, (int)(2 * c), b * 256, 0);
+        bulk_commit();
+        bulk_wait_read0();
+    }
+}
+
+// FSX_4STEP=1 selects k_fused_tma4 (measured slower on cfg2: 189 vs 165 us;
+// the transposed order scatters the symbol-table reads), default off.
+static int fused_4step() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_4STEP");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
 // Persistent variant: one CTA per SM walks the tiles with two shared-memory
 // stages; the TMA load of tile i+1 is in flight while tile i is transformed,
 // and a stage is refilled only after the bulk store that drained it has
@@ -160,7 +228,8 @@ k_cols_tma_pers(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol
     using FF = LineFFT<N, -1, true>;
     using FI = LineFFT<N, +1, true>;
     extern __shared__ __align__(128) double2 tile[];
-    __shared__ __align__(8) unsigned long long bar[2];
+    constexpr int NST = 3;  // stages: refilled stage's store was issued a full iteration earlier
+    __shared__ __align__(8) unsigned long long bar[NST];
     __shared__ double2 acoef[kMaxGroups][W];
     __shared__ double2 tapterm[MODE == 2 ? kMaxFusedTaps : 1][W];
     const int w = threadIdx.x % W, t = threadIdx.x / W;
@@ -189,19 +258,22 @@ k_cols_tma_pers(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol
             tma_load_3d(tile + s * STAGE + b * C::BOX * W, &map, (int)(2 * c0), b * C::BOX, (int)o, &bar[s]);
     };
     if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+#pragma unroll
+        for (int i = 0; i < NST; ++i) mbar_init(&bar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         if ((i64)blockIdx.x < ntiles) issue(blockIdx.x, 0);
     }
     __syncthreads();
-    unsigned phase[2] = {0u, 0u};
+    unsigned phase[NST] = {0u, 0u, 0u};
     int s = 0;
-    for (i64 tl = blockIdx.x; tl < ntiles; tl += gridDim.x, s ^= 1) {
+    for (i64 tl = blockIdx.x; tl < ntiles; tl += gridDim.x, s = (s + 1) % NST) {
         const i64 nxt = tl + gridDim.x;
+        const int ns = (s + 1) % NST;
         if (threadIdx.x == 0 && nxt < ntiles) {
-            bulk_wait_read0();  // the store of the tile that last used stage s^1 has read its smem
-            issue(nxt, s ^ 1);
+            // stage ns was last drained by the store issued two iterations ago;
+            // only the newest store group may still be reading shared memory
+            asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+            issue(nxt, ns);
         }
         i64 o, c0;
         pos(tl, o, c0);
@@ -218,7 +290,9 @@ k_cols_tma_pers(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol
 #pragma unroll
             for (int q = 0; q < C::R; ++q) v[q] = stg[(t + q * C::TPL) * W + w];
             double2* line = stg + w * C::LSW;
-            if constexpr (MODE == 1) {
+            if constexpr (MODE == 3) {
+                // copy-only (measurement of the TMA column I/O alone)
+            } else if constexpr (MODE == 1) {
                 FI::run(v, t, line, tw_all + N);
             } else {
                 FF::run(v, t, line, tw_all + N);
@@ -267,9 +341,9 @@ static int tma_persistent() {
 template <int N, int MODE>
 static cudaError_t cols_tma_n(const CUtensorMap& map, const AxisGeom& g, const FusedSymbol& sym, const double2* tw,
                               cudaStream_t s) {
-    if (tma_persistent() && 2 * TCfg<N>::W * TCfg<N>::LSW * 16 <= 220 * 1024) {
+    if (tma_persistent() && 3 * TCfg<N>::W * TCfg<N>::LSW * 16 <= 220 * 1024) {
         using C = TCfg<N>;
-        const size_t smem = (size_t)2 * C::W * C::LSW * sizeof(double2);
+        const size_t smem = (size_t)3 * C::W * C::LSW * sizeof(double2);
         const i64 ntiles = g.outer * ((g.ncols + C::W - 1) / C::W);
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
@@ -279,6 +353,16 @@ static cudaError_t cols_tma_n(const CUtensorMap& map, const AxisGeom& g, const F
         k_cols_tma_pers<N, MODE><<<grid, C::NT, smem, s>>>(map, g, sym, tw);
         return cudaGetLastError();
     }
+    if constexpr (N == 4096) {
+        if (tma_w2()) {
+            using C2 = TCfg<N, 2>;
+            const size_t smem = (size_t)C2::W * C2::LSW * sizeof(double2);
+            const i64 tiles = (g.ncols + C2::W - 1) / C2::W;
+            cudaFuncSetAttribute(k_cols_tma<N, MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_cols_tma<N, MODE, 2><<<(unsigned)(g.outer * tiles), C2::NT, smem, s>>>(map, g, sym, tw);
+            return cudaGetLastError();
+        }
+    }
     using C = TCfg<N>;
     const size_t smem = (size_t)C::W * C::LSW * sizeof(double2);
     const i64 tiles = (g.ncols + C::W - 1) / C::W;
@@ -287,15 +371,32 @@ static cudaError_t cols_tma_n(const CUtensorMap& map, const AxisGeom& g, const F
     return cudaGetLastError();
 }
 
+// FSX_TMA_W2=1: 2 columns (32 B rows) per 4096-point tile, 1 CTA/SM (measurement)
+static int tma_w2() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_TMA_W2");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
 // columns per TMA tile for a line length (the host builds the box to match)
-int tma_cols_width(i64 N) { return N >= 4096 ? 1 : (int)(4096 / N); }
+int tma_cols_width(i64 N) { return N == 4096 && tma_w2() ? 2 : (N >= 4096 ? 1 : (int)(4096 / N)); }
 
 bool tma_cols_ok(i64 N) { return N >= 512 && N <= 8192; }
 
 cudaError_t launch_cols_tma(const void* tensor_map, const AxisGeom& g, int mode, const FusedSymbol& sym,
                             const double2* tw, cudaStream_t s) {
     const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(tensor_map);
-#define FSX_TMA(N)                                                     \
+    if (getenv("FSX_TMA_COPYONLY") && g.n == 4096) return cols_tma_n<4096, 3>(map, g, sym, tw, s);  // measurement
+    if (mode == 2 && g.n == 4096 && g.outer == 1 && fused_4step()) {
+        const size_t smem = 4096 * sizeof(double2);
+        cudaFuncSetAttribute(k_fused_tma4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_fused_tma4<<<(unsigned)g.ncols, 256, smem, s>>>(map, g, sym, tw);
+        return cudaGetLastError();
+    }
+#define FSX_TMA(N)                                                    \
     case N:                                                            \
         return mode == 0 ? cols_tma_n<N, 0>(map, g, sym, tw, s)        \
              : mode == 1 ? cols_tma_n<N, 1>(map, g, sym, tw, s)        \
