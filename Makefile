@@ -13,10 +13,10 @@ all: $(LIB) oracle
 $(CSRC)/fsx_kernels.o: $(CSRC)/fsx_kernels.cu $(CSRC)/fsx_kernels.h $(CSRC)/fsx_device.cuh $(CSRC)/fsx_spectral.cuh
 	$(NVCC) $(NVFLAGS) -c $< -o $@ > build_ptxas.log 2>&1 || (cat build_ptxas.log; false)
 
-$(CSRC)/fsx_pipe.o: $(CSRC)/fsx_pipe.cu $(CSRC)/fsx_kernels.h $(CSRC)/fsx_device.cuh $(CSRC)/fsx_spectral.cuh
+$(CSRC)/fsx_pipe.o: $(CSRC)/fsx_pipe.cu $(CSRC)/fsx_kernels.h $(CSRC)/fsx_device.cuh $(CSRC)/fsx_spectral.cuh $(CSRC)/fsx_async.cuh
 	$(NVCC) $(NVFLAGS) -c $< -o $@ > build_ptxas_pipe.log 2>&1 || (cat build_ptxas_pipe.log; false)
 
-$(CSRC)/fsx_tma.o: $(CSRC)/fsx_tma.cu $(CSRC)/fsx_kernels.h $(CSRC)/fsx_device.cuh $(CSRC)/fsx_spectral.cuh
+$(CSRC)/fsx_tma.o: $(CSRC)/fsx_tma.cu $(CSRC)/fsx_kernels.h $(CSRC)/fsx_device.cuh $(CSRC)/fsx_spectral.cuh $(CSRC)/fsx_async.cuh
 	$(NVCC) $(NVFLAGS) -c $< -o $@ > build_ptxas_tma.log 2>&1 || (cat build_ptxas_tma.log; false)
 
 $(CSRC)/fsx_api.o: $(CSRC)/fsx_api.cpp $(CSRC)/fsx_kernels.h include/fsx.h

@@ -183,6 +183,10 @@ cudaError_t launch_c2r_pipe(const double2* H, double* x, i64 nrows, i64 L, const
 cudaError_t launch_cols_pipe(double2* H, const AxisGeom& g, int mode, const FusedSymbol& sym,
                              const double2* tw_all, cudaStream_t s);
 int rows_variant();
+cudaError_t launch_r2c_bulk(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw_all,
+                            cudaStream_t s);
+cudaError_t launch_c2r_bulk(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw_all,
+                            Flags* flags, cudaStream_t s);
 cudaError_t launch_r2c_reg(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw_all,
                            cudaStream_t s);
 cudaError_t launch_c2r_reg(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw_all,

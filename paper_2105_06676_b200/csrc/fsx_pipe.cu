@@ -15,6 +15,7 @@
 // complex (128 KB tiles) stay on the one-tile kernels in fsx_kernels.cu.
 #include <cstdlib>
 
+#include "fsx_async.cuh"
 #include "fsx_device.cuh"
 #include "fsx_kernels.h"
 #include "fsx_spectral.cuh"
@@ -138,6 +139,147 @@ k_c2r_pipe(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
         __syncthreads();
     }
     cp_wait<0>();
+    const unsigned any = __ballot_sync(0xffffffffu, bad);
+    if (any && (threadIdx.x & 31) == 0) atomicOr(&flags->nonfinite, 1u);
+}
+
+// ------------------------------------------------------------------ rows, bulk-copy staged
+// Same persistent two-stage structure, but the next row lands in shared
+// memory through ONE cp.async.bulk (the TMA engine moves it: no per-thread
+// cp.async, so neither the global read nor the shared-memory fill goes
+// through the LSU/L1 data pipe that bounds the row passes), and the R2C
+// split pairs k with M - k in registers where the FFT's last pass allows it
+// (LineFFT PAIRED: M = 2^(4a+3)), dropping the split exchange.  Pitch
+// layout only (element (row, k) at row * P + k).
+template <int M>
+__global__ void __launch_bounds__(PCfg<M>::TPL, PCfg<M>::MINB_ROW)
+k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, i64 P,
+           const double2* __restrict__ tw_all) {
+    using F = LineFFT<M, -1, true, true>;
+    constexpr int TPL = PCfg<M>::TPL, R = 16;
+    constexpr unsigned BYTES = M * sizeof(double2);
+    extern __shared__ __align__(128) double2 sm[];
+    __shared__ __align__(8) unsigned long long bar[2];
+    const int t = threadIdx.x;
+    const i64 G = gridDim.x;
+    i64 row = blockIdx.x;
+    if (t == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_init_fence();
+        if (row < nrows) {
+            mbar_expect_tx(&bar[0], BYTES);
+            bulk_load(sm, x + row * L, BYTES, &bar[0]);
+        }
+    }
+    __syncthreads();
+    unsigned par = 0;  // bit s: parity of the next completion of stage s
+    for (int s = 0; row < nrows; row += G, s ^= 1) {
+        const i64 nxt = row + G;
+        if (t == 0 && nxt < nrows) {
+            mbar_expect_tx(&bar[s ^ 1], BYTES);
+            bulk_load(sm + (s ^ 1) * M, x + nxt * L, BYTES, &bar[s ^ 1]);
+        }
+        mbar_wait(&bar[s], (par >> s) & 1u);
+        par ^= 1u << s;
+        double2* line = sm + s * M;
+        double2 v[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = line[t + q * TPL];
+        F::run(v, t, line, tw_all + M);
+        double2* h = H + row * P;
+        if constexpr (F::PAIRED) {
+            // v[i + 2u] = Z[item(i) + u M/8]; the mirror M - k lives in this thread
+            const int j1 = t == 0 ? TPL : 2 * TPL - t;
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = (i == 0 ? t : j1) + u * (M / 8);
+                    const int qp = (1 - i) + 2 * (7 - u);                        // partner slot, t != 0
+                    const int qz = i == 0 ? 2 * ((8 - u) & 7) : 1 + 2 * (7 - u);  // partner slot, t == 0
+                    const double2 zk = v[i + 2 * u];
+                    const double2 zm = cconj(t == 0 ? v[qz] : v[qp]);
+                    const double2 e = cscale(cadd(zk, zm), 0.5);
+                    const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
+                    h[k] = cadd(e, cmul(__ldg(tw_all + 2 * M + k), od));
+                    if (i == 0 && u == 0 && t == 0) h[M] = make_double2(zk.x - zk.y, 0.0);
+                }
+        } else {
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < R; ++q) line[swz(t + q * TPL)] = v[q];
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int k = t + q * TPL;
+                const double2 zk = v[q];
+                const double2 zm = cconj(line[swz((M - k) & (M - 1))]);
+                const double2 e = cscale(cadd(zk, zm), 0.5);
+                const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
+                h[k] = cadd(e, cmul(__ldg(tw_all + 2 * M + k), od));
+                if (k == 0) h[M] = make_double2(zk.x - zk.y, 0.0);
+            }
+        }
+        fence_proxy_async();  // generic writes of this stage before its next bulk fill
+        __syncthreads();
+    }
+}
+
+template <int M>
+__global__ void __launch_bounds__(PCfg<M>::TPL, PCfg<M>::MINB_ROW)
+k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, i64 P,
+           const double2* __restrict__ tw_all, Flags* flags) {
+    using F = LineFFT<M, +1, true>;
+    constexpr int TPL = PCfg<M>::TPL, R = 16;
+    constexpr int SS = M + 8;  // stage stride: M + 1 elements, 128 B aligned
+    constexpr unsigned BYTES = (M + 1) * sizeof(double2);
+    extern __shared__ __align__(128) double2 sm[];
+    __shared__ __align__(8) unsigned long long bar[2];
+    const int t = threadIdx.x;
+    const i64 G = gridDim.x;
+    bool bad = false;
+    i64 row = blockIdx.x;
+    if (t == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_init_fence();
+        if (row < nrows) {
+            mbar_expect_tx(&bar[0], BYTES);
+            bulk_load(sm, H + row * P, BYTES, &bar[0]);
+        }
+    }
+    __syncthreads();
+    unsigned par = 0;
+    for (int s = 0; row < nrows; row += G, s ^= 1) {
+        const i64 nxt = row + G;
+        if (t == 0 && nxt < nrows) {
+            mbar_expect_tx(&bar[s ^ 1], BYTES);
+            bulk_load(sm + (s ^ 1) * SS, H + nxt * P, BYTES, &bar[s ^ 1]);
+        }
+        mbar_wait(&bar[s], (par >> s) & 1u);
+        par ^= 1u << s;
+        double2* line = sm + s * SS;
+        double2 v[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int k = t + q * TPL;
+            const double2 xk = line[k];
+            const double2 xm = cconj(line[M - k]);
+            const double2 e = cadd(xk, xm);
+            const double2 od = cmulc(csub(xk, xm), __ldg(tw_all + 2 * M + k));
+            v[q] = cadd(e, cmul_si<+1>(od));
+        }
+        F::run(v, t, line, tw_all + M);
+        double2* dst = reinterpret_cast<double2*>(x + row * L);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            dst[t + q * TPL] = v[q];
+            bad |= !isfinite(v[q].x) || !isfinite(v[q].y);
+        }
+        fence_proxy_async();
+        __syncthreads();
+    }
     const unsigned any = __ballot_sync(0xffffffffu, bad);
     if (any && (threadIdx.x & 31) == 0) atomicOr(&flags->nonfinite, 1u);
 }
@@ -274,13 +416,14 @@ k_c2r_reg(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 
     if (any && (threadIdx.x & 31) == 0) atomicOr(&flags->nonfinite, 1u);
 }
 
-// FSX_ROWS: 0 = one-row-per-CTA kernels, 1 = cp.async staged (default, measured
-// fastest: cfg2 r2c 70 us / c2r 67 us), 2 = register double buffer (86 / 109 us)
+// FSX_ROWS: 0 = one-row-per-CTA kernels, 1 = cp.async staged (cfg2 r2c 70 us /
+// c2r 64 us), 2 = register double buffer (86 / 109 us), 3 = bulk-copy staged (default:
+// 67 / 63 us; cfg3 step 1.538 -> 1.466 ms)
 int rows_variant() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("FSX_ROWS");
-        v = e ? atoi(e) : 1;
+        v = e ? atoi(e) : 3;
     }
     return v;
 }
@@ -462,6 +605,25 @@ static cudaError_t c2r_pipe_m(const double2* H, double* x, i64 nrows, i64 L, con
     return cudaGetLastError();
 }
 
+template <int M>
+static cudaError_t r2c_bulk_m(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
+    const size_t smem = (size_t)2 * M * sizeof(double2);
+    cudaFuncSetAttribute(k_r2c_bulk<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = persistent_grid(k_r2c_bulk<M>, PCfg<M>::TPL, smem, nrows);
+    k_r2c_bulk<M><<<grid, PCfg<M>::TPL, smem, s>>>(x, H, nrows, L, P, tw);
+    return cudaGetLastError();
+}
+
+template <int M>
+static cudaError_t c2r_bulk_m(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
+                              cudaStream_t s) {
+    const size_t smem = (size_t)2 * (M + 8) * sizeof(double2);
+    cudaFuncSetAttribute(k_c2r_bulk<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = persistent_grid(k_c2r_bulk<M>, PCfg<M>::TPL, smem, nrows);
+    k_c2r_bulk<M><<<grid, PCfg<M>::TPL, smem, s>>>(H, x, nrows, L, P, tw, f);
+    return cudaGetLastError();
+}
+
 template <int N, int MODE>
 static cudaError_t cols_pipe_n(double2* H, const AxisGeom& g, const FusedSymbol& sym, const double2* tw, cudaStream_t s) {
     using C = PCfg<N>;
@@ -503,6 +665,27 @@ cudaError_t launch_c2r_pipe(const double2* H, double* x, i64 nrows, i64 L, const
         case 1024: return c2r_pipe_m<1024>(H, x, nrows, L, P, tw, f, s);
         case 2048: return c2r_pipe_m<2048>(H, x, nrows, L, P, tw, f, s);
         case 4096: return c2r_pipe_m<4096>(H, x, nrows, L, P, tw, f, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_r2c_bulk(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
+    switch (L / 2) {
+        case 512: return r2c_bulk_m<512>(x, H, nrows, L, P, tw, s);
+        case 1024: return r2c_bulk_m<1024>(x, H, nrows, L, P, tw, s);
+        case 2048: return r2c_bulk_m<2048>(x, H, nrows, L, P, tw, s);
+        case 4096: return r2c_bulk_m<4096>(x, H, nrows, L, P, tw, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_c2r_bulk(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
+                            cudaStream_t s) {
+    switch (L / 2) {
+        case 512: return c2r_bulk_m<512>(H, x, nrows, L, P, tw, f, s);
+        case 1024: return c2r_bulk_m<1024>(H, x, nrows, L, P, tw, f, s);
+        case 2048: return c2r_bulk_m<2048>(H, x, nrows, L, P, tw, f, s);
+        case 4096: return c2r_bulk_m<4096>(H, x, nrows, L, P, tw, f, s);
         default: return cudaErrorInvalidValue;
     }
 }
