@@ -309,10 +309,22 @@ Device& device_for(int ordinal) {
     d->ordinal = ordinal;
     FSX_CK(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
     // pow2 line twiddles: tw_all[N + x] = exp(-2 pi i x / N)
-    std::vector<double2> tw(2 * fsx::kMaxTwPow2);
-    tw[0] = make_double2(0, 0);
+    std::vector<double2> tw(fsx::kTwAllSize, make_double2(0, 0));
     for (i64 N = 1; N <= fsx::kMaxTwPow2; N <<= 1)
         for (i64 x = 0; x < N; ++x) tw[N + x] = expi_neg(x, N);
+    // per-pass gathered copies for LineFFT<N> (fsx_kernels.h, kPassTabBase)
+    for (i64 N = 16; N <= fsx::kMaxLine; N <<= 1) {
+        const int logn = ilog2(N), p16 = logn / 4, rem = logn % 4, npass = p16 + (rem > 0 ? 1 : 0);
+        i64 Ns = 1;
+        for (int S = 0; S < npass; ++S) {
+            const i64 r = S < p16 ? 16 : i64(1) << rem;
+            if (S > 0)
+                for (i64 u = 1; u < r; ++u)
+                    for (i64 k = 0; k < Ns; ++k)
+                        tw[fsx::kPassTabBase + 16 * N + 16 * Ns + (u - 1) * Ns + k] = tw[N + u * k * (N / (Ns * r))];
+            Ns *= r;
+        }
+    }
     d->tw_all.ensure(tw.size() * sizeof(double2));
     FSX_CK(cudaMemcpy(d->tw_all.p, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
     d->flags.ensure(sizeof(fsx::Flags));

@@ -13,7 +13,10 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
+
+#include "fsx_kernels.h"
 
 namespace fsx {
 
@@ -45,33 +48,47 @@ __device__ __forceinline__ double2 ctw(double2 a, double2 w) {
     return SIGN < 0 ? cmul(a, w) : cmulc(a, w);
 }
 
+// compile-time unrolled loop: f(std::integral_constant<int, I>) for I in [B, E)
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        static_for<B + 1, E>(f);
+    }
+}
+
 // ------------------------------------------------------------------ constant twiddles
-// cos(2 pi j / 16) for j = 0..4 (quarter wave); everything else by symmetry.
-__device__ __forceinline__ constexpr double cos16q(int j) {
+// cos(2 pi j / 32) for j = 0..8 (quarter wave); everything else by symmetry.
+__device__ __forceinline__ constexpr double cos32q(int j) {
     return j == 0 ? 1.0
-         : j == 1 ? 0.92387953251128673848
-         : j == 2 ? 0.70710678118654752440
-         : j == 3 ? 0.38268343236508977173
+         : j == 1 ? 0.98078528040323044913
+         : j == 2 ? 0.92387953251128673848
+         : j == 3 ? 0.83146961230254523708
+         : j == 4 ? 0.70710678118654752440
+         : j == 5 ? 0.55557023301960222474
+         : j == 6 ? 0.38268343236508977173
+         : j == 7 ? 0.19509032201612826785
                   : 0.0;
 }
 
-// Multiply a by exp(SIGN * 2 pi i * J / R) with J, R compile-time; the
-// trivial angles are folded to swaps/negations.
+// Multiply a by exp(SIGN * 2 pi i * J / R) with J, R compile-time (R divides
+// 32); the trivial angles are folded to swaps/negations.
 template <int J, int R, int SIGN>
 __device__ __forceinline__ double2 cmul_const(double2 a) {
-    constexpr int j16 = ((J * 16 / R) % 16 + 16) % 16;  // angle in sixteenths (R divides 16)
-    if constexpr (j16 == 0) return a;
-    else if constexpr (j16 == 8) return make_double2(-a.x, -a.y);
-    else if constexpr (j16 == 4) return cmul_si<SIGN>(a);
-    else if constexpr (j16 == 12) return cmul_si<-SIGN>(a);
+    static_assert(32 % R == 0, "cmul_const: R must divide 32");
+    constexpr int j32 = ((J * 32 / R) % 32 + 32) % 32;  // angle in 32nds
+    if constexpr (j32 == 0) return a;
+    else if constexpr (j32 == 16) return make_double2(-a.x, -a.y);
+    else if constexpr (j32 == 8) return cmul_si<SIGN>(a);
+    else if constexpr (j32 == 24) return cmul_si<-SIGN>(a);
     else {
-        // exp(i theta) with theta = 2 pi j16 / 16 (then conj for SIGN = -1)
-        constexpr int q = j16 % 4, quad = j16 / 4;
-        constexpr double c0 = cos16q(q), s0 = cos16q(4 - q);  // cos, sin in the first quadrant
+        // exp(i theta) with theta = 2 pi j32 / 32 (then conj for SIGN = -1)
+        constexpr int q = j32 % 8, quad = j32 / 8;
+        constexpr double c0 = cos32q(q), s0 = cos32q(8 - q);  // cos, sin in the first quadrant
         constexpr double c = quad == 0 ? c0 : quad == 1 ? -s0 : quad == 2 ? -c0 : s0;
         constexpr double s = quad == 0 ? s0 : quad == 1 ? c0 : quad == 2 ? -s0 : -c0;
         constexpr double ss = SIGN < 0 ? -s : s;
-        if constexpr (q == 2) {
+        if constexpr (q == 4) {
             // c, s = +-1/sqrt2
             return make_double2(c * a.x - ss * a.y, c * a.y + ss * a.x);
         } else {
@@ -182,7 +199,9 @@ __device__ __forceinline__ int swz(int p) { return p ^ (((p >> 3) ^ (p >> 4)) & 
 // then has its mirror N - p in the same thread, which lets a real-to-complex
 // split run in registers.  Output convention with PAIR: v[i + u * 2] holds
 // X[item(t, i) + u * N / 8].
-template <int N, int SIGN, bool PF = false, bool PAIR = false>
+// FT: read every twiddle of a pass from the gathered table (no derived
+// products: fewer FP64 instructions, more L1 loads) -- for compute-bound callers.
+template <int N, int SIGN, bool PF = false, bool PAIR = false, bool FT = false>
 struct LineFFT {
     static constexpr int LOGN = ilog2c(N);
     static constexpr int R = N < 16 ? N : 16;
@@ -208,23 +227,30 @@ struct LineFFT {
         else return t + i * TPL;
     }
 
-    // twiddles of pass S for this thread: w[i * r + u] = W_{Ns r}^{u k(i)}, u >= 1.
-    // Only the power-of-two exponents u = 1, 2, 4, 8 are read from the exact
-    // table; the others are products of at most two loaded/derived values
-    // (<= 3 roundings), which cuts the L1 traffic of the twiddles ~4x.
+    // twiddles of pass S for this thread: w[i * r + u] = W_{Ns r}^{u k(i)}, u >= 1,
+    // from the per-pass gathered table (kPassTabBase: row u - 1, contiguous in
+    // k, so a warp's load touches consecutive lines instead of one line per
+    // thread).  Without FT only the power-of-two exponents u = 1, 2, 4, 8 are
+    // read; the others are products of at most two loaded/derived values
+    // (<= 3 roundings).
     template <int S>
     __device__ __forceinline__ static void load_tw(int t, const double2* __restrict__ tw, double2 (&w)[R]) {
         constexpr int r = radix<S>();
         constexpr int Ns = ns<S>();
         constexpr int C = R / r;
-        constexpr int STEP = N / (Ns * r);
         if constexpr (Ns > 1) {
 #pragma unroll
             for (int i = 0; i < C; ++i) {
                 const int k = item<S>(t, i) & (Ns - 1);
                 double2* wi = w + i * r;
+                const double2* pt = tw + (kPassTabBase + 15 * N + 16 * Ns);  // tw = tw_all + N
+                if constexpr (FT) {
 #pragma unroll
-                for (int u = 1; u < r; u <<= 1) wi[u] = __ldg(tw + u * k * STEP);
+                    for (int u = 1; u < r; ++u) wi[u] = __ldg(pt + (u - 1) * Ns + k);
+                    continue;
+                }
+#pragma unroll
+                for (int u = 1; u < r; u <<= 1) wi[u] = __ldg(pt + (u - 1) * Ns + k);
                 if constexpr (r >= 4) wi[3] = cmul(wi[1], wi[2]);
                 if constexpr (r >= 8) {
                     wi[5] = cmul(wi[1], wi[4]);

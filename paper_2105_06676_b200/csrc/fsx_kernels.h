@@ -17,6 +17,13 @@ constexpr int kMaxRank = 8;
 constexpr int kMaxFusedTaps = 64;
 constexpr int kMaxGroups = 16;
 constexpr int kMaxDirect = 12288;   // direct-DFT line limit (non-pow2 axes)
+// Twiddle buffer layout (tw_all, one per device):
+//   tw_all[N + x] = exp(-2 pi i x / N)                   pow2 N <= kMaxTwPow2
+//   tw_all[kPassTabBase + 16 N + 16 Ns + (u - 1) Ns + k]  LineFFT<N> pass twiddles
+//       = exp(-2 pi i u k / (Ns r))  (pass with span Ns and radix r, 1 <= u < r,
+//       k < Ns): the same exact values gathered so a warp's loads are contiguous
+constexpr long long kPassTabBase = 2LL * kMaxTwPow2;
+constexpr long long kTwAllSize = kPassTabBase + 32LL * kMaxLine;
 
 // exp(-2 pi i x / n) for any x in [0, n): lo[x & mask] * hi[x >> shift]
 // (shift == 0: a single full table lo[x]).

@@ -189,37 +189,41 @@ k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
         F::run(v, t, line, tw_all + M);
         double2* h = H + row * P;
         if constexpr (F::PAIRED) {
-            // v[i + 2u] = Z[item(i) + u M/8]; the mirror M - k lives in this thread
+            // v[i + 2u] = Z[item(i) + u M/8]; the mirror M - k lives in this thread.
+            // Split twiddle W_L^(j + u M/8) = W_L^j * W_16^u: one load per item.
             const int j1 = t == 0 ? TPL : 2 * TPL - t;
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int k = (i == 0 ? t : j1) + u * (M / 8);
+            for (int i = 0; i < 2; ++i) {
+                const int j = i == 0 ? t : j1;
+                const double2 wj = __ldg(tw_all + 2 * M + j);
+                static_for<0, 8>([&](auto U) {
+                    constexpr int u = decltype(U)::value;
                     const int qp = (1 - i) + 2 * (7 - u);                        // partner slot, t != 0
                     const int qz = i == 0 ? 2 * ((8 - u) & 7) : 1 + 2 * (7 - u);  // partner slot, t == 0
                     const double2 zk = v[i + 2 * u];
                     const double2 zm = cconj(t == 0 ? v[qz] : v[qp]);
                     const double2 e = cscale(cadd(zk, zm), 0.5);
                     const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
-                    h[k] = cadd(e, cmul(__ldg(tw_all + 2 * M + k), od));
+                    h[j + u * (M / 8)] = cadd(e, cmul(cmul_const<u, 16, -1>(wj), od));
                     if (i == 0 && u == 0 && t == 0) h[M] = make_double2(zk.x - zk.y, 0.0);
-                }
+                });
+            }
         } else {
             __syncthreads();
 #pragma unroll
             for (int q = 0; q < R; ++q) line[swz(t + q * TPL)] = v[q];
             __syncthreads();
-#pragma unroll
-            for (int q = 0; q < R; ++q) {
+            const double2 wt = __ldg(tw_all + 2 * M + t);  // W_L^(t + q M/16) = W_L^t * W_32^q
+            static_for<0, R>([&](auto Q) {
+                constexpr int q = decltype(Q)::value;
                 const int k = t + q * TPL;
                 const double2 zk = v[q];
                 const double2 zm = cconj(line[swz((M - k) & (M - 1))]);
                 const double2 e = cscale(cadd(zk, zm), 0.5);
                 const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
-                h[k] = cadd(e, cmul(__ldg(tw_all + 2 * M + k), od));
+                h[k] = cadd(e, cmul(cmul_const<q, 32, -1>(wt), od));
                 if (k == 0) h[M] = make_double2(zk.x - zk.y, 0.0);
-            }
+            });
         }
         fence_proxy_async();  // generic writes of this stage before its next bulk fill
         __syncthreads();
@@ -261,15 +265,17 @@ k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
         par ^= 1u << s;
         double2* line = sm + s * SS;
         double2 v[R];
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
+        // split twiddle W_L^(t + q M/16) = W_L^t * W_32^q: one load per thread
+        const double2 wt = __ldg(tw_all + 2 * M + t);
+        static_for<0, R>([&](auto Q) {
+            constexpr int q = decltype(Q)::value;
             const int k = t + q * TPL;
             const double2 xk = line[k];
             const double2 xm = cconj(line[M - k]);
             const double2 e = cadd(xk, xm);
-            const double2 od = cmulc(csub(xk, xm), __ldg(tw_all + 2 * M + k));
+            const double2 od = cmulc(csub(xk, xm), cmul_const<q, 32, -1>(wt));
             v[q] = cadd(e, cmul_si<+1>(od));
-        }
+        });
         F::run(v, t, line, tw_all + M);
         double2* dst = reinterpret_cast<double2*>(x + row * L);
 #pragma unroll

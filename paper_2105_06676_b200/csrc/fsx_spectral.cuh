@@ -50,6 +50,94 @@ __device__ __forceinline__ double pow_realv(double lam, u64 T) {
     return acc;
 }
 
+// Element-parallel versions of pow_realv / pow_complex (same operation order
+// per element, so bitwise identical): the loop over the bits of T is uniform,
+// and CH independent elements per step give the FP64 pipe CH-way ILP instead
+// of one latency chain per element.
+template <int R, int CH = R>
+__device__ __forceinline__ void pow_real_vec(double (&x)[R], u64 T) {
+    static_assert(R % CH == 0, "chunk must divide R");
+#pragma unroll
+    for (int c = 0; c < R; c += CH) {
+        double acc[CH];
+        bool zero[CH];
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+            zero[q] = negligible_power(x[c + q] * x[c + q], T);
+            acc[q] = 1.0;
+        }
+        u64 t = T;
+        while (t) {
+            if (t & 1) {
+#pragma unroll
+                for (int q = 0; q < CH; ++q) acc[q] *= x[c + q];
+            }
+            t >>= 1;
+            if (t) {
+#pragma unroll
+                for (int q = 0; q < CH; ++q) x[c + q] *= x[c + q];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < CH; ++q) x[c + q] = zero[q] ? 0.0 : acc[q];
+    }
+}
+
+template <int R, int CH = R>
+__device__ __forceinline__ void pow_complex_vec(double2 (&x)[R], u64 T) {
+    static_assert(R % CH == 0, "chunk must divide R");
+#pragma unroll
+    for (int c = 0; c < R; c += CH) {
+        double2 acc[CH];
+        bool zero[CH];
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+            const double2 l = x[c + q];
+            zero[q] = negligible_power(fma(l.x, l.x, l.y * l.y), T);
+            acc[q] = make_double2(1.0, 0.0);
+        }
+        u64 t = T;
+        while (t) {
+            if (t & 1) {
+#pragma unroll
+                for (int q = 0; q < CH; ++q) acc[q] = cmul(acc[q], x[c + q]);
+            }
+            t >>= 1;
+            if (t) {
+#pragma unroll
+                for (int q = 0; q < CH; ++q) {
+                    const double2 sq = x[c + q];
+                    x[c + q] = make_double2(fma(sq.x, sq.x, -sq.y * sq.y), (sq.x + sq.x) * sq.y);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < CH; ++q) x[c + q] = zero[q] ? make_double2(0.0, 0.0) : acc[q];
+    }
+}
+
+// Real symbol lam(k0) for k0 = t + q * TPL (no power, no scale).
+template <int N, int R, int TPL, class AC>
+__device__ __forceinline__ void symbol_real(double (&lam)[R], int t, const FusedSymbol& sym,
+                                            const double2* __restrict__ tw_all, AC acoef) {
+#pragma unroll
+    for (int q = 0; q < R; ++q) lam[q] = 0.0;
+    for (int gi = 0; gi < sym.ngroups; ++gi) {
+        const double2 a = acoef(gi);
+        const i64 og = sym.group_off[gi];
+        if (og == 0) {  // exp(0) = 1: no table read
+#pragma unroll
+            for (int q = 0; q < R; ++q) lam[q] += a.x;
+            continue;
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const double2 e = eplus_tab(tw_all, N, (i64)(t + q * TPL) * og);
+            lam[q] = fma(a.x, e.x, fma(-a.y, e.y, lam[q]));
+        }
+    }
+}
+
 // One tap's contribution to the per-column group coefficient:
 // c * exp(+2 pi i (kx o_last / L + ky o1 / n1)).
 __device__ __forceinline__ double2 tap_term(const FusedSymbol& sym, const double2* tw_all, int j, i64 kx, i64 ky) {

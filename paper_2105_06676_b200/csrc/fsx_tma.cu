@@ -36,6 +36,10 @@ struct TCfg {
     static constexpr int LSW = GW > 1 ? N + 8 / GW : N;  // exchange line stride (bank padding)
     static constexpr int NT = W * TPL;
     static constexpr int MINB = NT <= 256 ? 2 : 1;
+    static constexpr bool PRE = N <= 4096;                // fused mode: real multipliers in smem
+    static constexpr size_t smem(int mode) {
+        return (size_t)W * LSW * 16 + (mode == 2 && PRE ? (size_t)NT * R * 8 : 0);
+    }
 };
 
 static int tma_w2();
@@ -48,8 +52,11 @@ __global__ void __launch_bounds__(TCfg<N, WW>::NT, TCfg<N, WW>::MINB)
 k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
     using C = TCfg<N, WW>;
     constexpr int W = C::W;
-    using FF = LineFFT<N, -1>;
-    using FI = LineFFT<N, +1>;
+    // full twiddle tables for the multi-column tiles (N < 4096); the one-column
+    // 4096 tiles measured faster with derived twiddles (cfg2 158 vs 165 us)
+    constexpr bool FT = N < 4096;
+    using FF = LineFFT<N, -1, false, false, FT>;
+    using FI = LineFFT<N, +1, false, false, FT>;
     extern __shared__ __align__(128) double2 tile[];
     __shared__ __align__(8) unsigned long long bar;
     __shared__ double2 acoef[kMaxGroups][W];
@@ -73,10 +80,33 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
         for (int b = 0; b < C::NBOX; ++b)
             tma_load_3d(tile + b * C::BOX * W, &map, (int)(2 * c0), b * C::BOX, (int)o, &bar);
     }
+    // MODE 2, real symbol: lam(k0)^T * scale for this thread's 16 frequencies is
+    // data independent -- computed while the tile is in flight and parked in
+    // shared memory (mult[q * NT + thread], thread-private) for after the FFT.
+    // Not for the 128 KB tiles (N = 8192): the extra 64 KB would squeeze the
+    // L1 that serves the table reads (cfg3 measured 0.87 -> 1.04 ms).
+    constexpr bool PRE = MODE == 2 && C::PRE;
+    double* mult = reinterpret_cast<double*>(tile + W * C::LSW);
     if constexpr (MODE == 2) {
         for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
     }
-    __syncthreads();  // barrier initialised before anyone waits on it
+    __syncthreads();  // barrier initialised before anyone waits on it; tap terms visible
+    if constexpr (MODE == 2) {
+        for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
+            double2 a = make_double2(0.0, 0.0);
+            for (int j = 0; j < sym.ntaps; ++j)
+                if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j][w]);
+            acoef[gi][w] = a;
+        }
+        __syncthreads();
+        if (PRE && sym.real) {
+            double lam[C::R];
+            symbol_real<N, C::R, C::TPL>(lam, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
+            pow_real_vec<C::R>(lam, sym.T);
+#pragma unroll
+            for (int q = 0; q < C::R; ++q) mult[q * C::NT + threadIdx.x] = lam[q] * sym.scale;
+        }
+    }
     mbar_wait(&bar, 0);
     double2 v[C::R];
 #pragma unroll
@@ -90,15 +120,12 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
         FF::run(v, t, line, tw_all + N);
     }
     if constexpr (MODE == 2) {
-        __syncthreads();
-        for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
-            double2 a = make_double2(0.0, 0.0);
-            for (int j = 0; j < sym.ntaps; ++j)
-                if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j][w]);
-            acoef[gi][w] = a;
+        if (PRE && sym.real) {
+#pragma unroll
+            for (int q = 0; q < C::R; ++q) v[q] = cscale(v[q], mult[q * C::NT + threadIdx.x]);
+        } else {
+            spectral_regs<N, C::R, C::TPL>(v, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
         }
-        __syncthreads();
-        spectral_regs<N, C::R, C::TPL>(v, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
         FI::run(v, t, line, tw_all + N);
     }
     __syncthreads();  // last exchange reads done before the tile is overwritten
@@ -320,7 +347,7 @@ static cudaError_t cols_tma_n(const CUtensorMap& map, const AxisGeom& g, const F
     if constexpr (N == 4096) {
         if (tma_w2()) {
             using C2 = TCfg<N, 2>;
-            const size_t smem = (size_t)C2::W * C2::LSW * sizeof(double2);
+            const size_t smem = C2::smem(MODE);
             const i64 tiles = (g.ncols + C2::W - 1) / C2::W;
             cudaFuncSetAttribute(k_cols_tma<N, MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             k_cols_tma<N, MODE, 2><<<(unsigned)(g.outer * tiles), C2::NT, smem, s>>>(map, g, sym, tw);
@@ -328,7 +355,8 @@ static cudaError_t cols_tma_n(const CUtensorMap& map, const AxisGeom& g, const F
         }
     }
     using C = TCfg<N>;
-    const size_t smem = (size_t)C::W * C::LSW * sizeof(double2);
+    // tile + (fused mode) the per-frequency real multipliers
+    const size_t smem = C::smem(MODE);
     const i64 tiles = (g.ncols + C::W - 1) / C::W;
     cudaFuncSetAttribute(k_cols_tma<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_cols_tma<N, MODE><<<(unsigned)(g.outer * tiles), C::NT, smem, s>>>(map, g, sym, tw);
