@@ -13,6 +13,10 @@
 // See DESIGN.md for the data layout and the roofline of each kernel.
 #include <cfloat>
 
+#include <map>
+#include <mutex>
+
+#include "fsx_async.cuh"
 #include "fsx_device.cuh"
 #include "fsx_kernels.h"
 #include "fsx_spectral.cuh"
@@ -816,7 +820,7 @@ static cudaError_t axis_pow2_n(const double2* in, double2* out, const AxisGeom& 
         const size_t smem = (size_t)C::LINES * C::LSL * sizeof(double2);
         const int blocks = (int)((g.outer + C::LINES - 1) / C::LINES);
         auto kf = sign < 0 ? k_contig<N, -1> : k_contig<N, +1>;
-        cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kernel_prepare((const void*)kf, smem);
         kf<<<blocks, C::LINES * C::TPL, smem, s>>>(in, out, g.outer, g.block, tw);
         return cudaGetLastError();
     }
@@ -826,7 +830,7 @@ static cudaError_t axis_pow2_n(const double2* in, double2* out, const AxisGeom& 
     void (*kf)(const double2*, double2*, AxisGeom, StepTwiddle, const double2*);
     if (sign < 0) kf = st.mode == 1 ? k_strided<N, -1, 1> : st.mode == 2 ? k_strided<N, -1, 2> : k_strided<N, -1, 0>;
     else kf = st.mode == 1 ? k_strided<N, +1, 1> : st.mode == 2 ? k_strided<N, +1, 2> : k_strided<N, +1, 0>;
-    cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_prepare((const void*)kf, smem);
     kf<<<(unsigned)blocks, C::W * C::TPL, smem, s>>>(in, out, g, st, tw);
     return cudaGetLastError();
 }
@@ -858,7 +862,7 @@ cudaError_t launch_axis_pow2(const double2* in, double2* out, const AxisGeom& g,
 cudaError_t launch_axis_direct(const double2* in, double2* out, const AxisGeom& g, int sign,
                                const PhaseTable& tab, cudaStream_t s) {
     const size_t smem = (size_t)g.n * sizeof(double2);
-    cudaFuncSetAttribute(k_direct_dft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_prepare((const void*)k_direct_dft, smem);
     const i64 lines = g.outer * g.ncols;
     k_direct_dft<<<(unsigned)lines, 256, smem, s>>>(in, out, g, sign, tab);
     return cudaGetLastError();
@@ -869,7 +873,7 @@ static cudaError_t r2c_m(const double* x, double2* H, i64 nrows, i64 L, const Ro
                          cudaStream_t s) {
     using C = Cfg<M>;
     const size_t smem = (size_t)C::LINES * C::LSL * sizeof(double2);
-    cudaFuncSetAttribute(k_r2c_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_prepare((const void*)k_r2c_rows<M>, smem);
     k_r2c_rows<M><<<(unsigned)((nrows + C::LINES - 1) / C::LINES), C::LINES * C::TPL, smem, s>>>(x, H, nrows, L, P, tw);
     return cudaGetLastError();
 }
@@ -879,9 +883,40 @@ static cudaError_t c2r_m(const double2* H, double* x, i64 nrows, i64 L, const Ro
                          cudaStream_t s) {
     using C = Cfg<M>;
     const size_t smem = (size_t)C::LINES * C::LSL * sizeof(double2);
-    cudaFuncSetAttribute(k_c2r_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_prepare((const void*)k_c2r_rows<M>, smem);
     k_c2r_rows<M><<<(unsigned)((nrows + C::LINES - 1) / C::LINES), C::LINES * C::TPL, smem, s>>>(H, x, nrows, L, P, tw, f);
     return cudaGetLastError();
+}
+
+bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+int kernel_prepare(const void* fn, size_t smem, int threads) {
+    struct Info {
+        size_t smem = 0;
+        int threads = -1, per_sm = 0;
+    };
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, Info> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    Info& e = cache[{fn, dev}];
+    if (e.smem != smem || e.threads != threads) {
+        // always (static + dynamic > 48 KB needs the opt-in even when dynamic alone is below it)
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e.per_sm = 0;
+        if (threads > 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&e.per_sm, fn, threads, smem);
+        e.smem = smem;
+        e.threads = threads;
+    }
+    return e.per_sm;
 }
 
 #define FSX_POW2_CASES(MACRO) \
@@ -921,7 +956,7 @@ static cudaError_t fused_nw(double2* H, const AxisGeom& g, const FusedSymbol& sy
     constexpr int LSW = GW > 1 ? N + 8 / GW : N;
     const size_t smem = (size_t)W * LSW * sizeof(double2);
     const i64 tiles = (g.ncols + W - 1) / W;
-    cudaFuncSetAttribute(k_fused_r2c<N, W, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_prepare((const void*)k_fused_r2c<N, W, MINB>, smem);
     k_fused_r2c<N, W, MINB><<<(unsigned)(g.outer * tiles), W * Cfg<N>::TPL, smem, s>>>(H, g, sym, tw);
     return cudaGetLastError();
 }
@@ -963,7 +998,7 @@ static cudaError_t rowpair_n(const RowPairArgs& a, cudaStream_t s) {
     using C = Cfg<N2>;
     constexpr int LS = N2 + ((C::TPL >= 8) ? 0 : 8 / (8 / C::TPL > 2 ? 2 : 8 / C::TPL));
     const size_t smem = (size_t)2 * LS * sizeof(double2);
-    cudaFuncSetAttribute(k_rowpair<N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_prepare((const void*)k_rowpair<N2>, smem);
     const i64 ctas = a.N1 / 2 + 1;
     k_rowpair<N2><<<(unsigned)(a.N1 == 1 ? 1 : ctas), 2 * C::TPL, smem, s>>>(a);
     return cudaGetLastError();

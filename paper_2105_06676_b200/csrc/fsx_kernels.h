@@ -155,6 +155,10 @@ struct Flags {
 };
 
 // ---------------------------------------------------------------- launchers
+// One-time per (kernel, device, smem) setup: the dynamic shared-memory
+// opt-in and (threads > 0) the resident CTAs per SM, cached so a launch costs
+// no driver attribute/occupancy queries after the first.
+int kernel_prepare(const void* fn, size_t smem, int threads = 0);
 // Twiddle tables: tw_all[N + x] = exp(-2 pi i x / N) for pow2 N <= kMaxTwPow2.
 cudaError_t launch_axis_pow2(const double2* in, double2* out, const AxisGeom& g, int sign,
                              const StepTwiddle& st, const double2* tw_all, cudaStream_t s);

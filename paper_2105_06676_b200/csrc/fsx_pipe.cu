@@ -167,6 +167,7 @@ k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         mbar_init_fence();
+        pdl_wait();  // x may be the predecessor's output
         if (row < nrows) {
             mbar_expect_tx(&bar[0], BYTES);
             bulk_load(sm, x + row * L, BYTES, &bar[0]);
@@ -180,6 +181,7 @@ k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
             mbar_expect_tx(&bar[s ^ 1], BYTES);
             bulk_load(sm + (s ^ 1) * M, x + nxt * L, BYTES, &bar[s ^ 1]);
         }
+        if (nxt >= nrows) pdl_trigger();  // last row of this CTA: let the successor launch
         mbar_wait(&bar[s], (par >> s) & 1u);
         par ^= 1u << s;
         double2* line = sm + s * M;
@@ -248,6 +250,7 @@ k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         mbar_init_fence();
+        pdl_wait();  // H is the predecessor's output
         if (row < nrows) {
             mbar_expect_tx(&bar[0], BYTES);
             bulk_load(sm, H + row * P, BYTES, &bar[0]);
@@ -261,6 +264,7 @@ k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
             mbar_expect_tx(&bar[s ^ 1], BYTES);
             bulk_load(sm + (s ^ 1) * SS, H + nxt * P, BYTES, &bar[s ^ 1]);
         }
+        if (nxt >= nrows) pdl_trigger();
         mbar_wait(&bar[s], (par >> s) & 1u);
         par ^= 1u << s;
         double2* line = sm + s * SS;
@@ -438,9 +442,9 @@ template <int M>
 static cudaError_t r2c_reg_m(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw,
                              cudaStream_t s) {
     const size_t smem = (size_t)M * sizeof(double2);
-    cudaFuncSetAttribute(k_r2c_reg<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_prepare((const void*)k_r2c_reg<M>, smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_r2c_reg<M>, RCfg<M>::TPL, smem);
+    per_sm = kernel_prepare((const void*)k_r2c_reg<M>, smem, RCfg<M>::TPL);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -453,9 +457,9 @@ template <int M>
 static cudaError_t c2r_reg_m(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw,
                              Flags* f, cudaStream_t s) {
     const size_t smem = (size_t)M * sizeof(double2);
-    cudaFuncSetAttribute(k_c2r_reg<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_prepare((const void*)k_c2r_reg<M>, smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_c2r_reg<M>, RCfg<M>::TPL, smem);
+    per_sm = kernel_prepare((const void*)k_c2r_reg<M>, smem, RCfg<M>::TPL);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -584,7 +588,7 @@ static int sm_count() {
 template <class K>
 static int persistent_grid(K kernel, int threads, size_t smem, i64 ntiles) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    per_sm = kernel_prepare((const void*)kernel, smem, threads);
     if (per_sm < 1) per_sm = 1;
     const i64 g = (i64)per_sm * sm_count();
     return (int)(ntiles < g ? ntiles : g);
@@ -594,7 +598,7 @@ template <int M>
 static cudaError_t r2c_pipe_m(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw, cudaStream_t s) {
     const size_t smem = (size_t)2 * M * sizeof(double2);
     auto kf = P.blk ? k_r2c_pipe<M, true> : k_r2c_pipe<M, false>;
-    cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_prepare((const void*)kf, smem);
     const int grid = persistent_grid(kf, PCfg<M>::TPL, smem, nrows);
     kf<<<grid, PCfg<M>::TPL, smem, s>>>(x, H, nrows, L, P, tw);
     return cudaGetLastError();
@@ -605,7 +609,7 @@ static cudaError_t c2r_pipe_m(const double2* H, double* x, i64 nrows, i64 L, con
                               cudaStream_t s) {
     const size_t smem = (size_t)2 * M * sizeof(double2);
     auto kf = P.blk ? k_c2r_pipe<M, true> : k_c2r_pipe<M, false>;
-    cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_prepare((const void*)kf, smem);
     const int grid = persistent_grid(kf, PCfg<M>::TPL, smem, nrows);
     kf<<<grid, PCfg<M>::TPL, smem, s>>>(H, x, nrows, L, P, tw, f);
     return cudaGetLastError();
@@ -614,27 +618,25 @@ static cudaError_t c2r_pipe_m(const double2* H, double* x, i64 nrows, i64 L, con
 template <int M>
 static cudaError_t r2c_bulk_m(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
     const size_t smem = (size_t)2 * M * sizeof(double2);
-    cudaFuncSetAttribute(k_r2c_bulk<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_prepare((const void*)k_r2c_bulk<M>, smem);
     const int grid = persistent_grid(k_r2c_bulk<M>, PCfg<M>::TPL, smem, nrows);
-    k_r2c_bulk<M><<<grid, PCfg<M>::TPL, smem, s>>>(x, H, nrows, L, P, tw);
-    return cudaGetLastError();
+    return launch_pdl(k_r2c_bulk<M>, dim3(grid), dim3(PCfg<M>::TPL), smem, s, x, H, nrows, L, P, tw);
 }
 
 template <int M>
 static cudaError_t c2r_bulk_m(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
                               cudaStream_t s) {
     const size_t smem = (size_t)2 * (M + 8) * sizeof(double2);
-    cudaFuncSetAttribute(k_c2r_bulk<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_prepare((const void*)k_c2r_bulk<M>, smem);
     const int grid = persistent_grid(k_c2r_bulk<M>, PCfg<M>::TPL, smem, nrows);
-    k_c2r_bulk<M><<<grid, PCfg<M>::TPL, smem, s>>>(H, x, nrows, L, P, tw, f);
-    return cudaGetLastError();
+    return launch_pdl(k_c2r_bulk<M>, dim3(grid), dim3(PCfg<M>::TPL), smem, s, H, x, nrows, L, P, tw, f);
 }
 
 template <int N, int MODE>
 static cudaError_t cols_pipe_n(double2* H, const AxisGeom& g, const FusedSymbol& sym, const double2* tw, cudaStream_t s) {
     using C = PCfg<N>;
     const size_t smem = (size_t)2 * C::TILE_W * sizeof(double2);
-    cudaFuncSetAttribute(k_cols_pipe<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kernel_prepare((const void*)k_cols_pipe<N, MODE>, smem);
     const i64 ntiles = g.outer * ((g.ncols + C::W - 1) / C::W);
     const int grid = persistent_grid(k_cols_pipe<N, MODE>, C::NT_W, smem, ntiles);
     k_cols_pipe<N, MODE><<<grid, C::NT_W, smem, s>>>(H, g, sym, tw);

@@ -74,40 +74,48 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
     }
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        mbar_init_fence();
+        pdl_wait();  // the tile is the predecessor's output (PDL: everything above overlaps its tail)
         mbar_expect_tx(&bar, (unsigned)(N * W * sizeof(double2)));
 #pragma unroll 1
         for (int b = 0; b < C::NBOX; ++b)
             tma_load_3d(tile + b * C::BOX * W, &map, (int)(2 * c0), b * C::BOX, (int)o, &bar);
     }
     // MODE 2, real symbol: lam(k0)^T * scale for this thread's 16 frequencies is
-    // data independent -- computed while the tile is in flight and parked in
-    // shared memory (mult[q * NT + thread], thread-private) for after the FFT.
+    // data independent -- computed while the tile is in flight (or, under PDL,
+    // while the row pass drains) and parked in shared memory (mult[q * NT +
+    // thread], thread-private) for after the FFT.  The group coefficients are
+    // summed per thread (broadcast loads), so no CTA barrier precedes it.
     // Not for the 128 KB tiles (N = 8192): the extra 64 KB would squeeze the
     // L1 that serves the table reads (cfg3 measured 0.87 -> 1.04 ms).
     constexpr bool PRE = MODE == 2 && C::PRE;
     double* mult = reinterpret_cast<double*>(tile + W * C::LSW);
     if constexpr (MODE == 2) {
-        for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
-    }
-    __syncthreads();  // barrier initialised before anyone waits on it; tap terms visible
-    if constexpr (MODE == 2) {
-        for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
-            double2 a = make_double2(0.0, 0.0);
-            for (int j = 0; j < sym.ntaps; ++j)
-                if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j][w]);
-            acoef[gi][w] = a;
-        }
-        __syncthreads();
         if (PRE && sym.real) {
             double lam[C::R];
-            symbol_real<N, C::R, C::TPL>(lam, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
+            symbol_real<N, C::R, C::TPL>(lam, t, sym, tw_all, [&](int gi) {
+                double2 a = make_double2(0.0, 0.0);
+                for (int j = 0; j < sym.ntaps; ++j)
+                    if (sym.tap_group[j] == gi) a = cadd(a, tap_term(sym, tw_all, j, kx, ky));
+                return a;
+            });
             pow_real_vec<C::R>(lam, sym.T);
 #pragma unroll
             for (int q = 0; q < C::R; ++q) mult[q * C::NT + threadIdx.x] = lam[q] * sym.scale;
+        } else {
+            for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
+            __syncthreads();
+            for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
+                double2 a = make_double2(0.0, 0.0);
+                for (int j = 0; j < sym.ntaps; ++j)
+                    if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j][w]);
+                acoef[gi][w] = a;
+            }
         }
     }
+    __syncthreads();  // barrier initialised before anyone waits on it; group coefficients visible
     mbar_wait(&bar, 0);
+    pdl_trigger();  // the successor may start its own prologue
     double2 v[C::R];
 #pragma unroll
     for (int q = 0; q < C::R; ++q) v[q] = tile[(t + q * C::TPL) * W + w];
@@ -339,7 +347,7 @@ static cudaError_t cols_tma_n(const CUtensorMap& map, const AxisGeom& g, const F
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_cols_tma_pers<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kernel_prepare((const void*)k_cols_tma_pers<N, MODE>, smem);
         const int grid = (int)(ntiles < sms ? ntiles : sms);
         k_cols_tma_pers<N, MODE><<<grid, C::NT, smem, s>>>(map, g, sym, tw);
         return cudaGetLastError();
@@ -349,7 +357,7 @@ static cudaError_t cols_tma_n(const CUtensorMap& map, const AxisGeom& g, const F
             using C2 = TCfg<N, 2>;
             const size_t smem = C2::smem(MODE);
             const i64 tiles = (g.ncols + C2::W - 1) / C2::W;
-            cudaFuncSetAttribute(k_cols_tma<N, MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kernel_prepare((const void*)k_cols_tma<N, MODE, 2>, smem);
             k_cols_tma<N, MODE, 2><<<(unsigned)(g.outer * tiles), C2::NT, smem, s>>>(map, g, sym, tw);
             return cudaGetLastError();
         }
@@ -358,9 +366,8 @@ static cudaError_t cols_tma_n(const CUtensorMap& map, const AxisGeom& g, const F
     // tile + (fused mode) the per-frequency real multipliers
     const size_t smem = C::smem(MODE);
     const i64 tiles = (g.ncols + C::W - 1) / C::W;
-    cudaFuncSetAttribute(k_cols_tma<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_cols_tma<N, MODE><<<(unsigned)(g.outer * tiles), C::NT, smem, s>>>(map, g, sym, tw);
-    return cudaGetLastError();
+    kernel_prepare((const void*)k_cols_tma<N, MODE>, smem);
+    return launch_pdl(k_cols_tma<N, MODE>, dim3((unsigned)(g.outer * tiles)), dim3(C::NT), smem, s, map, g, sym, tw);
 }
 
 // FSX_TMA_W2=1: 2 columns (32 B rows) per 4096-point tile, 1 CTA/SM (measurement)
@@ -384,7 +391,7 @@ cudaError_t launch_cols_tma(const void* tensor_map, const AxisGeom& g, int mode,
     if (getenv("FSX_TMA_COPYONLY") && g.n == 4096) return cols_tma_n<4096, 3>(map, g, sym, tw, s);  // measurement
     if (mode == 2 && g.n == 4096 && g.outer == 1 && fused_4step()) {
         const size_t smem = 4096 * sizeof(double2);
-        cudaFuncSetAttribute(k_fused_tma4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kernel_prepare((const void*)k_fused_tma4, smem);
         k_fused_tma4<<<(unsigned)g.ncols, 256, smem, s>>>(map, g, sym, tw);
         return cudaGetLastError();
     }

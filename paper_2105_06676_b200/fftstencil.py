@@ -76,11 +76,14 @@ class GridShape:
         return f"GridShape({list(self._dims)}, fields={self._fields})"
 
     def _c(self) -> _lib.FsxShape:
-        s = _lib.FsxShape()
-        s.rank = len(self._dims)
-        s.fields = self._fields
-        for i, d in enumerate(self._dims):
-            s.dims[i] = d
+        s = self.__dict__.get("_cs")  # immutable: build the C view once
+        if s is None:
+            s = _lib.FsxShape()
+            s.rank = len(self._dims)
+            s.fields = self._fields
+            for i, d in enumerate(self._dims):
+                s.dims[i] = d
+            self._cs = s
         return s
 
 
@@ -124,6 +127,7 @@ class StencilKernel:
             raise SpecError("StencilKernel: fields must be >= 1")
         self._rank, self._fields = int(rank), int(fields)
         self._taps: dict[tuple, np.ndarray] = {}
+        self._cc = None  # cached fsx_kernel view (dropped by add_tap)
 
     def add_tap(self, offset: Iterable[int], block) -> "StencilKernel":
         off = tuple(int(o) for o in offset)
@@ -139,6 +143,7 @@ class StencilKernel:
                 raise SpecError("StencilKernel: block must be fields x fields")
         if not np.isfinite(b).all():
             raise SpecError("StencilKernel: non-finite coefficient")
+        self._cc = None
         if off in self._taps:
             self._taps[off] = self._taps[off] + b
         else:
@@ -188,12 +193,14 @@ class StencilKernel:
         return np.ascontiguousarray(off), np.ascontiguousarray(blk)
 
     def _c(self):
-        off, blk = self.arrays()
-        k = _lib.FsxKernel()
-        k.rank, k.fields, k.ntaps = self._rank, self._fields, off.shape[0]
-        k.offsets = off.ctypes.data_as(_I64P)
-        k.blocks = blk.ctypes.data_as(_DP)
-        return k, (off, blk)
+        if self._cc is None:
+            off, blk = self.arrays()
+            k = _lib.FsxKernel()
+            k.rank, k.fields, k.ntaps = self._rank, self._fields, off.shape[0]
+            k.offsets = off.ctypes.data_as(_I64P)
+            k.blocks = blk.ctypes.data_as(_DP)
+            self._cc = (k, (off, blk))
+        return self._cc
 
 
 def fold_kernels(kset) -> StencilKernel:
@@ -292,13 +299,22 @@ class DiagonalSpectrum:
 CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the NULL stream's explicit handle
 
 
+_OPTS: dict = {}  # option structs are read-only for the library: reuse them
+
+
 def _opts(device: int = 0, path: int = 0, stream: int | None = None, stage_events: int = 0):
     """fsx_options.  stream None -> the library's own stream; a handle of 0
     (torch's default stream) is passed as cudaStreamLegacy so the work is
     ordered with the caller's NULL-stream work instead of the library stream."""
-    o = _lib.FsxOptions()
-    o.device, o.path, o.stage_events = device, path, stage_events
-    o.stream = None if stream is None else (stream or CUDA_STREAM_LEGACY)
+    key = (device, path, stream, stage_events)
+    o = _OPTS.get(key)
+    if o is None:
+        o = _lib.FsxOptions()
+        o.device, o.path, o.stage_events = device, path, stage_events
+        o.stream = None if stream is None else (stream or CUDA_STREAM_LEGACY)
+        if len(_OPTS) > 256:
+            _OPTS.clear()
+        _OPTS[key] = o
     return o
 
 
