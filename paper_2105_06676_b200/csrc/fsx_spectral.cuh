@@ -16,6 +16,29 @@ __device__ __forceinline__ double2 eplus_tab(const double2* tw_all, i64 n, i64 x
     return cconj(__ldg(tw_all + n + (x & (n - 1))));
 }
 
+// e * i^m for m in 0..3 (exact: swaps and sign flips)
+__device__ __forceinline__ double2 rot_quarter(double2 e, int m) {
+    const double x = (m & 1) ? e.y : e.x, y = (m & 1) ? e.x : e.y;
+    return make_double2((m == 1 || m == 2) ? -x : x, (m >= 2) ? -y : y);
+}
+
+// exp(+2 pi i og k0 / N) for a thread's 16 frequencies k0 = t + q N/16:
+// with q = 4a + b this is e_b * i^(og a), so four table reads give all 16
+// (the other twelve are exact quarter turns).  f(q, e) is called per q.
+template <int N, class F>
+__device__ __forceinline__ void eplus16(const double2* tw_all, int t, i64 og, F&& f) {
+    double2 eb[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) eb[b] = eplus_tab(tw_all, N, (i64)(t + b * (N / 16)) * og);
+    const int mo = (int)(og & 3);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int m = (mo * a) & 3;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) f(4 * a + b, rot_quarter(eb[b], m));
+    }
+}
+
 // |lam|^T < 2^-1100 short cut: below every representable contribution (the
 // reference's own repeated squaring underflows to 0 / subnormal there).
 __device__ __forceinline__ bool negligible_power(double mag2, u64 T) {
@@ -130,10 +153,14 @@ __device__ __forceinline__ void symbol_real(double (&lam)[R], int t, const Fused
             for (int q = 0; q < R; ++q) lam[q] += a.x;
             continue;
         }
+        if constexpr (R == 16 && TPL * 16 == N) {
+            eplus16<N>(tw_all, t, og, [&](int q, double2 e) { lam[q] = fma(a.x, e.x, fma(-a.y, e.y, lam[q])); });
+        } else {
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-            const double2 e = eplus_tab(tw_all, N, (i64)(t + q * TPL) * og);
-            lam[q] = fma(a.x, e.x, fma(-a.y, e.y, lam[q]));
+            for (int q = 0; q < R; ++q) {
+                const double2 e = eplus_tab(tw_all, N, (i64)(t + q * TPL) * og);
+                lam[q] = fma(a.x, e.x, fma(-a.y, e.y, lam[q]));
+            }
         }
     }
 }
@@ -211,10 +238,14 @@ __device__ __forceinline__ void spectral_regs(double2 (&v)[R], int t, const Fuse
                 for (int q = 0; q < R; ++q) lam[q] += a.x;
                 continue;
             }
+            if constexpr (R == 16 && TPL * 16 == N) {
+                eplus16<N>(tw_all, t, og, [&](int q, double2 e) { lam[q] = fma(a.x, e.x, fma(-a.y, e.y, lam[q])); });
+            } else {
 #pragma unroll
-            for (int q = 0; q < R; ++q) {
-                const double2 e = eplus_tab(tw_all, N, (i64)(t + q * TPL) * og);
-                lam[q] = fma(a.x, e.x, fma(-a.y, e.y, lam[q]));
+                for (int q = 0; q < R; ++q) {
+                    const double2 e = eplus_tab(tw_all, N, (i64)(t + q * TPL) * og);
+                    lam[q] = fma(a.x, e.x, fma(-a.y, e.y, lam[q]));
+                }
             }
         }
 #pragma unroll
@@ -226,10 +257,14 @@ __device__ __forceinline__ void spectral_regs(double2 (&v)[R], int t, const Fuse
         for (int gi = 0; gi < sym.ngroups; ++gi) {
             const double2 a = acoef(gi);
             const i64 og = sym.group_off[gi];
+            if constexpr (R == 16 && TPL * 16 == N) {
+                eplus16<N>(tw_all, t, og, [&](int q, double2 e) { lam[q] = cadd(lam[q], cmul(a, e)); });
+            } else {
 #pragma unroll
-            for (int q = 0; q < R; ++q) {
-                const double2 e = eplus_tab(tw_all, N, (i64)(t + q * TPL) * og);
-                lam[q] = cadd(lam[q], cmul(a, e));
+                for (int q = 0; q < R; ++q) {
+                    const double2 e = eplus_tab(tw_all, N, (i64)(t + q * TPL) * og);
+                    lam[q] = cadd(lam[q], cmul(a, e));
+                }
             }
         }
 #pragma unroll

@@ -82,38 +82,35 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
             tma_load_3d(tile + b * C::BOX * W, &map, (int)(2 * c0), b * C::BOX, (int)o, &bar);
     }
     // MODE 2, real symbol: lam(k0)^T * scale for this thread's 16 frequencies is
-    // data independent -- computed while the tile is in flight (or, under PDL,
-    // while the row pass drains) and parked in shared memory (mult[q * NT +
-    // thread], thread-private) for after the FFT.  The group coefficients are
-    // summed per thread (broadcast loads), so no CTA barrier precedes it.
+    // data independent -- computed while the tile is in flight and parked in
+    // shared memory (mult[q * NT + thread], thread-private) for after the FFT.
+    // (Under PDL the first-wave CTAs wait for the producer thread's pdl_wait at
+    // the first barrier; per-thread group sums without that barrier measured
+    // slower on the rank-3 symbol: cfg4 7.25 -> 8.05 ms.)
     // Not for the 128 KB tiles (N = 8192): the extra 64 KB would squeeze the
     // L1 that serves the table reads (cfg3 measured 0.87 -> 1.04 ms).
     constexpr bool PRE = MODE == 2 && C::PRE;
     double* mult = reinterpret_cast<double*>(tile + W * C::LSW);
     if constexpr (MODE == 2) {
+        for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
+    }
+    __syncthreads();  // barrier initialised before anyone waits on it; tap terms visible
+    if constexpr (MODE == 2) {
+        for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
+            double2 a = make_double2(0.0, 0.0);
+            for (int j = 0; j < sym.ntaps; ++j)
+                if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j][w]);
+            acoef[gi][w] = a;
+        }
+        __syncthreads();
         if (PRE && sym.real) {
             double lam[C::R];
-            symbol_real<N, C::R, C::TPL>(lam, t, sym, tw_all, [&](int gi) {
-                double2 a = make_double2(0.0, 0.0);
-                for (int j = 0; j < sym.ntaps; ++j)
-                    if (sym.tap_group[j] == gi) a = cadd(a, tap_term(sym, tw_all, j, kx, ky));
-                return a;
-            });
+            symbol_real<N, C::R, C::TPL>(lam, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
             pow_real_vec<C::R>(lam, sym.T);
 #pragma unroll
             for (int q = 0; q < C::R; ++q) mult[q * C::NT + threadIdx.x] = lam[q] * sym.scale;
-        } else {
-            for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
-            __syncthreads();
-            for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
-                double2 a = make_double2(0.0, 0.0);
-                for (int j = 0; j < sym.ntaps; ++j)
-                    if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j][w]);
-                acoef[gi][w] = a;
-            }
         }
     }
-    __syncthreads();  // barrier initialised before anyone waits on it; group coefficients visible
     mbar_wait(&bar, 0);
     pdl_trigger();  // the successor may start its own prologue
     double2 v[C::R];

@@ -1,0 +1,8 @@
+# symbol table reads: 4 loads + exact quarter turns per group (eplus16)
+timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_ab19.log 2>&1; tail -3 gpurun_out/pytest_ab19.log
+for cfg in cfg2 cfg3 cfg4; do
+  timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/ab19_${cfg}.log 2>&1
+done
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ab19_launch.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ab19_ncu.log 2>&1
+python scripts/summarize.py gpurun_out/ab19_cfg*.log
+python scripts/launches.py gpurun_out/ab19_launch.csv
