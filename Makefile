@@ -22,7 +22,10 @@ $(CSRC)/fsx_tma.o: $(CSRC)/fsx_tma.cu $(CSRC)/fsx_kernels.h $(CSRC)/fsx_device.c
 $(CSRC)/fsx_api.o: $(CSRC)/fsx_api.cpp $(CSRC)/fsx_kernels.h include/fsx.h
 	$(NVCC) $(ARCH) -O3 -std=c++17 -Xcompiler -fPIC -Iinclude -I$(CSRC) -x cu -c $< -o $@
 
-$(LIB): $(CSRC)/fsx_kernels.o $(CSRC)/fsx_pipe.o $(CSRC)/fsx_tma.o $(CSRC)/fsx_api.o
+$(CSRC)/fsx_naive.o: $(CSRC)/fsx_naive.cu $(CSRC)/fsx_kernels.h
+	$(NVCC) $(NVFLAGS) -c $< -o $@ > build_ptxas_naive.log 2>&1 || (cat build_ptxas_naive.log; false)
+
+$(LIB): $(CSRC)/fsx_kernels.o $(CSRC)/fsx_pipe.o $(CSRC)/fsx_tma.o $(CSRC)/fsx_naive.o $(CSRC)/fsx_api.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart_static -lrt -lpthread -ldl
 
 oracle:

@@ -214,4 +214,16 @@ inline FieldGrid solve_periodic_implicit(const StencilKernel& q, const StencilKe
     return out;
 }
 
+// Direct-stepping verifier on the GPU (oracle.hpp:15-20: step_periodic,
+// evolve_periodic_naive), bitwise equal to the reference loop.
+inline FieldGrid evolve_periodic_naive(const FieldGrid& a0, const StencilKernel& k, std::uint64_t T) {
+    FieldGrid out(a0.shape);
+    const fsx_shape s = a0.shape.c();
+    auto kv = k.c();
+    check(fsx_evolve_periodic_naive(&s, a0.data.data(), &kv.k, T, out.data.data(), nullptr));
+    return out;
+}
+
+inline FieldGrid step_periodic(const FieldGrid& a, const StencilKernel& k) { return evolve_periodic_naive(a, k, 1); }
+
 }  // namespace fftstencil_b200

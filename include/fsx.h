@@ -120,6 +120,21 @@ fsx_status fsx_solve_periodic_device(const fsx_shape* shape, const double* d_a0,
                                      uint64_t T, double* d_out, const fsx_options* opt);
 fsx_status fsx_device_check(const fsx_options* opt);
 
+/* Direct-stepping verifier (not the solve path): the reference's naive
+ * oracle step_periodic / evolve_periodic_naive (proj/src/oracle.cpp:90-115,
+ * oracle.hpp:15-20) on the GPU, bitwise equal to the reference loop (taps in
+ * sorted-offset order, products and sums rounded separately).  T direct
+ * steps; an independent full-size check of the FFT solver.  Host pointers
+ * (returns synchronized) or, for _device, device pointers enqueued on
+ * opt->stream.  Ranks 1-8; fields <= 8; for rank <= 3 the axes before the
+ * last must be <= 65535. */
+fsx_status fsx_step_periodic(const fsx_shape* shape, const double* a, const fsx_kernel* k, double* out,
+                             const fsx_options* opt);
+fsx_status fsx_evolve_periodic_naive(const fsx_shape* shape, const double* a0, const fsx_kernel* k, uint64_t T,
+                                     double* out, const fsx_options* opt);
+fsx_status fsx_evolve_periodic_naive_device(const fsx_shape* shape, const double* d_a0, const fsx_kernel* k,
+                                            uint64_t T, double* d_out, const fsx_options* opt);
+
 /* Stage durations (ms) of the most recent device solve enqueued with
  * opt->stage_events = 1: ms[0] forward passes, ms[1] the fused spectral
  * pass (plan 1: exactly one kernel, k_fused_r2c), ms[2] inverse passes.

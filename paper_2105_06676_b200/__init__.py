@@ -20,6 +20,8 @@ from .fftstencil import (  # noqa: F401
     StencilKernel,
     device_check,
     device_count,
+    evolve_periodic_naive,
+    evolve_periodic_naive_device,
     fft,
     fold_kernels,
     hadamard,
@@ -36,6 +38,7 @@ from .fftstencil import (  # noqa: F401
     solve_periodic_implicit,
     solve_periodic_vector,
     spectrum_from_kernel,
+    step_periodic,
 )
 from . import _lib  # noqa: F401
 

@@ -87,6 +87,9 @@ EXPORTS = (
     "fsx_solve_periodic_device",
     "fsx_device_check",
     "fsx_last_stage_ms",
+    "fsx_step_periodic",
+    "fsx_evolve_periodic_naive",
+    "fsx_evolve_periodic_naive_device",
     "fsx_slab_describe",
     "fsx_slab_forward",
     "fsx_slab_spectral",

@@ -939,6 +939,73 @@ cudaStream_t stream_of(Device& dev, const fsx_options* opt) {
     return (opt && opt->stream) ? reinterpret_cast<cudaStream_t>(opt->stream) : dev.stream;
 }
 
+// ------------------------------------------------------------------ naive stepping verifier
+// evolve_periodic_naive / step_periodic (proj/src/oracle.cpp:90-115) on the
+// GPU: T direct stencil steps, bitwise equal to the reference loop.  Not on
+// the solve path; a full-size independent check of the FFT solver.
+struct NaiveBufs {
+    DevBuf s0, s1, off, blk;
+};
+std::map<int, std::unique_ptr<NaiveBufs>> g_naive;
+
+void evolve_naive(const fsx_shape* shape, const double* a0, const fsx_kernel* k, u64 T, double* out,
+                  const fsx_options* opt, bool device_ptrs) {
+    const Shape s = parse_shape(shape);
+    const Taps taps = parse_kernel(k);
+    require_fits(taps, s);
+    if (!a0 || !out) throw SpecErr("fsx: null grid pointer");
+    const size_t bytes = (size_t)s.values() * 8;
+    if (T == 0 && !device_ptrs) {  // proj/src/oracle.cpp:103
+        if (out != a0) std::memmove(out, a0, bytes);
+        return;
+    }
+    if (s.fields > fsx::kMaxNaiveFields) throw SpecErr("evolve_periodic_naive: at most 8 fields on the GPU verifier");
+    const int rk = s.rank();
+    if (rk <= 3 && ((rk == 3 && s.dims[0] > 65535) || (rk >= 2 && s.dims[rk - 2] > 65535)))
+        throw SpecErr("evolve_periodic_naive: leading axes must be <= 65535");
+    std::lock_guard<std::mutex> lk(g_mu);
+    Device& dev = device_for(opt ? opt->device : 0);
+    cudaStream_t st = stream_of(dev, opt);
+    if (T == 0) {
+        if (out != a0) FSX_CK(cudaMemcpyAsync(out, a0, bytes, cudaMemcpyDeviceToDevice, st));
+        return;
+    }
+    auto& slot = g_naive[dev.ordinal];
+    if (!slot) slot = std::make_unique<NaiveBufs>();
+    NaiveBufs& nb = *slot;
+    fsx::NaiveGeom g;
+    g.rank = rk;
+    g.m = s.fields;
+    g.ntaps = (int)taps.map.size();
+    g.cells = s.cells;
+    const int ra = rk <= 3 ? 3 : rk;
+    for (int a = 0; a < ra; ++a) g.n[a] = 1;
+    for (int a = 0; a < rk; ++a) g.n[ra - rk + a] = s.dims[a];
+    std::vector<long long> off;
+    std::vector<double> blk;
+    for (const auto& kv : taps.map) {  // sorted offset order, as the reference's map
+        for (int a = 0; a < ra - rk; ++a) off.push_back(0);
+        for (int a = 0; a < rk; ++a) off.push_back(kv.first[a]);
+        blk.insert(blk.end(), kv.second.begin(), kv.second.end());
+    }
+    nb.off.ensure(off.size() * sizeof(long long));
+    nb.blk.ensure(blk.size() * sizeof(double));
+    nb.s0.ensure(bytes);
+    nb.s1.ensure(bytes);
+    // pageable sources: these copies complete before the call returns
+    FSX_CK(cudaMemcpyAsync(nb.off.p, off.data(), off.size() * sizeof(long long), cudaMemcpyHostToDevice, st));
+    FSX_CK(cudaMemcpyAsync(nb.blk.p, blk.data(), blk.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+    FSX_CK(cudaMemcpyAsync(nb.s0.p, a0, bytes, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    double* cur = nb.s0.as<double>();
+    double* nxt = nb.s1.as<double>();
+    for (u64 t = 0; t < T; ++t) {
+        FSX_CK(fsx::launch_step_naive(cur, nxt, g, nb.off.as<long long>(), nb.blk.as<double>(), st));
+        std::swap(cur, nxt);
+    }
+    FSX_CK(cudaMemcpyAsync(out, cur, bytes, device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    if (!device_ptrs) FSX_CK(cudaStreamSynchronize(st));
+}
+
 struct SolveReq {
     const fsx_shape* shape;
     const double* a0;
@@ -1105,6 +1172,21 @@ fsx_status fsx_solve_periodic_device(const fsx_shape* shape, const double* d_a0,
         rq.device_ptrs = true;
         solve(rq);
     });
+}
+
+fsx_status fsx_step_periodic(const fsx_shape* shape, const double* a, const fsx_kernel* k, double* out,
+                             const fsx_options* opt) {
+    return guarded([&] { evolve_naive(shape, a, k, 1, out, opt, false); });
+}
+
+fsx_status fsx_evolve_periodic_naive(const fsx_shape* shape, const double* a0, const fsx_kernel* k, uint64_t T,
+                                     double* out, const fsx_options* opt) {
+    return guarded([&] { evolve_naive(shape, a0, k, T, out, opt, false); });
+}
+
+fsx_status fsx_evolve_periodic_naive_device(const fsx_shape* shape, const double* d_a0, const fsx_kernel* k,
+                                            uint64_t T, double* d_out, const fsx_options* opt) {
+    return guarded([&] { evolve_naive(shape, d_a0, k, T, d_out, opt, true); });
 }
 
 fsx_status fsx_device_check(const fsx_options* opt) {

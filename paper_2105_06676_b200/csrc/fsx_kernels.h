@@ -147,6 +147,16 @@ struct RowPairArgs {
     i64 row_split = 0;   // rows stored digit-reversed by a four-step split of N1 (= N1b), 0: natural
 };
 
+// Direct stepping verifier (fsx_naive.cu).  rank <= 3: n[] padded to 3 axes
+// with leading 1s and the tap offsets padded the same way (stride 3);
+// rank 4..8: n[0..rank), offsets stride rank.
+constexpr int kMaxNaiveFields = 8;
+struct NaiveGeom {
+    int rank = 1, m = 1, ntaps = 0;
+    i64 n[kMaxRank];
+    i64 cells = 1;
+};
+
 struct Flags {
     unsigned int nonfinite;
     unsigned int pad;
@@ -202,6 +212,9 @@ cudaError_t launch_r2c_reg(const double* x, double2* H, i64 nrows, i64 L, const 
                            cudaStream_t s);
 cudaError_t launch_c2r_reg(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw_all,
                            Flags* flags, cudaStream_t s);
+// one direct periodic stencil step out = sum_taps B a[x + off] (verifier)
+cudaError_t launch_step_naive(const double* a, double* out, const NaiveGeom& g, const long long* off,
+                              const double* blk, cudaStream_t s);
 // TMA column passes (fsx_tma.cu); tensor_map points at a 64-byte aligned CUtensorMap
 bool tma_cols_ok(i64 N);
 int make_cols_tensor_map(void* out_map, void* base, const AxisGeom& g);

@@ -404,6 +404,40 @@ def solve_periodic_device(shape: GridShape, d_a0: int, k: StencilKernel, T: int,
     _lib.check(status)
 
 
+# ---------------------------------------------------------------- direct-stepping verifier
+def step_periodic(a: FieldGrid, k: StencilKernel) -> FieldGrid:
+    """proj/src/oracle.cpp:90-98 on the GPU (fsx_step_periodic): one direct
+    stencil step, bitwise equal to the reference loop."""
+    return evolve_periodic_naive(a, k, 1)
+
+
+def evolve_periodic_naive(a0: FieldGrid, k: StencilKernel, T: int) -> FieldGrid:
+    """proj/src/oracle.cpp:100-115 on the GPU (fsx_evolve_periodic_naive):
+    T direct steps -- an independent check of the FFT solver, not a solver."""
+    if T < 0 or T >= 1 << 64:
+        raise SpecError("T must be a nonnegative 64-bit integer")
+    L = _lib.load()
+    kc, keep = k._c()
+    out = np.empty_like(a0.data)
+    status = L.fsx_evolve_periodic_naive(ctypes.byref(a0.shape._c()), a0.data.ctypes.data_as(_DP), ctypes.byref(kc),
+                                         ctypes.c_uint64(int(T)), out.ctypes.data_as(_DP), ctypes.byref(_opts()))
+    del keep
+    _lib.check(status)
+    return FieldGrid(a0.shape, out)
+
+
+def evolve_periodic_naive_device(shape: GridShape, d_a0: int, k: StencilKernel, T: int, d_out: int,
+                                 stream: int | None = None, device: int = 0) -> None:
+    """Device-pointer variant of :func:`evolve_periodic_naive`, enqueued on ``stream``."""
+    L = _lib.load()
+    kc, keep = k._c()
+    status = L.fsx_evolve_periodic_naive_device(ctypes.byref(shape._c()), ctypes.c_void_p(d_a0), ctypes.byref(kc),
+                                                ctypes.c_uint64(int(T)), ctypes.c_void_p(d_out),
+                                                ctypes.byref(_opts(device, 0, stream)))
+    del keep
+    _lib.check(status)
+
+
 def last_stage_ms(device: int = 0) -> list:
     """[forward, fused spectral, inverse] ms of the last device solve enqueued with stage_events=1."""
     ms = (ctypes.c_double * 3)()
