@@ -238,9 +238,13 @@ struct LineFFT {
         constexpr int r = radix<S>();
         constexpr int Ns = ns<S>();
         constexpr int C = R / r;
+        // Last pass (Ns r = N, several items per thread): item i sits at
+        // t + i N/16, so W_N^(u (t + i N/16)) = W_N^(u t) W_16^(u i) -- only
+        // item 0 is read, the others are exact-constant rotations of it.
+        constexpr bool LAST_DERIVE = Ns * r == N && C > 1 && !(PAIRED && S == NPASS - 1);
         if constexpr (Ns > 1) {
 #pragma unroll
-            for (int i = 0; i < C; ++i) {
+            for (int i = 0; i < (LAST_DERIVE ? 1 : C); ++i) {
                 const int k = item<S>(t, i) & (Ns - 1);
                 double2* wi = w + i * r;
                 const double2* pt = tw + (kPassTabBase + 15 * N + 16 * Ns);  // tw = tw_all + N
@@ -261,6 +265,15 @@ struct LineFFT {
 #pragma unroll
                     for (int u = 9; u < 16; ++u) wi[u] = cmul(wi[u - 8], wi[8]);
                 }
+            }
+            if constexpr (LAST_DERIVE) {
+                static_for<1, C>([&](auto I) {
+                    constexpr int i = decltype(I)::value;
+                    static_for<1, r>([&](auto U) {
+                        constexpr int u = decltype(U)::value;
+                        w[i * r + u] = cmul_const<u * i, 16, -1>(w[u]);
+                    });
+                });
             }
         }
     }
