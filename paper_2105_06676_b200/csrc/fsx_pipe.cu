@@ -151,21 +151,30 @@ k_c2r_pipe(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
 // split pairs k with M - k in registers where the FFT's last pass allows it
 // (LineFFT PAIRED: M = 2^(4a+3)), dropping the split exchange.  Pitch
 // layout only (element (row, k) at row * P + k).
-template <int M>
-__global__ void __launch_bounds__(PCfg<M>::TPL, PCfg<M>::MINB_ROW)
+// ST stages: 2 = the next row streams in while this one is transformed
+// (one CTA's own pipeline); 1 = one 64 KB stage per CTA for the 4096-point
+// rows so two CTAs share an SM and overlap each other instead (the two-stage
+// version fits one 128 KB CTA per SM: 8 warps, 250 registers).
+template <int M, int ST>
+struct BulkCfg {
+    static constexpr int MINB = ST == 2 ? PCfg<M>::MINB_ROW : 2;
+};
+
+template <int M, int ST>
+__global__ void __launch_bounds__(PCfg<M>::TPL, BulkCfg<M, ST>::MINB)
 k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, i64 P,
            const double2* __restrict__ tw_all) {
     using F = LineFFT<M, -1, true, true>;
     constexpr int TPL = PCfg<M>::TPL, R = 16;
     constexpr unsigned BYTES = M * sizeof(double2);
     extern __shared__ __align__(128) double2 sm[];
-    __shared__ __align__(8) unsigned long long bar[2];
+    __shared__ __align__(8) unsigned long long bar[ST];
     const int t = threadIdx.x;
     const i64 G = gridDim.x;
     i64 row = blockIdx.x;
     if (t == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+#pragma unroll
+        for (int b = 0; b < ST; ++b) mbar_init(&bar[b], 1);
         mbar_init_fence();
         pdl_wait();  // x may be the predecessor's output
         if (row < nrows) {
@@ -175,9 +184,9 @@ k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
     }
     __syncthreads();
     unsigned par = 0;  // bit s: parity of the next completion of stage s
-    for (int s = 0; row < nrows; row += G, s ^= 1) {
+    for (int s = 0; row < nrows; row += G, s = (ST == 2 ? s ^ 1 : 0)) {
         const i64 nxt = row + G;
-        if (t == 0 && nxt < nrows) {
+        if (ST == 2 && t == 0 && nxt < nrows) {
             mbar_expect_tx(&bar[s ^ 1], BYTES);
             bulk_load(sm + (s ^ 1) * M, x + nxt * L, BYTES, &bar[s ^ 1]);
         }
@@ -229,11 +238,15 @@ k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
         }
         fence_proxy_async();  // generic writes of this stage before its next bulk fill
         __syncthreads();
+        if (ST == 1 && t == 0 && nxt < nrows) {
+            mbar_expect_tx(&bar[0], BYTES);
+            bulk_load(sm, x + nxt * L, BYTES, &bar[0]);
+        }
     }
 }
 
-template <int M>
-__global__ void __launch_bounds__(PCfg<M>::TPL, PCfg<M>::MINB_ROW)
+template <int M, int ST>
+__global__ void __launch_bounds__(PCfg<M>::TPL, BulkCfg<M, ST>::MINB)
 k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, i64 P,
            const double2* __restrict__ tw_all, Flags* flags) {
     using F = LineFFT<M, +1, true>;
@@ -241,14 +254,14 @@ k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
     constexpr int SS = M + 8;  // stage stride: M + 1 elements, 128 B aligned
     constexpr unsigned BYTES = (M + 1) * sizeof(double2);
     extern __shared__ __align__(128) double2 sm[];
-    __shared__ __align__(8) unsigned long long bar[2];
+    __shared__ __align__(8) unsigned long long bar[ST];
     const int t = threadIdx.x;
     const i64 G = gridDim.x;
     bool bad = false;
     i64 row = blockIdx.x;
     if (t == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+#pragma unroll
+        for (int b = 0; b < ST; ++b) mbar_init(&bar[b], 1);
         mbar_init_fence();
         pdl_wait();  // H is the predecessor's output
         if (row < nrows) {
@@ -258,9 +271,9 @@ k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
     }
     __syncthreads();
     unsigned par = 0;
-    for (int s = 0; row < nrows; row += G, s ^= 1) {
+    for (int s = 0; row < nrows; row += G, s = (ST == 2 ? s ^ 1 : 0)) {
         const i64 nxt = row + G;
-        if (t == 0 && nxt < nrows) {
+        if (ST == 2 && t == 0 && nxt < nrows) {
             mbar_expect_tx(&bar[s ^ 1], BYTES);
             bulk_load(sm + (s ^ 1) * SS, H + nxt * P, BYTES, &bar[s ^ 1]);
         }
@@ -289,6 +302,10 @@ k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
         }
         fence_proxy_async();
         __syncthreads();
+        if (ST == 1 && t == 0 && nxt < nrows) {
+            mbar_expect_tx(&bar[0], BYTES);
+            bulk_load(sm, H + nxt * P, BYTES, &bar[0]);
+        }
     }
     const unsigned any = __ballot_sync(0xffffffffu, bad);
     if (any && (threadIdx.x & 31) == 0) atomicOr(&flags->nonfinite, 1u);
@@ -615,21 +632,43 @@ static cudaError_t c2r_pipe_m(const double2* H, double* x, i64 nrows, i64 L, con
     return cudaGetLastError();
 }
 
+// FSX_ROW_STAGES=1 selects one stage x 2 CTAs/SM (A/B); default 2 stages
+static int row_stages(int M) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_ROW_STAGES");
+        v = e ? atoi(e) : 0;
+    }
+    return v == 1 ? 1 : 2;  // 1 stage x 2 CTAs measured slower at M = 4096 (269 vs 254 us)
+}
+
+template <int M, int ST>
+static cudaError_t r2c_bulk_ms(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
+    const size_t smem = (size_t)ST * M * sizeof(double2);
+    kernel_prepare((const void*)k_r2c_bulk<M, ST>, smem);
+    const int grid = persistent_grid(k_r2c_bulk<M, ST>, PCfg<M>::TPL, smem, nrows);
+    return launch_pdl(k_r2c_bulk<M, ST>, dim3(grid), dim3(PCfg<M>::TPL), smem, s, x, H, nrows, L, P, tw);
+}
+
 template <int M>
 static cudaError_t r2c_bulk_m(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
-    const size_t smem = (size_t)2 * M * sizeof(double2);
-    kernel_prepare((const void*)k_r2c_bulk<M>, smem);
-    const int grid = persistent_grid(k_r2c_bulk<M>, PCfg<M>::TPL, smem, nrows);
-    return launch_pdl(k_r2c_bulk<M>, dim3(grid), dim3(PCfg<M>::TPL), smem, s, x, H, nrows, L, P, tw);
+    return row_stages(M) == 1 ? r2c_bulk_ms<M, 1>(x, H, nrows, L, P, tw, s) : r2c_bulk_ms<M, 2>(x, H, nrows, L, P, tw, s);
+}
+
+template <int M, int ST>
+static cudaError_t c2r_bulk_ms(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
+                               cudaStream_t s) {
+    const size_t smem = (size_t)ST * (M + 8) * sizeof(double2);
+    kernel_prepare((const void*)k_c2r_bulk<M, ST>, smem);
+    const int grid = persistent_grid(k_c2r_bulk<M, ST>, PCfg<M>::TPL, smem, nrows);
+    return launch_pdl(k_c2r_bulk<M, ST>, dim3(grid), dim3(PCfg<M>::TPL), smem, s, H, x, nrows, L, P, tw, f);
 }
 
 template <int M>
 static cudaError_t c2r_bulk_m(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
                               cudaStream_t s) {
-    const size_t smem = (size_t)2 * (M + 8) * sizeof(double2);
-    kernel_prepare((const void*)k_c2r_bulk<M>, smem);
-    const int grid = persistent_grid(k_c2r_bulk<M>, PCfg<M>::TPL, smem, nrows);
-    return launch_pdl(k_c2r_bulk<M>, dim3(grid), dim3(PCfg<M>::TPL), smem, s, H, x, nrows, L, P, tw, f);
+    return row_stages(M) == 1 ? c2r_bulk_ms<M, 1>(H, x, nrows, L, P, tw, f, s)
+                              : c2r_bulk_ms<M, 2>(H, x, nrows, L, P, tw, f, s);
 }
 
 template <int N, int MODE>

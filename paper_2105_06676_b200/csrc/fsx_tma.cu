@@ -37,6 +37,13 @@ struct TCfg {
     static constexpr int NT = W * TPL;
     static constexpr int MINB = NT <= 256 ? 2 : 1;
     static constexpr bool PRE = N <= 4096;                // fused mode: real multipliers in smem
+    // ... or in tensor memory (16 warps x 32 columns): correct (tests cover it) but
+    // measured neutral on cfg3 (0.834 vs 0.824 ms), so off; FSX_TMEM_MULT=1 at build
+#ifdef FSX_TMEM_MULT
+    static constexpr bool TMEM = N == 8192;
+#else
+    static constexpr bool TMEM = false;
+#endif
     static constexpr size_t smem(int mode) {
         return (size_t)W * LSW * 16 + (mode == 2 && PRE ? (size_t)NT * R * 8 : 0);
     }
@@ -89,12 +96,22 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
     // slower on the rank-3 symbol: cfg4 7.25 -> 8.05 ms.)
     // Not for the 128 KB tiles (N = 8192): the extra 64 KB would squeeze the
     // L1 that serves the table reads (cfg3 measured 0.87 -> 1.04 ms).
+    // The 128 KB tiles (N = 8192, 16 warps, one CTA per SM) park the
+    // multipliers in tensor memory instead (128 columns; see fsx_async.cuh).
     constexpr bool PRE = MODE == 2 && C::PRE;
+    constexpr bool TM = MODE == 2 && C::TMEM;
     double* mult = reinterpret_cast<double*>(tile + W * C::LSW);
+    __shared__ unsigned tmem_base;
+    const int warp = threadIdx.x >> 5;
+    if constexpr (TM) {
+        if (warp == 0) tmem_alloc<128>(&tmem_base);
+        tmem_fence_before();
+    }
     if constexpr (MODE == 2) {
         for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
     }
     __syncthreads();  // barrier initialised before anyone waits on it; tap terms visible
+    if constexpr (TM) tmem_fence_after();
     if constexpr (MODE == 2) {
         for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
             double2 a = make_double2(0.0, 0.0);
@@ -103,12 +120,25 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
             acoef[gi][w] = a;
         }
         __syncthreads();
-        if (PRE && sym.real) {
+        if ((PRE || TM) && sym.real) {
             double lam[C::R];
             symbol_real<N, C::R, C::TPL>(lam, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
             pow_real_vec<C::R>(lam, sym.T);
+            if constexpr (TM) {
+                static_assert(C::R == 16, "TMEM parking holds 16 doubles per thread");
+                double h[8];
+                const unsigned ta = tmem_warp_addr(tmem_base, warp);
 #pragma unroll
-            for (int q = 0; q < C::R; ++q) mult[q * C::NT + threadIdx.x] = lam[q] * sym.scale;
+                for (int half = 0; half < 2; ++half) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) h[i] = lam[8 * half + i] * sym.scale;
+                    tmem_st8(ta + 16 * half, h);
+                }
+                tmem_wait_st();
+            } else {
+#pragma unroll
+                for (int q = 0; q < C::R; ++q) mult[q * C::NT + threadIdx.x] = lam[q] * sym.scale;
+            }
         }
     }
     mbar_wait(&bar, 0);
@@ -128,16 +158,32 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
         if (PRE && sym.real) {
 #pragma unroll
             for (int q = 0; q < C::R; ++q) v[q] = cscale(v[q], mult[q * C::NT + threadIdx.x]);
+        } else if (TM && sym.real) {
+            const unsigned ta = tmem_warp_addr(tmem_base, warp);
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                double h[8];
+                tmem_ld8(ta + 16 * half, h);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[8 * half + i] = cscale(v[8 * half + i], h[i]);
+            }
         } else {
             spectral_regs<N, C::R, C::TPL>(v, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
         }
         FI::run(v, t, line, tw_all + N);
     }
+    if constexpr (TM) tmem_fence_before();
     __syncthreads();  // last exchange reads done before the tile is overwritten
 #pragma unroll
     for (int q = 0; q < C::R; ++q) tile[(t + q * C::TPL) * W + w] = v[q];
     fence_proxy_async();
     __syncthreads();
+    if constexpr (TM) {
+        if (warp == 0) {
+            tmem_fence_after();
+            tmem_dealloc<128>(tmem_base);
+        }
+    }
     if (threadIdx.x == 0) {
 #pragma unroll 1
         for (int b = 0; b < C::NBOX; ++b) tma_store_3d(&map, tile + b * C::BOX * W, (int)(2 * c0), b * C::BOX, (int)o);

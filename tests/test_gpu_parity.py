@@ -350,6 +350,8 @@ PLAN_CASES = [
     ([1 << 14], 2, "leapfrog", 5000),
     ([96, 40], 1, "random", 11),
     ([1 << 14, 2], 1, "random", 3),
+    ([8192, 64], 1, "box9", 1000),       # 8192-point fused columns (multipliers parked in TMEM)
+    ([8192, 32], 1, "random", 5),        # ... with a complex symbol
 ]
 
 
