@@ -111,6 +111,16 @@ fsx_status fsx_solve_periodic_implicit(const fsx_shape* shape, const double* a0,
                                        const fsx_kernel* s, uint64_t T, double* out,
                                        const fsx_options* opt, fsx_stage_timings* st);
 
+/* Pipelined batch of nbatch independent solves of one shape, kernel and T
+ * (host pointers a0s[i] -> outs[i], each may alias).  Two internal lanes keep
+ * one solve's D2H, the next one's H2D and the kernels in flight together, so
+ * with PINNED host buffers a batch runs at ~max(H2D, D2H, kernels) per solve.
+ * Returns synchronized; FSX_ERR_NUMERIC names the first failing item (the
+ * other outputs are valid).  Extension for batched slab solves (the
+ * aperiodic recursion's rb_run, proj/src/aperiodic.cpp:226-244). */
+fsx_status fsx_solve_periodic_batch(const fsx_shape* shape, int64_t nbatch, const double* const* a0s,
+                                    const fsx_kernel* k, uint64_t T, double* const* outs, const fsx_options* opt);
+
 /* Device-resident variant: d_a0 / d_out are device pointers (may alias);
  * the work is enqueued on opt->stream and the call returns without
  * synchronizing.  The non-finite check is deferred: fsx_device_check()

@@ -33,6 +33,7 @@ from .fftstencil import (  # noqa: F401
     pow_spectrum,
     pseudo_inverse_spectrum,
     solve_periodic,
+    solve_periodic_batch,
     solve_periodic_cached,
     solve_periodic_device,
     solve_periodic_implicit,

@@ -85,6 +85,7 @@ EXPORTS = (
     "fsx_solve_periodic_cached",
     "fsx_solve_periodic_implicit",
     "fsx_solve_periodic_device",
+    "fsx_solve_periodic_batch",
     "fsx_device_check",
     "fsx_last_stage_ms",
     "fsx_step_periodic",

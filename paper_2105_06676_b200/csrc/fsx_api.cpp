@@ -286,6 +286,11 @@ struct Device {
     std::map<std::string, std::unique_ptr<Plan>> plans;
     cudaEvent_t ev[8];
     bool events = false;
+    // pipelined batch solves: two lanes (stream + plan copy) keep one solve's
+    // D2H, the next one's H2D and a third one's kernels in flight together
+    cudaStream_t lanes[2] = {nullptr, nullptr};
+    cudaEvent_t lane_ev[2];
+    DevBuf bflags;  // per-solve Flags of a batch
 };
 
 std::mutex g_mu;
@@ -388,7 +393,9 @@ std::string plan_key(const Shape& s, int kind_hint) {
     return k;
 }
 
-Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general) {
+// lane > 0: an independent copy of the plan (own workspaces and tensor maps)
+// for the pipelined batch solve, which keeps two solves in flight.
+Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general, int lane = 0) {
     // squeeze length-1 axes (their offsets are 0 by require_fits)
     Plan probe;
     probe.full = s;
@@ -403,10 +410,14 @@ Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general)
         probe.axes.push_back(0);
     }
     const int kind = choose_kind(probe, taps, force_general);
-    const std::string key = plan_key(s, kind);
+    const std::string base = plan_key(s, kind);
+    const std::string key = lane ? base + "|lane" + std::to_string(lane) : base;
     auto it = dev.plans.find(key);
     if (it != dev.plans.end()) return *it->second;
-    if (dev.plans.size() >= 8) dev.plans.clear();  // bounded cache
+    if (dev.plans.size() >= 8) {  // bounded cache; keep this shape's other lanes (a batch holds them)
+        for (auto e = dev.plans.begin(); e != dev.plans.end();)
+            e = e->first.rfind(base, 0) == 0 ? std::next(e) : dev.plans.erase(e);
+    }
 
     auto p = std::make_unique<Plan>();
     p->full = probe.full;
@@ -691,8 +702,8 @@ struct Stamps {
 // Runs one solve on device pointers; stage boundaries are stamped into
 // ev[0..3] when timings are requested.
 void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, const double* d_a0, double* d_out,
-              cudaStream_t st, Stamps& sp) {
-    fsx::Flags* flags = dev.flags.as<fsx::Flags>();
+              cudaStream_t st, Stamps& sp, fsx::Flags* flags_at = nullptr) {
+    fsx::Flags* flags = flags_at ? flags_at : dev.flags.as<fsx::Flags>();
     const double2* tw = dev.tw_all.as<double2>();
     const int r = (int)p.dims.size();
     sp.mark();
@@ -917,12 +928,8 @@ double bits_to_double(unsigned long long b) {
 
 // Decide NumericError from the device flags (realize_checked,
 // proj/src/periodic.cpp:53-63) and reset them.
-void check_flags(Device& dev, int kind, cudaStream_t st) {
-    fsx::Flags h;
-    FSX_CK(cudaMemcpyAsync(&h, dev.flags.p, sizeof(h), cudaMemcpyDeviceToHost, st));
-    FSX_CK(cudaStreamSynchronize(st));
-    FSX_CK(cudaMemsetAsync(dev.flags.p, 0, sizeof(fsx::Flags), st));
-    if (h.nonfinite) throw NumErr("solve_periodic: non-finite value after inverse FFT");
+void judge_flags(const fsx::Flags& h, int kind, const std::string& where = "") {
+    if (h.nonfinite) throw NumErr("solve_periodic: non-finite value after inverse FFT" + where);
     if (kind == kGeneral) {
         const double mre = bits_to_double(h.max_re_bits), mim = bits_to_double(h.max_im_bits);
         if (mim > 1e-6 * mre) {
@@ -930,9 +937,17 @@ void check_flags(Device& dev, int kind, cudaStream_t st) {
             std::snprintf(buf, sizeof buf,
                           "solve_periodic: imaginary residue %f exceeds 1e-6 * max |real| (%f); spectrum likely blew up",
                           mim, mre);
-            throw NumErr(buf);
+            throw NumErr(buf + where);
         }
     }
+}
+
+void check_flags(Device& dev, int kind, cudaStream_t st) {
+    fsx::Flags h;
+    FSX_CK(cudaMemcpyAsync(&h, dev.flags.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    FSX_CK(cudaStreamSynchronize(st));
+    FSX_CK(cudaMemsetAsync(dev.flags.p, 0, sizeof(fsx::Flags), st));
+    judge_flags(h, kind);
 }
 
 cudaStream_t stream_of(Device& dev, const fsx_options* opt) {
@@ -1082,6 +1097,69 @@ void solve(const SolveReq& rq) {
     }
 }
 
+// Pipelined batch of independent solves of one shape / kernel / T (host
+// pointers).  Solve i runs on lane i % 2 (own stream and plan copy): its H2D,
+// kernels and D2H are stream-ordered, and the two lanes overlap one solve's
+// D2H with the next one's H2D (PCIe is full duplex) and with kernels.  With
+// pinned host buffers the batch runs at ~max(H2D, D2H, kernels) per solve
+// instead of their sum.  Non-finite / residue checks per solve, reported for
+// the first failing index after the batch completes (outputs of the others
+// are valid).  SURVEY.md §8(f) item 1 (batched slab solves).
+void solve_batch(const fsx_shape* shape, i64 nb, const double* const* a0s, const fsx_kernel* k, u64 T,
+                 double* const* outs, const fsx_options* opt) {
+    const Shape s = parse_shape(shape);
+    const Taps taps = parse_kernel(k);
+    require_fits(taps, s);
+    if (nb < 0) throw SpecErr("fsx_solve_periodic_batch: negative batch size");
+    if (nb > 0 && (!a0s || !outs)) throw SpecErr("fsx: null grid pointer");
+    for (i64 i = 0; i < nb; ++i)
+        if (!a0s[i] || !outs[i]) throw SpecErr("fsx: null grid pointer");
+    const size_t bytes = (size_t)s.values() * 8;
+    if (T == 0) {
+        for (i64 i = 0; i < nb; ++i)
+            if (outs[i] != a0s[i]) std::memmove(outs[i], a0s[i], bytes);
+        return;
+    }
+    if (nb == 0) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    Device& dev = device_for(opt ? opt->device : 0);
+    const int force_general = opt && opt->path == 1;
+    Plan* pl[2];
+    for (int l = 0; l < 2; ++l) {
+        if (!dev.lanes[l]) {
+            FSX_CK(cudaStreamCreateWithFlags(&dev.lanes[l], cudaStreamNonBlocking));
+            FSX_CK(cudaEventCreateWithFlags(&dev.lane_ev[l], cudaEventDisableTiming));
+        }
+        pl[l] = &get_plan(dev, s, taps, force_general, l);
+        pl[l]->d_in.ensure(bytes);
+        pl[l]->d_out.ensure(bytes);
+    }
+    dev.bflags.ensure((size_t)nb * sizeof(fsx::Flags));
+    fsx::Flags* fl = dev.bflags.as<fsx::Flags>();
+    FSX_CK(cudaMemsetAsync(fl, 0, (size_t)nb * sizeof(fsx::Flags), dev.lanes[0]));
+    // order after the caller's stream (if any) and the flag reset
+    if (opt && opt->stream) {
+        FSX_CK(cudaEventRecord(dev.lane_ev[1], reinterpret_cast<cudaStream_t>(opt->stream)));
+        FSX_CK(cudaStreamWaitEvent(dev.lanes[0], dev.lane_ev[1], 0));
+    }
+    FSX_CK(cudaEventRecord(dev.lane_ev[0], dev.lanes[0]));
+    FSX_CK(cudaStreamWaitEvent(dev.lanes[1], dev.lane_ev[0], 0));
+    for (i64 i = 0; i < nb; ++i) {
+        const int l = (int)(i & 1);
+        Plan& p = *pl[l];
+        cudaStream_t st = dev.lanes[l];
+        Stamps sp{&dev, false, st};
+        FSX_CK(cudaMemcpyAsync(p.d_in.p, a0s[i], bytes, cudaMemcpyHostToDevice, st));
+        run_plan(p, dev, taps, nullptr, T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp, fl + i);
+        FSX_CK(cudaMemcpyAsync(outs[i], p.d_out.p, bytes, cudaMemcpyDeviceToHost, st));
+    }
+    std::vector<fsx::Flags> h((size_t)nb);
+    FSX_CK(cudaStreamSynchronize(dev.lanes[1]));
+    FSX_CK(cudaMemcpyAsync(h.data(), fl, (size_t)nb * sizeof(fsx::Flags), cudaMemcpyDeviceToHost, dev.lanes[0]));
+    FSX_CK(cudaStreamSynchronize(dev.lanes[0]));
+    for (i64 i = 0; i < nb; ++i) judge_flags(h[(size_t)i], pl[0]->kind, " (batch item " + std::to_string(i) + ")");
+}
+
 template <class F>
 fsx_status guarded(F&& f) {
     try {
@@ -1187,6 +1265,11 @@ fsx_status fsx_evolve_periodic_naive(const fsx_shape* shape, const double* a0, c
 fsx_status fsx_evolve_periodic_naive_device(const fsx_shape* shape, const double* d_a0, const fsx_kernel* k,
                                             uint64_t T, double* d_out, const fsx_options* opt) {
     return guarded([&] { evolve_naive(shape, d_a0, k, T, d_out, opt, true); });
+}
+
+fsx_status fsx_solve_periodic_batch(const fsx_shape* shape, int64_t nbatch, const double* const* a0s,
+                                    const fsx_kernel* k, uint64_t T, double* const* outs, const fsx_options* opt) {
+    return guarded([&] { solve_batch(shape, nbatch, a0s, k, T, outs, opt); });
 }
 
 fsx_status fsx_device_check(const fsx_options* opt) {

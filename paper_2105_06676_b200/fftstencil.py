@@ -389,6 +389,40 @@ def solve_periodic_implicit(q: StencilKernel, s: StencilKernel, a0: FieldGrid, T
     return FieldGrid(a0.shape, out)
 
 
+def solve_periodic_batch(a0s, k: StencilKernel, T: int, outs=None) -> list:
+    """Pipelined batch of independent solves (fsx_solve_periodic_batch): one
+    shape, kernel and T for every grid.  ``a0s`` are FieldGrids; ``outs``
+    optionally supplies the host result arrays (pinned for full H2D/D2H
+    overlap).  Returns the output arrays."""
+    if T < 0 or T >= 1 << 64:
+        raise SpecError("T must be a nonnegative 64-bit integer")
+    grids = list(a0s)
+    if not grids:
+        return []
+    shape = grids[0].shape
+    for g in grids:
+        if g.shape.dims() != shape.dims() or g.shape.fields() != shape.fields():
+            raise SpecError("solve_periodic_batch: all grids must share one shape")
+    if outs is None:
+        outs = [np.empty_like(g.data) for g in grids]
+    outs = list(outs)
+    if len(outs) != len(grids):
+        raise SpecError("solve_periodic_batch: one output per input")
+    for o in outs:
+        if o.dtype != np.float64 or o.size != grids[0].data.size or not o.flags.c_contiguous:
+            raise SpecError("out must be a contiguous float64 array of the grid's size")
+    n = len(grids)
+    ins = (ctypes.c_void_p * n)(*[g.data.ctypes.data for g in grids])
+    ous = (ctypes.c_void_p * n)(*[o.ctypes.data for o in outs])
+    L = _lib.load()
+    kc, keep = k._c()
+    status = L.fsx_solve_periodic_batch(ctypes.byref(shape._c()), ctypes.c_int64(n), ins, ctypes.byref(kc),
+                                        ctypes.c_uint64(int(T)), ous, ctypes.byref(_opts()))
+    del keep
+    _lib.check(status)
+    return outs
+
+
 def solve_periodic_device(shape: GridShape, d_a0: int, k: StencilKernel, T: int, d_out: int,
                           stream: int | None = None, device: int = 0, path: int = 0, stage_events: int = 0) -> None:
     """Device-resident solve (fsx_solve_periodic_device): pointers are CUDA

@@ -516,3 +516,31 @@ def test_cfg5_protocol(orc):
             continue
         e_orc = rel_l2(want, truth)
         assert e_gpu <= max(1e-12, 1.5 * e_orc), (n, e_gpu, e_orc)
+
+
+# ------------------------------------------------------------------ pipelined batch API
+@pytest.mark.parametrize("dims,m,kind,T", [([256, 128], 1, "box9", 1000), ([1 << 14], 2, "leapfrog", 500),
+                                          ([32, 16, 64], 1, "heat7", 40)])
+def test_batch_equals_single_solves(orc, dims, m, kind, T):
+    """fsx_solve_periodic_batch: each item bitwise equal to its own solve_periodic
+    (two lanes = two plan copies running the same kernels)."""
+    k = K(_case_kernel(kind, len(dims), 9000 + T))
+    n = int(np.prod(dims)) * m
+    grids = [G(dims, orc.splitmix_fill(300 + i, n, True), m) for i in range(5)]
+    outs = fs.solve_periodic_batch(grids, k, T)
+    for g, o in zip(grids, outs):
+        assert np.array_equal(o, fs.solve_periodic(g, k, T).data)
+    assert fs.solve_periodic_batch([], k, T) == []
+    same = fs.solve_periodic_batch(grids[:2], k, 0)
+    assert np.array_equal(same[1], grids[1].data)
+
+
+def test_batch_reports_failing_item():
+    """A non-finite input in item 2 raises NumericError naming it (realize_checked)."""
+    k = fs.StencilKernel(2).add_tap([0, 0], 0.5).add_tap([1, 0], 0.25).add_tap([0, -1], 0.25)
+    grids = [G([64, 64], np.random.default_rng(i).random(4096)) for i in range(4)]
+    grids[2].data[17] = np.nan
+    with pytest.raises(fs.NumericError, match="batch item 2"):
+        fs.solve_periodic_batch(grids, k, 10)
+    with pytest.raises(fs.SpecError):
+        fs.solve_periodic_batch([grids[0], G([32, 32], np.zeros(1024))], k, 10)
