@@ -549,6 +549,8 @@ fsx::FusedSymbol fused_symbol(const Plan& p, const Taps& taps, u64 T) {
     s.P = p.P;
     s.M = p.M;
     s.T = T;
+    // |lam|^2 < neg_mag2  <=>  |lam|^T < 2^-1100 (0 in fp64 for T = 1: never)
+    s.neg_mag2 = std::exp2(-2200.0 / (double)T);
     s.scale = 1.0 / (double)p.cells;
     std::map<i64, int> gid;
     int j = 0;

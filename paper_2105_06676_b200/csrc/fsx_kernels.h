@@ -73,6 +73,7 @@ struct FusedSymbol {
     u64 T = 1;
     double scale = 1.0;          // 1 / prod(dims)
     int real = 0;                // taps symmetric under o -> -o: lam is real
+    double neg_mag2 = 0.0;       // |lam|^2 below this: |lam|^T < 2^-1100 (power skipped, 0)
     i64 c_off = 0;               // slab decomposition: global frequency of local column block start
                                  // (rank 2: kx offset; rank 3: ky offset)
 };

@@ -73,22 +73,21 @@ __device__ __forceinline__ double pow_realv(double lam, u64 T) {
     return acc;
 }
 
-// Element-parallel versions of pow_realv / pow_complex (same operation order
-// per element, so bitwise identical): the loop over the bits of T is uniform,
-// and CH independent elements per step give the FP64 pipe CH-way ILP instead
-// of one latency chain per element.
+// Element-parallel versions of pow_realv / pow_complex (the same loop per
+// element): the loop over the bits of T is uniform, and CH independent
+// elements per step give the FP64 pipe CH-way ILP instead of one latency
+// chain per element.  No underflow short cut here: the loop runs for every
+// element anyway, and where |lam|^T < 2^-1100 its own product underflows to 0
+// (or a subnormal) exactly as the reference's loop does -- the frexp/log2
+// test cost ~13 % of the fused pass's issue slots.
 template <int R, int CH = R>
 __device__ __forceinline__ void pow_real_vec(double (&x)[R], u64 T) {
     static_assert(R % CH == 0, "chunk must divide R");
 #pragma unroll
     for (int c = 0; c < R; c += CH) {
         double acc[CH];
-        bool zero[CH];
 #pragma unroll
-        for (int q = 0; q < CH; ++q) {
-            zero[q] = negligible_power(x[c + q] * x[c + q], T);
-            acc[q] = 1.0;
-        }
+        for (int q = 0; q < CH; ++q) acc[q] = 1.0;
         u64 t = T;
         while (t) {
             if (t & 1) {
@@ -102,7 +101,7 @@ __device__ __forceinline__ void pow_real_vec(double (&x)[R], u64 T) {
             }
         }
 #pragma unroll
-        for (int q = 0; q < CH; ++q) x[c + q] = zero[q] ? 0.0 : acc[q];
+        for (int q = 0; q < CH; ++q) x[c + q] = acc[q];
     }
 }
 
@@ -112,13 +111,8 @@ __device__ __forceinline__ void pow_complex_vec(double2 (&x)[R], u64 T) {
 #pragma unroll
     for (int c = 0; c < R; c += CH) {
         double2 acc[CH];
-        bool zero[CH];
 #pragma unroll
-        for (int q = 0; q < CH; ++q) {
-            const double2 l = x[c + q];
-            zero[q] = negligible_power(fma(l.x, l.x, l.y * l.y), T);
-            acc[q] = make_double2(1.0, 0.0);
-        }
+        for (int q = 0; q < CH; ++q) acc[q] = make_double2(1.0, 0.0);
         u64 t = T;
         while (t) {
             if (t & 1) {
@@ -135,7 +129,47 @@ __device__ __forceinline__ void pow_complex_vec(double2 (&x)[R], u64 T) {
             }
         }
 #pragma unroll
-        for (int q = 0; q < CH; ++q) x[c + q] = zero[q] ? make_double2(0.0, 0.0) : acc[q];
+        for (int q = 0; q < CH; ++q) x[c + q] = acc[q];
+    }
+}
+
+// pow_real_vec with the underflow short cut at warp granularity: elements
+// with |lam|^2 < neg_mag2 (host: 2^(-2200/T)) are 0; a chunk whose elements
+// are negligible in every lane of the warp skips the power loop (a compare
+// and a vote instead of the per-element frexp/log2 test).
+template <int R, int CH>
+__device__ __forceinline__ void pow_real_vec_skip(double (&x)[R], u64 T, double neg_mag2) {
+    static_assert(R % CH == 0, "chunk must divide R");
+#pragma unroll
+    for (int c = 0; c < R; c += CH) {
+        bool neg[CH], all = true;
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+            neg[q] = x[c + q] * x[c + q] < neg_mag2;
+            all &= neg[q];
+        }
+        if (__all_sync(0xffffffffu, all)) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q) x[c + q] = 0.0;
+            continue;
+        }
+        double acc[CH];
+#pragma unroll
+        for (int q = 0; q < CH; ++q) acc[q] = 1.0;
+        u64 t = T;
+        while (t) {
+            if (t & 1) {
+#pragma unroll
+                for (int q = 0; q < CH; ++q) acc[q] *= x[c + q];
+            }
+            t >>= 1;
+            if (t) {
+#pragma unroll
+                for (int q = 0; q < CH; ++q) x[c + q] *= x[c + q];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < CH; ++q) x[c + q] = neg[q] ? 0.0 : acc[q];
     }
 }
 

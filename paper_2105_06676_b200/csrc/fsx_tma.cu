@@ -123,7 +123,7 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
         if ((PRE || TM) && sym.real) {
             double lam[C::R];
             symbol_real<N, C::R, C::TPL>(lam, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
-            pow_real_vec<C::R>(lam, sym.T);
+            pow_real_vec_skip<C::R, 4>(lam, sym.T, sym.neg_mag2);
             if constexpr (TM) {
                 static_assert(C::R == 16, "TMEM parking holds 16 doubles per thread");
                 double h[8];
