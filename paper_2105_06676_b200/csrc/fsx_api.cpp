@@ -587,6 +587,7 @@ fsx::RowPairArgs rowpair_args(const Plan& p, const Taps& taps, u64 T, double2* z
     a.tw_all = dev.tw_all.as<double2>();
     a.wk = p.tables.get(p.t_wk);
     a.T = T;
+    a.neg_mag2 = std::exp2(-2200.0 / (double)T);
     a.scale = 1.0 / (double)(p.m == 1 ? p.dims[0] : p.Mc);
     int j = 0;
     for (const auto& kv : taps.map) {

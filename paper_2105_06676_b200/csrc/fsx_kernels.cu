@@ -395,8 +395,8 @@ __device__ __forceinline__ void pair_mode0(const RowPairArgs& a, double2& zk, do
     const double2 xp = cadd(cconj(e), cmul(wp, cconj(od)));
     double2 yk, yp;
     if (a.real) {
-        yk = cscale(xk, pow_realv(sym1(a, k, L).x, a.T) * a.scale);
-        yp = cscale(xp, pow_realv(sym1(a, kp, L).x, a.T) * a.scale);
+        yk = cscale(xk, pow_realv(sym1(a, k, L).x, a.T, a.neg_mag2) * a.scale);
+        yp = cscale(xp, pow_realv(sym1(a, kp, L).x, a.T, a.neg_mag2) * a.scale);
     } else {
         yk = cscale(cmul(pow_scalar(sym1(a, k, L), a.T), xk), a.scale);
         yp = cscale(cmul(pow_scalar(sym1(a, kp, L), a.T), xp), a.scale);
@@ -434,11 +434,12 @@ __device__ __forceinline__ void pair_mode1(const RowPairArgs& a, double2& zk, do
             }
             t >>= 1;
             if (t) {
-                const double s00 = fma(l00, l00, l01 * l10), s01 = fma(l00, l01, l01 * l11);
-                const double s10 = fma(l10, l00, l11 * l10), s11 = fma(l10, l01, l11 * l11);
+                // L^2 = [[l00^2 + p, l01 tr], [l10 tr, l11^2 + p]], p = l01 l10, tr = l00 + l11
+                const double pp = l01 * l10, tr = l00 + l11;
+                const double s00 = fma(l00, l00, pp), s11 = fma(l11, l11, pp);
+                l01 *= tr;
+                l10 *= tr;
                 l00 = s00;
-                l01 = s01;
-                l10 = s10;
                 l11 = s11;
             }
         }

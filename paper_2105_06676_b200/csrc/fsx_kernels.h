@@ -145,6 +145,7 @@ struct RowPairArgs {
     u64 T = 1;
     double scale = 1.0;
     int real = 0;        // symmetric taps: the (block) symbol is real
+    double neg_mag2 = 0.0;  // scalar symbol: |lam|^2 below this -> |lam|^T < 2^-1100 (power skipped)
     i64 row_split = 0;   // rows stored digit-reversed by a four-step split of N1 (= N1b), 0: natural
 };
 

@@ -49,8 +49,8 @@ __device__ __forceinline__ bool negligible_power(double mag2, u64 T) {
     return l2 * (0.5f * (float)T) < -2200.0f;
 }
 
-__device__ __forceinline__ double2 pow_complex(double2 lam, u64 T) {
-    if (negligible_power(fma(lam.x, lam.x, lam.y * lam.y), T)) return make_double2(0.0, 0.0);
+__device__ __forceinline__ double2 pow_complex(double2 lam, u64 T, double neg_mag2) {
+    if (fma(lam.x, lam.x, lam.y * lam.y) < neg_mag2) return make_double2(0.0, 0.0);
     double2 acc = make_double2(1.0, 0.0), sq = lam;
     u64 t = T;
     while (t) {
@@ -61,8 +61,10 @@ __device__ __forceinline__ double2 pow_complex(double2 lam, u64 T) {
     return acc;
 }
 
-__device__ __forceinline__ double pow_realv(double lam, u64 T) {
-    if (negligible_power(lam * lam, T)) return 0.0;
+// neg_mag2 = 2^(-2200/T) from the host (FusedSymbol): the same short cut as
+// negligible_power with one compare instead of frexp + log2
+__device__ __forceinline__ double pow_realv(double lam, u64 T, double neg_mag2) {
+    if (lam * lam < neg_mag2) return 0.0;
     double acc = 1.0, sq = lam;
     u64 t = T;
     while (t) {
@@ -238,7 +240,7 @@ __device__ __forceinline__ void spectral_regs_at(double2 (&v)[R], int kbase, int
             }
         }
 #pragma unroll
-        for (int q = 0; q < R; ++q) v[q] = cscale(v[q], pow_realv(lam[q], sym.T) * sym.scale);
+        for (int q = 0; q < R; ++q) v[q] = cscale(v[q], pow_realv(lam[q], sym.T, sym.neg_mag2) * sym.scale);
     } else {
         double2 lam[R];
 #pragma unroll
@@ -253,7 +255,7 @@ __device__ __forceinline__ void spectral_regs_at(double2 (&v)[R], int kbase, int
             }
         }
 #pragma unroll
-        for (int q = 0; q < R; ++q) v[q] = cscale(cmul(pow_complex(lam[q], sym.T), v[q]), sym.scale);
+        for (int q = 0; q < R; ++q) v[q] = cscale(cmul(pow_complex(lam[q], sym.T, sym.neg_mag2), v[q]), sym.scale);
     }
 }
 
@@ -283,7 +285,7 @@ __device__ __forceinline__ void spectral_regs(double2 (&v)[R], int t, const Fuse
             }
         }
 #pragma unroll
-        for (int q = 0; q < R; ++q) v[q] = cscale(v[q], pow_realv(lam[q], sym.T) * sym.scale);
+        for (int q = 0; q < R; ++q) v[q] = cscale(v[q], pow_realv(lam[q], sym.T, sym.neg_mag2) * sym.scale);
     } else {
         double2 lam[R];
 #pragma unroll
@@ -302,7 +304,7 @@ __device__ __forceinline__ void spectral_regs(double2 (&v)[R], int t, const Fuse
             }
         }
 #pragma unroll
-        for (int q = 0; q < R; ++q) v[q] = cscale(cmul(pow_complex(lam[q], sym.T), v[q]), sym.scale);
+        for (int q = 0; q < R; ++q) v[q] = cscale(cmul(pow_complex(lam[q], sym.T, sym.neg_mag2), v[q]), sym.scale);
     }
 }
 
