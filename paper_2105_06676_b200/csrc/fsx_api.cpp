@@ -732,9 +732,12 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
         FSX_CK(fsx::launch_c2r_rows(H, d_out, p.rows, p.L, lay, tw, flags, st));
         sp.mark();
     } else if (p.kind == kRowPair1D) {
-        if (d_out != d_a0)
+        // the first column pass reads a0 and writes the output buffer (out of
+        // place); only without a column pass is a0 copied in first
+        if (d_out != d_a0 && p.N1 <= 1)
             FSX_CK(cudaMemcpyAsync(d_out, d_a0, (size_t)p.cells * p.m * 8, cudaMemcpyDeviceToDevice, st));
         double2* z = reinterpret_cast<double2*>(d_out);
+        const double2* z0 = reinterpret_cast<const double2*>(d_a0);
         fsx::StepTwiddle tf;
         tf.mode = 1;
         tf.col_div = 1;
@@ -752,10 +755,10 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
             tB.kmul = p.N1a;
             tB.omul = 1;
             tB.tab = p.tables.get(p.t_M);
-            FSX_CK(fsx::launch_axis_pow2(z, z, gA, -1, tA, tw, st));
+            FSX_CK(fsx::launch_axis_pow2(z0, z, gA, -1, tA, tw, st));
             FSX_CK(fsx::launch_axis_pow2(z, z, gB, -1, tB, tw, st));
         } else if (p.N1 > 1) {
-            FSX_CK(fsx::launch_axis_pow2(z, z, p.colg, -1, tf, tw, st));
+            FSX_CK(fsx::launch_axis_pow2(z0, z, p.colg, -1, tf, tw, st));
         }
         sp.mark();
         const fsx::RowPairArgs a = rowpair_args(p, taps, T, z, dev);
@@ -763,15 +766,17 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
         sp.mark();
         fsx::StepTwiddle ti = tf;
         ti.mode = 2;
+        // the last inverse column pass also does the non-finite scan
         if (p.N1a) {
             tA.mode = 2;
             tB.mode = 2;
             FSX_CK(fsx::launch_axis_pow2(z, z, gB, +1, tB, tw, st));
-            FSX_CK(fsx::launch_axis_pow2(z, z, gA, +1, tA, tw, st));
+            FSX_CK(fsx::launch_axis_pow2(z, z, gA, +1, tA, tw, st, flags));
         } else if (p.N1 > 1) {
-            FSX_CK(fsx::launch_axis_pow2(z, z, p.colg, +1, ti, tw, st));
+            FSX_CK(fsx::launch_axis_pow2(z, z, p.colg, +1, ti, tw, st, flags));
+        } else {
+            FSX_CK(fsx::launch_finite_check(d_out, p.cells * p.m, flags, st));
         }
-        FSX_CK(fsx::launch_finite_check(d_out, p.cells * p.m, flags, st));
         sp.mark();
     } else {
         double2* Z = p.work.as<double2>();

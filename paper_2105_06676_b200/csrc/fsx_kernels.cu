@@ -177,7 +177,8 @@ k_contig(const double2* in, double2* out, i64 nlines, i64 pitch, const double2* 
 // Strided lines: W adjacent columns per CTA, the axis in shared memory.
 template <int N, int SIGN, int TWM>
 __global__ void __launch_bounds__(Cfg<N>::W * Cfg<N>::TPL, Cfg<N>::MINB_W)
-k_strided(const double2* in, double2* out, AxisGeom g, StepTwiddle st, const double2* __restrict__ tw_all) {
+k_strided(const double2* in, double2* out, AxisGeom g, StepTwiddle st, const double2* __restrict__ tw_all,
+          Flags* flags) {
     using C = Cfg<N>;
     using F = LineFFT<N, SIGN>;
     extern __shared__ double2 sm[];
@@ -207,6 +208,12 @@ k_strided(const double2* in, double2* out, AxisGeom g, StepTwiddle st, const dou
     if (ok) {
 #pragma unroll
         for (int q = 0; q < C::R; ++q) out[base + (i64)(t + q * C::TPL) * g.inner] = v[q];
+    }
+    if (flags) {  // last pass of a solve: the non-finite scan rides along (realize_checked)
+        bool bad = false;
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) bad |= ok && (!isfinite(v[q].x) || !isfinite(v[q].y));
+        flag_nonfinite(bad, flags);
     }
 }
 
@@ -815,7 +822,7 @@ static int grid_for(i64 n, int threads) {
 
 template <int N>
 static cudaError_t axis_pow2_n(const double2* in, double2* out, const AxisGeom& g, int sign,
-                               const StepTwiddle& st, const double2* tw, cudaStream_t s) {
+                               const StepTwiddle& st, const double2* tw, cudaStream_t s, Flags* flags) {
     using C = Cfg<N>;
     if (g.inner == 1 && st.mode == 0) {
         const size_t smem = (size_t)C::LINES * C::LSL * sizeof(double2);
@@ -823,39 +830,40 @@ static cudaError_t axis_pow2_n(const double2* in, double2* out, const AxisGeom& 
         auto kf = sign < 0 ? k_contig<N, -1> : k_contig<N, +1>;
         kernel_prepare((const void*)kf, smem);
         kf<<<blocks, C::LINES * C::TPL, smem, s>>>(in, out, g.outer, g.block, tw);
+        if (flags) return launch_finite_check(reinterpret_cast<const double*>(out), 2 * g.outer * g.block, flags, s);
         return cudaGetLastError();
     }
     const size_t smem = (size_t)C::W * C::LSW * sizeof(double2);
     const i64 tiles = (g.ncols + C::W - 1) / C::W;
     const i64 blocks = g.outer * tiles;
-    void (*kf)(const double2*, double2*, AxisGeom, StepTwiddle, const double2*);
+    void (*kf)(const double2*, double2*, AxisGeom, StepTwiddle, const double2*, Flags*);
     if (sign < 0) kf = st.mode == 1 ? k_strided<N, -1, 1> : st.mode == 2 ? k_strided<N, -1, 2> : k_strided<N, -1, 0>;
     else kf = st.mode == 1 ? k_strided<N, +1, 1> : st.mode == 2 ? k_strided<N, +1, 2> : k_strided<N, +1, 0>;
     kernel_prepare((const void*)kf, smem);
-    kf<<<(unsigned)blocks, C::W * C::TPL, smem, s>>>(in, out, g, st, tw);
+    kf<<<(unsigned)blocks, C::W * C::TPL, smem, s>>>(in, out, g, st, tw, flags);
     return cudaGetLastError();
 }
 
 cudaError_t launch_axis_pow2(const double2* in, double2* out, const AxisGeom& g, int sign,
-                             const StepTwiddle& st, const double2* tw, cudaStream_t s) {
-    if (pipe_enabled() && pipe_cols_ok(g.n) && g.inner > 1 && st.mode == 0 && in == out) {
+                             const StepTwiddle& st, const double2* tw, cudaStream_t s, Flags* flags) {
+    if (pipe_enabled() && pipe_cols_ok(g.n) && g.inner > 1 && st.mode == 0 && in == out && !flags) {
         FusedSymbol none;
         return launch_cols_pipe(out, g, sign < 0 ? 0 : 1, none, tw, s);
     }
     switch (g.n) {
-        case 2: return axis_pow2_n<2>(in, out, g, sign, st, tw, s);
-        case 4: return axis_pow2_n<4>(in, out, g, sign, st, tw, s);
-        case 8: return axis_pow2_n<8>(in, out, g, sign, st, tw, s);
-        case 16: return axis_pow2_n<16>(in, out, g, sign, st, tw, s);
-        case 32: return axis_pow2_n<32>(in, out, g, sign, st, tw, s);
-        case 64: return axis_pow2_n<64>(in, out, g, sign, st, tw, s);
-        case 128: return axis_pow2_n<128>(in, out, g, sign, st, tw, s);
-        case 256: return axis_pow2_n<256>(in, out, g, sign, st, tw, s);
-        case 512: return axis_pow2_n<512>(in, out, g, sign, st, tw, s);
-        case 1024: return axis_pow2_n<1024>(in, out, g, sign, st, tw, s);
-        case 2048: return axis_pow2_n<2048>(in, out, g, sign, st, tw, s);
-        case 4096: return axis_pow2_n<4096>(in, out, g, sign, st, tw, s);
-        case 8192: return axis_pow2_n<8192>(in, out, g, sign, st, tw, s);
+        case 2: return axis_pow2_n<2>(in, out, g, sign, st, tw, s, flags);
+        case 4: return axis_pow2_n<4>(in, out, g, sign, st, tw, s, flags);
+        case 8: return axis_pow2_n<8>(in, out, g, sign, st, tw, s, flags);
+        case 16: return axis_pow2_n<16>(in, out, g, sign, st, tw, s, flags);
+        case 32: return axis_pow2_n<32>(in, out, g, sign, st, tw, s, flags);
+        case 64: return axis_pow2_n<64>(in, out, g, sign, st, tw, s, flags);
+        case 128: return axis_pow2_n<128>(in, out, g, sign, st, tw, s, flags);
+        case 256: return axis_pow2_n<256>(in, out, g, sign, st, tw, s, flags);
+        case 512: return axis_pow2_n<512>(in, out, g, sign, st, tw, s, flags);
+        case 1024: return axis_pow2_n<1024>(in, out, g, sign, st, tw, s, flags);
+        case 2048: return axis_pow2_n<2048>(in, out, g, sign, st, tw, s, flags);
+        case 4096: return axis_pow2_n<4096>(in, out, g, sign, st, tw, s, flags);
+        case 8192: return axis_pow2_n<8192>(in, out, g, sign, st, tw, s, flags);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -172,8 +172,9 @@ struct Flags {
 // no driver attribute/occupancy queries after the first.
 int kernel_prepare(const void* fn, size_t smem, int threads = 0);
 // Twiddle tables: tw_all[N + x] = exp(-2 pi i x / N) for pow2 N <= kMaxTwPow2.
+// flags != nullptr: the output is also scanned for non-finite values
 cudaError_t launch_axis_pow2(const double2* in, double2* out, const AxisGeom& g, int sign,
-                             const StepTwiddle& st, const double2* tw_all, cudaStream_t s);
+                             const StepTwiddle& st, const double2* tw_all, cudaStream_t s, Flags* flags = nullptr);
 cudaError_t launch_axis_direct(const double2* in, double2* out, const AxisGeom& g, int sign,
                                const PhaseTable& tab, cudaStream_t s);
 cudaError_t launch_r2c_rows(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P,
