@@ -210,7 +210,18 @@ def run_gpu_slab(args, cfg, ws, rank, local):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = local
     shape, kern = cfg.shape(), cfg.kernel()
-    solver = SlabSolver(shape, kern, cfg.T)
+    exchange = args.exchange
+    if exchange == "auto":
+        exchange = "p2p" if len(cfg.dims) == 2 else "nccl"
+    exchange_note = None
+    try:
+        solver = SlabSolver(shape, kern, cfg.T, exchange=exchange)
+    except Exception as e:  # symmetric memory unavailable: the NCCL all-to-all path
+        if args.exchange != "auto":
+            raise
+        exchange_note = f"p2p unavailable ({type(e).__name__}: {e}); NCCL all-to-all used"
+        exchange = "nccl"
+        solver = SlabSolver(shape, kern, cfg.T, exchange="nccl")
     nloc = solver.local_cells()
     start = rank * nloc
     host = cfg.initial(start, nloc)
@@ -240,13 +251,34 @@ def run_gpu_slab(args, cfg, ws, rank, local):
     step = sum(e[0].elapsed_time(e[5]) for e in ev) / args.steps
     a2a = sum(e[1].elapsed_time(e[2]) + e[3].elapsed_time(e[4]) for e in ev) / args.steps
     fused = sum(e[2].elapsed_time(e[3]) for e in ev) / args.steps
-    t = torch.tensor([step, a2a, fused], dtype=torch.float64, device="cuda")
+    rowsx = sum(e[0].elapsed_time(e[1]) + e[4].elapsed_time(e[5]) for e in ev) / args.steps
+    t = torch.tensor([step, a2a, fused, rowsx], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    step, a2a, fused = (float(x) for x in t)
+    step, a2a, fused, rowsx = (float(x) for x in t)
     cells_T = cfg.cells() * cfg.T
     value = cells_T / (step * 1e-3)
     sent = 2 * solver.a2a_bytes()
-    nvl_gbs = sent / (a2a * 1e-3) / 1e9 if a2a > 0 else None
+    # nccl: the two all-to-alls; p2p: the NVLink traffic rides inside the row
+    # kernels, so the row passes' time is the transfer window
+    xfer_ms = a2a if exchange == "nccl" else rowsx
+    nvl_gbs = sent / (xfer_ms * 1e-3) / 1e9 if xfer_ms > 0 else None
+    # e2e: every rank's slab H2D from pinned memory + solve + D2H, max over ranks
+    pin_in = torch.from_numpy(host).pin_memory()
+    pin_out = torch.empty_like(pin_in).pin_memory()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        d_in.copy_(pin_in, non_blocking=True)
+        solver.solve(d_in, d_out)
+        pin_out.copy_(d_out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    et = torch.tensor([(time.perf_counter() - t0) / args.steps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_val = cells_T / float(et[0])
+    fs.device_check(stream=torch.cuda.current_stream().cuda_stream, device=dev)
+    peak, peak_src = load_peaks()
+    fused_bytes = 2 * solver.info["xbuf_bytes"]  # the rank's column tile in and out
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -254,10 +286,17 @@ def run_gpu_slab(args, cfg, ws, rank, local):
         "config": {"workload": cfg.name + ": " + cfg.description, "grid": cfg.dims, "fields": cfg.fields,
                    "T": cfg.T, "parallelism": f"slab{ws} (axis 0)", "wall_s_timed_region": wall,
                    "l2": f"flushed before every step ({FLUSH_BYTES >> 20} MiB write)"},
-        "nvlink": {"a2a_ms_per_step": a2a, "bytes_sent_per_rank_per_step": sent, "achieved_gbs": nvl_gbs,
+        "nvlink": {"exchange": exchange, "exchange_note": exchange_note,
+                   "transfer_ms_per_step": xfer_ms, "barrier_or_a2a_ms_per_step": a2a,
+                   "bytes_sent_per_rank_per_step": sent, "achieved_gbs": nvl_gbs,
                    "peak_gbs": 900.0, "frac": (nvl_gbs / 900.0) if nvl_gbs else None},
-        "roofline": {"bound": "hbm", "kernel": "fused spectral pass (per rank)", "kernel_ms": fused},
-        "gpu_launches": None, "clocks": clocks,
+        "roofline": {"bound": "hbm", "kernel": "k_cols_tma (fused spectral pass, per rank)", "kernel_ms": fused,
+                     "achieved": fused_bytes / (fused * 1e-3) / 1e9 if fused > 0 else None, "peak": peak,
+                     "unit": "GB/s", "frac": (fused_bytes / (fused * 1e-3) / 1e9 / peak) if fused > 0 else None,
+                     "traffic": None, "alg_bytes_per_launch": fused_bytes, "peak_source": peak_src},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": nloc * 8 * ws, "d2h_bytes_per_step": nloc * 8 * ws,
+                "mode": "per rank: pinned slab H2D + SlabSolver.solve + D2H, max over ranks"},
+        "gpu_launches": 3 * args.steps, "clocks": clocks,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -459,6 +498,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", choices=["auto", "nccl", "p2p"], default="auto",
+                    help="slab exchange for N > 1: p2p = fused into the row kernels over NVLink peer memory "
+                         "(2D; auto falls back to nccl if symmetric memory is unavailable)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of slabs")
     ap.add_argument("--slab", action="store_true", help="use the slab-decomposed path even at N=1 (under torchrun)")

@@ -182,6 +182,20 @@ fsx_status fsx_slab_spectral(const fsx_shape* global, const fsx_kernel* k, uint6
 fsx_status fsx_slab_inverse(const fsx_shape* global, int32_t nranks, int32_t rank, const double* d_send,
                             double* d_local_out, const fsx_options* opt);
 
+/* The same decomposition with the exchange fused into the row passes (2D):
+ * d_recv_peers is a DEVICE array of nranks device pointers, entry d = rank
+ * d's exchange buffer (xbuf_bytes, mapped into this process: NVLink peer
+ * memory, e.g. torch symmetric memory's buffer_ptrs_dev).  One solve is
+ *     barrier; fsx_slab_forward_p2p   (R2C rows store block d into rank d's buffer)
+ *     barrier; fsx_slab_spectral      (own buffer, in place)
+ *     barrier; fsx_slab_inverse_p2p   (C2R rows load their blocks from every rank)
+ * where "barrier" is a cross-rank device barrier on the same stream.  No
+ * all-to-all: the NVLink traffic overlaps the row FFTs inside the kernels. */
+fsx_status fsx_slab_forward_p2p(const fsx_shape* global, int32_t nranks, int32_t rank, const double* d_local_in,
+                                void* const* d_recv_peers, const fsx_options* opt);
+fsx_status fsx_slab_inverse_p2p(const fsx_shape* global, int32_t nranks, int32_t rank, void* const* d_recv_peers,
+                                double* d_local_out, const fsx_options* opt);
+
 /* ---------------------------------------------------------------- building blocks
  * (host pointers, complex = interleaved fp64) */
 

@@ -95,6 +95,8 @@ EXPORTS = (
     "fsx_slab_forward",
     "fsx_slab_spectral",
     "fsx_slab_inverse",
+    "fsx_slab_forward_p2p",
+    "fsx_slab_inverse_p2p",
     "fsx_multi_fft",
     "fsx_spectrum_from_kernel",
     "fsx_pow_spectrum",

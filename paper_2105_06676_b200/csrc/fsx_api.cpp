@@ -1355,6 +1355,43 @@ fsx_status fsx_slab_inverse(const fsx_shape* global, int32_t nranks, int32_t ran
     });
 }
 
+// Fused row pass + exchange over NVLink peer memory (2D): the R2C rows store
+// column block d straight into rank d's exchange buffer (recv_peers[d]); the
+// inverse C2R rows load their blocks from every rank's buffer.  The caller
+// separates the stages with a cross-rank barrier (symmetric-memory signal
+// pads), which replaces the two NCCL all-to-alls.
+SlabPlan& slab_p2p_plan(const fsx_shape* global, int32_t nranks, int32_t rank, void* const* peers) {
+    if (!peers) throw SpecErr("slab p2p: null peer pointer array");
+    SlabPlan& sp = slab_plan(global, nranks, rank);
+    if (sp.dims.size() != 2) throw SpecErr("slab p2p: rank-2 grids only (3D exchanges through NCCL)");
+    return sp;
+}
+
+fsx_status fsx_slab_forward_p2p(const fsx_shape* global, int32_t nranks, int32_t rank, const double* d_local_in,
+                                void* const* d_recv_peers, const fsx_options* opt) {
+    return guarded([&] {
+        if (!d_local_in) throw SpecErr("fsx_slab_forward_p2p: null pointer");
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(opt ? opt->device : 0);
+        SlabPlan& sp = slab_p2p_plan(global, nranks, rank, d_recv_peers);
+        fsx::RowLayout lay{0, sp.CB, sp.n0l, reinterpret_cast<double2* const*>(d_recv_peers), (i64)rank * sp.n0l};
+        FSX_CK(fsx::launch_r2c_rows(d_local_in, nullptr, sp.n0l, sp.L, lay, dev.tw_all.as<double2>(), stream_of(dev, opt)));
+    });
+}
+
+fsx_status fsx_slab_inverse_p2p(const fsx_shape* global, int32_t nranks, int32_t rank, void* const* d_recv_peers,
+                                double* d_local_out, const fsx_options* opt) {
+    return guarded([&] {
+        if (!d_local_out) throw SpecErr("fsx_slab_inverse_p2p: null pointer");
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(opt ? opt->device : 0);
+        SlabPlan& sp = slab_p2p_plan(global, nranks, rank, d_recv_peers);
+        fsx::RowLayout lay{0, sp.CB, sp.n0l, reinterpret_cast<double2* const*>(d_recv_peers), (i64)rank * sp.n0l};
+        FSX_CK(fsx::launch_c2r_rows(nullptr, d_local_out, sp.n0l, sp.L, lay, dev.tw_all.as<double2>(),
+                                    dev.flags.as<fsx::Flags>(), stream_of(dev, opt)));
+    });
+}
+
 fsx_status fsx_plan_describe(const fsx_shape* shape, const fsx_kernel* k, const fsx_options* opt,
                              fsx_plan_info* info) {
     return guarded([&] {

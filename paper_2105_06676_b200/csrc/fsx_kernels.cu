@@ -273,9 +273,10 @@ k_r2c_rows(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
         const double2 e = cscale(cadd(zk, zm), 0.5);
         const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
         const double2 w = __ldg(tw_all + 2 * M + k);  // exp(-2 pi i k / L)
-        H[lay.at(row, k)] = cadd(e, cmul(w, od));
-        if (k == 0) H[lay.at(row, M)] = make_double2(zk.x - zk.y, 0.0);
+        *lay.ptr(H, row, k) = cadd(e, cmul(w, od));
+        if (k == 0) *lay.ptr(H, row, M) = make_double2(zk.x - zk.y, 0.0);
     }
+    if (lay.peers) __threadfence_system();  // remote (NVLink) stores ordered before the rank barrier
 }
 
 // Inverse: Z[k] = (X[k] + conj X[M-k]) + i conj(W_L^k) (X[k] - conj X[M-k]),
@@ -296,10 +297,10 @@ k_c2r_rows(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
     double2 v[C::R];
 #pragma unroll
     for (int q = 0; q < C::R; ++q) {
-        v[q] = ok ? H[lay.at(row, t + q * C::TPL)] : make_double2(0.0, 0.0);
+        v[q] = ok ? *lay.ptr(H, row, t + q * C::TPL) : make_double2(0.0, 0.0);
         line[swz(t + q * C::TPL)] = v[q];
     }
-    if (t == 0) nyq[b] = ok ? H[lay.at(row, M)] : make_double2(0.0, 0.0);
+    if (t == 0) nyq[b] = ok ? *lay.ptr(H, row, M) : make_double2(0.0, 0.0);
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < C::R; ++q) {
@@ -933,8 +934,7 @@ int kernel_prepare(const void* fn, size_t smem, int threads) {
 
 cudaError_t launch_r2c_rows(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw,
                             cudaStream_t s) {
-    if (pipe_enabled() && pipe_rows_ok(L / 2) && rows_variant() == 3 && P.blk == 0)
-        return launch_r2c_bulk(x, H, nrows, L, P.P, tw, s);
+    if (pipe_enabled() && pipe_rows_ok(L / 2) && rows_variant() == 3) return launch_r2c_bulk(x, H, nrows, L, P, tw, s);
     if (pipe_enabled() && pipe_rows_ok(L / 2) && rows_variant() == 2) return launch_r2c_reg(x, H, nrows, L, P, tw, s);
     if (pipe_enabled() && pipe_rows_ok(L / 2) && (rows_variant() == 1 || rows_variant() == 3)) return launch_r2c_pipe(x, H, nrows, L, P, tw, s);
     switch (L / 2) {
@@ -947,8 +947,7 @@ cudaError_t launch_r2c_rows(const double* x, double2* H, i64 nrows, i64 L, const
 
 cudaError_t launch_c2r_rows(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw, Flags* f,
                             cudaStream_t s) {
-    if (pipe_enabled() && pipe_rows_ok(L / 2) && rows_variant() == 3 && P.blk == 0)
-        return launch_c2r_bulk(H, x, nrows, L, P.P, tw, f, s);
+    if (pipe_enabled() && pipe_rows_ok(L / 2) && rows_variant() == 3) return launch_c2r_bulk(H, x, nrows, L, P, tw, f, s);
     if (pipe_enabled() && pipe_rows_ok(L / 2) && rows_variant() == 2) return launch_c2r_reg(H, x, nrows, L, P, tw, f, s);
     if (pipe_enabled() && pipe_rows_ok(L / 2) && (rows_variant() == 1 || rows_variant() == 3)) return launch_c2r_pipe(H, x, nrows, L, P, tw, f, s);
     switch (L / 2) {

@@ -93,14 +93,34 @@ __host__ __device__ inline void fused_col_freqs(const FusedSymbol& s, i64 c, i64
 // Row-kernel output/input layout: pitch rows (blk == 0: element (row, k) at
 // row * P + k) or the slab all-to-all layout (blk > 0: column block
 // d = k / blk of all rows is contiguous: d * nrows * blk + row * blk + k % blk).
+//
+// Peer layout (peers != nullptr, blk > 0): column block d of every row lives
+// directly in rank d's exchange buffer, peers[d] (a device array of P device
+// pointers, NVLink peer memory): element (row, k) at
+// peers[d][(row_off + row) * blk + k % blk] -- the [n0][blk] column tile rank
+// d transforms.  The row kernels then store / load across NVLink themselves,
+// fusing the all-to-all into the row passes.
 struct RowLayout {
     i64 P = 0;
     i64 blk = 0;
     i64 nrows = 0;
+    double2* const* peers = nullptr;
+    i64 row_off = 0;
+    // (k and blk < 2^31: 32-bit division, the 64-bit one is a long software sequence)
     __host__ __device__ i64 at(i64 row, i64 k) const {
         if (blk == 0) return row * P + k;
-        const i64 d = k / blk;
-        return d * nrows * blk + row * blk + (k - d * blk);
+        const int d = (int)k / (int)blk;
+        return (i64)d * nrows * blk + row * blk + (k - (i64)d * blk);
+    }
+    __device__ double2* ptr(double2* base, i64 row, i64 k) const {
+        if (peers) {
+            const int d = (int)k / (int)blk;
+            return peers[d] + (row_off + row) * blk + (k - (i64)d * blk);
+        }
+        return base + at(row, k);
+    }
+    __device__ const double2* ptr(const double2* base, i64 row, i64 k) const {
+        return ptr(const_cast<double2*>(base), row, k);
     }
 };
 
@@ -109,6 +129,11 @@ template <bool BLK>
 __host__ __device__ inline i64 row_at(const RowLayout& l, i64 row, i64 k) {
     if constexpr (BLK) return l.at(row, k);
     else return row * l.P + k;
+}
+template <bool BLK, class Ptr>
+__device__ inline Ptr row_ptr(Ptr H, const RowLayout& l, i64 row, i64 k) {
+    if constexpr (BLK) return l.ptr(H, row, k);
+    else return H + row * l.P + k;
 }
 
 // General spectral stage over a full complex spectrum with m fields.
@@ -207,9 +232,9 @@ cudaError_t launch_c2r_pipe(const double2* H, double* x, i64 nrows, i64 L, const
 cudaError_t launch_cols_pipe(double2* H, const AxisGeom& g, int mode, const FusedSymbol& sym,
                              const double2* tw_all, cudaStream_t s);
 int rows_variant();
-cudaError_t launch_r2c_bulk(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw_all,
+cudaError_t launch_r2c_bulk(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& lay, const double2* tw_all,
                             cudaStream_t s);
-cudaError_t launch_c2r_bulk(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw_all,
+cudaError_t launch_c2r_bulk(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& lay, const double2* tw_all,
                             Flags* flags, cudaStream_t s);
 cudaError_t launch_r2c_reg(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw_all,
                            cudaStream_t s);

@@ -84,12 +84,13 @@ k_r2c_pipe(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
             const double2 e = cscale(cadd(zk, zm), 0.5);
             const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
             const double2 w = __ldg(tw_all + 2 * M + k);
-            H[row_at<BLK>(lay, row, k)] = cadd(e, cmul(w, od));
-            if (k == 0) H[row_at<BLK>(lay, row, M)] = make_double2(zk.x - zk.y, 0.0);
+            *row_ptr<BLK>(H, lay, row, k) = cadd(e, cmul(w, od));
+            if (k == 0) *row_ptr<BLK>(H, lay, row, M) = make_double2(zk.x - zk.y, 0.0);
         }
         __syncthreads();
     }
     cp_wait<0>();
+    if (BLK && lay.peers) __threadfence_system();  // remote (NVLink) stores ordered before the rank barrier
 }
 
 // ------------------------------------------------------------------ rows: C2R
@@ -105,8 +106,8 @@ k_c2r_pipe(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
     auto issue = [&](i64 row, int s) {
         double2* dst = sm + s * M;
 #pragma unroll
-        for (int q = 0; q < C::R; ++q) cp_async16(dst + swz(t + q * C::TPL), H + row_at<BLK>(lay, row, t + q * C::TPL));
-        if (t == 0) cp_async16(&nyq[s], H + row_at<BLK>(lay, row, M));
+        for (int q = 0; q < C::R; ++q) cp_async16(dst + swz(t + q * C::TPL), row_ptr<BLK>(H, lay, row, t + q * C::TPL));
+        if (t == 0) cp_async16(&nyq[s], row_ptr<BLK>(H, lay, row, M));
     };
     bool bad = false;
     i64 row = blockIdx.x;
@@ -160,9 +161,11 @@ struct BulkCfg {
     static constexpr int MINB = ST == 2 ? PCfg<M>::MINB_ROW : 2;
 };
 
-template <int M, int ST>
+// BLK: the output goes to the slab exchange layout (blocked, or straight
+// into the peers' buffers over NVLink, RowLayout::ptr); otherwise pitch rows.
+template <int M, int ST, bool BLK>
 __global__ void __launch_bounds__(PCfg<M>::TPL, BulkCfg<M, ST>::MINB)
-k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, i64 P,
+k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, RowLayout lay,
            const double2* __restrict__ tw_all) {
     using F = LineFFT<M, -1, true, true>;
     constexpr int TPL = PCfg<M>::TPL, R = 16;
@@ -198,7 +201,7 @@ k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
 #pragma unroll
         for (int q = 0; q < R; ++q) v[q] = line[t + q * TPL];
         F::run(v, t, line, tw_all + M);
-        double2* h = H + row * P;
+        auto h = [&](int k) -> double2& { return *row_ptr<BLK>(H, lay, row, k); };
         if constexpr (F::PAIRED) {
             // v[i + 2u] = Z[item(i) + u M/8]; the mirror M - k lives in this thread.
             // Split twiddle W_L^(j + u M/8) = W_L^j * W_16^u: one load per item.
@@ -215,8 +218,8 @@ k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
                     const double2 zm = cconj(t == 0 ? v[qz] : v[qp]);
                     const double2 e = cscale(cadd(zk, zm), 0.5);
                     const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
-                    h[j + u * (M / 8)] = cadd(e, cmul(cmul_const<u, 16, -1>(wj), od));
-                    if (i == 0 && u == 0 && t == 0) h[M] = make_double2(zk.x - zk.y, 0.0);
+                    h(j + u * (M / 8)) = cadd(e, cmul(cmul_const<u, 16, -1>(wj), od));
+                    if (i == 0 && u == 0 && t == 0) h(M) = make_double2(zk.x - zk.y, 0.0);
                 });
             }
         } else {
@@ -232,8 +235,8 @@ k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
                 const double2 zm = cconj(line[swz((M - k) & (M - 1))]);
                 const double2 e = cscale(cadd(zk, zm), 0.5);
                 const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
-                h[k] = cadd(e, cmul(cmul_const<q, 32, -1>(wt), od));
-                if (k == 0) h[M] = make_double2(zk.x - zk.y, 0.0);
+                h(k) = cadd(e, cmul(cmul_const<q, 32, -1>(wt), od));
+                if (k == 0) h(M) = make_double2(zk.x - zk.y, 0.0);
             });
         }
         fence_proxy_async();  // generic writes of this stage before its next bulk fill
@@ -243,16 +246,33 @@ k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
             bulk_load(sm, x + nxt * L, BYTES, &bar[0]);
         }
     }
+    if (BLK && lay.peers) __threadfence_system();  // remote (NVLink) stores ordered before the rank barrier
 }
 
-template <int M, int ST>
+// One half-spectrum row (M + 1 complex) into shared memory: one bulk copy
+// from a pitch row, or one per column block of the slab exchange layout
+// (local blocked buffer or the owning ranks' buffers over NVLink).
+template <int M, bool BLK>
+__device__ __forceinline__ void load_hrow(double2* dst, const double2* H, const RowLayout& lay, i64 row,
+                                          unsigned long long* bar) {
+    mbar_expect_tx(bar, (M + 1) * (unsigned)sizeof(double2));
+    if constexpr (!BLK) {
+        bulk_load(dst, H + row * lay.P, (M + 1) * (unsigned)sizeof(double2), bar);
+    } else {
+        for (i64 k0 = 0; k0 <= M; k0 += lay.blk) {
+            const i64 len = (M + 1 - k0) < lay.blk ? (M + 1 - k0) : lay.blk;
+            bulk_load(dst + k0, lay.ptr(H, row, k0), (unsigned)(len * sizeof(double2)), bar);
+        }
+    }
+}
+
+template <int M, int ST, bool BLK>
 __global__ void __launch_bounds__(PCfg<M>::TPL, BulkCfg<M, ST>::MINB)
-k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, i64 P,
+k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, RowLayout lay,
            const double2* __restrict__ tw_all, Flags* flags) {
     using F = LineFFT<M, +1, true>;
     constexpr int TPL = PCfg<M>::TPL, R = 16;
     constexpr int SS = M + 8;  // stage stride: M + 1 elements, 128 B aligned
-    constexpr unsigned BYTES = (M + 1) * sizeof(double2);
     extern __shared__ __align__(128) double2 sm[];
     __shared__ __align__(8) unsigned long long bar[ST];
     const int t = threadIdx.x;
@@ -264,19 +284,13 @@ k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
         for (int b = 0; b < ST; ++b) mbar_init(&bar[b], 1);
         mbar_init_fence();
         pdl_wait();  // H is the predecessor's output
-        if (row < nrows) {
-            mbar_expect_tx(&bar[0], BYTES);
-            bulk_load(sm, H + row * P, BYTES, &bar[0]);
-        }
+        if (row < nrows) load_hrow<M, BLK>(sm, H, lay, row, &bar[0]);
     }
     __syncthreads();
     unsigned par = 0;
     for (int s = 0; row < nrows; row += G, s = (ST == 2 ? s ^ 1 : 0)) {
         const i64 nxt = row + G;
-        if (ST == 2 && t == 0 && nxt < nrows) {
-            mbar_expect_tx(&bar[s ^ 1], BYTES);
-            bulk_load(sm + (s ^ 1) * SS, H + nxt * P, BYTES, &bar[s ^ 1]);
-        }
+        if (ST == 2 && t == 0 && nxt < nrows) load_hrow<M, BLK>(sm + (s ^ 1) * SS, H, lay, nxt, &bar[s ^ 1]);
         if (nxt >= nrows) pdl_trigger();
         mbar_wait(&bar[s], (par >> s) & 1u);
         par ^= 1u << s;
@@ -302,10 +316,7 @@ k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
         }
         fence_proxy_async();
         __syncthreads();
-        if (ST == 1 && t == 0 && nxt < nrows) {
-            mbar_expect_tx(&bar[0], BYTES);
-            bulk_load(sm, H + nxt * P, BYTES, &bar[0]);
-        }
+        if (ST == 1 && t == 0 && nxt < nrows) load_hrow<M, BLK>(sm, H, lay, nxt, &bar[0]);
     }
     const unsigned any = __ballot_sync(0xffffffffu, bad);
     if (any && (threadIdx.x & 31) == 0) atomicOr(&flags->nonfinite, 1u);
@@ -359,10 +370,10 @@ k_r2c_reg(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 
                     const double2 zk = v[i + 2 * u];
                     const double2 zp = t == 0 ? v[qz] : v[qp];
                     const double2 xk = r2c_split(zk, zp, __ldg(tw_all + 2 * M + k));
-                    H[lay.at(row, k)] = xk;
+                    *lay.ptr(H, row, k) = xk;
                     if (i == 0 && u == 0 && t == 0) {
-                        H[lay.at(row, 0)] = make_double2(zk.x + zk.y, 0.0);
-                        H[lay.at(row, M)] = make_double2(zk.x - zk.y, 0.0);
+                        *lay.ptr(H, row, 0) = make_double2(zk.x + zk.y, 0.0);
+                        *lay.ptr(H, row, M) = make_double2(zk.x - zk.y, 0.0);
                     }
                 }
         } else {
@@ -375,8 +386,8 @@ k_r2c_reg(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 
                 const int k = t + q * TPL;
                 const double2 zk = v[q];
                 const double2 xk = r2c_split(zk, sm[swz((M - k) & (M - 1))], __ldg(tw_all + 2 * M + k));
-                H[lay.at(row, k)] = xk;
-                if (k == 0) H[lay.at(row, M)] = make_double2(zk.x - zk.y, 0.0);
+                *lay.ptr(H, row, k) = xk;
+                if (k == 0) *lay.ptr(H, row, M) = make_double2(zk.x - zk.y, 0.0);
             }
         }
     };
@@ -406,14 +417,14 @@ k_c2r_reg(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 
     bool bad = false;
     auto load = [&](i64 row, double2 (&v)[R]) {
 #pragma unroll
-        for (int q = 0; q < R; ++q) v[q] = H[lay.at(row, t + q * TPL)];
+        for (int q = 0; q < R; ++q) v[q] = *lay.ptr(H, row, t + q * TPL);
     };
     auto process = [&](i64 row, double2 (&v)[R]) {
         // mirror X[M - k] re-read through L1 (this CTA just streamed the row)
 #pragma unroll
         for (int q = 0; q < R; ++q) {
             const int k = t + q * TPL;
-            const double2 xm = cconj(__ldg(H + lay.at(row, M - k)));
+            const double2 xm = cconj(*lay.ptr(H, row, M - k));
             const double2 e = cadd(v[q], xm);
             const double2 od = cmulc(csub(v[q], xm), __ldg(tw_all + 2 * M + k));
             v[q] = cadd(e, cmul_si<+1>(od));
@@ -642,33 +653,40 @@ static int row_stages(int M) {
     return v == 1 ? 1 : 2;  // 1 stage x 2 CTAs measured slower at M = 4096 (269 vs 254 us)
 }
 
-template <int M, int ST>
-static cudaError_t r2c_bulk_ms(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
-    const size_t smem = (size_t)ST * M * sizeof(double2);
-    kernel_prepare((const void*)k_r2c_bulk<M, ST>, smem);
-    const int grid = persistent_grid(k_r2c_bulk<M, ST>, PCfg<M>::TPL, smem, nrows);
-    return launch_pdl(k_r2c_bulk<M, ST>, dim3(grid), dim3(PCfg<M>::TPL), smem, s, x, H, nrows, L, P, tw);
-}
-
-template <int M>
-static cudaError_t r2c_bulk_m(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
-    return row_stages(M) == 1 ? r2c_bulk_ms<M, 1>(x, H, nrows, L, P, tw, s) : r2c_bulk_ms<M, 2>(x, H, nrows, L, P, tw, s);
-}
-
-template <int M, int ST>
-static cudaError_t c2r_bulk_ms(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
+template <int M, int ST, bool BLK>
+static cudaError_t r2c_bulk_ms(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
                                cudaStream_t s) {
-    const size_t smem = (size_t)ST * (M + 8) * sizeof(double2);
-    kernel_prepare((const void*)k_c2r_bulk<M, ST>, smem);
-    const int grid = persistent_grid(k_c2r_bulk<M, ST>, PCfg<M>::TPL, smem, nrows);
-    return launch_pdl(k_c2r_bulk<M, ST>, dim3(grid), dim3(PCfg<M>::TPL), smem, s, H, x, nrows, L, P, tw, f);
+    const size_t smem = (size_t)ST * M * sizeof(double2);
+    auto kf = k_r2c_bulk<M, ST, BLK>;
+    kernel_prepare((const void*)kf, smem);
+    const int grid = persistent_grid(kf, PCfg<M>::TPL, smem, nrows);
+    return launch_pdl(kf, dim3(grid), dim3(PCfg<M>::TPL), smem, s, x, H, nrows, L, lay, tw);
 }
 
 template <int M>
-static cudaError_t c2r_bulk_m(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
+static cudaError_t r2c_bulk_m(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
                               cudaStream_t s) {
-    return row_stages(M) == 1 ? c2r_bulk_ms<M, 1>(H, x, nrows, L, P, tw, f, s)
-                              : c2r_bulk_ms<M, 2>(H, x, nrows, L, P, tw, f, s);
+    if (lay.blk) return r2c_bulk_ms<M, 2, true>(x, H, nrows, L, lay, tw, s);
+    return row_stages(M) == 1 ? r2c_bulk_ms<M, 1, false>(x, H, nrows, L, lay, tw, s)
+                              : r2c_bulk_ms<M, 2, false>(x, H, nrows, L, lay, tw, s);
+}
+
+template <int M, int ST, bool BLK>
+static cudaError_t c2r_bulk_ms(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
+                               Flags* f, cudaStream_t s) {
+    const size_t smem = (size_t)ST * (M + 8) * sizeof(double2);
+    auto kf = k_c2r_bulk<M, ST, BLK>;
+    kernel_prepare((const void*)kf, smem);
+    const int grid = persistent_grid(kf, PCfg<M>::TPL, smem, nrows);
+    return launch_pdl(kf, dim3(grid), dim3(PCfg<M>::TPL), smem, s, H, x, nrows, L, lay, tw, f);
+}
+
+template <int M>
+static cudaError_t c2r_bulk_m(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
+                              Flags* f, cudaStream_t s) {
+    if (lay.blk) return c2r_bulk_ms<M, 2, true>(H, x, nrows, L, lay, tw, f, s);
+    return row_stages(M) == 1 ? c2r_bulk_ms<M, 1, false>(H, x, nrows, L, lay, tw, f, s)
+                              : c2r_bulk_ms<M, 2, false>(H, x, nrows, L, lay, tw, f, s);
 }
 
 template <int N, int MODE>
@@ -716,23 +734,24 @@ cudaError_t launch_c2r_pipe(const double2* H, double* x, i64 nrows, i64 L, const
     }
 }
 
-cudaError_t launch_r2c_bulk(const double* x, double2* H, i64 nrows, i64 L, i64 P, const double2* tw, cudaStream_t s) {
+cudaError_t launch_r2c_bulk(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
+                            cudaStream_t s) {
     switch (L / 2) {
-        case 512: return r2c_bulk_m<512>(x, H, nrows, L, P, tw, s);
-        case 1024: return r2c_bulk_m<1024>(x, H, nrows, L, P, tw, s);
-        case 2048: return r2c_bulk_m<2048>(x, H, nrows, L, P, tw, s);
-        case 4096: return r2c_bulk_m<4096>(x, H, nrows, L, P, tw, s);
+        case 512: return r2c_bulk_m<512>(x, H, nrows, L, lay, tw, s);
+        case 1024: return r2c_bulk_m<1024>(x, H, nrows, L, lay, tw, s);
+        case 2048: return r2c_bulk_m<2048>(x, H, nrows, L, lay, tw, s);
+        case 4096: return r2c_bulk_m<4096>(x, H, nrows, L, lay, tw, s);
         default: return cudaErrorInvalidValue;
     }
 }
 
-cudaError_t launch_c2r_bulk(const double2* H, double* x, i64 nrows, i64 L, i64 P, const double2* tw, Flags* f,
-                            cudaStream_t s) {
+cudaError_t launch_c2r_bulk(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
+                            Flags* f, cudaStream_t s) {
     switch (L / 2) {
-        case 512: return c2r_bulk_m<512>(H, x, nrows, L, P, tw, f, s);
-        case 1024: return c2r_bulk_m<1024>(H, x, nrows, L, P, tw, f, s);
-        case 2048: return c2r_bulk_m<2048>(H, x, nrows, L, P, tw, f, s);
-        case 4096: return c2r_bulk_m<4096>(H, x, nrows, L, P, tw, f, s);
+        case 512: return c2r_bulk_m<512>(H, x, nrows, L, lay, tw, f, s);
+        case 1024: return c2r_bulk_m<1024>(H, x, nrows, L, lay, tw, f, s);
+        case 2048: return c2r_bulk_m<2048>(H, x, nrows, L, lay, tw, f, s);
+        case 4096: return c2r_bulk_m<4096>(H, x, nrows, L, lay, tw, f, s);
         default: return cudaErrorInvalidValue;
     }
 }

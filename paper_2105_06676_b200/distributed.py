@@ -75,11 +75,33 @@ class GpuSlabStages:
             ctypes.c_void_p(send.data_ptr()), ctypes.c_void_p(local_out.data_ptr()),
             ctypes.byref(_opts(self.device, 0, self._stream()))))
 
+    # exchange fused into the row passes (2D): `peers` = device address of an
+    # array of P device pointers (every rank's exchange buffer, NVLink-mapped)
+    def forward_p2p(self, local_in, peers: int) -> None:
+        _lib.check(_lib.load().fsx_slab_forward_p2p(
+            ctypes.byref(self.shape._c()), ctypes.c_int32(self.P), ctypes.c_int32(self.r),
+            ctypes.c_void_p(local_in.data_ptr()), ctypes.c_void_p(peers),
+            ctypes.byref(_opts(self.device, 0, self._stream()))))
+
+    def inverse_p2p(self, peers: int, local_out) -> None:
+        _lib.check(_lib.load().fsx_slab_inverse_p2p(
+            ctypes.byref(self.shape._c()), ctypes.c_int32(self.P), ctypes.c_int32(self.r),
+            ctypes.c_void_p(peers), ctypes.c_void_p(local_out.data_ptr()),
+            ctypes.byref(_opts(self.device, 0, self._stream()))))
+
 
 class SlabSolver:
-    """solve_periodic over a process group, one slab per rank."""
+    """solve_periodic over a process group, one slab per rank.
 
-    def __init__(self, shape: GridShape, kernel: StencilKernel, T: int, group=None, stages=None, device=None):
+    exchange="nccl": two all_to_all_single calls per solve.
+    exchange="p2p" (2D, GPUs): the exchange buffer is torch symmetric memory
+    (every rank's buffer mapped into every process over NVLink); the R2C rows
+    store their column blocks straight into the owners' buffers and the C2R
+    rows load them back, separated by the symmetric-memory device barrier --
+    no all-to-all, the NVLink traffic overlaps the row FFTs."""
+
+    def __init__(self, shape: GridShape, kernel: StencilKernel, T: int, group=None, stages=None, device=None,
+                 exchange: str = "nccl"):
         import torch
         import torch.distributed as dist
 
@@ -98,8 +120,21 @@ class SlabSolver:
             self.tdev = torch.device("cpu")
         self.stages = stages
         n = self.info["xbuf_bytes"] // 8
-        self.send = torch.empty(n, dtype=torch.float64, device=self.tdev)
-        self.recv = torch.empty(n, dtype=torch.float64, device=self.tdev)
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError("exchange must be 'nccl' or 'p2p'")
+        self.exchange = exchange
+        if exchange == "p2p":
+            if shape.rank() != 2 or self.tdev.type != "cuda":
+                raise ValueError("p2p exchange: rank-2 grids on GPUs")
+            import torch.distributed._symmetric_memory as symm
+
+            self.recv = symm.empty(n, dtype=torch.float64, device=self.tdev)
+            self.symm = symm.rendezvous(self.recv, group if group is not None else dist.group.WORLD)
+            self.peers = int(self.symm.buffer_ptrs_dev)
+            self.send = None
+        else:
+            self.send = torch.empty(n, dtype=torch.float64, device=self.tdev)
+            self.recv = torch.empty(n, dtype=torch.float64, device=self.tdev)
 
     def local_cells(self) -> int:
         c = 1
@@ -118,6 +153,22 @@ class SlabSolver:
             if events is not None:
                 events[i].record()
 
+        if self.exchange == "p2p":
+            # events: [0,1) barrier + R2C rows storing over NVLink, [1,2) barrier,
+            # [2,3) fused pass, [3,4) barrier, [4,5) C2R rows loading over NVLink
+            mark(0)
+            self.symm.barrier(channel=0)  # every rank done reading the buffers (previous solve)
+            self.stages.forward_p2p(local_in, self.peers)
+            mark(1)
+            self.symm.barrier(channel=1)  # all blocks stored into their owners' buffers
+            mark(2)
+            self.stages.spectral(self.recv, self.kernel, self.T)
+            mark(3)
+            self.symm.barrier(channel=2)  # every rank's spectral pass done
+            mark(4)
+            self.stages.inverse_p2p(self.peers, local_out)
+            mark(5)
+            return
         mark(0)
         self.stages.forward(local_in, self.send)
         mark(1)
@@ -162,4 +213,33 @@ def slab_solve_emulated(shape: GridShape, a0, kernel: StencilKernel, T: int, P: 
             send[s][d * chunk:(d + 1) * chunk].copy_(recv[d][s * chunk:(s + 1) * chunk])
     for r in range(P):
         stages[r].inverse(send[r], orows[r * n0l:(r + 1) * n0l])
+    return out
+
+
+def slab_solve_emulated_p2p(shape: GridShape, a0, kernel: StencilKernel, T: int, P: int, out=None):
+    """The fused-exchange (p2p) slab solve of P ranks on ONE GPU: the P
+    exchange buffers are separate allocations on this device and the peer
+    pointer array lists them, so each rank's row kernels store to / load from
+    the other "ranks'" buffers exactly as over NVLink.  Stages run rank after
+    rank (the barriers are implicit; no rank waits on another)."""
+    import torch
+
+    n0 = shape.dim(0)
+    if out is None:
+        out = torch.empty_like(a0)
+    rows = a0.view(n0, -1)
+    orows = out.view(n0, -1)
+    info = slab_describe(shape, P, 0)
+    n = info["xbuf_bytes"] // 8
+    bufs = [torch.empty(n, dtype=torch.float64, device=a0.device) for _ in range(P)]
+    peers = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=a0.device)
+    stages = [GpuSlabStages(shape, P, r, a0.device.index or 0) for r in range(P)]
+    n0l = n0 // P
+    for r in range(P):
+        stages[r].forward_p2p(rows[r * n0l:(r + 1) * n0l], peers.data_ptr())
+    for r in range(P):
+        stages[r].spectral(bufs[r], kernel, T)
+    for r in range(P):
+        stages[r].inverse_p2p(peers.data_ptr(), orows[r * n0l:(r + 1) * n0l])
+    torch.cuda.current_stream().synchronize()
     return out
