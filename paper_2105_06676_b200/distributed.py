@@ -90,6 +90,23 @@ class GpuSlabStages:
             ctypes.byref(_opts(self.device, 0, self._stream()))))
 
 
+class SymmetricPeerMemory:
+    """The p2p exchange buffer: torch symmetric memory (each rank's buffer
+    mapped into every process over NVLink) and its device-side barrier."""
+
+    def __init__(self, nelem: int, device, group):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        self.local = symm.empty(nelem, dtype=torch.float64, device=device)
+        self.handle = symm.rendezvous(self.local, group if group is not None else dist.group.WORLD)
+        self.peers = int(self.handle.buffer_ptrs_dev)  # device array of P device pointers
+
+    def barrier(self, channel: int) -> None:
+        self.handle.barrier(channel=channel)
+
+
 class SlabSolver:
     """solve_periodic over a process group, one slab per rank.
 
@@ -101,7 +118,7 @@ class SlabSolver:
     no all-to-all, the NVLink traffic overlaps the row FFTs."""
 
     def __init__(self, shape: GridShape, kernel: StencilKernel, T: int, group=None, stages=None, device=None,
-                 exchange: str = "nccl"):
+                 exchange: str = "nccl", peer_memory=None):
         import torch
         import torch.distributed as dist
 
@@ -124,13 +141,15 @@ class SlabSolver:
             raise ValueError("exchange must be 'nccl' or 'p2p'")
         self.exchange = exchange
         if exchange == "p2p":
-            if shape.rank() != 2 or self.tdev.type != "cuda":
-                raise ValueError("p2p exchange: rank-2 grids on GPUs")
-            import torch.distributed._symmetric_memory as symm
-
-            self.recv = symm.empty(n, dtype=torch.float64, device=self.tdev)
-            self.symm = symm.rendezvous(self.recv, group if group is not None else dist.group.WORLD)
-            self.peers = int(self.symm.buffer_ptrs_dev)
+            if shape.rank() != 2:
+                raise ValueError("p2p exchange: rank-2 grids")
+            if peer_memory is None:
+                if self.tdev.type != "cuda":
+                    raise ValueError("p2p exchange on CPU ranks needs an explicit peer_memory")
+                peer_memory = SymmetricPeerMemory(n, self.tdev, group)
+            self.pm = peer_memory
+            self.recv = peer_memory.local
+            self.peers = peer_memory.peers
             self.send = None
         else:
             self.send = torch.empty(n, dtype=torch.float64, device=self.tdev)
@@ -157,14 +176,14 @@ class SlabSolver:
             # events: [0,1) barrier + R2C rows storing over NVLink, [1,2) barrier,
             # [2,3) fused pass, [3,4) barrier, [4,5) C2R rows loading over NVLink
             mark(0)
-            self.symm.barrier(channel=0)  # every rank done reading the buffers (previous solve)
+            self.pm.barrier(0)  # every rank done reading the buffers (previous solve)
             self.stages.forward_p2p(local_in, self.peers)
             mark(1)
-            self.symm.barrier(channel=1)  # all blocks stored into their owners' buffers
+            self.pm.barrier(1)  # all blocks stored into their owners' buffers
             mark(2)
             self.stages.spectral(self.recv, self.kernel, self.T)
             mark(3)
-            self.symm.barrier(channel=2)  # every rank's spectral pass done
+            self.pm.barrier(2)  # every rank's spectral pass done
             mark(4)
             self.stages.inverse_p2p(self.peers, local_out)
             mark(5)

@@ -6,8 +6,10 @@ the exchange buffers, and the two equal-split all-to-alls over
 torch.distributed.  The per-rank numerical stages are replaced by a numpy
 reference of the same stage contract (test infrastructure), so the layouts,
 global column offsets and exchange pattern are checked end to end against
-the CPU oracle without a GPU.  The GPU stages are checked with the same
-layouts in tests/test_gpu_slab.py.
+the CPU oracle without a GPU.  The fused-exchange (p2p) sequence runs the
+same way with every rank's exchange buffer a memory-mapped file opened by all
+ranks (the CPU stand-in for NVLink symmetric memory) and gloo barriers.  The
+GPU stages are checked with the same layouts in tests/test_gpu_slab.py.
 """
 import os
 import socket
@@ -83,6 +85,27 @@ class NumpyStages:
             lam = self._symbol([k0[:, None, None], ky[None, :, None], kx[None, None, :]])
             a[:] = np.fft.ifft(np.fft.fft(a, axis=0) * lam ** T / N, axis=0) * n0
 
+    # p2p contract (fsx_slab_forward_p2p / _inverse_p2p): `peers` lists every
+    # rank's exchange buffer; block d of this rank's rows goes to / comes from
+    # rows [r n0l, (r+1) n0l) of buffer d
+    def forward_p2p(self, local_in, peers):
+        x = local_in.numpy().reshape(self.n0l, self.L)
+        X = np.fft.rfft(x, axis=-1)
+        for d in range(self.P):
+            lo, hi = d * self.CB, min((d + 1) * self.CB, self.M + 1)
+            dst = peers[d].view(np.complex128).reshape(self.dims[0], self.CB)
+            rows = dst[self.r * self.n0l:(self.r + 1) * self.n0l]
+            rows[:] = 0
+            if lo < hi:
+                rows[:, :hi - lo] = X[:, lo:hi]
+
+    def inverse_p2p(self, peers, local_out):
+        parts = [peers[d].view(np.complex128).reshape(self.dims[0], self.CB)[self.r * self.n0l:(self.r + 1) * self.n0l]
+                 for d in range(self.P)]
+        X = np.concatenate(parts, axis=1)[:, :self.M + 1]
+        y = np.fft.irfft(X, n=self.L, axis=-1) * self.L
+        local_out.numpy()[:] = y.reshape(-1)
+
     def inverse(self, send, local_out):
         z = self._c(send)
         if len(self.dims) == 2:
@@ -97,13 +120,30 @@ class NumpyStages:
         local_out.numpy()[:] = y.reshape(-1)
 
 
+class FilePeerMemory:
+    """CPU stand-in for the symmetric-memory exchange buffer: every rank's
+    buffer is a memory-mapped file all ranks open, the barrier is gloo's."""
+
+    def __init__(self, nelem, rank, world, root):
+        path = lambda r: os.path.join(root, f"xbuf{r}.bin")  # noqa: E731
+        np.lib.format.open_memmap(path(rank), mode="w+", dtype=np.float64, shape=(nelem,)).flush()
+        dist.barrier()
+        self.peers = [np.lib.format.open_memmap(path(r), mode="r+") for r in range(world)]
+        self.local = torch.from_numpy(self.peers[rank])
+
+    def barrier(self, channel):
+        for p in self.peers:
+            p.flush()
+        dist.barrier()
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, dims, seed, T, outdir):
+def _worker(rank, world, port, dims, seed, T, outdir, exchange="nccl"):
     from paper_2105_06676_b200 import GridShape, StencilKernel
     from paper_2105_06676_b200.distributed import SlabSolver
 
@@ -121,9 +161,13 @@ def _worker(rank, world, port, dims, seed, T, outdir):
         from paper_2105_06676_b200.distributed import slab_describe
 
         info = slab_describe(shape, world, rank)
-        solver = SlabSolver(shape, k, T, stages=NumpyStages(dims, world, rank, info, kern))
+        pm = FilePeerMemory(info["xbuf_bytes"] // 8, rank, world, outdir) if exchange == "p2p" else None
+        solver = SlabSolver(shape, k, T, stages=NumpyStages(dims, world, rank, info, kern), exchange=exchange,
+                            peer_memory=pm)
         out = torch.empty(slab.size, dtype=torch.float64)
         solver.solve(torch.from_numpy(slab), out)
+        if exchange == "p2p":
+            solver.solve(torch.from_numpy(slab), out)  # second solve: buffers reused behind the leading barrier
         np.save(os.path.join(outdir, f"r{rank}.npy"), out.numpy())
         np.save(os.path.join(outdir, "a0.npy"), a0)
     finally:
@@ -136,6 +180,22 @@ def test_slab_decomposition_gloo_world2(orc, dims, T):
     seed = 4242 + len(dims)
     with tempfile.TemporaryDirectory() as td:
         mp.spawn(_worker, args=(world, _free_port(), dims, seed, T, td), nprocs=world, join=True)
+        got = np.concatenate([np.load(os.path.join(td, f"r{r}.npy")) for r in range(world)])
+        a0 = np.load(os.path.join(td, "a0.npy"))
+    kern = R.random_kernel(R.Rng(seed), len(dims), 1, 1, 0.95)
+    want = orc.solve_periodic(a0, dims, 1, *kern.arrays(), T)
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-12
+
+
+@pytest.mark.parametrize("dims,T", [([16, 32], 7), ([8, 64], 50)])
+def test_slab_p2p_exchange_gloo_world2(orc, dims, T):
+    """The fused-exchange (p2p) sequence of SlabSolver -- stores into the
+    owners' buffers, barrier, spectral pass, barrier, loads -- with every
+    rank's buffer a shared file (the CPU stand-in for symmetric memory)."""
+    world = 2
+    seed = 5151 + dims[0]
+    with tempfile.TemporaryDirectory() as td:
+        mp.spawn(_worker, args=(world, _free_port(), dims, seed, T, td, "p2p"), nprocs=world, join=True)
         got = np.concatenate([np.load(os.path.join(td, f"r{r}.npy")) for r in range(world)])
         a0 = np.load(os.path.join(td, "a0.npy"))
     kern = R.random_kernel(R.Rng(seed), len(dims), 1, 1, 0.95)
