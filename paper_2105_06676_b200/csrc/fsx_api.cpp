@@ -260,7 +260,8 @@ struct Plan {
     i64 L = 0, M = 0, P = 0, rows = 0;
     fsx::AxisGeom ax1, ax0;
     alignas(64) unsigned char map0[128], map1[128];  // CUtensorMaps for TMA column passes
-    bool tma0 = false, tma1 = false;
+    alignas(64) unsigned char map2[128];             // parity-split view (8192-point halves pass)
+    bool tma0 = false, tma1 = false, halves = false;
     // kind 2
     i64 N1 = 1, N2 = 1, Mc = 0;
     i64 N1a = 0, N1b = 0;  // split column FFT (N1 > kMaxLine)
@@ -450,6 +451,7 @@ Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general,
         if (tma_enabled()) {
             p->tma0 = fsx::tma_cols_ok(p->ax0.n) && fsx::make_cols_tensor_map(p->map0, p->work.p, p->ax0) == 0;
             p->tma1 = r == 3 && fsx::tma_cols_ok(p->ax1.n) && fsx::make_cols_tensor_map(p->map1, p->work.p, p->ax1) == 0;
+            p->halves = fsx::halves_ok(p->ax0) && fsx::make_cols_tensor_map_par(p->map2, p->work.p, p->ax0) == 0;
         }
         const i64 H = p->rows * (p->M + 1) * 16;
         p->fused_bytes = 2 * H;
@@ -722,7 +724,8 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
             else FSX_CK(fsx::launch_axis_pow2(H, H, p.ax1, -1, none, tw, st));
         }
         sp.mark();
-        if (p.tma0) FSX_CK(fsx::launch_cols_tma(p.map0, p.ax0, 2, sym, tw, st));
+        if (p.halves) FSX_CK(fsx::launch_fused_halves(p.map2, p.ax0, sym, tw, st));
+        else if (p.tma0) FSX_CK(fsx::launch_cols_tma(p.map0, p.ax0, 2, sym, tw, st));
         else FSX_CK(fsx::launch_fused_r2c(H, p.ax0, sym, tw, st));
         sp.mark();
         if (r == 3) {
@@ -922,7 +925,9 @@ void slab_spectral(SlabPlan& sp, Device& dev, const Taps& taps, u64 T, double2* 
     const i64 inner = rk == 3 ? sp.n1b * sp.Pp : sp.CB;
     const fsx::AxisGeom g{sp.dims[0], inner, 1, sp.dims[0] * inner, inner};
     alignas(64) unsigned char map[128];
-    if (tma_enabled() && fsx::tma_cols_ok(g.n) && fsx::make_cols_tensor_map(map, recv, g) == 0)
+    if (tma_enabled() && fsx::halves_ok(g) && fsx::make_cols_tensor_map_par(map, recv, g) == 0)
+        FSX_CK(fsx::launch_fused_halves(map, g, sym, tw, st));
+    else if (tma_enabled() && fsx::tma_cols_ok(g.n) && fsx::make_cols_tensor_map(map, recv, g) == 0)
         FSX_CK(fsx::launch_cols_tma(map, g, 2, sym, tw, st));
     else
         FSX_CK(fsx::launch_fused_r2c(recv, g, sym, tw, st));

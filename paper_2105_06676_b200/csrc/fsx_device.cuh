@@ -201,7 +201,16 @@ __device__ __forceinline__ int swz(int p) { return p ^ (((p >> 3) ^ (p >> 4)) & 
 // X[item(t, i) + u * N / 8].
 // FT: read every twiddle of a pass from the gathered table (no derived
 // products: fewer FP64 instructions, more L1 loads) -- for compute-bound callers.
-template <int N, int SIGN, bool PF = false, bool PAIR = false, bool FT = false>
+// NB > 0: the exchanges synchronize NB-thread groups with named barriers
+// (id 1 + threadIdx.x / NB) instead of the whole CTA, so independent groups
+// of one CTA (e.g. the two half-columns of the 8192-point pass) drift apart.
+template <int NB>
+__device__ __forceinline__ void group_sync() {
+    if constexpr (NB == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;\n" ::"r"(1 + (int)(threadIdx.x / NB)), "n"(NB) : "memory");
+}
+
+template <int N, int SIGN, bool PF = false, bool PAIR = false, bool FT = false, int NB = 0>
 struct LineFFT {
     static constexpr int LOGN = ilog2c(N);
     static constexpr int R = N < 16 ? N : 16;
@@ -300,7 +309,7 @@ struct LineFFT {
         }
         if constexpr (S + 1 < NPASS) {
             if constexpr (PF) load_tw<S + 1>(t, tw, w);
-            __syncthreads();
+            group_sync<NB>();
 #pragma unroll
             for (int i = 0; i < C; ++i) {
                 const int j = t + i * TPL;
@@ -309,7 +318,7 @@ struct LineFFT {
 #pragma unroll
                 for (int u = 0; u < r; ++u) line[swz(base + u * Ns)] = v[i + u * C];
             }
-            __syncthreads();
+            group_sync<NB>();
             constexpr int r2 = radix<S + 1>();
             constexpr int C2 = R / r2;
 #pragma unroll

@@ -243,6 +243,11 @@ cudaError_t launch_c2r_reg(const double2* H, double* x, i64 nrows, i64 L, const 
 // one direct periodic stencil step out = sum_taps B a[x + off] (verifier)
 cudaError_t launch_step_naive(const double* a, double* out, const NaiveGeom& g, const long long* off,
                               const double* blk, cudaStream_t s);
+// 8192-point fused pass as two parity halves (fsx_tma.cu)
+bool halves_ok(const AxisGeom& g);
+int make_cols_tensor_map_par(void* out_map, void* base, const AxisGeom& g);
+cudaError_t launch_fused_halves(const void* tensor_map2, const AxisGeom& g, const FusedSymbol& sym,
+                                const double2* tw_all, cudaStream_t s);
 // TMA column passes (fsx_tma.cu); tensor_map points at a 64-byte aligned CUtensorMap
 bool tma_cols_ok(i64 N);
 int make_cols_tensor_map(void* out_map, void* base, const AxisGeom& g);

@@ -14,6 +14,7 @@
 // Tensor map: the complex array viewed as fp64 [outer][n][2 * inner]
 // (dims {2 * inner, n, outer}), box {2, min(n, 256), 1}; built on the host
 // (fsx_api.cpp) with cuTensorMapEncodeTiled.
+#include <cooperative_groups.h>
 #include <cuda.h>
 
 #include <cstdlib>
@@ -245,6 +246,258 @@ k_fused_tma4(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sy
     }
 }
 
+// Spectral multiply of the 8192-point halves passes: v[q] = X[k0],
+// k0 = th + 256 q + 4096 h = th + 256 b + 2048 (a + 2 h) for q = 8 a + b, so
+// exp(2 pi i og k0 / 8192) = e_b i^(og (a + 2 h)): eight reads per group, all
+// in the table's first 2048 entries, and exact quarter turns.
+__device__ __forceinline__ void spectral_halves(double2 (&v)[16], int th, int h, const FusedSymbol& sym,
+                                                const double2* __restrict__ tw_all, const double2* acoef) {
+    constexpr int N = 8192, NH = 4096;
+    if (sym.real) {
+        double lam[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) lam[q] = 0.0;
+        for (int gi = 0; gi < sym.ngroups; ++gi) {
+            const double2 a = acoef[gi];
+            const i64 og = sym.group_off[gi];
+            if (og == 0) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) lam[q] += a.x;
+                continue;
+            }
+            double2 eb[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) eb[b] = eplus_tab(tw_all, N, (i64)(th + 256 * b) * og);
+            const int mo = (int)(og & 3);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const double2 e = rot_quarter(eb[q & 7], (mo * ((q >> 3) + 2 * h)) & 3);
+                lam[q] = fma(a.x, e.x, fma(-a.y, e.y, lam[q]));
+            }
+        }
+        pow_real_vec_skip<16, 4>(lam, sym.T, sym.neg_mag2);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = cscale(v[q], lam[q] * sym.scale);
+    } else {
+        spectral_regs_at<N, 16>(v, th + NH * h, 256, sym, tw_all, [&](int gi) { return acoef[gi]; });
+    }
+}
+
+// Fused spectral pass for 8192-point columns as two 4096-point halves.
+// A 128 KB column tile fits one CTA per SM, whose CTA-wide barriers then
+// serialize every FFT phase of the SM.  Here the CTA splits the column by
+// sample parity (x[2n], x[2n+1]: a 4-D tensor map {2 inner, parity, n/2,
+// outer} loads each half contiguously) and two 256-thread groups run
+// independent 4096-point FFTs with named barriers, so one group's exchanges
+// overlap the other's arithmetic.  The radix-2 step joins them through
+// shared memory: X[k] = E[k] + W^k O[k], X[k + 4096] = E[k] - W^k O[k]
+// (group h then owns frequencies k + 4096 h), spectral multiply, and the
+// inverse split e = X[k] + X[k+4096], o = (X[k] - X[k+4096]) W^-k feeds the
+// two inverse FFTs whose outputs are again the even / odd samples.
+__global__ void __launch_bounds__(512, 1)
+k_fused8192h(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
+    constexpr int N = 8192, NH = 4096, TH = 256;
+    using FF = LineFFT<NH, -1, false, false, false, TH>;
+    using FI = LineFFT<NH, +1, false, false, false, TH>;
+    extern __shared__ __align__(128) double2 tile[];
+    __shared__ __align__(8) unsigned long long bar[2];  // one per parity half: a group starts on its own half
+    __shared__ double2 acoef[kMaxGroups];
+    __shared__ double2 tapterm[kMaxFusedTaps];
+    const int h = threadIdx.x >> 8, th = threadIdx.x & (TH - 1);
+    const i64 c = blockIdx.x;
+    i64 kx, ky;
+    fused_col_freqs(sym, c, kx, ky);
+    if (sym.rank == 3 && c - (c / sym.P) * sym.P > sym.M) return;  // pitch padding of a 3D plane
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_init_fence();
+        pdl_wait();
+#pragma unroll 1
+        for (int p = 0; p < 2; ++p) {
+            mbar_expect_tx(&bar[p], (unsigned)(NH * sizeof(double2)));
+#pragma unroll 1
+            for (int b = 0; b < NH / 256; ++b)
+                tma_load_4d(tile + p * NH + b * 256, &map2, (int)(2 * c), p, b * 256, 0, &bar[p]);
+        }
+    }
+    for (int j = threadIdx.x; j < sym.ntaps; j += 2 * TH) tapterm[j] = tap_term(sym, tw_all, j, kx, ky);
+    __syncthreads();
+    for (int gi = threadIdx.x; gi < sym.ngroups; gi += 2 * TH) {
+        double2 a = make_double2(0.0, 0.0);
+        for (int j = 0; j < sym.ntaps; ++j)
+            if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j]);
+        acoef[gi] = a;
+    }
+    __syncthreads();
+    mbar_wait(&bar[h], 0);
+    pdl_trigger();
+    double2* reg = tile + h * NH;
+    const double2* other = tile + (h ^ 1) * NH;
+    double2 v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = reg[th + 256 * q];
+    FF::run(v, th, reg, tw_all + NH);
+    // forward radix-2 join; W_8192^(th + 256 q) = W_8192^th W_32^q
+    const double2 wt = __ldg(tw_all + N + th);
+    if (h == 1) {
+        static_for<0, 16>([&](auto Q) {
+            constexpr int q = decltype(Q)::value;
+            v[q] = cmul(v[q], cmul_const<q, 32, -1>(wt));
+        });
+    }
+    group_sync<TH>();  // this group's last exchange reads are done
+#pragma unroll
+    for (int q = 0; q < 16; ++q) reg[th + 256 * q] = v[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const double2 o = other[th + 256 * q];
+        v[q] = h == 0 ? cadd(v[q], o) : csub(o, v[q]);
+    }
+    spectral_halves(v, th, h, sym, tw_all, acoef);
+    __syncthreads();  // both groups done reading the other half
+#pragma unroll
+    for (int q = 0; q < 16; ++q) reg[th + 256 * q] = v[q];
+    __syncthreads();
+    if (h == 0) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = cadd(v[q], other[th + 256 * q]);
+    } else {
+        static_for<0, 16>([&](auto Q) {
+            constexpr int q = decltype(Q)::value;
+            v[q] = cmulc(csub(other[th + 256 * q], v[q]), cmul_const<q, 32, -1>(wt));
+        });
+    }
+    __syncthreads();  // the inverse FFTs' exchanges overwrite the halves just read
+    FI::run(v, th, reg, tw_all + NH);
+    group_sync<TH>();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) reg[th + 256 * q] = v[q];
+    fence_proxy_async();
+    group_sync<TH>();  // each group stores its own parity as soon as it is done
+    if (th == 0) {
+#pragma unroll 1
+        for (int b = 0; b < NH / 256; ++b) tma_store_4d(&map2, reg + b * 256, (int)(2 * c), h, b * 256, 0);
+        bulk_commit();
+        bulk_wait_read0();
+    }
+}
+
+// The same two-halves algorithm with the halves in two CTAs of a cluster
+// (64 KB tile each, two CTAs per SM): a CTA's TMA load / prologue / store
+// tail overlaps another CTA's arithmetic on the same SM, which one 128 KB
+// CTA per SM cannot do.  The radix-2 joins read the partner CTA's half
+// through distributed shared memory (contiguous 16-byte reads per thread).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
+k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
+    namespace cg = cooperative_groups;
+    constexpr int N = 8192, NH = 4096;
+    using FF = LineFFT<NH, -1>;
+    using FI = LineFFT<NH, +1>;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(128) double2 tile[];
+    __shared__ __align__(8) unsigned long long bar;
+    __shared__ double2 acoef[kMaxGroups];
+    __shared__ double2 tapterm[kMaxFusedTaps];
+    const int h = (int)cluster.block_rank(), t = threadIdx.x;
+    const i64 c = blockIdx.x >> 1;
+    i64 kx, ky;
+    fused_col_freqs(sym, c, kx, ky);
+    if (sym.rank == 3 && c - (c / sym.P) * sym.P > sym.M) return;  // both CTAs of the cluster agree
+    if (t == 0) {
+        mbar_init(&bar, 1);
+        mbar_init_fence();
+        pdl_wait();
+        mbar_expect_tx(&bar, (unsigned)(NH * sizeof(double2)));
+#pragma unroll 1
+        for (int b = 0; b < NH / 256; ++b) tma_load_4d(tile + b * 256, &map2, (int)(2 * c), h, b * 256, 0, &bar);
+    }
+    for (int j = t; j < sym.ntaps; j += 256) tapterm[j] = tap_term(sym, tw_all, j, kx, ky);
+    __syncthreads();
+    for (int gi = t; gi < sym.ngroups; gi += 256) {
+        double2 a = make_double2(0.0, 0.0);
+        for (int j = 0; j < sym.ntaps; ++j)
+            if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j]);
+        acoef[gi] = a;
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    pdl_trigger();
+    const double2* peer = cluster.map_shared_rank(tile, h ^ 1);
+    double2 v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = tile[t + 256 * q];
+    FF::run(v, t, tile, tw_all + NH);
+    const double2 wt = __ldg(tw_all + N + t);  // W_8192^(t + 256 q) = W_8192^t W_32^q
+    if (h == 1) {
+        static_for<0, 16>([&](auto Q) {
+            constexpr int q = decltype(Q)::value;
+            v[q] = cmul(v[q], cmul_const<q, 32, -1>(wt));
+        });
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) tile[t + 256 * q] = v[q];
+    cluster.sync();  // both halves published
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const double2 o = peer[t + 256 * q];
+        v[q] = h == 0 ? cadd(v[q], o) : csub(o, v[q]);
+    }
+    spectral_halves(v, t, h, sym, tw_all, acoef);
+    cluster.sync();  // the partner has read this tile
+#pragma unroll
+    for (int q = 0; q < 16; ++q) tile[t + 256 * q] = v[q];
+    cluster.sync();
+    if (h == 0) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = cadd(v[q], peer[t + 256 * q]);
+    } else {
+        static_for<0, 16>([&](auto Q) {
+            constexpr int q = decltype(Q)::value;
+            v[q] = cmulc(csub(peer[t + 256 * q], v[q]), cmul_const<q, 32, -1>(wt));
+        });
+    }
+    cluster.sync();  // the partner's reads of this tile are done before the inverse FFT reuses it
+    FI::run(v, t, tile, tw_all + NH);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) tile[t + 256 * q] = v[q];
+    fence_proxy_async();
+    __syncthreads();
+    if (t == 0) {
+#pragma unroll 1
+        for (int b = 0; b < NH / 256; ++b) tma_store_4d(&map2, tile + b * 256, (int)(2 * c), h, b * 256, 0);
+        bulk_commit();
+        bulk_wait_read0();
+    }
+}
+
+static int fused_halves() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_HALVES");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
+bool halves_ok(const AxisGeom& g) { return g.n == 8192 && g.outer == 1 && fused_halves(); }
+
+cudaError_t launch_fused_halves(const void* tensor_map2, const AxisGeom& g, const FusedSymbol& sym,
+                                const double2* tw, cudaStream_t s) {
+    const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(tensor_map2);
+    if (fused_halves() == 2) {  // two-CTA cluster variant
+        const size_t smem = 4096 * sizeof(double2);
+        kernel_prepare((const void*)k_fused8192c, smem);
+        return launch_pdl(k_fused8192c, dim3((unsigned)(2 * g.ncols)), dim3(256), smem, s, map, g, sym, tw);
+    }
+    const size_t smem = 8192 * sizeof(double2);
+    kernel_prepare((const void*)k_fused8192h, smem);
+    return launch_pdl(k_fused8192h, dim3((unsigned)g.ncols), dim3(512), smem, s, map, g, sym, tw);
+}
+
 // FSX_4STEP=1 selects k_fused_tma4 (measured slower on cfg2: 189 vs 165 us;
 // the transposed order scatters the symbol-table reads), default off.
 static int fused_4step() {
@@ -458,6 +711,29 @@ cudaError_t launch_cols_tma(const void* tensor_map, const AxisGeom& g, int mode,
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// Parity-split view for k_fused8192h: dims {2 inner, 2 (row parity), n/2, outer},
+// box {2, 1, 256, 1}: one box = 256 rows of one parity of one column.
+int make_cols_tensor_map_par(void* out_map, void* base, const AxisGeom& g) {
+    static EncodeTiledFn encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return -1;
+        encode = reinterpret_cast<EncodeTiledFn>(fn);
+    }
+    if (g.n % 2 || g.n / 2 < 256) return -2;
+    const cuuint64_t dims[4] = {(cuuint64_t)(2 * g.inner), 2, (cuuint64_t)(g.n / 2), (cuuint64_t)g.outer};
+    const cuuint64_t strides[3] = {(cuuint64_t)(g.inner * 16), (cuuint64_t)(2 * g.inner * 16), (cuuint64_t)(g.block * 16)};
+    const cuuint32_t box[4] = {2, 1, 256, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode(reinterpret_cast<CUtensorMap*>(out_map), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : (int)r;
+}
 
 int make_cols_tensor_map(void* out_map, void* base, const AxisGeom& g) {
     static EncodeTiledFn encode = nullptr;

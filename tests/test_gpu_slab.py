@@ -43,6 +43,7 @@ CASES = [
     ([1024, 1024], "box9", 100000, (8,)),
     ([32, 64, 128], "random3", 20, (1, 2, 4)),
     ([64, 1024, 64], "random3", 7, (4,)),
+    ([8192, 128], "random2", 9, (2, 8)),     # 8192-point fused columns (parity halves)
 ]
 
 
