@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <set>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -274,6 +275,7 @@ struct Plan {
     DevBuf work;      // H (kind 1) / complex Z (kind 3)
     DevBuf d_in, d_out;
     DevBuf taps_dev;  // general path tap arrays
+    DevBuf qmax;      // implicit fused symbol: max |lamQ| (bits)
     std::vector<char> taps_host;
     int launches = 0;
     i64 alg_bytes = 0, fused_bytes = 0;
@@ -541,7 +543,8 @@ bool symmetric_taps(const Taps& taps) {
     return true;
 }
 
-fsx::FusedSymbol fused_symbol(const Plan& p, const Taps& taps, u64 T) {
+fsx::FusedSymbol fused_symbol(const Plan& p, const Taps& taps, u64 T, const Taps* q = nullptr,
+                              const unsigned long long* qmax_bits = nullptr) {
     fsx::FusedSymbol s;
     const int r = (int)p.dims.size();
     s.rank = r;
@@ -554,30 +557,52 @@ fsx::FusedSymbol fused_symbol(const Plan& p, const Taps& taps, u64 T) {
     // |lam|^2 < neg_mag2  <=>  |lam|^T < 2^-1100 (0 in fp64 for T = 1: never)
     s.neg_mag2 = std::exp2(-2200.0 / (double)T);
     s.scale = 1.0 / (double)p.cells;
-    std::map<i64, int> gid;
+    // groups keyed by (tap set, axis-0 offset): set 0 = S, set 1 = Q (implicit)
+    std::map<std::pair<int, i64>, int> gid;
     int j = 0;
-    for (const auto& kv : taps.map) {
-        const auto& off = kv.first;
-        const i64 o0 = off[p.axes[0]];
-        auto it = gid.find(o0);
-        int g;
-        if (it == gid.end()) {
-            g = (int)gid.size();
-            gid.emplace(o0, g);
-            s.group_off[g] = (int)o0;
-        } else {
-            g = it->second;
+    auto add_set = [&](const Taps& t, int set) {
+        for (const auto& kv : t.map) {
+            const auto& off = kv.first;
+            const std::pair<int, i64> key{set, off[p.axes[0]]};
+            auto it = gid.find(key);
+            int g;
+            if (it == gid.end()) {
+                g = (int)gid.size();
+                gid.emplace(key, g);
+                s.group_off[g] = (int)key.second;
+                s.group_set[g] = set;
+            } else {
+                g = it->second;
+            }
+            s.tap_group[j] = g;
+            s.tap_o1[j] = r == 3 ? (int)off[p.axes[1]] : 0;
+            s.tap_olast[j] = (int)off[p.axes[r - 1]];
+            s.tap_c[j] = kv.second[0];
+            ++j;
         }
-        s.tap_group[j] = g;
-        s.tap_o1[j] = r == 3 ? (int)off[p.axes[1]] : 0;
-        s.tap_olast[j] = (int)off[p.axes[r - 1]];
-        s.tap_c[j] = kv.second[0];
-        ++j;
+    };
+    add_set(taps, 0);
+    if (q) {
+        add_set(*q, 1);
+        s.implicit = 1;
+        s.qmax_bits = qmax_bits;
     }
     s.ntaps = j;
     s.ngroups = (int)gid.size();
-    s.real = symmetric_taps(taps) ? 1 : 0;
+    s.real = symmetric_taps(taps) && (!q || symmetric_taps(*q)) ? 1 : 0;
     return s;
+}
+
+// The implicit solve fuses into plan 1 when the symbol is real and the fused
+// pass is the TMA column kernel that precomputes its multipliers (N <= 4096).
+bool implicit_fusable(const Plan& p, const Taps& s, const Taps& q) {
+    if (p.kind != kFusedR2C || !p.tma0 || p.halves || p.ax0.n > 4096) return false;
+    if (!symmetric_taps(s) || !symmetric_taps(q)) return false;
+    if ((i64)(s.map.size() + q.map.size()) > fsx::kMaxFusedTaps) return false;
+    std::set<std::pair<int, i64>> g;
+    for (const auto& kv : s.map) g.insert({0, kv.first[p.axes[0]]});
+    for (const auto& kv : q.map) g.insert({1, kv.first[p.axes[0]]});
+    return (int)g.size() <= fsx::kMaxGroups;
 }
 
 fsx::RowPairArgs rowpair_args(const Plan& p, const Taps& taps, u64 T, double2* z, const Device& dev) {
@@ -717,13 +742,17 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
         const fsx::RowLayout lay{p.P, 0, p.rows};
         FSX_CK(fsx::launch_r2c_rows(d_a0, H, p.rows, p.L, lay, tw, st));
         fsx::StepTwiddle none;
-        const fsx::FusedSymbol sym = fused_symbol(p, taps, T);
+        const fsx::FusedSymbol sym = fused_symbol(p, taps, T, q, q ? p.qmax.as<unsigned long long>() : nullptr);
         fsx::FusedSymbol nosym;
         if (r == 3) {
             if (p.tma1) FSX_CK(fsx::launch_cols_tma(p.map1, p.ax1, 0, nosym, tw, st));
             else FSX_CK(fsx::launch_axis_pow2(H, H, p.ax1, -1, none, tw, st));
         }
         sp.mark();
+        if (q) {  // implicit: max |lamQ| for the pinv threshold first
+            FSX_CK(cudaMemsetAsync(p.qmax.p, 0, 8, st));
+            FSX_CK(fsx::launch_fused_qmax(sym, p.ax0.ncols, p.qmax.as<unsigned long long>(), tw, st));
+        }
         if (p.halves) FSX_CK(fsx::launch_fused_halves(p.map2, p.ax0, sym, tw, st));
         else if (p.tma0) FSX_CK(fsx::launch_cols_tma(p.map0, p.ax0, 2, sym, tw, st));
         else FSX_CK(fsx::launch_fused_r2c(H, p.ax0, sym, tw, st));
@@ -1080,8 +1109,11 @@ void solve(const SolveReq& rq) {
         if (rq.out != rq.a0) FSX_CK(cudaMemcpyAsync(rq.out, rq.a0, bytes, cudaMemcpyDeviceToDevice, st));
         return;
     }
-    const int force_general = (rq.opt && rq.opt->path == 1) || rq.q != nullptr;
-    Plan& p = get_plan(dev, s, taps, force_general);
+    const int force_general = rq.opt && rq.opt->path == 1;
+    Plan* pp = &get_plan(dev, s, taps, force_general);
+    if (rq.q && !implicit_fusable(*pp, taps, qtaps)) pp = &get_plan(dev, s, taps, 1);
+    Plan& p = *pp;
+    if (rq.q && p.kind == kFusedR2C) p.qmax.ensure(8);
     Stamps sp{&dev, rq.st != nullptr || (rq.device_ptrs && rq.opt && rq.opt->stage_events), st};
     if (rq.device_ptrs) {
         run_plan(p, dev, taps, rq.q ? &qtaps : nullptr, rq.T, rq.a0, rq.out, st, sp);

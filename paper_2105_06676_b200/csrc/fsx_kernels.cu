@@ -929,6 +929,40 @@ int kernel_prepare(const void* fn, size_t smem, int threads) {
     return e.per_sm;
 }
 
+// max |lamQ(k)| over the half spectrum for the implicit fused symbol: the
+// pinv threshold of the reference (proj/src/spectrum.cpp:85-96) needs it
+// before any multiplier is formed.  |lam(-k)| = |lam(k)| for real taps, so
+// the half spectrum covers the full one.
+__global__ void k_fused_qmax(FusedSymbol sym, i64 ncols, unsigned long long* out, const double2* __restrict__ tw_all) {
+    double m = 0.0;
+    const i64 total = sym.n0 * ncols;
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (i64)gridDim.x * blockDim.x) {
+        const i64 k0 = i / ncols, c = i - k0 * ncols;
+        i64 kx, ky;
+        fused_col_freqs(sym, c, kx, ky);
+        if (kx > sym.M) continue;
+        double2 lam = make_double2(0.0, 0.0);
+        for (int j = 0; j < sym.ntaps; ++j) {
+            const int g = sym.tap_group[j];
+            if (sym.group_set[g] != 1) continue;
+            const double2 e = cmul(tap_term(sym, tw_all, j, kx, ky), eplus_tab(tw_all, sym.n0, k0 * (i64)sym.group_off[g]));
+            lam = cadd(lam, e);
+        }
+        m = fmax(m, hypot(lam.x, lam.y));
+    }
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out, m);
+}
+
+cudaError_t launch_fused_qmax(const FusedSymbol& sym, i64 ncols, unsigned long long* out, const double2* tw,
+                              cudaStream_t s) {
+    const i64 total = sym.n0 * ncols;
+    i64 blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_fused_qmax<<<(unsigned)blocks, 256, 0, s>>>(sym, ncols, out, tw);
+    return cudaGetLastError();
+}
+
 #define FSX_POW2_CASES(MACRO) \
     MACRO(8) MACRO(16) MACRO(32) MACRO(64) MACRO(128) MACRO(256) MACRO(512) MACRO(1024) MACRO(2048) MACRO(4096) MACRO(8192)
 

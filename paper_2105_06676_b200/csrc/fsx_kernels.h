@@ -74,6 +74,12 @@ struct FusedSymbol {
     double scale = 1.0;          // 1 / prod(dims)
     int real = 0;                // taps symmetric under o -> -o: lam is real
     double neg_mag2 = 0.0;       // |lam|^2 below this: |lam|^T < 2^-1100 (power skipped, 0)
+    // implicit solve (solve_periodic_implicit): groups of the mass kernel Q
+    // carry group_set = 1; lam = pinv(lamQ) * lamS with the pinv threshold
+    // 1e-12 * max |lamQ| (*qmax_bits, filled by launch_fused_qmax first)
+    int implicit = 0;
+    int group_set[kMaxGroups];
+    const unsigned long long* qmax_bits = nullptr;
     i64 c_off = 0;               // slab decomposition: global frequency of local column block start
                                  // (rank 2: kx offset; rank 3: ky offset)
 };
@@ -243,6 +249,10 @@ cudaError_t launch_c2r_reg(const double2* H, double* x, i64 nrows, i64 L, const 
 // one direct periodic stencil step out = sum_taps B a[x + off] (verifier)
 cudaError_t launch_step_naive(const double* a, double* out, const NaiveGeom& g, const long long* off,
                               const double* blk, cudaStream_t s);
+// max |lamQ| over the half spectrum of an implicit fused symbol (bits of a
+// nonnegative double; *out zeroed by the caller)
+cudaError_t launch_fused_qmax(const FusedSymbol& sym, i64 ncols, unsigned long long* out, const double2* tw_all,
+                              cudaStream_t s);
 // 8192-point fused pass as two parity halves (fsx_tma.cu)
 bool halves_ok(const AxisGeom& g);
 int make_cols_tensor_map_par(void* out_map, void* base, const AxisGeom& g);

@@ -175,13 +175,15 @@ __device__ __forceinline__ void pow_real_vec_skip(double (&x)[R], u64 T, double 
     }
 }
 
-// Real symbol lam(k0) for k0 = t + q * TPL (no power, no scale).
+// Real symbol lam(k0) for k0 = t + q * TPL (no power, no scale), over the
+// groups of one tap set (set 0: the stencil S; set 1: an implicit solve's Q).
 template <int N, int R, int TPL, class AC>
-__device__ __forceinline__ void symbol_real(double (&lam)[R], int t, const FusedSymbol& sym,
-                                            const double2* __restrict__ tw_all, AC acoef) {
+__device__ __forceinline__ void symbol_real_set(double (&lam)[R], int t, const FusedSymbol& sym,
+                                                const double2* __restrict__ tw_all, AC acoef, int set) {
 #pragma unroll
     for (int q = 0; q < R; ++q) lam[q] = 0.0;
     for (int gi = 0; gi < sym.ngroups; ++gi) {
+        if (sym.implicit && sym.group_set[gi] != set) continue;
         const double2 a = acoef(gi);
         const i64 og = sym.group_off[gi];
         if (og == 0) {  // exp(0) = 1: no table read
@@ -198,6 +200,21 @@ __device__ __forceinline__ void symbol_real(double (&lam)[R], int t, const Fused
                 lam[q] = fma(a.x, e.x, fma(-a.y, e.y, lam[q]));
             }
         }
+    }
+}
+
+template <int N, int R, int TPL, class AC>
+__device__ __forceinline__ void symbol_real(double (&lam)[R], int t, const FusedSymbol& sym,
+                                            const double2* __restrict__ tw_all, AC acoef) {
+    symbol_real_set<N, R, TPL>(lam, t, sym, tw_all, acoef, 0);
+    if (sym.implicit) {
+        // solve_periodic_implicit (proj/src/periodic.cpp:108-124): lam = pinv(lamQ) lamS,
+        // pinv(v) = |v| <= 1e-12 max|lamQ| ? 0 : 1/v (proj/src/spectrum.cpp:85-96)
+        double lq[R];
+        symbol_real_set<N, R, TPL>(lq, t, sym, tw_all, acoef, 1);
+        const double eps = 1e-12 * __longlong_as_double((long long)*sym.qmax_bits);
+#pragma unroll
+        for (int q = 0; q < R; ++q) lam[q] = fabs(lq[q]) <= eps ? 0.0 : (1.0 / lq[q]) * lam[q];
     }
 }
 

@@ -323,6 +323,37 @@ def test_implicit(orc):
         assert np.abs(got - want).max() <= 1e-12
 
 
+@pytest.mark.parametrize("dims,T", [([1024, 256], 200), ([512, 64, 32], 30), ([2048, 128], 1)])
+def test_implicit_fused_vs_oracle(orc, dims, T):
+    """solve_periodic_implicit on the fused plan (real symbols, N0 in the TMA
+    multiplier path): Crank-Nicolson q = I - (b/2) L, s = I + (b/2) L of the
+    axial Laplacian, vs the oracle (periodic.cpp:108-124)."""
+    r = len(dims)
+    b = 0.2
+    qd, sd = {(0,) * r: 1.0 + b * r}, {(0,) * r: 1.0 - b * r}
+    for a in range(r):
+        for sgn in (-1, 1):
+            off = tuple(sgn if i == a else 0 for i in range(r))
+            qd[off], sd[off] = -b / 2, b / 2
+    q, sk = R.kern_from(qd, r), R.kern_from(sd, r)
+    a0 = orc.splitmix_fill(61 + T, int(np.prod(dims)), True)
+    got = fs.solve_periodic_implicit(K(q), K(sk), G(dims, a0), T).data
+    want = orc.solve_periodic_implicit(a0, dims, q.arrays(), sk.arrays(), T)
+    assert rel_l2(got, want) <= 1e-10
+
+
+def test_implicit_fused_pinv_threshold(orc):
+    """A singular mass kernel (the Laplacian itself: lamQ(0) = 0) exercises the
+    1e-12 max|lamQ| pseudo-inverse threshold on the fused plan."""
+    dims = [1024, 128]
+    q = R.kern_from({(0, 0): 4.0, (1, 0): -1.0, (-1, 0): -1.0, (0, 1): -1.0, (0, -1): -1.0}, 2)
+    sk = R.kern_from({(0, 0): 0.5, (1, 0): 0.125, (-1, 0): 0.125, (0, 1): 0.125, (0, -1): 0.125}, 2)
+    a0 = orc.splitmix_fill(73, 1024 * 128, True)
+    got = fs.solve_periodic_implicit(K(q), K(sk), G(dims, a0), 3).data
+    want = orc.solve_periodic_implicit(a0, dims, q.arrays(), sk.arrays(), 3)
+    assert rel_l2(got, want) <= 1e-10
+
+
 def test_cached_and_timings():
     cache = fs.SpectrumCache()
     a = R.random_grid(Rng(5), 4096)
