@@ -78,7 +78,7 @@ struct FusedSymbol {
     // carry group_set = 1; lam = pinv(lamQ) * lamS with the pinv threshold
     // 1e-12 * max |lamQ| (*qmax_bits, filled by launch_fused_qmax first)
     int implicit = 0;
-    int group_set[kMaxGroups];
+    int group_set[kMaxGroups] = {};
     const unsigned long long* qmax_bits = nullptr;
     i64 c_off = 0;               // slab decomposition: global frequency of local column block start
                                  // (rank 2: kx offset; rank 3: ky offset)

@@ -183,7 +183,7 @@ __device__ __forceinline__ void symbol_real_set(double (&lam)[R], int t, const F
 #pragma unroll
     for (int q = 0; q < R; ++q) lam[q] = 0.0;
     for (int gi = 0; gi < sym.ngroups; ++gi) {
-        if (sym.implicit && sym.group_set[gi] != set) continue;
+        if (sym.group_set[gi] != set) continue;
         const double2 a = acoef(gi);
         const i64 og = sym.group_off[gi];
         if (og == 0) {  // exp(0) = 1: no table read
@@ -203,11 +203,11 @@ __device__ __forceinline__ void symbol_real_set(double (&lam)[R], int t, const F
     }
 }
 
-template <int N, int R, int TPL, class AC>
+template <int N, int R, int TPL, bool IMPL = false, class AC>
 __device__ __forceinline__ void symbol_real(double (&lam)[R], int t, const FusedSymbol& sym,
                                             const double2* __restrict__ tw_all, AC acoef) {
     symbol_real_set<N, R, TPL>(lam, t, sym, tw_all, acoef, 0);
-    if (sym.implicit) {
+    if constexpr (IMPL) {
         // solve_periodic_implicit (proj/src/periodic.cpp:108-124): lam = pinv(lamQ) lamS,
         // pinv(v) = |v| <= 1e-12 max|lamQ| ? 0 : 1/v (proj/src/spectrum.cpp:85-96)
         double lq[R];

@@ -46,19 +46,21 @@ struct TCfg {
     static constexpr bool TMEM = false;
 #endif
     static constexpr size_t smem(int mode) {
-        return (size_t)W * LSW * 16 + (mode == 2 && PRE ? (size_t)NT * R * 8 : 0);
+        return (size_t)W * LSW * 16 + ((mode == 2 || mode == 4) && PRE ? (size_t)NT * R * 8 : 0);
     }
 };
 
 static int tma_w2();
 
-// MODE 0: forward C2C, 1: inverse C2C, 2: fused R2C spectral pass.
+// MODE 0: forward C2C, 1: inverse C2C, 2: fused R2C spectral pass, 4: the
+// same with an implicit (pinv(lamQ) lamS) real symbol, 3: copy only.
 // The TMA tile is [N rows][W columns] (row-major, as the boxes land); the
 // FFT exchanges reuse the same buffer as W line-major rows of LSW.
 template <int N, int MODE, int WW = 0>
 __global__ void __launch_bounds__(TCfg<N, WW>::NT, TCfg<N, WW>::MINB)
 k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
     using C = TCfg<N, WW>;
+    constexpr bool FUSED = MODE == 2 || MODE == 4;  // 4: implicit symbol (pinv(lamQ) lamS)
     constexpr int W = C::W;
     // full twiddle tables for the multi-column tiles (N < 4096); the one-column
     // 4096 tiles measured faster with derived twiddles (cfg2 158 vs 165 us)
@@ -68,14 +70,14 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
     extern __shared__ __align__(128) double2 tile[];
     __shared__ __align__(8) unsigned long long bar;
     __shared__ double2 acoef[kMaxGroups][W];
-    __shared__ double2 tapterm[MODE == 2 ? kMaxFusedTaps : 1][W];
+    __shared__ double2 tapterm[MODE >= 2 ? kMaxFusedTaps : 1][W];
     const int w = threadIdx.x % W, t = threadIdx.x / W;
     const i64 tiles = (g.ncols + W - 1) / W;
     const i64 o = (i64)blockIdx.x / tiles;
     const i64 c0 = ((i64)blockIdx.x - o * tiles) * W;
     const i64 c = c0 + w;
     i64 kx = c, ky = 0;
-    if constexpr (MODE == 2) {
+    if constexpr (FUSED) {
         fused_col_freqs(sym, c, kx, ky);
         // pitch-padding tiles of a 3D plane (W divides P, so a tile is all-padding or none)
         if (c0 - (c0 / sym.P) * sym.P > sym.M && sym.rank == 3) return;
@@ -99,8 +101,8 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
     // L1 that serves the table reads (cfg3 measured 0.87 -> 1.04 ms).
     // The 128 KB tiles (N = 8192, 16 warps, one CTA per SM) park the
     // multipliers in tensor memory instead (128 columns; see fsx_async.cuh).
-    constexpr bool PRE = MODE == 2 && C::PRE;
-    constexpr bool TM = MODE == 2 && C::TMEM;
+    constexpr bool PRE = FUSED && C::PRE;
+    constexpr bool TM = FUSED && C::TMEM;
     double* mult = reinterpret_cast<double*>(tile + W * C::LSW);
     __shared__ unsigned tmem_base;
     const int warp = threadIdx.x >> 5;
@@ -108,12 +110,12 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
         if (warp == 0) tmem_alloc<128>(&tmem_base);
         tmem_fence_before();
     }
-    if constexpr (MODE == 2) {
+    if constexpr (FUSED) {
         for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
     }
     __syncthreads();  // barrier initialised before anyone waits on it; tap terms visible
     if constexpr (TM) tmem_fence_after();
-    if constexpr (MODE == 2) {
+    if constexpr (FUSED) {
         for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
             double2 a = make_double2(0.0, 0.0);
             for (int j = 0; j < sym.ntaps; ++j)
@@ -123,7 +125,7 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
         __syncthreads();
         if ((PRE || TM) && sym.real) {
             double lam[C::R];
-            symbol_real<N, C::R, C::TPL>(lam, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
+            symbol_real<N, C::R, C::TPL, MODE == 4>(lam, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
             pow_real_vec_skip<C::R, 4>(lam, sym.T, sym.neg_mag2);
             if constexpr (TM) {
                 static_assert(C::R == 16, "TMEM parking holds 16 doubles per thread");
@@ -155,7 +157,7 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
     } else {
         FF::run(v, t, line, tw_all + N);
     }
-    if constexpr (MODE == 2) {
+    if constexpr (FUSED) {
         if (PRE && sym.real) {
 #pragma unroll
             for (int q = 0; q < C::R; ++q) v[q] = cscale(v[q], mult[q * C::NT + threadIdx.x]);
@@ -636,7 +638,7 @@ static int tma_persistent() {
 template <int N, int MODE>
 static cudaError_t cols_tma_n(const CUtensorMap& map, const AxisGeom& g, const FusedSymbol& sym, const double2* tw,
                               cudaStream_t s) {
-    if (tma_persistent() && 3 * TCfg<N>::W * TCfg<N>::LSW * 16 <= 220 * 1024) {
+    if (MODE != 4 && tma_persistent() && 3 * TCfg<N>::W * TCfg<N>::LSW * 16 <= 220 * 1024) {
         using C = TCfg<N>;
         const size_t smem = (size_t)3 * C::W * C::LSW * sizeof(double2);
         const i64 ntiles = g.outer * ((g.ncols + C::W - 1) / C::W);
@@ -695,7 +697,8 @@ cudaError_t launch_cols_tma(const void* tensor_map, const AxisGeom& g, int mode,
     case N:                                                            \
         return mode == 0 ? cols_tma_n<N, 0>(map, g, sym, tw, s)        \
              : mode == 1 ? cols_tma_n<N, 1>(map, g, sym, tw, s)        \
-                         : cols_tma_n<N, 2>(map, g, sym, tw, s);
+             : sym.implicit ? cols_tma_n<N, 4>(map, g, sym, tw, s)     \
+                            : cols_tma_n<N, 2>(map, g, sym, tw, s);
     switch (g.n) {
         FSX_TMA(512)
         FSX_TMA(1024)
