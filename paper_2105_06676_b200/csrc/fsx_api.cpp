@@ -1074,6 +1074,7 @@ struct SolveReq {
     fsx_stage_timings* st;
     bool vector = false;
     bool device_ptrs = false;
+    const Taps* cached = nullptr;  // solve_periodic_cached: the spectrum's kernel from the cache
 };
 
 void solve(const SolveReq& rq) {
@@ -1093,6 +1094,7 @@ void solve(const SolveReq& rq) {
     } else {
         taps = parse_kernel(rq.k);
         require_fits(taps, s);
+        if (rq.cached) taps = *rq.cached;
     }
     if (!rq.a0 || !rq.out) throw SpecErr("fsx: null grid pointer");
     const size_t bytes = (size_t)s.values() * 8;
@@ -1231,9 +1233,13 @@ fsx_status guarded(F&& f) {
 
 }  // namespace
 
+// SpectrumCache (proj/include/fftstencil/periodic.hpp:28-35, periodic.cpp:67-74):
+// memoised by dims only -- the first kernel seen for a dims vector defines
+// the spectrum every later call with those dims uses, as in the reference.
+// The spectrum itself is analytic on the GPU, so the cache keeps the kernel.
 struct fsx_spectrum_cache {
     std::mutex mu;
-    int used = 0;
+    std::map<std::vector<i64>, Taps> by_dims;
 };
 
 extern "C" {
@@ -1272,9 +1278,19 @@ fsx_status fsx_solve_periodic_cached(const fsx_shape* shape, const double* a0, c
                                      fsx_stage_timings* st) {
     return guarded([&] {
         if (!cache) throw SpecErr("solve_periodic_cached: null cache");
-        std::lock_guard<std::mutex> lk(cache->mu);
-        ++cache->used;
-        solve({shape, a0, k, nullptr, T, out, opt, st});
+        const Shape sh = parse_shape(shape);
+        const Taps taps = parse_kernel(k);
+        require_fits(taps, sh);  // the passed kernel is checked (periodic.cpp:91)
+        Taps cached;
+        {
+            std::lock_guard<std::mutex> lk(cache->mu);
+            auto it = cache->by_dims.find(sh.dims);
+            if (it == cache->by_dims.end()) it = cache->by_dims.emplace(sh.dims, taps).first;
+            cached = it->second;
+        }
+        SolveReq rq{shape, a0, k, nullptr, T, out, opt, st};
+        rq.cached = &cached;
+        solve(rq);
     });
 }
 

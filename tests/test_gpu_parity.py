@@ -368,6 +368,24 @@ def test_cached_and_timings():
     assert st.sum() > before  # accumulated, not reset
 
 
+def test_cache_is_keyed_by_dims_only():
+    """SpectrumCache::get (periodic.cpp:67-74) memoises by dims alone: a later
+    call with the same dims but another kernel reuses the first kernel's
+    spectrum; other dims get their own.  The passed kernel is still checked
+    by require_fits."""
+    cache = fs.SpectrumCache()
+    a = R.random_grid(Rng(15), 64 * 32)
+    kA, kB = K(R.random_kernel(Rng(16), 2, 1)), K(R.random_kernel(Rng(17), 2, 1))
+    first = fs.solve_periodic_cached(G([64, 32], a), kA, 4, cache).data
+    again = fs.solve_periodic_cached(G([64, 32], a), kB, 4, cache).data
+    assert np.array_equal(first, fs.solve_periodic(G([64, 32], a), kA, 4).data)
+    assert np.array_equal(again, first)
+    other = fs.solve_periodic_cached(G([32, 64], a), kB, 4, cache).data
+    assert np.array_equal(other, fs.solve_periodic(G([32, 64], a), kB, 4).data)
+    with pytest.raises(fs.SpecError):
+        fs.solve_periodic_cached(G([1, 1], a[:1]), kB, 4, cache)
+
+
 # ------------------------------------------------------------------ per-plan parity vs the oracle
 PLAN_CASES = [
     # (dims, m, taps-kind, T)   fused R2C rank 2/3, 1D row-pair (m = 1, 2), general
