@@ -24,11 +24,6 @@
 namespace fsx {
 
 // ------------------------------------------------------------------ helpers
-__device__ __forceinline__ double2 phase_at(const PhaseTable& t, i64 x) {
-    if (t.shift == 0) return __ldg(t.lo + x);
-    return cmul(__ldg(t.hi + (x >> t.shift)), __ldg(t.lo + (x & t.mask)));
-}
-
 __device__ __forceinline__ i64 modp(i64 a, i64 n) {
     const i64 r = a % n;
     return r < 0 ? r + n : r;
@@ -144,11 +139,6 @@ __device__ __forceinline__ void pow_block(double2 (&lam)[MM][MM], u64 T) {
     for (int r = 0; r < MM; ++r)
 #pragma unroll
         for (int c = 0; c < MM; ++c) lam[r][c] = acc[r][c];
-}
-
-__device__ __forceinline__ void flag_nonfinite(bool bad, Flags* f) {
-    const unsigned any = __ballot_sync(0xffffffffu, bad);
-    if (any && (threadIdx.x & 31) == 0) atomicOr(&f->nonfinite, 1u);
 }
 
 // ------------------------------------------------------------------ C2C passes
@@ -847,6 +837,10 @@ static cudaError_t axis_pow2_n(const double2* in, double2* out, const AxisGeom& 
 
 cudaError_t launch_axis_pow2(const double2* in, double2* out, const AxisGeom& g, int sign,
                              const StepTwiddle& st, const double2* tw, cudaStream_t s, Flags* flags) {
+    {
+        const cudaError_t e = launch_axis_tma(in, out, g, sign, st, tw, s, flags);
+        if (e != cudaErrorNotSupported) return e;
+    }
     if (pipe_enabled() && pipe_cols_ok(g.n) && g.inner > 1 && st.mode == 0 && in == out && !flags) {
         FusedSymbol none;
         return launch_cols_pipe(out, g, sign < 0 ? 0 : 1, none, tw, s);

@@ -253,6 +253,10 @@ cudaError_t launch_step_naive(const double* a, double* out, const NaiveGeom& g, 
 // nonnegative double; *out zeroed by the caller)
 cudaError_t launch_fused_qmax(const FusedSymbol& sym, i64 ncols, unsigned long long* out, const double2* tw_all,
                               cudaStream_t s);
+// C2C strided pass with TMA column I/O, four-step twiddles and an optional
+// non-finite scan (fsx_tma.cu); cudaErrorNotSupported when not applicable
+cudaError_t launch_axis_tma(const double2* in, double2* out, const AxisGeom& g, int sign, const StepTwiddle& st,
+                            const double2* tw_all, cudaStream_t s, Flags* flags);
 // 8192-point fused pass as two parity halves (fsx_tma.cu)
 bool halves_ok(const AxisGeom& g);
 int make_cols_tensor_map_par(void* out_map, void* base, const AxisGeom& g);
@@ -260,6 +264,7 @@ cudaError_t launch_fused_halves(const void* tensor_map2, const AxisGeom& g, cons
                                 const double2* tw_all, cudaStream_t s);
 // TMA column passes (fsx_tma.cu); tensor_map points at a 64-byte aligned CUtensorMap
 bool tma_cols_ok(i64 N);
+int tma_cols_width(i64 N);  // columns per TMA tile (the box width the host encodes)
 int make_cols_tensor_map(void* out_map, void* base, const AxisGeom& g);
 cudaError_t launch_cols_tma(const void* tensor_map, const AxisGeom& g, int mode, const FusedSymbol& sym,
                             const double2* tw_all, cudaStream_t s);

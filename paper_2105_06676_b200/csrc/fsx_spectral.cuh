@@ -11,6 +11,18 @@
 
 namespace fsx {
 
+// exp(-2 pi i x / n) for x in [0, n) from a (two-level) phase table
+__device__ __forceinline__ double2 phase_at(const PhaseTable& t, i64 x) {
+    if (t.shift == 0) return __ldg(t.lo + x);
+    return cmul(__ldg(t.hi + (x >> t.shift)), __ldg(t.lo + (x & t.mask)));
+}
+
+// any lane's `bad` sets the solve's non-finite flag (realize_checked)
+__device__ __forceinline__ void flag_nonfinite(bool bad, Flags* f) {
+    const unsigned any = __ballot_sync(0xffffffffu, bad);
+    if (any && (threadIdx.x & 31) == 0) atomicOr(&f->nonfinite, 1u);
+}
+
 // exp(+2 pi i x / n) for pow2 n from the exact table: conj(tw_all[n + (x mod n)])
 __device__ __forceinline__ double2 eplus_tab(const double2* tw_all, i64 n, i64 x) {
     return cconj(__ldg(tw_all + n + (x & (n - 1))));

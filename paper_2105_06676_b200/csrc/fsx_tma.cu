@@ -18,6 +18,7 @@
 #include <cuda.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "fsx_async.cuh"
 #include "fsx_device.cuh"
@@ -192,6 +193,129 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
         for (int b = 0; b < C::NBOX; ++b) tma_store_3d(&map, tile + b * C::BOX * W, (int)(2 * c0), b * C::BOX, (int)o);
         bulk_commit();
         bulk_wait_read0();
+    }
+}
+
+// C2C strided pass with TMA column I/O for the general axis launcher
+// (launch_axis_pow2): optional four-step twiddle (TWM 1: post-multiply by
+// W^(b k), 2: pre-multiply by its conjugate; b = column / col_div, exponent as
+// StepTwiddle), out of place (separate load / store maps), and the solve's
+// non-finite scan on its output when `flags` is set.  Used by the 1D plan's
+// column FFTs (128-point columns for cfg5, 512 for cfg1).
+template <int N, int SIGN, int TWM>
+__global__ void __launch_bounds__(TCfg<N>::NT, TCfg<N>::MINB)
+k_axis_tma(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_out, AxisGeom g,
+           StepTwiddle st, const double2* __restrict__ tw_all, Flags* flags) {
+    using C = TCfg<N>;
+    constexpr int W = C::W;
+    using F = LineFFT<N, SIGN, false, false, N < 4096>;
+    extern __shared__ __align__(128) double2 tile[];
+    __shared__ __align__(8) unsigned long long bar;
+    const int w = threadIdx.x % W, t = threadIdx.x / W;
+    const i64 tiles = (g.ncols + W - 1) / W;
+    const i64 o = (i64)blockIdx.x / tiles;
+    const i64 c0 = ((i64)blockIdx.x - o * tiles) * W;
+    const i64 c = c0 + w;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_init_fence();
+        pdl_wait();
+        mbar_expect_tx(&bar, (unsigned)(N * W * sizeof(double2)));
+#pragma unroll 1
+        for (int b = 0; b < C::NBOX; ++b) tma_load_3d(tile + b * C::BOX * W, &map_in, (int)(2 * c0), b * C::BOX, (int)o, &bar);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    pdl_trigger();
+    double2 v[C::R];
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) v[q] = tile[(t + q * C::TPL) * W + w];
+    const i64 bq = c / st.col_div;
+    if constexpr (TWM == 2) {
+#pragma unroll
+        for (int q = 0; q < C::R; ++q)
+            v[q] = cmulc(v[q], phase_at(st.tab, bq * ((i64)(t + q * C::TPL) * st.kmul + o * st.omul)));
+    }
+    F::run(v, t, tile + w * C::LSW, tw_all + N);
+    if constexpr (TWM == 1) {
+#pragma unroll
+        for (int q = 0; q < C::R; ++q)
+            v[q] = cmul(v[q], phase_at(st.tab, bq * ((i64)(t + q * C::TPL) * st.kmul + o * st.omul)));
+    }
+    if (flags) {
+        bool bad = false;
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) bad |= c < g.ncols && (!isfinite(v[q].x) || !isfinite(v[q].y));
+        flag_nonfinite(bad, flags);
+    }
+    __syncthreads();  // last exchange reads done before the tile is overwritten
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) tile[(t + q * C::TPL) * W + w] = v[q];
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll 1
+        for (int b = 0; b < C::NBOX; ++b) tma_store_3d(&map_out, tile + b * C::BOX * W, (int)(2 * c0), b * C::BOX, (int)o);
+        bulk_commit();
+        bulk_wait_read0();
+    }
+}
+
+static int axis_tma_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_TMA_AXIS");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+
+template <int N, int SIGN, int TWM>
+static cudaError_t axis_tma_nst(const CUtensorMap& mi, const CUtensorMap& mo, const AxisGeom& g, const StepTwiddle& st,
+                                const double2* tw, Flags* f, cudaStream_t s) {
+    using C = TCfg<N>;
+    const size_t smem = (size_t)C::W * C::LSW * sizeof(double2);
+    const i64 tiles = (g.ncols + C::W - 1) / C::W;
+    auto kf = k_axis_tma<N, SIGN, TWM>;
+    kernel_prepare((const void*)kf, smem);
+    return launch_pdl(kf, dim3((unsigned)(g.outer * tiles)), dim3(C::NT), smem, s, mi, mo, g, st, tw, f);
+}
+
+template <int N>
+static cudaError_t axis_tma_n(const CUtensorMap& mi, const CUtensorMap& mo, const AxisGeom& g, int sign,
+                              const StepTwiddle& st, const double2* tw, Flags* f, cudaStream_t s) {
+    if (sign < 0)
+        return st.mode == 1 ? axis_tma_nst<N, -1, 1>(mi, mo, g, st, tw, f, s)
+             : st.mode == 2 ? axis_tma_nst<N, -1, 2>(mi, mo, g, st, tw, f, s)
+                            : axis_tma_nst<N, -1, 0>(mi, mo, g, st, tw, f, s);
+    return st.mode == 1 ? axis_tma_nst<N, +1, 1>(mi, mo, g, st, tw, f, s)
+         : st.mode == 2 ? axis_tma_nst<N, +1, 2>(mi, mo, g, st, tw, f, s)
+                        : axis_tma_nst<N, +1, 0>(mi, mo, g, st, tw, f, s);
+}
+
+// Returns cudaErrorNotSupported when the TMA path does not apply (the caller
+// falls back to the per-thread strided kernel).
+cudaError_t launch_axis_tma(const double2* in, double2* out, const AxisGeom& g, int sign, const StepTwiddle& st,
+                            const double2* tw, cudaStream_t s, Flags* flags) {
+    // 128-point columns measured slower than the per-thread strided kernel (cfg5: 540 vs 511 us)
+    if (!axis_tma_enabled() || g.inner <= 1 || g.n < 512 || g.n > 4096) return cudaErrorNotSupported;
+    if (g.n == 4096 && tma_w2()) return cudaErrorNotSupported;  // map width would not match TCfg<4096>
+    const int W = tma_cols_width(g.n);
+    if (g.ncols % W || (reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) % 16) return cudaErrorNotSupported;
+    alignas(64) unsigned char mi[128], mo[128];
+    if (make_cols_tensor_map(mi, const_cast<double2*>(in), g) != 0) return cudaErrorNotSupported;
+    if (out == in) std::memcpy(mo, mi, sizeof mo);
+    else if (make_cols_tensor_map(mo, out, g) != 0) return cudaErrorNotSupported;
+    const CUtensorMap& MI = *reinterpret_cast<const CUtensorMap*>(mi);
+    const CUtensorMap& MO = *reinterpret_cast<const CUtensorMap*>(mo);
+    switch (g.n) {
+        case 128: return axis_tma_n<128>(MI, MO, g, sign, st, tw, flags, s);
+        case 256: return axis_tma_n<256>(MI, MO, g, sign, st, tw, flags, s);
+        case 512: return axis_tma_n<512>(MI, MO, g, sign, st, tw, flags, s);
+        case 1024: return axis_tma_n<1024>(MI, MO, g, sign, st, tw, flags, s);
+        case 2048: return axis_tma_n<2048>(MI, MO, g, sign, st, tw, flags, s);
+        case 4096: return axis_tma_n<4096>(MI, MO, g, sign, st, tw, flags, s);
+        default: return cudaErrorNotSupported;
     }
 }
 
