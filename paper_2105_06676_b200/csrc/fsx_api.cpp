@@ -200,6 +200,15 @@ HostTable make_phase(i64 n) {
 
 // Packs several host tables into one device buffer; returns PhaseTables
 // pointing into it.
+// exp(-i pi x^2 / n) for x < n with x^2 reduced mod 2n exactly (proj/src/fft.cpp:20-25)
+HostTable make_chirp(i64 n) {
+    HostTable t;
+    t.n = n;
+    t.lo.resize(n);
+    for (i64 x = 0; x < n; ++x) t.lo[x] = expi_neg((i64)(((__int128)x * x) % (2 * n)), 2 * n);
+    return t;
+}
+
 struct TableSet {
     std::vector<double2> host;
     struct Ref {
@@ -247,7 +256,13 @@ struct GenAxis {
     i64 n = 1, n1 = 0, n2 = 0;  // split: n = n1 * n2 (n1 == 0: not split)
     int direct = 0;
     int table = -1;             // phase table for n
+    // Bluestein (non-pow2 n > kBlueMin): convolution length P (pow2 >= 2n - 1)
+    int blue = 0;
+    i64 P = 0;
+    int t_chirp = -1, t_P = -1;  // chirp e^(-i pi x^2 / n) (table lo = values), phase table of P
+    i64 bhat_off = 0;            // filter spectrum offset in Plan::blue_bhat (complex elements)
 };
+constexpr i64 kBlueMin = 256;  // non-pow2 axes above this use Bluestein, below the direct DFT
 
 struct Plan {
     int kind = 0;
@@ -275,6 +290,7 @@ struct Plan {
     DevBuf work;      // H (kind 1) / complex Z (kind 3)
     DevBuf d_in, d_out;
     DevBuf taps_dev;  // general path tap arrays
+    DevBuf blue_bhat, blue_buf;  // Bluestein filter spectra and [lines][P] workspace
     DevBuf qmax;      // implicit fused symbol: max |lamQ| (bits)
     std::vector<char> taps_host;
     int launches = 0;
@@ -396,6 +412,65 @@ std::string plan_key(const Shape& s, int kind_hint) {
     return k;
 }
 
+// Batched pow2 FFT of `lines` contiguous lines of length P (P <= 2^26; above
+// kMaxLine a four-step split whose frequency order is transposed -- the
+// Bluestein filter spectrum is computed with the same split, so the pointwise
+// product and the inverse split undo it).
+void fft_lines(const Plan& p, const Device& dev, double2* buf, i64 lines, i64 P, int t_P, int sign, cudaStream_t st) {
+    const double2* tw = dev.tw_all.as<double2>();
+    fsx::StepTwiddle none;
+    if (P <= fsx::kMaxLine) {
+        const fsx::AxisGeom g{P, 1, lines, P, 1};
+        FSX_CK(fsx::launch_axis_pow2(buf, buf, g, sign, none, tw, st));
+        return;
+    }
+    i64 p1, p2;
+    if (!split_pow2(P, p1, p2)) throw SpecErr("fsx: Bluestein length beyond 2^26");
+    const fsx::AxisGeom g1{p1, p2, lines, P, p2};
+    const fsx::AxisGeom g2{p2, 1, lines * p1, p2, 1};
+    fsx::StepTwiddle t1;
+    t1.col_div = 1;
+    t1.tab = p.tables.get(t_P);
+    if (sign < 0) {
+        t1.mode = 1;
+        FSX_CK(fsx::launch_axis_pow2(buf, buf, g1, sign, t1, tw, st));
+        FSX_CK(fsx::launch_axis_pow2(buf, buf, g2, sign, none, tw, st));
+    } else {
+        t1.mode = 2;
+        FSX_CK(fsx::launch_axis_pow2(buf, buf, g2, sign, none, tw, st));
+        FSX_CK(fsx::launch_axis_pow2(buf, buf, g1, sign, t1, tw, st));
+    }
+}
+
+// Filter spectra Bhat = FFT_P(b), b[x] = conj(chirp[x]) for |x| < n (wrapped),
+// and the [lines][P] workspace of the general plan's Bluestein axes.
+void setup_bluestein(Plan& p, Device& dev) {
+    i64 total = 0, work = 0;
+    for (auto& ga : p.gax)
+        if (ga.blue) {
+            ga.bhat_off = total;
+            total += ga.P;
+            work = std::max<i64>(work, p.cells * p.m / ga.n * ga.P);
+        }
+    if (!total) return;
+    p.blue_bhat.ensure((size_t)total * sizeof(double2));
+    p.blue_buf.ensure((size_t)work * sizeof(double2));
+    for (const auto& ga : p.gax) {
+        if (!ga.blue) continue;
+        std::vector<double2> b((size_t)ga.P, make_double2(0, 0));
+        const HostTable ch = make_chirp(ga.n);
+        for (i64 x = 0; x < ga.n; ++x) {
+            const double2 c = make_double2(ch.lo[x].x, -ch.lo[x].y);
+            b[x] = c;
+            if (x) b[ga.P - x] = c;
+        }
+        double2* dst = p.blue_bhat.as<double2>() + ga.bhat_off;
+        FSX_CK(cudaMemcpy(dst, b.data(), b.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        fft_lines(p, dev, dst, 1, ga.P, ga.t_P, -1, dev.stream);
+    }
+    FSX_CK(cudaStreamSynchronize(dev.stream));
+}
+
 // lane > 0: an independent copy of the plan (own workspaces and tensor maps)
 // for the pipelined batch solve, which keeps two solves in flight.
 Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general, int lane = 0) {
@@ -508,18 +583,26 @@ Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general,
                     if (!split_pow2(ga.n, ga.n1, ga.n2))
                         throw SpecErr("fsx: axis length " + std::to_string(ga.n) + " exceeds the GPU path limit (2^26)");
                     nl += 4;
-                } else {
-                    if (ga.n > fsx::kMaxDirect)
-                        throw SpecErr("fsx: non-power-of-two axis length " + std::to_string(ga.n) +
-                                      " exceeds the GPU direct-DFT limit (" + std::to_string(fsx::kMaxDirect) + ")");
+                } else if (ga.n <= kBlueMin) {
                     ga.direct = 1;
                     nl += 2;
+                } else {
+                    ga.blue = 1;
+                    ga.P = 1;
+                    while (ga.P < 2 * ga.n - 1) ga.P <<= 1;
+                    i64 q1, q2;
+                    if (ga.P > fsx::kMaxLine && !split_pow2(ga.P, q1, q2))
+                        throw SpecErr("fsx: axis length " + std::to_string(ga.n) + " exceeds the GPU path limit (Bluestein 2^26)");
+                    ga.t_chirp = p->tables.add(make_chirp(ga.n));
+                    if (ga.P > fsx::kMaxLine) ga.t_P = p->tables.add(make_phase(ga.P));
+                    nl += 8;
                 }
             }
             ga.table = p->tables.add(make_phase(ga.n));
             p->gax.push_back(ga);
         }
         p->tables.upload();
+        setup_bluestein(*p, dev);
         p->launches = (int)nl + 3;
         const i64 Z = s.values() * 16;
         p->fused_bytes = 2 * Z;
@@ -688,7 +771,19 @@ void general_axes(Plan& p, const Device& dev, double2* Z, bool inverse, cudaStre
         for (int b = a + 1; b < r; ++b) inner *= p.dims[b];
         for (int b = 0; b < a; ++b) outer *= p.dims[b];
         fsx::StepTwiddle none;
-        if (ga.direct) {
+        if (ga.blue) {
+            // proj/src/fft.cpp:103-139; inverse as conj(forward(conj x)) (fft.cpp:151-154)
+            const fsx::AxisGeom g{ga.n, inner, outer, ga.n * inner, inner};
+            const i64 lines = outer * inner;
+            double2* buf = p.blue_buf.as<double2>();
+            const double2* chirp = p.tables.get(ga.t_chirp).lo;
+            const int cj = inverse ? 1 : 0;
+            FSX_CK(fsx::launch_blue_pre(Z, buf, g, ga.P, chirp, cj, st));
+            fft_lines(p, dev, buf, lines, ga.P, ga.t_P, -1, st);
+            FSX_CK(fsx::launch_blue_mul(buf, lines, ga.P, p.blue_bhat.as<double2>() + ga.bhat_off, st));
+            fft_lines(p, dev, buf, lines, ga.P, ga.t_P, +1, st);
+            FSX_CK(fsx::launch_blue_post(buf, Z, g, ga.P, chirp, 1.0 / (double)ga.P, cj, st));
+        } else if (ga.direct) {
             fsx::AxisGeom g{ga.n, inner, outer, ga.n * inner, inner};
             FSX_CK(fsx::launch_axis_direct(Z, Z, g, sign, p.tables.get(ga.table), st));
         } else if (!ga.n1) {

@@ -811,6 +811,64 @@ static int grid_for(i64 n, int threads) {
     return (int)(b < 1 ? 1 : b);
 }
 
+// ------------------------------------------------------------------ Bluestein (non-pow2 axes)
+// The reference's Bluestein transform (proj/src/fft.cpp:103-139, chirp
+// e^(-i pi n^2 / n_len) with n^2 reduced mod 2 n_len): the lines of an axis are
+// gathered into a [lines][P] buffer (P = pow2 >= 2n - 1) premultiplied by the
+// chirp, convolved with the chirp filter by pow2 FFTs (filter spectrum Bhat
+// precomputed per plan), and scattered back postmultiplied by the chirp.
+// Inverse = conj(forward(conj x)) (fft.cpp:151-154), unnormalized.
+__global__ void k_blue_pre(const double2* __restrict__ Z, double2* __restrict__ buf, AxisGeom g, i64 P,
+                           const double2* __restrict__ chirp, int conj_in) {
+    const i64 total = g.outer * g.ncols * P;
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (i64)gridDim.x * blockDim.x) {
+        const i64 l = i / P, n = i - l * P;
+        double2 v = make_double2(0.0, 0.0);
+        if (n < g.n) {
+            const i64 o = l / g.ncols, c = l - o * g.ncols;
+            double2 x = Z[o * g.block + c + n * g.inner];
+            if (conj_in) x = cconj(x);
+            v = cmul(x, chirp[n]);
+        }
+        buf[i] = v;
+    }
+}
+
+__global__ void k_blue_mul(double2* __restrict__ buf, i64 total, i64 P, const double2* __restrict__ bhat) {
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (i64)gridDim.x * blockDim.x)
+        buf[i] = cmul(buf[i], bhat[i % P]);
+}
+
+__global__ void k_blue_post(const double2* __restrict__ buf, double2* __restrict__ Z, AxisGeom g, i64 P,
+                            const double2* __restrict__ chirp, double scale, int conj_out) {
+    const i64 total = g.outer * g.ncols * g.n;
+    for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (i64)gridDim.x * blockDim.x) {
+        const i64 l = i / g.n, k = i - l * g.n;
+        const i64 o = l / g.ncols, c = l - o * g.ncols;
+        double2 v = cscale(cmul(buf[l * P + k], chirp[k]), scale);
+        if (conj_out) v = cconj(v);
+        Z[o * g.block + c + k * g.inner] = v;
+    }
+}
+
+cudaError_t launch_blue_pre(const double2* Z, double2* buf, const AxisGeom& g, i64 P, const double2* chirp, int conj_in,
+                            cudaStream_t s) {
+    k_blue_pre<<<grid_for(g.outer * g.ncols * P, 256), 256, 0, s>>>(Z, buf, g, P, chirp, conj_in);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_blue_mul(double2* buf, i64 lines, i64 P, const double2* bhat, cudaStream_t s) {
+    k_blue_mul<<<grid_for(lines * P, 256), 256, 0, s>>>(buf, lines * P, P, bhat);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_blue_post(const double2* buf, double2* Z, const AxisGeom& g, i64 P, const double2* chirp,
+                             double scale, int conj_out, cudaStream_t s) {
+    k_blue_post<<<grid_for(g.outer * g.ncols * g.n, 256), 256, 0, s>>>(buf, Z, g, P, chirp, scale, conj_out);
+    return cudaGetLastError();
+}
+
+
 template <int N>
 static cudaError_t axis_pow2_n(const double2* in, double2* out, const AxisGeom& g, int sign,
                                const StepTwiddle& st, const double2* tw, cudaStream_t s, Flags* flags) {

@@ -216,6 +216,13 @@ cudaError_t launch_fused_r2c(double2* H, const AxisGeom& g, const FusedSymbol& s
                              const double2* tw_all, cudaStream_t s);
 cudaError_t launch_rowpair(const RowPairArgs& a, cudaStream_t s);
 cudaError_t launch_promote(const double* x, double2* z, i64 n, cudaStream_t s);
+// Bluestein stages for non-pow2 axes (fsx_kernels.cu): gather * chirp into [lines][P],
+// pointwise * Bhat, scatter * chirp * scale (conj in / out for the inverse)
+cudaError_t launch_blue_pre(const double2* Z, double2* buf, const AxisGeom& g, i64 P, const double2* chirp, int conj_in,
+                            cudaStream_t s);
+cudaError_t launch_blue_mul(double2* buf, i64 lines, i64 P, const double2* bhat, cudaStream_t s);
+cudaError_t launch_blue_post(const double2* buf, double2* Z, const AxisGeom& g, i64 P, const double2* chirp,
+                             double scale, int conj_out, cudaStream_t s);
 cudaError_t launch_extract(const double2* z, double* x, i64 n, Flags* flags, cudaStream_t s);
 cudaError_t launch_scale(double2* z, i64 n, double scale, cudaStream_t s);
 cudaError_t launch_finite_check(const double* x, i64 n, Flags* flags, cudaStream_t s);

@@ -110,6 +110,32 @@ def test_fft_vs_direct_dft():
         assert np.abs(got - want).max() <= 1e-10 * (1 + np.abs(want).max()), n
 
 
+@pytest.mark.parametrize("dims", [[1000], [3001], [12289], [40000], [300, 50], [24, 777], [7, 12, 513]])
+def test_bluestein_axes_vs_numpy(dims):
+    """Non-pow2 axes above 256 run the GPU Bluestein transform (fft.cpp:103-139):
+    forward and inverse against numpy, including lengths past the old
+    direct-DFT cap and a P > 8192 (split) convolution."""
+    rng = np.random.default_rng(sum(dims))
+    z = rng.standard_normal(int(np.prod(dims))) + 1j * rng.standard_normal(int(np.prod(dims)))
+    shape = fs.GridShape(dims)
+    got = fs.multi_fft(fs.ComplexGrid(shape, z)).data
+    want = np.fft.fftn(z.reshape(dims)).reshape(-1)
+    assert np.abs(got - want).max() <= 1e-11 * np.abs(want).max(), dims
+    back = fs.multi_ifft(fs.ComplexGrid(shape, want)).data  # normalized (fft.cpp:151-154)
+    assert np.abs(back - z).max() <= 1e-11 * np.abs(z).max(), dims
+
+
+@pytest.mark.parametrize("dims,T", [([20000], 300), ([1000, 300], 40), ([4097], 1000)])
+def test_bluestein_solve_vs_oracle(orc, dims, T):
+    """solve_periodic on non-pow2 grids beyond the direct-DFT range (general
+    plan + Bluestein) vs the oracle (which runs the reference's Bluestein)."""
+    k = R.random_kernel(Rng(300 + T), len(dims), 2, 1, 0.95)
+    a0 = orc.splitmix_fill(77, int(np.prod(dims)), True)
+    got = fs.solve_periodic(G(dims, a0), K(k), T).data
+    want = orc.solve_periodic(a0, dims, 1, *k.arrays(), T)
+    assert rel_l2(got, want) <= 1e-10
+
+
 def test_multi_fft_vs_nested_sum():
     rng = Rng(29)
     for dims, m in (([12], 1), ([6, 10], 2), ([3, 4, 5], 1), ([16, 32], 1), ([8, 4, 64], 2)):
