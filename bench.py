@@ -54,6 +54,26 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def load_fp64(cfg_name, kernel_ms):
+    """FP64 roofline of the dominant kernel: its per-launch FP64 pipe
+    instructions (committed ncu count) over its live CUDA-event time, against
+    the measured DFMA instruction rate (profiles/fp64_peak.json)."""
+    try:
+        cnt = json.load(open(os.path.join(ROOT, "profiles", "ncu_fp64.json"))).get(cfg_name)
+        peak = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+    except Exception:
+        return None
+    if not cnt or not kernel_ms:
+        return None
+    peak_ops = peak["fp64_fma_tflops"] / 2.0  # DFMA instructions (tera) per second
+    ach = cnt["pipe_ops"] / (kernel_ms * 1e-3) / 1e12
+    return {"bound": "fp64 pipe", "achieved_tops": ach, "peak_tops": peak_ops, "frac": ach / peak_ops,
+            "achieved_tflops": cnt["flops"] / (kernel_ms * 1e-3) / 1e12, "peak_tflops": peak["fp64_fma_tflops"],
+            "pipe_ops_per_launch": cnt["pipe_ops"],
+            "source": "ncu DADD+DMUL+DFMA thread instructions (profiles/ncu_fp64.json); peak measured by "
+                      "scripts/micro/fp64_peak.cu (profiles/fp64_peak.json)"}
+
+
 def load_traffic(cfg_name):
     """dram bytes per launch of the dominant kernel from the committed ncu capture."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -459,6 +479,7 @@ def run_gpu(args, cfg):
             "alg_bytes_per_launch": info["fused_bytes"],
             "kernel_ms": fms,
             "peak_source": peak_src,
+            "fp64": load_fp64(cfg.name, fms),
         },
         "pipeline": {"alg_bytes_per_step": info["alg_bytes"], "achieved_gbs": pipe_gbs, "frac": pipe_gbs / peak},
         "gpu_launches": info["launches"] * args.steps,
