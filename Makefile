@@ -3,7 +3,7 @@
 # runs the same recipe.
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH = -gencode arch=compute_100a,code=sm_100a
-NVFLAGS = $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v -Iinclude -Ipaper_2105_06676_b200/csrc
+NVFLAGS = $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v -Iinclude -Ipaper_2105_06676_b200/csrc $(EXTRA)
 CSRC = paper_2105_06676_b200/csrc
 LIB = paper_2105_06676_b200/libfsx.so
 PIPE_O = $(CSRC)/fsx_pipe.o

@@ -199,8 +199,8 @@ __device__ __forceinline__ int swz(int p) { return p ^ (((p >> 3) ^ (p >> 4)) & 
 // then has its mirror N - p in the same thread, which lets a real-to-complex
 // split run in registers.  Output convention with PAIR: v[i + u * 2] holds
 // X[item(t, i) + u * N / 8].
-// FT: read every twiddle of a pass from the gathered table (no derived
-// products: fewer FP64 instructions, more L1 loads) -- for compute-bound callers.
+// FT (bit S set: pass S): read every twiddle of that pass from the gathered
+// table (no derived products: fewer FP64 instructions, more L1 loads).
 // NB > 0: the exchanges synchronize NB-thread groups with named barriers
 // (id 1 + threadIdx.x / NB) instead of the whole CTA, so independent groups
 // of one CTA (e.g. the two half-columns of the 8192-point pass) drift apart.
@@ -210,7 +210,7 @@ __device__ __forceinline__ void group_sync() {
     else asm volatile("bar.sync %0, %1;\n" ::"r"(1 + (int)(threadIdx.x / NB)), "n"(NB) : "memory");
 }
 
-template <int N, int SIGN, bool PF = false, bool PAIR = false, bool FT = false, int NB = 0>
+template <int N, int SIGN, bool PF = false, bool PAIR = false, int FT = 0, int NB = 0>
 struct LineFFT {
     static constexpr int LOGN = ilog2c(N);
     static constexpr int R = N < 16 ? N : 16;
@@ -257,7 +257,7 @@ struct LineFFT {
                 const int k = item<S>(t, i) & (Ns - 1);
                 double2* wi = w + i * r;
                 const double2* pt = tw + (kPassTabBase + 15 * N + 16 * Ns);  // tw = tw_all + N
-                if constexpr (FT) {
+                if constexpr (((FT >> S) & 1) != 0) {
 #pragma unroll
                     for (int u = 1; u < r; ++u) wi[u] = __ldg(pt + (u - 1) * Ns + k);
                     continue;

@@ -65,7 +65,10 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
     constexpr int W = C::W;
     // full twiddle tables for the multi-column tiles (N < 4096); the one-column
     // 4096 tiles measured faster with derived twiddles (cfg2 158 vs 165 us)
-    constexpr bool FT = N < 4096;
+#ifndef FSX_FT4096
+#define FSX_FT4096 0
+#endif
+    constexpr int FT = N < 4096 ? ~0 : FSX_FT4096;
     using FF = LineFFT<N, -1, false, false, FT>;
     using FI = LineFFT<N, +1, false, false, FT>;
     extern __shared__ __align__(128) double2 tile[];
@@ -208,7 +211,7 @@ k_axis_tma(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ C
            StepTwiddle st, const double2* __restrict__ tw_all, Flags* flags) {
     using C = TCfg<N>;
     constexpr int W = C::W;
-    using F = LineFFT<N, SIGN, false, false, N < 4096>;
+    using F = LineFFT<N, SIGN, false, false, (N < 4096 ? ~0 : 0)>;
     extern __shared__ __align__(128) double2 tile[];
     __shared__ __align__(8) unsigned long long bar;
     const int w = threadIdx.x % W, t = threadIdx.x / W;
