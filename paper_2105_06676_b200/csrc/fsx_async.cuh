@@ -71,59 +71,6 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
-// ------------------------------------------------------------------ tensor memory as thread-private scratch
-// TMEM (256 KB/SM, 128 lanes x 512 columns x 32 bit) holds data-independent
-// per-thread values across a phase that needs all the registers: warp w of
-// the CTA owns lanes 32 (w % 4) .. + 31 and a 32-column block (w / 4) of the
-// allocation (so 16 warps use 128 columns).  The 32x32b shapes map thread i
-// of the warp to lane i: no cross-thread movement.
-template <int COLS>
-__device__ __forceinline__ void tmem_alloc(unsigned* smem_dst) {  // one full warp
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(smem_dst)),
-                 "n"(COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-}
-template <int COLS>
-__device__ __forceinline__ void tmem_dealloc(unsigned taddr) {  // the allocating warp
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "n"(COLS) : "memory");
-}
-__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-// this warp's 32-column block: lane base in bits 31:16, column in 15:0
-__device__ __forceinline__ unsigned tmem_warp_addr(unsigned base, int warp) {
-    return base + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)(32 * (warp >> 2));
-}
-// 8 doubles (16 columns) per call at column offset c16 * 16
-__device__ __forceinline__ void tmem_st8(unsigned taddr, const double (&d)[8]) {
-    unsigned r[16];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        r[2 * i] = __double2loint(d[i]);
-        r[2 * i + 1] = __double2hiint(d[i]);
-    }
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15, %16};\n" ::"r"(taddr),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-        : "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
-__device__ __forceinline__ void tmem_ld8(unsigned taddr, double (&d)[8]) {
-    unsigned r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15}, [%16];\n"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr)
-        : "memory");
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 8; ++i) d[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
-}
-
 }  // namespace fsx
 
 // ------------------------------------------------------------------ programmatic dependent launch

@@ -337,88 +337,5 @@ struct LineFFT {
     }
 };
 
-// ------------------------------------------------------------------ 4096-point transposed four-step
-// N = 16 x 256 with 256 threads x 16 registers.  forward() takes the natural
-// layout (thread t holds x[t + 256 q]) to the transposed frequency layout:
-// thread u = 16 k1 + j holds X[k1 + 16 j + 256 q]; inverse() maps that layout
-// back to natural order (unnormalized).  Only the first exchange is CTA-wide;
-// the second is a 16 x 16 transpose inside each half-warp (rows of the
-// shared buffer are owned by one half-warp group, so __syncwarp suffices),
-// and the inverse needs a single __syncthreads.
-//   buf: >= 4096 elements of shared memory; tw4096 = tw_all + 4096,
-//   tw256 = tw_all + 256 (tw[x] = exp(-2 pi i x / n)).
-struct Fft4096T {
-    // element (k2a, t1) of a half-warp group's 256-block, XOR-swizzled so both
-    // the row writes and the column reads are conflict-free per quarter warp
-    __device__ __forceinline__ static int sw2(int k2a, int t1) { return k2a * 16 + (t1 ^ (k2a & 7)); }
-
-    template <int SIGN>
-    __device__ __forceinline__ static void twiddle16(double2 (&v)[16], const double2* __restrict__ tab, int base) {
-        // v[k] *= W^(base k) (SIGN -1) or conj (SIGN +1), W^x = tab[x]; powers from 1, 2, 4, 8
-        double2 w[16];
-        w[1] = __ldg(tab + base);
-        w[2] = __ldg(tab + 2 * base);
-        w[4] = __ldg(tab + 4 * base);
-        w[8] = __ldg(tab + 8 * base);
-        w[3] = cmul(w[1], w[2]);
-        w[5] = cmul(w[1], w[4]);
-        w[6] = cmul(w[2], w[4]);
-        w[7] = cmul(w[3], w[4]);
-#pragma unroll
-        for (int u = 9; u < 16; ++u) w[u] = cmul(w[u - 8], w[8]);
-#pragma unroll
-        for (int u = 1; u < 16; ++u) v[u] = ctw<SIGN>(v[u], w[u]);
-    }
-
-    // natural -> transposed.  The caller must __syncthreads() before if buf
-    // still holds data other threads read (e.g. the input tile).
-    __device__ __forceinline__ static void forward(double2 (&v)[16], int u, double2* buf, const double2* __restrict__ tw_all) {
-        const int t = u;
-        Dft<16, -1>::run(v);                           // over q -> k1
-        twiddle16<-1>(v, tw_all + 4096, t);            // W_4096^(t k1)
-#pragma unroll
-        for (int k1 = 0; k1 < 16; ++k1) buf[k1 * 256 + t] = v[k1];
-        __syncthreads();
-        const int k1 = u >> 4, t1 = u & 15;
-        double2* row = buf + k1 * 256;
-#pragma unroll
-        for (int t2 = 0; t2 < 16; ++t2) v[t2] = row[t1 + 16 * t2];
-        Dft<16, -1>::run(v);                           // over t2 -> k2a
-        twiddle16<-1>(v, tw_all + 256, t1);            // W_256^(t1 k2a)
-        __syncwarp();
-#pragma unroll
-        for (int k2a = 0; k2a < 16; ++k2a) row[sw2(k2a, t1)] = v[k2a];
-        __syncwarp();
-        const int j = t1;                              // this thread now owns k2a = j
-#pragma unroll
-        for (int t1p = 0; t1p < 16; ++t1p) v[t1p] = row[sw2(j, t1p)];
-        Dft<16, -1>::run(v);                           // over t1 -> k2b
-    }
-
-    // transposed -> natural (unnormalized inverse)
-    __device__ __forceinline__ static void inverse(double2 (&v)[16], int u, double2* buf, const double2* __restrict__ tw_all) {
-        const int k1 = u >> 4, j = u & 15;
-        double2* row = buf + k1 * 256;
-        Dft<16, +1>::run(v);                           // over k2b -> t1
-        __syncwarp();
-#pragma unroll
-        for (int t1 = 0; t1 < 16; ++t1) row[sw2(j, t1)] = v[t1];
-        __syncwarp();
-        const int t1 = j;
-#pragma unroll
-        for (int k2a = 0; k2a < 16; ++k2a) v[k2a] = row[sw2(k2a, t1)];
-        twiddle16<+1>(v, tw_all + 256, t1);
-        Dft<16, +1>::run(v);                           // over k2a -> t2
-        __syncwarp();
-#pragma unroll
-        for (int t2 = 0; t2 < 16; ++t2) row[t1 + 16 * t2] = v[t2];
-        __syncthreads();
-        const int t = u;
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) v[kk] = buf[kk * 256 + t];
-        twiddle16<+1>(v, tw_all + 4096, t);
-        Dft<16, +1>::run(v);                           // over k1 -> q
-    }
-};
 
 }  // namespace fsx

@@ -1021,7 +1021,6 @@ cudaError_t launch_fused_qmax(const FusedSymbol& sym, i64 ncols, unsigned long l
 cudaError_t launch_r2c_rows(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw,
                             cudaStream_t s) {
     if (pipe_enabled() && pipe_rows_ok(L / 2) && rows_variant() == 3) return launch_r2c_bulk(x, H, nrows, L, P, tw, s);
-    if (pipe_enabled() && pipe_rows_ok(L / 2) && rows_variant() == 2) return launch_r2c_reg(x, H, nrows, L, P, tw, s);
     if (pipe_enabled() && pipe_rows_ok(L / 2) && (rows_variant() == 1 || rows_variant() == 3)) return launch_r2c_pipe(x, H, nrows, L, P, tw, s);
     switch (L / 2) {
 #define C_(M) case M: return r2c_m<M>(x, H, nrows, L, P, tw, s);
@@ -1034,7 +1033,6 @@ cudaError_t launch_r2c_rows(const double* x, double2* H, i64 nrows, i64 L, const
 cudaError_t launch_c2r_rows(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw, Flags* f,
                             cudaStream_t s) {
     if (pipe_enabled() && pipe_rows_ok(L / 2) && rows_variant() == 3) return launch_c2r_bulk(H, x, nrows, L, P, tw, f, s);
-    if (pipe_enabled() && pipe_rows_ok(L / 2) && rows_variant() == 2) return launch_c2r_reg(H, x, nrows, L, P, tw, f, s);
     if (pipe_enabled() && pipe_rows_ok(L / 2) && (rows_variant() == 1 || rows_variant() == 3)) return launch_c2r_pipe(H, x, nrows, L, P, tw, f, s);
     switch (L / 2) {
 #define C_(M) case M: return c2r_m<M>(H, x, nrows, L, P, tw, f, s);

@@ -249,10 +249,6 @@ cudaError_t launch_r2c_bulk(const double* x, double2* H, i64 nrows, i64 L, const
                             cudaStream_t s);
 cudaError_t launch_c2r_bulk(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& lay, const double2* tw_all,
                             Flags* flags, cudaStream_t s);
-cudaError_t launch_r2c_reg(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw_all,
-                           cudaStream_t s);
-cudaError_t launch_c2r_reg(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw_all,
-                           Flags* flags, cudaStream_t s);
 // one direct periodic stencil step out = sum_taps B a[x + off] (verifier)
 cudaError_t launch_step_naive(const double* a, double* out, const NaiveGeom& g, const long long* off,
                               const double* blk, cudaStream_t s);

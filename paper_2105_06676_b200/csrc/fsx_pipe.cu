@@ -322,141 +322,10 @@ k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
     if (any && (threadIdx.x & 31) == 0) atomicOr(&flags->nonfinite, 1u);
 }
 
-// ------------------------------------------------------------------ rows, register double buffer
-// Persistent row kernels that prefetch the NEXT row straight into a second
-// register array (plain LDG, no shared-memory staging): the row loads
-// overlap the current row's FFT, and the only shared-memory traffic left is
-// the FFT exchanges (the row passes were L1TEX-bound at ~1.5 wavefronts per
-// element with cp.async staging and a post-processing exchange).
-template <int M>
-struct RCfg {
-    static constexpr int TPL = M / 16;
-    static constexpr int MINB = TPL <= 128 ? 3 : 1;
-};
-
-// R2C split of pair (Zk, Zp) where Zp = Z[M - k] (k > 0); returns X[k].
-__device__ __forceinline__ double2 r2c_split(double2 zk, double2 zp, double2 wk) {
-    const double2 zm = cconj(zp);
-    const double2 e = cscale(cadd(zk, zm), 0.5);
-    const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
-    return cadd(e, cmul(wk, od));
-}
-
-template <int M>
-__global__ void __launch_bounds__(RCfg<M>::TPL, RCfg<M>::MINB)
-k_r2c_reg(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, RowLayout lay,
-          const double2* __restrict__ tw_all) {
-    using F = LineFFT<M, -1, false, true>;
-    constexpr int TPL = RCfg<M>::TPL, R = 16;
-    extern __shared__ double2 sm[];
-    const int t = threadIdx.x;
-    auto load = [&](i64 row, double2 (&v)[R]) {
-        const double2* src = reinterpret_cast<const double2*>(x + row * L);
-#pragma unroll
-        for (int q = 0; q < R; ++q) v[q] = src[t + q * TPL];
-    };
-    auto process = [&](i64 row, double2 (&v)[R]) {
-        F::run(v, t, sm, tw_all + M);
-        if constexpr (F::PAIRED) {
-            // v[i + 2u] = Z[item(i) + u M/8]; mirror M - k lives in this thread
-            const int j0 = t, j1 = t == 0 ? TPL : 2 * TPL - t;
-#pragma unroll
-            for (int i = 0; i < 2; ++i)
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int k = (i == 0 ? j0 : j1) + u * (M / 8);
-                    const int qp = (1 - i) + 2 * (7 - u);                        // partner slot, t != 0
-                    const int qz = i == 0 ? 2 * ((8 - u) & 7) : 1 + 2 * (7 - u);  // partner slot, t == 0
-                    const double2 zk = v[i + 2 * u];
-                    const double2 zp = t == 0 ? v[qz] : v[qp];
-                    const double2 xk = r2c_split(zk, zp, __ldg(tw_all + 2 * M + k));
-                    *lay.ptr(H, row, k) = xk;
-                    if (i == 0 && u == 0 && t == 0) {
-                        *lay.ptr(H, row, 0) = make_double2(zk.x + zk.y, 0.0);
-                        *lay.ptr(H, row, M) = make_double2(zk.x - zk.y, 0.0);
-                    }
-                }
-        } else {
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < R; ++q) sm[swz(t + q * TPL)] = v[q];
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < R; ++q) {
-                const int k = t + q * TPL;
-                const double2 zk = v[q];
-                const double2 xk = r2c_split(zk, sm[swz((M - k) & (M - 1))], __ldg(tw_all + 2 * M + k));
-                *lay.ptr(H, row, k) = xk;
-                if (k == 0) *lay.ptr(H, row, M) = make_double2(zk.x - zk.y, 0.0);
-            }
-        }
-    };
-    double2 va[R], vb[R];
-    i64 row = blockIdx.x;
-    const i64 G = gridDim.x;
-    if (row < nrows) load(row, va);
-    for (; row < nrows; row += 2 * G) {
-        const i64 r1 = row + G;
-        if (r1 < nrows) load(r1, vb);
-        process(row, va);
-        if (r1 < nrows) {
-            if (r1 + G < nrows) load(r1 + G, va);
-            process(r1, vb);
-        }
-    }
-}
-
-template <int M>
-__global__ void __launch_bounds__(RCfg<M>::TPL, RCfg<M>::MINB)
-k_c2r_reg(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, RowLayout lay,
-          const double2* __restrict__ tw_all, Flags* flags) {
-    using F = LineFFT<M, +1>;
-    constexpr int TPL = RCfg<M>::TPL, R = 16;
-    extern __shared__ double2 sm[];
-    const int t = threadIdx.x;
-    bool bad = false;
-    auto load = [&](i64 row, double2 (&v)[R]) {
-#pragma unroll
-        for (int q = 0; q < R; ++q) v[q] = *lay.ptr(H, row, t + q * TPL);
-    };
-    auto process = [&](i64 row, double2 (&v)[R]) {
-        // mirror X[M - k] re-read through L1 (this CTA just streamed the row)
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-            const int k = t + q * TPL;
-            const double2 xm = cconj(*lay.ptr(H, row, M - k));
-            const double2 e = cadd(v[q], xm);
-            const double2 od = cmulc(csub(v[q], xm), __ldg(tw_all + 2 * M + k));
-            v[q] = cadd(e, cmul_si<+1>(od));
-        }
-        F::run(v, t, sm, tw_all + M);
-        double2* dst = reinterpret_cast<double2*>(x + row * L);
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-            dst[t + q * TPL] = v[q];
-            bad |= !isfinite(v[q].x) || !isfinite(v[q].y);
-        }
-    };
-    double2 va[R], vb[R];
-    i64 row = blockIdx.x;
-    const i64 G = gridDim.x;
-    if (row < nrows) load(row, va);
-    for (; row < nrows; row += 2 * G) {
-        const i64 r1 = row + G;
-        if (r1 < nrows) load(r1, vb);
-        process(row, va);
-        if (r1 < nrows) {
-            if (r1 + G < nrows) load(r1 + G, va);
-            process(r1, vb);
-        }
-    }
-    const unsigned any = __ballot_sync(0xffffffffu, bad);
-    if (any && (threadIdx.x & 31) == 0) atomicOr(&flags->nonfinite, 1u);
-}
-
 // FSX_ROWS: 0 = one-row-per-CTA kernels, 1 = cp.async staged (cfg2 r2c 70 us /
-// c2r 64 us), 2 = register double buffer (86 / 109 us), 3 = bulk-copy staged (default:
-// 67 / 63 us; cfg3 step 1.538 -> 1.466 ms)
+// c2r 64 us at the time), 3 = bulk-copy staged (default: 67 / 63 us then, 52 / 51 us
+// with the later twiddle work).  A register double-buffered variant (86 / 109 us)
+// was removed.
 int rows_variant() {
     static int v = -1;
     if (v < 0) {
@@ -466,57 +335,6 @@ int rows_variant() {
     return v;
 }
 
-template <int M>
-static cudaError_t r2c_reg_m(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw,
-                             cudaStream_t s) {
-    const size_t smem = (size_t)M * sizeof(double2);
-    kernel_prepare((const void*)k_r2c_reg<M>, smem);
-    int per_sm = 0;
-    per_sm = kernel_prepare((const void*)k_r2c_reg<M>, smem, RCfg<M>::TPL);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const i64 g = (i64)(per_sm < 1 ? 1 : per_sm) * sms;
-    k_r2c_reg<M><<<(int)(nrows < g ? nrows : g), RCfg<M>::TPL, smem, s>>>(x, H, nrows, L, P, tw);
-    return cudaGetLastError();
-}
-
-template <int M>
-static cudaError_t c2r_reg_m(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw,
-                             Flags* f, cudaStream_t s) {
-    const size_t smem = (size_t)M * sizeof(double2);
-    kernel_prepare((const void*)k_c2r_reg<M>, smem);
-    int per_sm = 0;
-    per_sm = kernel_prepare((const void*)k_c2r_reg<M>, smem, RCfg<M>::TPL);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const i64 g = (i64)(per_sm < 1 ? 1 : per_sm) * sms;
-    k_c2r_reg<M><<<(int)(nrows < g ? nrows : g), RCfg<M>::TPL, smem, s>>>(H, x, nrows, L, P, tw, f);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_r2c_reg(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& P, const double2* tw,
-                           cudaStream_t s) {
-    switch (L / 2) {
-        case 512: return r2c_reg_m<512>(x, H, nrows, L, P, tw, s);
-        case 1024: return r2c_reg_m<1024>(x, H, nrows, L, P, tw, s);
-        case 2048: return r2c_reg_m<2048>(x, H, nrows, L, P, tw, s);
-        case 4096: return r2c_reg_m<4096>(x, H, nrows, L, P, tw, s);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-cudaError_t launch_c2r_reg(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& P, const double2* tw,
-                           Flags* f, cudaStream_t s) {
-    switch (L / 2) {
-        case 512: return c2r_reg_m<512>(H, x, nrows, L, P, tw, f, s);
-        case 1024: return c2r_reg_m<1024>(H, x, nrows, L, P, tw, f, s);
-        case 2048: return c2r_reg_m<2048>(H, x, nrows, L, P, tw, f, s);
-        case 4096: return c2r_reg_m<4096>(H, x, nrows, L, P, tw, f, s);
-        default: return cudaErrorInvalidValue;
-    }
-}
 
 // ------------------------------------------------------------------ columns
 // Tile = W adjacent columns x N of a strided axis.  MODE 0: forward C2C,
