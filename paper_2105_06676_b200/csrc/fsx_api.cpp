@@ -385,6 +385,8 @@ int choose_kind(const Plan& p, const Taps& taps, int force_general) {
     if (p.m == 1 && (r == 2 || r == 3)) {
         const i64 L = p.dims[r - 1];
         if (L < 16 || L > 2 * fsx::kMaxLine) return kGeneral;
+        // the fused axis-0 kernels are instantiated for 8 <= n0 <= 8192
+        if (p.dims[0] < 8) return kGeneral;
         for (int a = 0; a + 1 < r; ++a)
             if (p.dims[a] < 2 || p.dims[a] > fsx::kMaxLine) return kGeneral;
         std::map<i64, int> groups;

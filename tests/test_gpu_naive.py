@@ -126,3 +126,30 @@ def test_cfg5_full_size_vs_naive_short_horizon():
     diff = _device_pair(cfg, 2000, 5)
     print(f"cfg5 full size, T=2000: rel L2 (FFT solver vs direct stepping) = {diff:.3e}")
     assert diff <= 1e-8
+
+
+@pytest.mark.parametrize("dims,T", [([8192, 16384], 20), ([4, 8192, 4096], 10), ([1 << 26], 50)])
+def test_solver_vs_naive_max_plan_sizes(dims, T):
+    """The largest grids the fast plans take (plan 1: last axis 16384 = 2 kMaxLine,
+    axis 0 8192; 3D; plan 2: 2^26 reals) against direct stepping."""
+    cells = int(np.prod(dims))
+    shape = fs.GridShape(dims)
+    k = fs.StencilKernel(len(dims))
+    k.add_tap([0] * len(dims), 0.5)
+    for a in range(len(dims)):
+        for sgn in (-1, 1):
+            off = [0] * len(dims)
+            off[a] = sgn
+            k.add_tap(off, 0.25 / len(dims))
+    g = torch.Generator(device="cuda").manual_seed(7)
+    a0 = torch.rand(cells, dtype=torch.float64, device="cuda", generator=g)
+    fft_out = torch.empty_like(a0)
+    naive_out = torch.empty_like(a0)
+    fs.solve_periodic_device(shape, a0.data_ptr(), k, T, fft_out.data_ptr(), stream=0)
+    fs.device_check(stream=0)
+    fs.evolve_periodic_naive_device(shape, a0.data_ptr(), k, T, naive_out.data_ptr(), stream=0)
+    torch.cuda.synchronize()
+    diff = float(torch.linalg.vector_norm(fft_out - naive_out) / torch.linalg.vector_norm(naive_out))
+    del a0, fft_out, naive_out
+    torch.cuda.empty_cache()
+    assert diff <= 1e-12, (dims, diff)

@@ -425,7 +425,12 @@ PLAN_CASES = [
     ([1 << 14], 2, "leapfrog", 5000),
     ([96, 40], 1, "random", 11),
     ([1 << 14, 2], 1, "random", 3),
-    ([8192, 64], 1, "box9", 1000),       # 8192-point fused columns (multipliers parked in TMEM)
+    ([8192, 64], 1, "box9", 1000),       # 8192-point fused columns (parity halves)
+    ([4, 64], 1, "jacobi5", 30),         # axis 0 below the fused kernels' range: general plan
+    ([2, 32, 16], 1, "random", 5),
+    ([8, 16, 32], 1, "heat7", 9),
+    ([16, 2, 32], 1, "heat7", 7),        # 2-point axis-1 pass
+    ([16, 4, 64], 1, "random", 3),
     ([8192, 32], 1, "random", 5),        # ... with a complex symbol
 ]
 
