@@ -572,7 +572,8 @@ Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general,
         p->alg_bytes = (2 + 4 * col_passes) * R + R;
         p->launches = 2 * col_passes + 1 + 1;
     } else {
-        // general: complex Z of cells * m
+        // general: complex Z of cells * m (block kernels instantiated for m <= 8)
+        if (p->m > 8) throw SpecErr("fsx: more than 8 fields per cell is not supported on the GPU path");
         p->work.ensure((size_t)s.values() * sizeof(double2));
         i64 nl = 0;
         for (int a = 0; a < r; ++a) {
@@ -1606,7 +1607,7 @@ fsx_status fsx_spectrum_from_kernel(const fsx_shape* shape, const fsx_kernel* k,
         const Taps taps = parse_kernel(k);
         require_fits(taps, s);
         if (!out) throw SpecErr("spectrum_from_kernel: null output");
-        if (s.fields > 4) throw SpecErr("spectrum_from_kernel: fields > 4 not supported on the GPU path");
+        if (s.fields > 8) throw SpecErr("spectrum_from_kernel: fields > 8 not supported on the GPU path");
         std::lock_guard<std::mutex> lk(g_mu);
         Device& dev = device_for(0);
         cudaStream_t st = dev.stream;
@@ -1624,7 +1625,7 @@ fsx_status fsx_spectrum_from_kernel(const fsx_shape* shape, const fsx_kernel* k,
 
 static void spectral_io(const fsx_shape* shape, Shape& s, size_t& bytes) {
     s = parse_shape(shape);
-    if (s.fields > 4) throw SpecErr("spectrum: fields > 4 not supported on the GPU path");
+    if (s.fields > 8) throw SpecErr("spectrum: fields > 8 not supported on the GPU path");
     bytes = (size_t)s.cells * s.fields * s.fields * 16;
 }
 

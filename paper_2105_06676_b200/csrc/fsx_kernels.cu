@@ -1137,6 +1137,10 @@ cudaError_t launch_spectral_general(double2* z, const GeneralSymbol& sym, cudaSt
         case 2: k_spectral_general<2><<<g, 128, 0, s>>>(z, sym); break;
         case 3: k_spectral_general<3><<<g, 128, 0, s>>>(z, sym); break;
         case 4: k_spectral_general<4><<<g, 128, 0, s>>>(z, sym); break;
+        case 5: k_spectral_general<5><<<g, 128, 0, s>>>(z, sym); break;
+        case 6: k_spectral_general<6><<<g, 128, 0, s>>>(z, sym); break;
+        case 7: k_spectral_general<7><<<g, 128, 0, s>>>(z, sym); break;
+        case 8: k_spectral_general<8><<<g, 128, 0, s>>>(z, sym); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -1149,6 +1153,10 @@ cudaError_t launch_symbol_blocks(double2* out, const GeneralSymbol& sym, int whi
         case 2: k_symbol_blocks<2><<<g, 128, 0, s>>>(out, sym, which_q); break;
         case 3: k_symbol_blocks<3><<<g, 128, 0, s>>>(out, sym, which_q); break;
         case 4: k_symbol_blocks<4><<<g, 128, 0, s>>>(out, sym, which_q); break;
+        case 5: k_symbol_blocks<5><<<g, 128, 0, s>>>(out, sym, which_q); break;
+        case 6: k_symbol_blocks<6><<<g, 128, 0, s>>>(out, sym, which_q); break;
+        case 7: k_symbol_blocks<7><<<g, 128, 0, s>>>(out, sym, which_q); break;
+        case 8: k_symbol_blocks<8><<<g, 128, 0, s>>>(out, sym, which_q); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -1166,6 +1174,10 @@ cudaError_t launch_pow_blocks(const double2* in, double2* out, i64 cells, int m,
         case 2: k_pow_blocks<2><<<g, 128, 0, s>>>(in, out, cells, T); break;
         case 3: k_pow_blocks<3><<<g, 128, 0, s>>>(in, out, cells, T); break;
         case 4: k_pow_blocks<4><<<g, 128, 0, s>>>(in, out, cells, T); break;
+        case 5: k_pow_blocks<5><<<g, 128, 0, s>>>(in, out, cells, T); break;
+        case 6: k_pow_blocks<6><<<g, 128, 0, s>>>(in, out, cells, T); break;
+        case 7: k_pow_blocks<7><<<g, 128, 0, s>>>(in, out, cells, T); break;
+        case 8: k_pow_blocks<8><<<g, 128, 0, s>>>(in, out, cells, T); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -1188,6 +1200,10 @@ cudaError_t launch_block_mul(const double2* a, const double2* b, double2* out, i
         case 2: k_block_mul<2><<<g, 128, 0, s>>>(a, b, out, cells); break;
         case 3: k_block_mul<3><<<g, 128, 0, s>>>(a, b, out, cells); break;
         case 4: k_block_mul<4><<<g, 128, 0, s>>>(a, b, out, cells); break;
+        case 5: k_block_mul<5><<<g, 128, 0, s>>>(a, b, out, cells); break;
+        case 6: k_block_mul<6><<<g, 128, 0, s>>>(a, b, out, cells); break;
+        case 7: k_block_mul<7><<<g, 128, 0, s>>>(a, b, out, cells); break;
+        case 8: k_block_mul<8><<<g, 128, 0, s>>>(a, b, out, cells); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -1200,6 +1216,10 @@ cudaError_t launch_block_matvec(const double2* lam, const double2* x, double2* y
         case 2: k_block_matvec<2><<<g, 128, 0, s>>>(lam, x, y, cells); break;
         case 3: k_block_matvec<3><<<g, 128, 0, s>>>(lam, x, y, cells); break;
         case 4: k_block_matvec<4><<<g, 128, 0, s>>>(lam, x, y, cells); break;
+        case 5: k_block_matvec<5><<<g, 128, 0, s>>>(lam, x, y, cells); break;
+        case 6: k_block_matvec<6><<<g, 128, 0, s>>>(lam, x, y, cells); break;
+        case 7: k_block_matvec<7><<<g, 128, 0, s>>>(lam, x, y, cells); break;
+        case 8: k_block_matvec<8><<<g, 128, 0, s>>>(lam, x, y, cells); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -624,3 +624,14 @@ def test_batch_reports_failing_item():
         fs.solve_periodic_batch(grids, k, 10)
     with pytest.raises(fs.SpecError):
         fs.solve_periodic_batch([grids[0], G([32, 32], np.zeros(1024))], k, 10)
+
+
+@pytest.mark.parametrize("dims,m,T", [([32, 16], 5, 7), ([64], 8, 5), ([8, 4, 6], 6, 3)])
+def test_many_fields_vs_oracle(orc, dims, m, T):
+    """m-vector cells beyond the 2-field fast plans (general plan, block symbol
+    and block power for m up to 8; periodic.cpp:101-106 with Eigen blocks)."""
+    k = R.random_kernel(Rng(500 + m), len(dims), 1, m, 0.9)
+    a0 = orc.splitmix_fill(90 + m, int(np.prod(dims)) * m, True)
+    got = fs.solve_periodic_vector(G(dims, a0, m), K(k), T).data
+    want = orc.solve_periodic(a0, dims, m, *k.arrays(), T, vector=True)
+    assert rel_l2(got, want) <= 1e-10
