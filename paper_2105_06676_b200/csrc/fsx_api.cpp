@@ -976,7 +976,9 @@ void slab_geom(const fsx_shape* global, int P, int r, SlabPlan& sp) {
 // Device plan (call with g_mu held and the device selected).
 SlabPlan& slab_plan(const fsx_shape* global, int P, int r) {
     const Shape s = parse_shape(global);
-    std::string key = std::to_string(P) + "/" + std::to_string(r);
+    int dev = 0;
+    cudaGetDevice(&dev);  // the caller selected the device (device_for): plans hold its buffers
+    std::string key = std::to_string(dev) + "#" + std::to_string(P) + "/" + std::to_string(r);
     for (i64 d : s.dims) key += ":" + std::to_string(d);
     auto it = g_slabs.find(key);
     if (it != g_slabs.end()) return *it->second;
