@@ -466,6 +466,68 @@ __device__ __forceinline__ void pair_mode1(const RowPairArgs& a, double2& zk, do
     zp = cadd(cconj(u2), cmul_si<+1>(cconj(v2)));
 }
 
+// Real 2x2 symbols of two frequencies at once: the two binary-exponentiation
+// chains are independent, so interleaving them doubles the FP64 ILP of the
+// power (the row-pair pass of cfg5 is bound by this loop at T = 1e6).
+__device__ __forceinline__ void real_block_symbol(const RowPairArgs& a, i64 k, i64 N, double (&l)[4]) {
+    l[0] = l[1] = l[2] = l[3] = 0.0;
+    for (int j = 0; j < a.ntaps; ++j) {
+        const double c = phase_at(a.wk, modp(k * (i64)a.tap_off[j], N)).x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) l[e] = fma(a.tap_b[j][e], c, l[e]);
+    }
+}
+
+__device__ __forceinline__ void pair_mode1_real_x2(const RowPairArgs& a, double2 (&zk)[2], double2 (&zp)[2],
+                                                   const i64 (&k)[2], i64 N) {
+    double l[2][4], acc[2][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        real_block_symbol(a, k[i], N, l[i]);
+        acc[i][0] = 1.0;
+        acc[i][1] = 0.0;
+        acc[i][2] = 0.0;
+        acc[i][3] = 1.0;
+    }
+    u64 t = a.T;
+    while (t) {
+        if (t & 1) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const double b00 = fma(acc[i][0], l[i][0], acc[i][1] * l[i][2]), b01 = fma(acc[i][0], l[i][1], acc[i][1] * l[i][3]);
+                const double b10 = fma(acc[i][2], l[i][0], acc[i][3] * l[i][2]), b11 = fma(acc[i][2], l[i][1], acc[i][3] * l[i][3]);
+                acc[i][0] = b00;
+                acc[i][1] = b01;
+                acc[i][2] = b10;
+                acc[i][3] = b11;
+            }
+        }
+        t >>= 1;
+        if (t) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const double pp = l[i][1] * l[i][2], tr = l[i][0] + l[i][3];
+                const double s00 = fma(l[i][0], l[i][0], pp), s11 = fma(l[i][3], l[i][3], pp);
+                l[i][1] *= tr;
+                l[i][2] *= tr;
+                l[i][0] = s00;
+                l[i][3] = s11;
+            }
+        }
+    }
+    const double sc = a.scale;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double2 cz = cconj(zp[i]);
+        const double2 u = cscale(cadd(zk[i], cz), 0.5);
+        const double2 vv = cscale(cmul_si<-1>(csub(zk[i], cz)), 0.5);
+        const double2 u2 = make_double2(sc * fma(acc[i][0], u.x, acc[i][1] * vv.x), sc * fma(acc[i][0], u.y, acc[i][1] * vv.y));
+        const double2 v2 = make_double2(sc * fma(acc[i][2], u.x, acc[i][3] * vv.x), sc * fma(acc[i][2], u.y, acc[i][3] * vv.y));
+        zk[i] = cadd(u2, cmul_si<+1>(v2));
+        zp[i] = cadd(cconj(u2), cmul_si<+1>(cconj(v2)));
+    }
+}
+
 template <int N2>
 __global__ void __launch_bounds__(2 * Cfg<N2>::TPL)
 k_rowpair(RowPairArgs a) {
@@ -497,7 +559,26 @@ k_rowpair(RowPairArgs a) {
     double2* lb = self ? sm : sm + LS;
     const int nth = blockDim.x;
     if (!self) {
-        for (int cpos = threadIdx.x; cpos < N2; cpos += nth) {
+        int cpos = threadIdx.x;
+        if (a.mode == 1 && a.real) {  // two independent power chains per step
+            for (; cpos + nth < N2; cpos += 2 * nth) {
+                double2 zk[2], zp[2];
+                i64 k[2];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    zk[i] = la[swz(cpos + i * nth)];
+                    zp[i] = lb[swz(N2 - 1 - (cpos + i * nth))];
+                    k[i] = ra + N1 * (cpos + i * nth);
+                }
+                pair_mode1_real_x2(a, zk, zp, k, M);
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    la[swz(cpos + i * nth)] = zk[i];
+                    lb[swz(N2 - 1 - (cpos + i * nth))] = zp[i];
+                }
+            }
+        }
+        for (; cpos < N2; cpos += nth) {
             const int cp = N2 - 1 - cpos;
             double2 zk = la[swz(cpos)], zp = lb[swz(cp)];
             const i64 k = ra + N1 * cpos;
