@@ -182,18 +182,31 @@ k_strided(const double2* in, double2* out, AxisGeom g, StepTwiddle st, const dou
 #pragma unroll
     for (int q = 0; q < C::R; ++q)
         v[q] = ok ? in[base + (i64)(t + q * C::TPL) * g.inner] : make_double2(0.0, 0.0);
-    if constexpr (TWM == 2) {
+    // four-step twiddle W^(b (k kmul + o omul)) for k = t + q TPL: the
+    // exponents of one thread form an arithmetic progression in q, so two
+    // table reads (base, ratio) and a running product replace 16 two-level
+    // lookups (<= 15 extra roundings; the per-element lookups were as much
+    // L2 traffic as the data of the 1D plan's column passes)
+    double2 tq = make_double2(1.0, 0.0), tr = tq;
+    if constexpr (TWM != 0) {
         const i64 bq = c / st.col_div;
+        tq = phase_at(st.tab, bq * ((i64)t * st.kmul + o * st.omul));
+        tr = phase_at(st.tab, bq * (i64)C::TPL * st.kmul);
+    }
+    if constexpr (TWM == 2) {
 #pragma unroll
-        for (int q = 0; q < C::R; ++q)
-            v[q] = cmulc(v[q], phase_at(st.tab, bq * ((i64)(t + q * C::TPL) * st.kmul + o * st.omul)));
+        for (int q = 0; q < C::R; ++q) {
+            v[q] = cmulc(v[q], tq);
+            tq = cmul(tq, tr);
+        }
     }
     F::run(v, t, sm + w * C::LSW, tw_all + N);
     if constexpr (TWM == 1) {
-        const i64 bq = c / st.col_div;
 #pragma unroll
-        for (int q = 0; q < C::R; ++q)
-            v[q] = cmul(v[q], phase_at(st.tab, bq * ((i64)(t + q * C::TPL) * st.kmul + o * st.omul)));
+        for (int q = 0; q < C::R; ++q) {
+            v[q] = cmul(v[q], tq);
+            tq = cmul(tq, tr);
+        }
     }
     if (ok) {
 #pragma unroll

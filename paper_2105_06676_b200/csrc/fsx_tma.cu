@@ -185,17 +185,28 @@ k_axis_tma(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ C
     double2 v[C::R];
 #pragma unroll
     for (int q = 0; q < C::R; ++q) v[q] = tile[(t + q * C::TPL) * W + w];
-    const i64 bq = c / st.col_div;
+    // twiddles as an arithmetic progression of exponents: base and ratio reads
+    // and a running product (see k_strided)
+    double2 tq = make_double2(1.0, 0.0), tr = tq;
+    if constexpr (TWM != 0) {
+        const i64 bq = c / st.col_div;
+        tq = phase_at(st.tab, bq * ((i64)t * st.kmul + o * st.omul));
+        tr = phase_at(st.tab, bq * (i64)C::TPL * st.kmul);
+    }
     if constexpr (TWM == 2) {
 #pragma unroll
-        for (int q = 0; q < C::R; ++q)
-            v[q] = cmulc(v[q], phase_at(st.tab, bq * ((i64)(t + q * C::TPL) * st.kmul + o * st.omul)));
+        for (int q = 0; q < C::R; ++q) {
+            v[q] = cmulc(v[q], tq);
+            tq = cmul(tq, tr);
+        }
     }
     F::run(v, t, tile + w * C::LSW, tw_all + N);
     if constexpr (TWM == 1) {
 #pragma unroll
-        for (int q = 0; q < C::R; ++q)
-            v[q] = cmul(v[q], phase_at(st.tab, bq * ((i64)(t + q * C::TPL) * st.kmul + o * st.omul)));
+        for (int q = 0; q < C::R; ++q) {
+            v[q] = cmul(v[q], tq);
+            tq = cmul(tq, tr);
+        }
     }
     if (flags) {
         bool bad = false;
