@@ -231,7 +231,7 @@ static int axis_tma_enabled() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("FSX_TMA_AXIS");
-        v = e ? atoi(e) : 1;
+        v = e ? atoi(e) : 512;
     }
     return v;
 }
@@ -263,8 +263,9 @@ static cudaError_t axis_tma_n(const CUtensorMap& mi, const CUtensorMap& mo, cons
 // falls back to the per-thread strided kernel).
 cudaError_t launch_axis_tma(const double2* in, double2* out, const AxisGeom& g, int sign, const StepTwiddle& st,
                             const double2* tw, cudaStream_t s, Flags* flags) {
-    // 128-point columns measured slower than the per-thread strided kernel (cfg5: 540 vs 511 us)
-    if (!axis_tma_enabled() || g.inner <= 1 || g.n < 512 || g.n > 4096) return cudaErrorNotSupported;
+    // FSX_TMA_AXIS (default 512): the shortest column length taken by this path
+    const int nmin = axis_tma_enabled();
+    if (!nmin || g.inner <= 1 || g.n < nmin || g.n > 4096) return cudaErrorNotSupported;
     const int W = tma_cols_width(g.n);
     if (g.ncols % W || (reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) % 16) return cudaErrorNotSupported;
     alignas(64) unsigned char mi[128], mo[128];
