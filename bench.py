@@ -318,7 +318,18 @@ def run_gpu_slab(args, cfg, ws, rank, local):
                 "mode": "per rank: pinned slab H2D + SlabSolver.solve + D2H, max over ranks"},
         "gpu_launches": 3 * args.steps, "clocks": clocks,
     }
+    # parity self-check of the decomposed solve: the slabs gathered on rank 0
+    # against rank 0's own single-GPU solve of the whole grid
+    gathered = [torch.empty_like(d_out) for _ in range(ws)] if rank == 0 else None
+    dist.gather(d_out, gathered, dst=0)
     if rank == 0:
+        full_in = torch.from_numpy(cfg.initial()).cuda()
+        full_out = torch.empty_like(full_in)
+        fs.solve_periodic_device(shape, full_in.data_ptr(), kern, cfg.T, full_out.data_ptr(), stream=0, device=dev)
+        fs.device_check(stream=0, device=dev)
+        slab = torch.cat(gathered)
+        line["parity_vs_single_gpu_rel_l2"] = float(torch.linalg.vector_norm(slab - full_out) /
+                                                    torch.linalg.vector_norm(full_out))
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
