@@ -187,6 +187,50 @@ __device__ __forceinline__ void pow_real_vec_skip(double (&x)[R], u64 T, double 
     }
 }
 
+// pow_complex for R elements with the same warp-level short cut: the loop
+// over T's bits is uniform and CH independent elements per step give CH-way
+// ILP (the per-element pow_complex is one latency chain per element and
+// diverges on its own early out).  Per element the operations are those of
+// pow_complex, so the results are bitwise identical.
+template <int R, int CH>
+__device__ __forceinline__ void pow_complex_vec_skip(double2 (&x)[R], u64 T, double neg_mag2) {
+    static_assert(R % CH == 0, "chunk must divide R");
+#pragma unroll
+    for (int c = 0; c < R; c += CH) {
+        bool neg[CH], all = true;
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+            neg[q] = fma(x[c + q].x, x[c + q].x, x[c + q].y * x[c + q].y) < neg_mag2;
+            all &= neg[q];
+        }
+        if (__all_sync(0xffffffffu, all)) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q) x[c + q] = make_double2(0.0, 0.0);
+            continue;
+        }
+        double2 acc[CH];
+#pragma unroll
+        for (int q = 0; q < CH; ++q) acc[q] = make_double2(1.0, 0.0);
+        u64 t = T;
+        while (t) {
+            if (t & 1) {
+#pragma unroll
+                for (int q = 0; q < CH; ++q) acc[q] = cmul(acc[q], x[c + q]);
+            }
+            t >>= 1;
+            if (t) {
+#pragma unroll
+                for (int q = 0; q < CH; ++q) {
+                    const double2 sq = x[c + q];
+                    x[c + q] = make_double2(fma(sq.x, sq.x, -sq.y * sq.y), (sq.x + sq.x) * sq.y);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < CH; ++q) x[c + q] = neg[q] ? make_double2(0.0, 0.0) : acc[q];
+    }
+}
+
 // Real symbol lam(k0) for k0 = t + q * TPL (no power, no scale), over the
 // groups of one tap set (set 0: the stencil S; set 1: an implicit solve's Q).
 template <int N, int R, int TPL, class AC>
@@ -269,7 +313,9 @@ __device__ __forceinline__ void spectral_regs_at(double2 (&v)[R], int kbase, int
             }
         }
 #pragma unroll
-        for (int q = 0; q < R; ++q) v[q] = cscale(v[q], pow_realv(lam[q], sym.T, sym.neg_mag2) * sym.scale);
+        pow_real_vec_skip<R, (R % 4 == 0 ? 4 : R)>(lam, sym.T, sym.neg_mag2);
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = cscale(v[q], lam[q] * sym.scale);
     } else {
         double2 lam[R];
 #pragma unroll
@@ -284,7 +330,9 @@ __device__ __forceinline__ void spectral_regs_at(double2 (&v)[R], int kbase, int
             }
         }
 #pragma unroll
-        for (int q = 0; q < R; ++q) v[q] = cscale(cmul(pow_complex(lam[q], sym.T, sym.neg_mag2), v[q]), sym.scale);
+        pow_complex_vec_skip<R, (R % 4 == 0 ? 4 : R)>(lam, sym.T, sym.neg_mag2);
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = cscale(cmul(lam[q], v[q]), sym.scale);
     }
 }
 
@@ -314,7 +362,9 @@ __device__ __forceinline__ void spectral_regs(double2 (&v)[R], int t, const Fuse
             }
         }
 #pragma unroll
-        for (int q = 0; q < R; ++q) v[q] = cscale(v[q], pow_realv(lam[q], sym.T, sym.neg_mag2) * sym.scale);
+        pow_real_vec_skip<R, (R % 4 == 0 ? 4 : R)>(lam, sym.T, sym.neg_mag2);
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = cscale(v[q], lam[q] * sym.scale);
     } else {
         double2 lam[R];
 #pragma unroll
@@ -333,7 +383,9 @@ __device__ __forceinline__ void spectral_regs(double2 (&v)[R], int t, const Fuse
             }
         }
 #pragma unroll
-        for (int q = 0; q < R; ++q) v[q] = cscale(cmul(pow_complex(lam[q], sym.T, sym.neg_mag2), v[q]), sym.scale);
+        pow_complex_vec_skip<R, (R % 4 == 0 ? 4 : R)>(lam, sym.T, sym.neg_mag2);
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = cscale(cmul(lam[q], v[q]), sym.scale);
     }
 }
 

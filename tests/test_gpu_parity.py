@@ -91,6 +91,18 @@ def test_golden_errors(golden):
         fs.solve_periodic_vector(G([8], np.zeros(8)), K(R.kern_from({(0,): 1.0}, 1)), 1)
 
 
+def test_2d_fused_errors_and_identity(orc):
+    """2D fused plan: the non-finite scan of the C2R rows raises
+    NumericError (periodic.cpp:55-56); the identity stencil returns a0 to
+    rounding."""
+    dims = [512, 1024]
+    a = orc.splitmix_fill(91, 512 * 1024, True)
+    with pytest.raises(fs.NumericError):
+        fs.solve_periodic(G(dims, a), K(R.kern_from({(0, 0): 2.0}, 2)), 2000)
+    got = fs.solve_periodic(G(dims, a), K(R.kern_from({(0, 0): 1.0}, 2)), 12345).data
+    assert np.max(np.abs(got - a)) <= 1e-13
+
+
 def test_golden_cli_fixtures(golden, orc):
     c = golden["cli_verify_heat1d"]
     k = R.kern_from({tuple(o): v for o, v in zip(c["offsets"], c["values"])}, 1)
@@ -349,7 +361,7 @@ def test_implicit(orc):
         assert np.abs(got - want).max() <= 1e-12
 
 
-@pytest.mark.parametrize("dims,T", [([1024, 256], 200), ([512, 64, 32], 30), ([2048, 128], 1)])
+@pytest.mark.parametrize("dims,T", [([1024, 256], 200), ([512, 64, 32], 30), ([2048, 128], 1), ([512, 2048], 40)])
 def test_implicit_fused_vs_oracle(orc, dims, T):
     """solve_periodic_implicit on the fused plan (real symbols, N0 in the TMA
     multiplier path): Crank-Nicolson q = I - (b/2) L, s = I + (b/2) L of the
@@ -432,6 +444,12 @@ PLAN_CASES = [
     ([16, 2, 32], 1, "heat7", 7),        # 2-point axis-1 pass
     ([16, 4, 64], 1, "random", 3),
     ([8192, 32], 1, "random", 5),        # ... with a complex symbol
+    # 2D fused plan across row lengths and TMA tile widths
+    ([512, 1024], 1, "random", 13),      # L = 1024, 8-column tiles, complex symbol
+    ([1024, 2048], 1, "box9", 1000),     # L = 2048, 4-column tiles
+    ([2048, 4096], 1, "jacobi5", 500),   # L = 4096, 2-column tiles
+    ([4096, 1024], 1, "random", 3),      # one-column tiles
+    ([512, 4096], 1, "box9", 100000),
 ]
 
 
