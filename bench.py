@@ -357,16 +357,19 @@ def run_gpu(args, cfg):
     sptr = stream.cuda_stream
     shape, kern = cfg.shape(), cfg.kernel()
     info = fs.plan_describe(shape, kern)
-    host = cfg.initial()
+    f32 = args.precision == 32  # fp32 storage mode: float grids in and out, fp64 arithmetic
+    host = cfg.initial().astype(np.float32 if f32 else np.float64)
     n = host.size
+    esz = host.itemsize
     d_a0 = torch.from_numpy(host).to(f"cuda:{dev}")
     d_out = torch.empty_like(d_a0)
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device=f"cuda:{dev}")
     torch.cuda.synchronize()
 
+    solve_dev = fs.solve_periodic_device_f32 if f32 else fs.solve_periodic_device
+
     def solve(stage=0):
-        fs.solve_periodic_device(shape, d_a0.data_ptr(), kern, cfg.T, d_out.data_ptr(), stream=sptr,
-                                 device=dev, stage_events=stage)
+        solve_dev(shape, d_a0.data_ptr(), kern, cfg.T, d_out.data_ptr(), stream=sptr, device=dev, stage_events=stage)
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -423,28 +426,42 @@ def run_gpu(args, cfg):
     # e2e through the public host API: pinned host in/out, H2D + solve + D2H per step
     e2e_val = e2e_single = None
     if not args.no_e2e:
+        tdt = torch.float32 if f32 else torch.float64
         pin_in = torch.from_numpy(host).pin_memory()
-        pin_out = torch.empty(n, dtype=torch.float64).pin_memory()
-        grid = fs.FieldGrid(shape, pin_in.numpy())
+        pin_out = torch.empty(n, dtype=tdt).pin_memory()
         out_np = pin_out.numpy()
+        if f32:
+            def host_solve(out):
+                fs.solve_periodic_f32(shape, pin_in.numpy(), kern, cfg.T, out=out)
+
+            def host_batch(k, outs):
+                fs.solve_periodic_batch_f32(shape, [pin_in.numpy()] * k, kern, cfg.T, outs)
+        else:
+            grid = fs.FieldGrid(shape, pin_in.numpy())
+
+            def host_solve(out):
+                fs.solve_periodic(grid, kern, cfg.T, out=out)
+
+            def host_batch(k, outs):
+                fs.solve_periodic_batch([grid] * k, kern, cfg.T, outs)
         for _ in range(max(1, args.warmup)):
-            fs.solve_periodic(grid, kern, cfg.T, out=out_np)
+            host_solve(out_np)
         # (a) one synchronous host call per step
         e2e_t = []
         for _ in range(args.steps):
             t0 = time.perf_counter()
-            fs.solve_periodic(grid, kern, cfg.T, out=out_np)
+            host_solve(out_np)
             e2e_t.append(time.perf_counter() - t0)
         et1 = sum(e2e_t) / len(e2e_t)
         # parity sanity: host result equals the device result
         assert np.array_equal(out_np, d_out.cpu().numpy())
         # (b) the K steps as one pipelined batch call (every step still moves its
         # input H2D and its result D2H; the lanes overlap them across steps)
-        pin_out2 = torch.empty(n, dtype=torch.float64).pin_memory()
+        pin_out2 = torch.empty(n, dtype=tdt).pin_memory()
         outs = [out_np, pin_out2.numpy()]
-        fs.solve_periodic_batch([grid] * max(2, args.warmup), kern, cfg.T, [outs[i & 1] for i in range(max(2, args.warmup))])
+        host_batch(max(2, args.warmup), [outs[i & 1] for i in range(max(2, args.warmup))])
         t0 = time.perf_counter()
-        fs.solve_periodic_batch([grid] * args.steps, kern, cfg.T, [outs[i & 1] for i in range(args.steps)])
+        host_batch(args.steps, [outs[i & 1] for i in range(args.steps)])
         etb = (time.perf_counter() - t0) / args.steps
         assert np.array_equal(outs[(args.steps - 1) & 1], d_out.cpu().numpy())
         t = torch.tensor([et1, etb], dtype=torch.float64, device=f"cuda:{dev}")
@@ -456,7 +473,10 @@ def run_gpu(args, cfg):
 
     peak, peak_src = load_peaks()
     fused_gbs = info["fused_bytes"] / (fms * 1e-3) / 1e9 if fms > 0 else None
-    pipe_gbs = info["alg_bytes"] / (ms * 1e-3) / 1e9
+    alg_step = info["alg_bytes"]
+    if f32:  # plan 1 reads / writes the grid as floats; the others widen (R/2 + R) and narrow (R + R/2)
+        alg_step += -n * 8 if info["path"] == 1 else 3 * n * 8
+    pipe_gbs = alg_step / (ms * 1e-3) / 1e9
     kernel_name = {1: "k_cols_tma", 2: "k_rowpair", 3: "k_spectral_general"}[info["path"]]
     line = {
         "metric": METRIC,
@@ -475,7 +495,8 @@ def run_gpu(args, cfg):
             "workload": cfg.name + ": " + cfg.description,
             "grid": cfg.dims, "fields": cfg.fields, "T": cfg.T,
             "parallelism": "replicas" if ws > 1 else "single",
-            "l2": f"flushed before every step ({FLUSH_BYTES >> 20} MiB write), grid {n * 8 >> 20} MiB",
+            "l2": f"flushed before every step ({FLUSH_BYTES >> 20} MiB write), grid {n * esz >> 20} MiB",
+            "storage": "f32 (fp32 storage mode: float grids in and out, fp64 arithmetic)" if f32 else "f64",
             "plan": info["path"],
             "wall_s_timed_region": wall,
         },
@@ -492,17 +513,18 @@ def run_gpu(args, cfg):
             "peak_source": peak_src,
             "fp64": load_fp64(cfg.name, fms),
         },
-        "pipeline": {"alg_bytes_per_step": info["alg_bytes"], "achieved_gbs": pipe_gbs, "frac": pipe_gbs / peak},
+        "pipeline": {"alg_bytes_per_step": alg_step, "achieved_gbs": pipe_gbs, "frac": pipe_gbs / peak},
         "gpu_launches": info["launches"] * args.steps,
         "host_enqueue_us": sorted(host_us)[len(host_us) // 2],
         "clocks": clocks,
     }
     if e2e_val is not None:
-        line["e2e"] = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 8,
-                       "mode": f"fsx_solve_periodic_batch of the {args.steps} steps (pinned host in/out; two lanes "
+        sfx = "_f32" if f32 else ""
+        line["e2e"] = {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": n * esz, "d2h_bytes_per_step": n * esz,
+                       "mode": f"fsx_solve_periodic_batch{sfx} of the {args.steps} steps (pinned host in/out; two lanes "
                                "overlap one step's D2H with the next step's H2D and kernels)",
                        "single_call_value": e2e_single,
-                       "single_call_mode": "one synchronous fsx_solve_periodic per step"}
+                       "single_call_mode": f"one synchronous fsx_solve_periodic{sfx} per step"}
     if rank == 0 and ws == 1 and not args.no_cpu:
         from oracle import oracle as orc
 
@@ -534,6 +556,8 @@ def main():
                     help="slab exchange for N > 1: p2p = fused into the row kernels over NVLink peer memory "
                          "(2D; auto falls back to nccl if symmetric memory is unavailable)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--precision", type=int, choices=[64, 32], default=64,
+                    help="32: the fp32 storage mode (float grids in/out, fp64 arithmetic; single GPU)")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of slabs")
     ap.add_argument("--slab", action="store_true", help="use the slab-decomposed path even at N=1 (under torchrun)")
     args = ap.parse_args()

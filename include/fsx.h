@@ -130,6 +130,26 @@ fsx_status fsx_solve_periodic_device(const fsx_shape* shape, const double* d_a0,
                                      uint64_t T, double* d_out, const fsx_options* opt);
 fsx_status fsx_device_check(const fsx_options* opt);
 
+/* fp32 storage mode (north star: an optional fp32 mode at <= 1e-4 relative L2
+ * vs the fp64 reference).  Float grids in and out; the arithmetic stays fp64
+ * (symbol power, FFTs), so the result is the fp64 solve of the widened input
+ * rounded once to float (~6e-8 relative).  What it buys is bytes: half the
+ * PCIe traffic of the host entry points and, on the fused 2D/3D plan, half
+ * the HBM bytes of the first and last row passes (the row kernels read and
+ * write floats directly; the other plans widen / narrow around their fp64
+ * buffers).  A result outside the float range raises FSX_ERR_NUMERIC.
+ * Same shapes, kernels, T == 0 (bit-exact copy) and error rules as
+ * fsx_solve_periodic / fsx_solve_periodic_device / fsx_solve_periodic_batch;
+ * no implicit or cached variants.  No reference counterpart (the reference
+ * library is fp64 only, proj/include/fftstencil/grid.hpp:86-100). */
+fsx_status fsx_solve_periodic_f32(const fsx_shape* shape, const float* a0, const fsx_kernel* k, uint64_t T,
+                                  float* out, const fsx_options* opt, fsx_stage_timings* st);
+fsx_status fsx_solve_periodic_device_f32(const fsx_shape* shape, const float* d_a0, const fsx_kernel* k,
+                                         uint64_t T, float* d_out, const fsx_options* opt);
+fsx_status fsx_solve_periodic_batch_f32(const fsx_shape* shape, int64_t nbatch, const float* const* a0s,
+                                        const fsx_kernel* k, uint64_t T, float* const* outs,
+                                        const fsx_options* opt);
+
 /* Direct-stepping verifier (not the solve path): the reference's naive
  * oracle step_periodic / evolve_periodic_naive (proj/src/oracle.cpp:90-115,
  * oracle.hpp:15-20) on the GPU, bitwise equal to the reference loop (taps in

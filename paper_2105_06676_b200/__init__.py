@@ -35,7 +35,10 @@ from .fftstencil import (  # noqa: F401
     solve_periodic,
     solve_periodic_batch,
     solve_periodic_cached,
+    solve_periodic_batch_f32,
     solve_periodic_device,
+    solve_periodic_device_f32,
+    solve_periodic_f32,
     solve_periodic_implicit,
     solve_periodic_vector,
     spectrum_from_kernel,

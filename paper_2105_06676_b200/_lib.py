@@ -86,6 +86,9 @@ EXPORTS = (
     "fsx_solve_periodic_implicit",
     "fsx_solve_periodic_device",
     "fsx_solve_periodic_batch",
+    "fsx_solve_periodic_f32",
+    "fsx_solve_periodic_device_f32",
+    "fsx_solve_periodic_batch_f32",
     "fsx_device_check",
     "fsx_last_stage_ms",
     "fsx_step_periodic",

@@ -289,6 +289,7 @@ struct Plan {
     // workspaces
     DevBuf work;      // H (kind 1) / complex Z (kind 3)
     DevBuf d_in, d_out;
+    DevBuf f_in, f_out;  // fp32 storage mode: host-API staging of float grids
     DevBuf taps_dev;  // general path tap arrays
     DevBuf blue_bhat, blue_buf;  // Bluestein filter spectra and [lines][P] workspace
     DevBuf qmax;      // implicit fused symbol: max |lamQ| (bits)
@@ -829,8 +830,11 @@ struct Stamps {
 
 // Runs one solve on device pointers; stage boundaries are stamped into
 // ev[0..3] when timings are requested.
+// fin / fout (fp32 storage mode, plan 1 only): the row passes read and write
+// floats directly instead of d_a0 / d_out.
 void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, const double* d_a0, double* d_out,
-              cudaStream_t st, Stamps& sp, fsx::Flags* flags_at = nullptr) {
+              cudaStream_t st, Stamps& sp, fsx::Flags* flags_at = nullptr, const float* fin = nullptr,
+              float* fout = nullptr) {
     fsx::Flags* flags = flags_at ? flags_at : dev.flags.as<fsx::Flags>();
     const double2* tw = dev.tw_all.as<double2>();
     const int r = (int)p.dims.size();
@@ -838,7 +842,8 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
     if (p.kind == kFusedR2C) {
         double2* H = p.work.as<double2>();
         const fsx::RowLayout lay{p.P, 0, p.rows};
-        FSX_CK(fsx::launch_r2c_rows(d_a0, H, p.rows, p.L, lay, tw, st));
+        if (fin) FSX_CK(fsx::launch_r2c_rows_f32(fin, H, p.rows, p.L, lay, tw, st));
+        else FSX_CK(fsx::launch_r2c_rows(d_a0, H, p.rows, p.L, lay, tw, st));
         fsx::StepTwiddle none;
         const fsx::FusedSymbol sym = fused_symbol(p, taps, T, q, q ? p.qmax.as<unsigned long long>() : nullptr);
         fsx::FusedSymbol nosym;
@@ -859,7 +864,8 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
             if (p.tma1) FSX_CK(fsx::launch_cols_tma(p.map1, p.ax1, 1, nosym, tw, st));
             else FSX_CK(fsx::launch_axis_pow2(H, H, p.ax1, +1, none, tw, st));
         }
-        FSX_CK(fsx::launch_c2r_rows(H, d_out, p.rows, p.L, lay, tw, flags, st));
+        if (fout) FSX_CK(fsx::launch_c2r_rows_f32(H, fout, p.rows, p.L, lay, tw, flags, st));
+        else FSX_CK(fsx::launch_c2r_rows(H, d_out, p.rows, p.L, lay, tw, flags, st));
         sp.mark();
     } else if (p.kind == kRowPair1D) {
         // the first column pass reads a0 and writes the output buffer (out of
@@ -1163,6 +1169,24 @@ void evolve_naive(const fsx_shape* shape, const double* a0, const fsx_kernel* k,
     if (!device_ptrs) FSX_CK(cudaStreamSynchronize(st));
 }
 
+// fp32 storage mode (float grids in and out, fp64 arithmetic): plan 1 reads and
+// writes the floats in its row passes; the other plans widen into / narrow out
+// of their fp64 buffers (the narrowing flags values outside the float range).
+void run_plan_f32(Plan& p, Device& dev, const Taps& taps, u64 T, const float* fin, float* fout, cudaStream_t st,
+                  Stamps& sp, fsx::Flags* flags_at = nullptr) {
+    const auto a16 = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) == 0; };
+    if (p.kind == kFusedR2C && fsx::rows_f32_ok(p.L) && a16(fin) && a16(fout)) {
+        run_plan(p, dev, taps, nullptr, T, nullptr, nullptr, st, sp, flags_at, fin, fout);
+        return;
+    }
+    const i64 n = p.cells * p.m;
+    p.d_in.ensure((size_t)n * 8);
+    p.d_out.ensure((size_t)n * 8);
+    FSX_CK(fsx::launch_widen(fin, p.d_in.as<double>(), n, st));
+    run_plan(p, dev, taps, nullptr, T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp, flags_at);
+    FSX_CK(fsx::launch_narrow(p.d_out.as<double>(), fout, n, flags_at ? flags_at : dev.flags.as<fsx::Flags>(), st));
+}
+
 struct SolveReq {
     const fsx_shape* shape;
     const double* a0;
@@ -1175,6 +1199,8 @@ struct SolveReq {
     bool vector = false;
     bool device_ptrs = false;
     const Taps* cached = nullptr;  // solve_periodic_cached: the spectrum's kernel from the cache
+    const float* a0f = nullptr;    // fp32 storage mode (a0 / out unused)
+    float* outf = nullptr;
 };
 
 void solve(const SolveReq& rq) {
@@ -1196,19 +1222,23 @@ void solve(const SolveReq& rq) {
         require_fits(taps, s);
         if (rq.cached) taps = *rq.cached;
     }
-    if (!rq.a0 || !rq.out) throw SpecErr("fsx: null grid pointer");
-    const size_t bytes = (size_t)s.values() * 8;
+    const bool f32 = rq.a0f || rq.outf;
+    const void* in = f32 ? (const void*)rq.a0f : (const void*)rq.a0;
+    void* out = f32 ? (void*)rq.outf : (void*)rq.out;
+    if (!in || !out) throw SpecErr("fsx: null grid pointer");
+    if (f32 && rq.q) throw SpecErr("fsx: fp32 storage mode covers solve_periodic only");
+    const size_t bytes = (size_t)s.values() * (f32 ? 4 : 8);
     const int ordinal = rq.opt ? rq.opt->device : 0;
     if (rq.T == 0 && !rq.device_ptrs) {
         // proj/src/periodic.cpp:79: the input, bit for bit (a copy, no arithmetic)
-        if (rq.out != rq.a0) std::memmove(rq.out, rq.a0, bytes);
+        if (out != in) std::memmove(out, in, bytes);
         return;
     }
     std::lock_guard<std::mutex> lk(g_mu);
     Device& dev = device_for(ordinal);
     cudaStream_t st = stream_of(dev, rq.opt);
     if (rq.T == 0) {
-        if (rq.out != rq.a0) FSX_CK(cudaMemcpyAsync(rq.out, rq.a0, bytes, cudaMemcpyDeviceToDevice, st));
+        if (out != in) FSX_CK(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, st));
         return;
     }
     const int force_general = rq.opt && rq.opt->path == 1;
@@ -1218,16 +1248,20 @@ void solve(const SolveReq& rq) {
     if (rq.q && p.kind == kFusedR2C) p.qmax.ensure(8);
     Stamps sp{&dev, rq.st != nullptr || (rq.device_ptrs && rq.opt && rq.opt->stage_events), st};
     if (rq.device_ptrs) {
-        run_plan(p, dev, taps, rq.q ? &qtaps : nullptr, rq.T, rq.a0, rq.out, st, sp);
+        if (f32) run_plan_f32(p, dev, taps, rq.T, rq.a0f, rq.outf, st, sp);
+        else run_plan(p, dev, taps, rq.q ? &qtaps : nullptr, rq.T, rq.a0, rq.out, st, sp);
         return;
     }
-    p.d_in.ensure(bytes);
-    p.d_out.ensure(bytes);
+    DevBuf& bin = f32 ? p.f_in : p.d_in;
+    DevBuf& bout = f32 ? p.f_out : p.d_out;
+    bin.ensure(bytes);
+    bout.ensure(bytes);
     cudaEvent_t h0 = dev.ev[6], h1 = dev.ev[7];
     if (sp.on) FSX_CK(cudaEventRecord(h0, st));
-    FSX_CK(cudaMemcpyAsync(p.d_in.p, rq.a0, bytes, cudaMemcpyHostToDevice, st));
-    run_plan(p, dev, taps, rq.q ? &qtaps : nullptr, rq.T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp);
-    FSX_CK(cudaMemcpyAsync(rq.out, p.d_out.p, bytes, cudaMemcpyDeviceToHost, st));
+    FSX_CK(cudaMemcpyAsync(bin.p, in, bytes, cudaMemcpyHostToDevice, st));
+    if (f32) run_plan_f32(p, dev, taps, rq.T, p.f_in.as<float>(), p.f_out.as<float>(), st, sp);
+    else run_plan(p, dev, taps, rq.q ? &qtaps : nullptr, rq.T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp);
+    FSX_CK(cudaMemcpyAsync(out, bout.p, bytes, cudaMemcpyDeviceToHost, st));
     if (sp.on) FSX_CK(cudaEventRecord(h1, st));
     check_flags(dev, p.kind, st);
     if (sp.on) {
@@ -1252,8 +1286,10 @@ void solve(const SolveReq& rq) {
 // instead of their sum.  Non-finite / residue checks per solve, reported for
 // the first failing index after the batch completes (outputs of the others
 // are valid).  SURVEY.md §8(f) item 1 (batched slab solves).
-void solve_batch(const fsx_shape* shape, i64 nb, const double* const* a0s, const fsx_kernel* k, u64 T,
-                 double* const* outs, const fsx_options* opt) {
+template <class TE>
+void solve_batch(const fsx_shape* shape, i64 nb, const TE* const* a0s, const fsx_kernel* k, u64 T,
+                 TE* const* outs, const fsx_options* opt) {
+    constexpr bool f32 = sizeof(TE) == 4;
     const Shape s = parse_shape(shape);
     const Taps taps = parse_kernel(k);
     require_fits(taps, s);
@@ -1261,7 +1297,7 @@ void solve_batch(const fsx_shape* shape, i64 nb, const double* const* a0s, const
     if (nb > 0 && (!a0s || !outs)) throw SpecErr("fsx: null grid pointer");
     for (i64 i = 0; i < nb; ++i)
         if (!a0s[i] || !outs[i]) throw SpecErr("fsx: null grid pointer");
-    const size_t bytes = (size_t)s.values() * 8;
+    const size_t bytes = (size_t)s.values() * sizeof(TE);
     if (T == 0) {
         for (i64 i = 0; i < nb; ++i)
             if (outs[i] != a0s[i]) std::memmove(outs[i], a0s[i], bytes);
@@ -1278,8 +1314,8 @@ void solve_batch(const fsx_shape* shape, i64 nb, const double* const* a0s, const
             FSX_CK(cudaEventCreateWithFlags(&dev.lane_ev[l], cudaEventDisableTiming));
         }
         pl[l] = &get_plan(dev, s, taps, force_general, l);
-        pl[l]->d_in.ensure(bytes);
-        pl[l]->d_out.ensure(bytes);
+        (f32 ? pl[l]->f_in : pl[l]->d_in).ensure(bytes);
+        (f32 ? pl[l]->f_out : pl[l]->d_out).ensure(bytes);
     }
     dev.bflags.ensure((size_t)nb * sizeof(fsx::Flags));
     fsx::Flags* fl = dev.bflags.as<fsx::Flags>();
@@ -1296,9 +1332,12 @@ void solve_batch(const fsx_shape* shape, i64 nb, const double* const* a0s, const
         Plan& p = *pl[l];
         cudaStream_t st = dev.lanes[l];
         Stamps sp{&dev, false, st};
-        FSX_CK(cudaMemcpyAsync(p.d_in.p, a0s[i], bytes, cudaMemcpyHostToDevice, st));
-        run_plan(p, dev, taps, nullptr, T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp, fl + i);
-        FSX_CK(cudaMemcpyAsync(outs[i], p.d_out.p, bytes, cudaMemcpyDeviceToHost, st));
+        DevBuf& bin = f32 ? p.f_in : p.d_in;
+        DevBuf& bout = f32 ? p.f_out : p.d_out;
+        FSX_CK(cudaMemcpyAsync(bin.p, a0s[i], bytes, cudaMemcpyHostToDevice, st));
+        if constexpr (f32) run_plan_f32(p, dev, taps, T, p.f_in.as<float>(), p.f_out.as<float>(), st, sp, fl + i);
+        else run_plan(p, dev, taps, nullptr, T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp, fl + i);
+        FSX_CK(cudaMemcpyAsync(outs[i], bout.p, bytes, cudaMemcpyDeviceToHost, st));
     }
     std::vector<fsx::Flags> h((size_t)nb);
     FSX_CK(cudaStreamSynchronize(dev.lanes[1]));
@@ -1430,7 +1469,33 @@ fsx_status fsx_evolve_periodic_naive_device(const fsx_shape* shape, const double
 
 fsx_status fsx_solve_periodic_batch(const fsx_shape* shape, int64_t nbatch, const double* const* a0s,
                                     const fsx_kernel* k, uint64_t T, double* const* outs, const fsx_options* opt) {
-    return guarded([&] { solve_batch(shape, nbatch, a0s, k, T, outs, opt); });
+    return guarded([&] { solve_batch<double>(shape, nbatch, a0s, k, T, outs, opt); });
+}
+
+fsx_status fsx_solve_periodic_f32(const fsx_shape* shape, const float* a0, const fsx_kernel* k, uint64_t T, float* out,
+                                  const fsx_options* opt, fsx_stage_timings* st) {
+    return guarded([&] {
+        SolveReq rq{shape, nullptr, k, nullptr, T, nullptr, opt, st};
+        rq.a0f = a0;
+        rq.outf = out;
+        solve(rq);
+    });
+}
+
+fsx_status fsx_solve_periodic_device_f32(const fsx_shape* shape, const float* d_a0, const fsx_kernel* k, uint64_t T,
+                                         float* d_out, const fsx_options* opt) {
+    return guarded([&] {
+        SolveReq rq{shape, nullptr, k, nullptr, T, nullptr, opt, nullptr};
+        rq.a0f = d_a0;
+        rq.outf = d_out;
+        rq.device_ptrs = true;
+        solve(rq);
+    });
+}
+
+fsx_status fsx_solve_periodic_batch_f32(const fsx_shape* shape, int64_t nbatch, const float* const* a0s,
+                                        const fsx_kernel* k, uint64_t T, float* const* outs, const fsx_options* opt) {
+    return guarded([&] { solve_batch<float>(shape, nbatch, a0s, k, T, outs, opt); });
 }
 
 fsx_status fsx_device_check(const fsx_options* opt) {

@@ -1209,6 +1209,30 @@ cudaError_t launch_extract(const double2* z, double* x, i64 n, Flags* f, cudaStr
     return cudaGetLastError();
 }
 
+// fp32 storage mode around the fp64 plans that have no fp32 row kernels
+__global__ void k_widen(const float* __restrict__ x, double* __restrict__ y, i64 n) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) y[i] = x[i];
+}
+__global__ void k_narrow(const double* __restrict__ x, float* __restrict__ y, i64 n, Flags* flags) {
+    bool bad = false;
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        const float f = (float)x[i];
+        y[i] = f;
+        bad |= !isfinite(f);
+    }
+    flag_nonfinite(bad, flags);
+}
+
+cudaError_t launch_widen(const float* x, double* y, i64 n, cudaStream_t s) {
+    k_widen<<<grid_for(n, 256), 256, 0, s>>>(x, y, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_narrow(const double* x, float* y, i64 n, Flags* f, cudaStream_t s) {
+    k_narrow<<<grid_for(n, 256), 256, 0, s>>>(x, y, n, f);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_finite_check(const double* x, i64 n, Flags* f, cudaStream_t s) {
     k_finite<<<grid_for(n, 256), 256, 0, s>>>(x, n, f);
     return cudaGetLastError();

@@ -216,6 +216,15 @@ cudaError_t launch_fused_r2c(double2* H, const AxisGeom& g, const FusedSymbol& s
                              const double2* tw_all, cudaStream_t s);
 cudaError_t launch_rowpair(const RowPairArgs& a, cudaStream_t s);
 cudaError_t launch_promote(const double* x, double2* z, i64 n, cudaStream_t s);
+// fp32 storage mode: widen / narrow (non-finite float results flagged), and
+// the plan-1 row passes reading / writing floats directly
+cudaError_t launch_widen(const float* x, double* y, i64 n, cudaStream_t s);
+cudaError_t launch_narrow(const double* x, float* y, i64 n, Flags* flags, cudaStream_t s);
+bool rows_f32_ok(i64 L);
+cudaError_t launch_r2c_rows_f32(const float* x, double2* H, i64 nrows, i64 L, const RowLayout& lay,
+                                const double2* tw_all, cudaStream_t s);
+cudaError_t launch_c2r_rows_f32(const double2* H, float* x, i64 nrows, i64 L, const RowLayout& lay,
+                                const double2* tw_all, Flags* flags, cudaStream_t s);
 // Bluestein stages for non-pow2 axes (fsx_kernels.cu): gather * chirp into [lines][P],
 // pointwise * Bhat, scatter * chirp * scale (conj in / out for the inverse)
 cudaError_t launch_blue_pre(const double2* Z, double2* buf, const AxisGeom& g, i64 P, const double2* chirp, int conj_in,

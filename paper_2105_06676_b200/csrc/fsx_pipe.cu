@@ -163,13 +163,15 @@ struct BulkCfg {
 
 // BLK: the output goes to the slab exchange layout (blocked, or straight
 // into the peers' buffers over NVLink, RowLayout::ptr); otherwise pitch rows.
-template <int M, int ST, bool BLK>
+// TI = float: fp32 storage mode (the row lands as floats, half the bytes, and
+// is widened to fp64 as it is read into registers; the arithmetic is fp64).
+template <int M, int ST, bool BLK, class TI = double>
 __global__ void __launch_bounds__(PCfg<M>::TPL, BulkCfg<M, ST>::MINB)
-k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, RowLayout lay,
+k_r2c_bulk(const TI* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, RowLayout lay,
            const double2* __restrict__ tw_all) {
     using F = LineFFT<M, -1, true, true>;
     constexpr int TPL = PCfg<M>::TPL, R = 16;
-    constexpr unsigned BYTES = M * sizeof(double2);
+    constexpr unsigned BYTES = 2 * M * sizeof(TI);
     extern __shared__ __align__(128) double2 sm[];
     __shared__ __align__(8) unsigned long long bar[ST];
     const int t = threadIdx.x;
@@ -198,8 +200,17 @@ k_r2c_bulk(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64
         par ^= 1u << s;
         double2* line = sm + s * M;
         double2 v[R];
+        if constexpr (sizeof(TI) == 8) {
 #pragma unroll
-        for (int q = 0; q < R; ++q) v[q] = line[t + q * TPL];
+            for (int q = 0; q < R; ++q) v[q] = line[t + q * TPL];
+        } else {
+            const float2* lf = reinterpret_cast<const float2*>(line);
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const float2 f = lf[t + q * TPL];
+                v[q] = make_double2(f.x, f.y);
+            }
+        }
         F::run(v, t, line, tw_all + M);
         auto h = [&](int k) -> double2& { return *row_ptr<BLK>(H, lay, row, k); };
         if constexpr (F::PAIRED) {
@@ -266,9 +277,11 @@ __device__ __forceinline__ void load_hrow(double2* dst, const double2* H, const 
     }
 }
 
-template <int M, int ST, bool BLK>
+// TO = float: fp32 storage mode (rounded to nearest on the store; a value
+// outside the float range becomes inf and raises the non-finite flag).
+template <int M, int ST, bool BLK, class TO = double>
 __global__ void __launch_bounds__(PCfg<M>::TPL, BulkCfg<M, ST>::MINB)
-k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, RowLayout lay,
+k_c2r_bulk(const double2* __restrict__ H, TO* __restrict__ x, i64 nrows, i64 L, RowLayout lay,
            const double2* __restrict__ tw_all, Flags* flags) {
     using F = LineFFT<M, +1, true>;
     constexpr int TPL = PCfg<M>::TPL, R = 16;
@@ -308,11 +321,21 @@ k_c2r_bulk(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
             v[q] = cadd(e, cmul_si<+1>(od));
         });
         F::run(v, t, line, tw_all + M);
-        double2* dst = reinterpret_cast<double2*>(x + row * L);
+        if constexpr (sizeof(TO) == 8) {
+            double2* dst = reinterpret_cast<double2*>(x + row * L);
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-            dst[t + q * TPL] = v[q];
-            bad |= !isfinite(v[q].x) || !isfinite(v[q].y);
+            for (int q = 0; q < R; ++q) {
+                dst[t + q * TPL] = v[q];
+                bad |= !isfinite(v[q].x) || !isfinite(v[q].y);
+            }
+        } else {
+            float2* dst = reinterpret_cast<float2*>(x + row * L);
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const float2 f = make_float2((float)v[q].x, (float)v[q].y);
+                dst[t + q * TPL] = f;
+                bad |= !isfinite(f.x) || !isfinite(f.y);
+            }
         }
         fence_proxy_async();
         __syncthreads();
@@ -570,6 +593,53 @@ cudaError_t launch_c2r_bulk(const double2* H, double* x, i64 nrows, i64 L, const
         case 1024: return c2r_bulk_m<1024>(H, x, nrows, L, lay, tw, f, s);
         case 2048: return c2r_bulk_m<2048>(H, x, nrows, L, lay, tw, f, s);
         case 4096: return c2r_bulk_m<4096>(H, x, nrows, L, lay, tw, f, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// fp32 storage mode rows (pitch layout, two stages as the fp64 default)
+template <int M>
+static cudaError_t r2c_bulk_f32_m(const float* x, double2* H, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
+                                  cudaStream_t s) {
+    const size_t smem = (size_t)2 * M * sizeof(double2);
+    auto kf = k_r2c_bulk<M, 2, false, float>;
+    kernel_prepare((const void*)kf, smem);
+    const int grid = persistent_grid(kf, PCfg<M>::TPL, smem, nrows);
+    return launch_pdl(kf, dim3(grid), dim3(PCfg<M>::TPL), smem, s, x, H, nrows, L, lay, tw);
+}
+
+template <int M>
+static cudaError_t c2r_bulk_f32_m(const double2* H, float* x, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
+                                  Flags* f, cudaStream_t s) {
+    const size_t smem = (size_t)2 * (M + 8) * sizeof(double2);
+    auto kf = k_c2r_bulk<M, 2, false, float>;
+    kernel_prepare((const void*)kf, smem);
+    const int grid = persistent_grid(kf, PCfg<M>::TPL, smem, nrows);
+    return launch_pdl(kf, dim3(grid), dim3(PCfg<M>::TPL), smem, s, H, x, nrows, L, lay, tw, f);
+}
+
+bool rows_f32_ok(i64 L) { return pipe_enabled() && pipe_rows_ok(L / 2) && rows_variant() == 3; }
+
+cudaError_t launch_r2c_rows_f32(const float* x, double2* H, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
+                                cudaStream_t s) {
+    if (lay.blk) return cudaErrorInvalidValue;
+    switch (L / 2) {
+        case 512: return r2c_bulk_f32_m<512>(x, H, nrows, L, lay, tw, s);
+        case 1024: return r2c_bulk_f32_m<1024>(x, H, nrows, L, lay, tw, s);
+        case 2048: return r2c_bulk_f32_m<2048>(x, H, nrows, L, lay, tw, s);
+        case 4096: return r2c_bulk_f32_m<4096>(x, H, nrows, L, lay, tw, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_c2r_rows_f32(const double2* H, float* x, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
+                                Flags* f, cudaStream_t s) {
+    if (lay.blk) return cudaErrorInvalidValue;
+    switch (L / 2) {
+        case 512: return c2r_bulk_f32_m<512>(H, x, nrows, L, lay, tw, f, s);
+        case 1024: return c2r_bulk_f32_m<1024>(H, x, nrows, L, lay, tw, f, s);
+        case 2048: return c2r_bulk_f32_m<2048>(H, x, nrows, L, lay, tw, f, s);
+        case 4096: return c2r_bulk_f32_m<4096>(H, x, nrows, L, lay, tw, f, s);
         default: return cudaErrorInvalidValue;
     }
 }

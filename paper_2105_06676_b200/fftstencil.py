@@ -438,6 +438,76 @@ def solve_periodic_device(shape: GridShape, d_a0: int, k: StencilKernel, T: int,
     _lib.check(status)
 
 
+# ---------------------------------------------------------------- fp32 storage mode
+_FP = ctypes.POINTER(ctypes.c_float)
+
+
+def _f32(a, n: int, what: str) -> np.ndarray:
+    if not isinstance(a, np.ndarray) or a.dtype != np.float32 or a.size != n or not a.flags.c_contiguous:
+        raise SpecError(f"{what} must be a contiguous float32 array of the grid's size")
+    return a
+
+
+def solve_periodic_f32(shape: GridShape, a0: np.ndarray, k: StencilKernel, T: int, st: StageTimings | None = None,
+                       *, path: int = 0, out: np.ndarray | None = None) -> np.ndarray:
+    """fp32 storage mode (fsx_solve_periodic_f32): float32 grid in and out,
+    fp64 arithmetic inside; the north star's optional fp32 mode (<= 1e-4
+    relative L2 vs the fp64 reference; the result is the fp64 solve of the
+    widened input rounded once to float).  Returns the float32 result."""
+    if T < 0 or T >= 1 << 64:
+        raise SpecError("T must be a nonnegative 64-bit integer")
+    n = int(np.prod(shape.dims())) * shape.fields()
+    a0 = _f32(a0, n, "a0")
+    out = np.empty_like(a0) if out is None else _f32(out, n, "out")
+    L = _lib.load()
+    kc, keep = k._c()
+    stc = st._push() if st is not None else None
+    status = L.fsx_solve_periodic_f32(ctypes.byref(shape._c()), a0.ctypes.data_as(_FP), ctypes.byref(kc),
+                                      ctypes.c_uint64(int(T)), out.ctypes.data_as(_FP), ctypes.byref(_opts(path=path)),
+                                      ctypes.byref(stc) if stc is not None else None)
+    del keep
+    _lib.check(status)
+    if st is not None:
+        st._pull(stc)
+    return out
+
+
+def solve_periodic_batch_f32(shape: GridShape, a0s, k: StencilKernel, T: int, outs=None) -> list:
+    """Pipelined batch in the fp32 storage mode (fsx_solve_periodic_batch_f32)."""
+    if T < 0 or T >= 1 << 64:
+        raise SpecError("T must be a nonnegative 64-bit integer")
+    n = int(np.prod(shape.dims())) * shape.fields()
+    ins = [_f32(a, n, "a0") for a in a0s]
+    if not ins:
+        return []
+    outs = [np.empty_like(a) for a in ins] if outs is None else [_f32(o, n, "out") for o in outs]
+    if len(outs) != len(ins):
+        raise SpecError("solve_periodic_batch_f32: one output per input")
+    m = len(ins)
+    pi = (ctypes.c_void_p * m)(*[a.ctypes.data for a in ins])
+    po = (ctypes.c_void_p * m)(*[o.ctypes.data for o in outs])
+    L = _lib.load()
+    kc, keep = k._c()
+    status = L.fsx_solve_periodic_batch_f32(ctypes.byref(shape._c()), ctypes.c_int64(m), pi, ctypes.byref(kc),
+                                            ctypes.c_uint64(int(T)), po, ctypes.byref(_opts()))
+    del keep
+    _lib.check(status)
+    return outs
+
+
+def solve_periodic_device_f32(shape: GridShape, d_a0: int, k: StencilKernel, T: int, d_out: int,
+                              stream: int | None = None, device: int = 0, path: int = 0, stage_events: int = 0) -> None:
+    """Device-resident fp32 storage mode (fsx_solve_periodic_device_f32):
+    float32 device buffers; asynchronous like :func:`solve_periodic_device`."""
+    L = _lib.load()
+    kc, keep = k._c()
+    status = L.fsx_solve_periodic_device_f32(ctypes.byref(shape._c()), ctypes.c_void_p(d_a0), ctypes.byref(kc),
+                                             ctypes.c_uint64(int(T)), ctypes.c_void_p(d_out),
+                                             ctypes.byref(_opts(device, path, stream, stage_events)))
+    del keep
+    _lib.check(status)
+
+
 # ---------------------------------------------------------------- direct-stepping verifier
 def step_periodic(a: FieldGrid, k: StencilKernel) -> FieldGrid:
     """proj/src/oracle.cpp:90-98 on the GPU (fsx_step_periodic): one direct
