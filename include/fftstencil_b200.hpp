@@ -214,6 +214,19 @@ inline FieldGrid solve_periodic_implicit(const StencilKernel& q, const StencilKe
     return out;
 }
 
+// fp32 storage mode (no reference counterpart: the reference is fp64 only):
+// float cells in and out, fp64 arithmetic inside (fsx_solve_periodic_f32).
+inline std::vector<float> solve_periodic_f32(const GridShape& shape, const std::vector<float>& a0,
+                                             const StencilKernel& k, std::uint64_t T, StageTimings* st = nullptr) {
+    std::vector<float> out(a0.size());
+    const fsx_shape s = shape.c();
+    auto kv = k.c();
+    fsx_stage_timings t = detail::to_c(st);
+    check(fsx_solve_periodic_f32(&s, a0.data(), &kv.k, T, out.data(), nullptr, st ? &t : nullptr));
+    detail::from_c(t, st);
+    return out;
+}
+
 // Direct-stepping verifier on the GPU (oracle.hpp:15-20: step_periodic,
 // evolve_periodic_naive), bitwise equal to the reference loop.
 inline FieldGrid evolve_periodic_naive(const FieldGrid& a0, const StencilKernel& k, std::uint64_t T) {

@@ -48,7 +48,14 @@ int main(int argc, char** argv) {
     CHECK(throws<SpecError>([&] { solve_periodic_vector(a, k, 1); }));
     CHECK(throws<SpecError>([&] { StencilKernel(1).add_tap({0}, NAN); }));
     CHECK(throws<SpecError>([&] { solve_periodic(a, StencilKernel(1), 1); }));
+    // fp32 storage mode, T == 0: a bit-exact copy (no device)
+    const std::vector<float> a32 = {1.f, 2.f, 3.f, 4.f};
+    CHECK(solve_periodic_f32(GridShape({4}), a32, k, 0) == a32);
     if (gpu) {
+        // the Appendix step matrix in fp32 storage: [1,2,3,4] -> [-1,9,11,1]
+        const std::vector<float> o32 = solve_periodic_f32(GridShape({4}), a32, k, 1);
+        const float w32[4] = {-1, 9, 11, 1};
+        for (int i = 0; i < 4; ++i) CHECK(std::fabs(o32[i] - w32[i]) <= 1e-5f);
         const double want[4] = {-1, 9, 11, 1};
         FieldGrid out = solve_periodic(a, k, 1);
         for (int i = 0; i < 4; ++i) CHECK(std::fabs(out.data[i] - want[i]) <= 1e-12);
