@@ -44,6 +44,9 @@ UNIT = "cell-updates/s"
 FLUSH_BYTES = 256 << 20
 
 
+NOMINAL_HBM_GBS = 8000.0  # the north star's "~8 TB/s" denominator, reported beside the measured copy peak
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -507,13 +510,15 @@ def run_gpu(args, cfg):
             "peak": peak,
             "unit": "GB/s",
             "frac": (fused_gbs / peak) if fused_gbs else None,
+            "frac_vs_nominal_8tbs": (fused_gbs / NOMINAL_HBM_GBS) if fused_gbs else None,
             "traffic": load_traffic(cfg.name),
             "alg_bytes_per_launch": info["fused_bytes"],
             "kernel_ms": fms,
             "peak_source": peak_src,
             "fp64": load_fp64(cfg.name, fms),
         },
-        "pipeline": {"alg_bytes_per_step": alg_step, "achieved_gbs": pipe_gbs, "frac": pipe_gbs / peak},
+        "pipeline": {"alg_bytes_per_step": alg_step, "achieved_gbs": pipe_gbs, "frac": pipe_gbs / peak,
+                     "frac_vs_nominal_8tbs": pipe_gbs / NOMINAL_HBM_GBS},
         "gpu_launches": info["launches"] * args.steps,
         "host_enqueue_us": sorted(host_us)[len(host_us) // 2],
         "clocks": clocks,
