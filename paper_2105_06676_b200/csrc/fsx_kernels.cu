@@ -417,6 +417,51 @@ __device__ __forceinline__ void pair_mode0(const RowPairArgs& a, double2& zk, do
     if (k != 0) zp = cadd(cadd(yp, cyk), cmul_si<+1>(cmulc(csub(yp, cyk), wp)));
 }
 
+// pair_mode0 for a real (symmetric) symbol, four frequencies k at once (the
+// partners kp = M - k come with them): the phase reads of all four are issued
+// together and the eight powers run element-parallel with the warp-level
+// underflow skip, where pair_mode0 is one latency chain per frequency (cfg1's
+// row-pair pass ran at ~7 warps per SM on those chains).  With L = 2M,
+// cos(2 pi kp o / L) = (-1)^o cos(2 pi k o / L) and W_L^kp = -conj(W_L^k), so
+// the partners need no reads of their own.  k != 0 (the k = 0 / Nyquist pair
+// stays on pair_mode0).
+__device__ __forceinline__ void pair_mode0_real_x4(const RowPairArgs& a, double2 (&zk)[4], double2 (&zp)[4],
+                                                   const i64 (&k)[4], i64 M) {
+    const i64 L = 2 * M;
+    double2 wk[4];
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        wk[i] = phase_at(a.wk, k[i]);
+        x[i] = x[4 + i] = 0.0;
+    }
+    for (int j = 0; j < a.ntaps; ++j) {
+        const int o = a.tap_off[j];
+        const double b = a.tap_b[j][0], bp = (o & 1) ? -b : b;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double c = phase_at(a.wk, modp(k[i] * (i64)o, L)).x;
+            x[i] = fma(b, c, x[i]);
+            x[4 + i] = fma(bp, c, x[4 + i]);
+        }
+    }
+    pow_real_vec_skip<8, 4>(x, a.T, a.neg_mag2);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double2 cz = cconj(zp[i]);
+        const double2 e = cscale(cadd(zk[i], cz), 0.5);
+        const double2 od = cscale(cmul_si<-1>(csub(zk[i], cz)), 0.5);
+        const double2 wp = make_double2(-wk[i].x, wk[i].y);
+        const double2 xk = cadd(e, cmul(wk[i], od));
+        const double2 xp = cadd(cconj(e), cmul(wp, cconj(od)));
+        const double2 yk = cscale(xk, x[i] * a.scale);
+        const double2 yp = cscale(xp, x[4 + i] * a.scale);
+        const double2 cyp = cconj(yp), cyk = cconj(yk);
+        zk[i] = cadd(cadd(yk, cyp), cmul_si<+1>(cmulc(csub(yk, cyp), wk[i])));
+        zp[i] = cadd(cadd(yp, cyk), cmul_si<+1>(cmulc(csub(yp, cyk), wp)));
+    }
+}
+
 __device__ __forceinline__ void pair_mode1(const RowPairArgs& a, double2& zk, double2& zp, i64 k, i64 N) {
     const double2 cz = cconj(zp);
     const double2 u = cscale(cadd(zk, cz), 0.5);
@@ -573,6 +618,24 @@ k_rowpair(RowPairArgs a) {
     const int nth = blockDim.x;
     if (!self) {
         int cpos = threadIdx.x;
+        if (a.mode == 0 && a.real && nth >= 32) {  // four frequencies (+ partners) per step (full warps: vote)
+            for (; cpos + 3 * nth < N2; cpos += 4 * nth) {
+                double2 zk[4], zp[4];
+                i64 k[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    zk[i] = la[swz(cpos + i * nth)];
+                    zp[i] = lb[swz(N2 - 1 - (cpos + i * nth))];
+                    k[i] = ra + N1 * (cpos + i * nth);
+                }
+                pair_mode0_real_x4(a, zk, zp, k, M);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    la[swz(cpos + i * nth)] = zk[i];
+                    lb[swz(N2 - 1 - (cpos + i * nth))] = zp[i];
+                }
+            }
+        }
         if (a.mode == 1 && a.real) {  // two independent power chains per step
             for (; cpos + nth < N2; cpos += 2 * nth) {
                 double2 zk[2], zp[2];
