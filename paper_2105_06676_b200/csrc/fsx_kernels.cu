@@ -536,11 +536,12 @@ __device__ __forceinline__ void real_block_symbol(const RowPairArgs& a, i64 k, i
     }
 }
 
-__device__ __forceinline__ void pair_mode1_real_x2(const RowPairArgs& a, double2 (&zk)[2], double2 (&zp)[2],
-                                                   const i64 (&k)[2], i64 N) {
-    double l[2][4], acc[2][4];
+template <int NX>
+__device__ __forceinline__ void pair_mode1_real_xn(const RowPairArgs& a, double2 (&zk)[NX], double2 (&zp)[NX],
+                                                   const i64 (&k)[NX], i64 N) {
+    double l[NX][4], acc[NX][4];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NX; ++i) {
         real_block_symbol(a, k[i], N, l[i]);
         acc[i][0] = 1.0;
         acc[i][1] = 0.0;
@@ -551,7 +552,7 @@ __device__ __forceinline__ void pair_mode1_real_x2(const RowPairArgs& a, double2
     while (t) {
         if (t & 1) {
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
+            for (int i = 0; i < NX; ++i) {
                 const double b00 = fma(acc[i][0], l[i][0], acc[i][1] * l[i][2]), b01 = fma(acc[i][0], l[i][1], acc[i][1] * l[i][3]);
                 const double b10 = fma(acc[i][2], l[i][0], acc[i][3] * l[i][2]), b11 = fma(acc[i][2], l[i][1], acc[i][3] * l[i][3]);
                 acc[i][0] = b00;
@@ -563,7 +564,7 @@ __device__ __forceinline__ void pair_mode1_real_x2(const RowPairArgs& a, double2
         t >>= 1;
         if (t) {
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
+            for (int i = 0; i < NX; ++i) {
                 const double pp = l[i][1] * l[i][2], tr = l[i][0] + l[i][3];
                 const double s00 = fma(l[i][0], l[i][0], pp), s11 = fma(l[i][3], l[i][3], pp);
                 l[i][1] *= tr;
@@ -575,7 +576,7 @@ __device__ __forceinline__ void pair_mode1_real_x2(const RowPairArgs& a, double2
     }
     const double sc = a.scale;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NX; ++i) {
         const double2 cz = cconj(zp[i]);
         const double2 u = cscale(cadd(zk[i], cz), 0.5);
         const double2 vv = cscale(cmul_si<-1>(csub(zk[i], cz)), 0.5);
@@ -586,6 +587,9 @@ __device__ __forceinline__ void pair_mode1_real_x2(const RowPairArgs& a, double2
     }
 }
 
+#ifndef FSX_RP_NX
+#define FSX_RP_NX 4  // cfg5: 4 chains 1.85 ms vs 2 chains 1.90 ms (same box)
+#endif
 template <int N2>
 __global__ void __launch_bounds__(2 * Cfg<N2>::TPL)
 k_rowpair(RowPairArgs a) {
@@ -636,19 +640,19 @@ k_rowpair(RowPairArgs a) {
                 }
             }
         }
-        if (a.mode == 1 && a.real) {  // two independent power chains per step
-            for (; cpos + nth < N2; cpos += 2 * nth) {
-                double2 zk[2], zp[2];
-                i64 k[2];
+        if (a.mode == 1 && a.real) {  // FSX_RP_NX independent power chains per step
+            for (; cpos + (FSX_RP_NX - 1) * nth < N2; cpos += FSX_RP_NX * nth) {
+                double2 zk[FSX_RP_NX], zp[FSX_RP_NX];
+                i64 k[FSX_RP_NX];
 #pragma unroll
-                for (int i = 0; i < 2; ++i) {
+                for (int i = 0; i < FSX_RP_NX; ++i) {
                     zk[i] = la[swz(cpos + i * nth)];
                     zp[i] = lb[swz(N2 - 1 - (cpos + i * nth))];
                     k[i] = ra + N1 * (cpos + i * nth);
                 }
-                pair_mode1_real_x2(a, zk, zp, k, M);
+                pair_mode1_real_xn<FSX_RP_NX>(a, zk, zp, k, M);
 #pragma unroll
-                for (int i = 0; i < 2; ++i) {
+                for (int i = 0; i < FSX_RP_NX; ++i) {
                     la[swz(cpos + i * nth)] = zk[i];
                     lb[swz(N2 - 1 - (cpos + i * nth))] = zp[i];
                 }
