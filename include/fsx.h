@@ -76,7 +76,13 @@ typedef struct fsx_options {
     int32_t path;       /* 0 = auto (fused fast path when eligible), 1 = force general path */
     int32_t stage_events; /* device API: record CUDA events at the stage boundaries of each
                              solve (read back with fsx_last_stage_ms) */
-    int32_t reserved1;
+    int32_t spectral_cut; /* 1 = exact spectral cut (2D fused plan, explicit scalar solve): the
+                             columns kx whose multipliers lam^T all underflow to 0 (the same
+                             |lam|^T < 2^-1100 test the fused pass applies per element, bounded
+                             by sum_g |A_g(kx)| on the host) are neither stored by the forward
+                             rows nor transformed; the inverse rows read them as 0.  The result
+                             is bitwise the full solve's (those columns are exactly 0 there).
+                             Default 0: every column moves (the reference's work). */
     void* stream;       /* cudaStream_t to enqueue on (NULL = library stream) */
 } fsx_options;
 
@@ -253,6 +259,10 @@ typedef struct fsx_plan_info {
     int64_t fused_bytes;     /* algorithmic bytes of the dominant (fused) kernel */
     int64_t work_bytes;      /* device workspace of the plan */
 } fsx_plan_info;
+/* Columns the exact spectral cut keeps for this solve (kept <= total = L/2 + 1;
+ * kept == total when the cut does not apply: other plans, rank 3, T == 1, ...). */
+fsx_status fsx_spectral_cut_columns(const fsx_shape* shape, const fsx_kernel* k, uint64_t T, int64_t* kept,
+                                    int64_t* total);
 fsx_status fsx_plan_describe(const fsx_shape* shape, const fsx_kernel* k, const fsx_options* opt,
                              fsx_plan_info* info);
 

@@ -41,6 +41,7 @@ from .fftstencil import (  # noqa: F401
     solve_periodic_f32,
     solve_periodic_implicit,
     solve_periodic_vector,
+    spectral_cut_columns,
     spectrum_from_kernel,
     step_periodic,
 )

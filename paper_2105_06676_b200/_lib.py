@@ -61,7 +61,7 @@ class FsxOptions(ctypes.Structure):
         ("device", ctypes.c_int32),
         ("path", ctypes.c_int32),
         ("stage_events", ctypes.c_int32),
-        ("reserved1", ctypes.c_int32),
+        ("spectral_cut", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
     ]
 
@@ -110,6 +110,7 @@ EXPORTS = (
     "fsx_version",
     "fsx_device_count",
     "fsx_plan_describe",
+    "fsx_spectral_cut_columns",
 )
 
 _lib = None

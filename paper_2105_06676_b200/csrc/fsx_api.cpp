@@ -274,6 +274,11 @@ struct Plan {
     TableSet tables;
     // kind 1
     i64 L = 0, M = 0, P = 0, rows = 0;
+    // exact spectral cut (fsx_options.spectral_cut): kcut for (cut_taps, cut_T), cached
+    bool cut_valid = false;
+    Taps cut_taps;
+    u64 cut_T = 0;
+    i64 kcut = -1;
     fsx::AxisGeom ax1, ax0;
     alignas(64) unsigned char map0[128], map1[128];  // CUtensorMaps for TMA column passes
     alignas(64) unsigned char map2[128];             // parity-split view (8192-point halves pass)
@@ -680,6 +685,52 @@ fsx::FusedSymbol fused_symbol(const Plan& p, const Taps& taps, u64 T, const Taps
     return s;
 }
 
+// Exact spectral cut (2D fused plan, explicit scalar solve).  The fused pass
+// sets an element's multiplier to exactly 0 when |lam|^2 < neg_mag2 =
+// 2^(-2200/T) (|lam|^T < 2^-1100: below every representable contribution,
+// where the reference's own repeated squaring underflows).  With taps grouped
+// by their axis-0 offset O_g, lam(k0, kx) = sum_g A_g(kx) e^{2 pi i k0 O_g / n0},
+// so |lam(k0, kx)| <= B(kx) = sum_g |A_g(kx)| for every k0: a column with
+// B(kx)^2 below neg_mag2 (with a 1e-9 relative margin for the device's
+// rounding of lam) is exactly 0 after the fused pass in the full solve.
+// Returns the largest column that is not provably 0 (>= 0, so column 0 -- and
+// with it a non-finite input -- always goes through), or -1 when the cut does
+// not apply.  Columns above it are neither stored by the forward rows, nor
+// transformed, nor read by the inverse rows (which take them as 0).
+i64 compute_kcut(const Plan& p, const Taps& taps, u64 T) {
+    if (p.kind != kFusedR2C || p.dims.size() != 2 || p.m != 1 || !fsx::rows_f32_ok(p.L)) return -1;
+    const double neg = std::exp2(-2200.0 / (double)T);
+    if (!(neg > 0.0)) return -1;
+    const double thr = neg * (1.0 - 1e-9);
+    std::map<i64, std::vector<std::pair<i64, double>>> groups;  // O_g -> (o_last, c)
+    for (const auto& kv : taps.map) groups[kv.first[p.axes[0]]].push_back({kv.first[p.axes[1]], kv.second[0]});
+    const double w = 2.0 * 3.14159265358979323846 / (double)p.L;
+    for (i64 kx = p.M; kx > 0; --kx) {
+        double B = 0.0;
+        for (const auto& g : groups) {
+            double re = 0.0, im = 0.0;
+            for (const auto& oc : g.second) {
+                const i64 ph = ((kx * oc.first) % p.L + p.L) % p.L;  // exact integer phase
+                re += oc.second * std::cos(w * (double)ph);
+                im += oc.second * std::sin(w * (double)ph);
+            }
+            B += std::sqrt(re * re + im * im);
+        }
+        if (B * B >= thr) return kx;
+    }
+    return 0;
+}
+
+i64 plan_kcut(Plan& p, const Taps& taps, u64 T) {
+    if (!(p.cut_valid && p.cut_T == T && p.cut_taps.map == taps.map)) {
+        p.kcut = compute_kcut(p, taps, T);
+        p.cut_taps = taps;
+        p.cut_T = T;
+        p.cut_valid = true;
+    }
+    return p.kcut;
+}
+
 // The implicit solve fuses into plan 1 when the symbol is real and the fused
 // pass is the TMA column kernel that precomputes its multipliers (N <= 4096).
 bool implicit_fusable(const Plan& p, const Taps& s, const Taps& q) {
@@ -834,14 +885,18 @@ struct Stamps {
 // floats directly instead of d_a0 / d_out.
 void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, const double* d_a0, double* d_out,
               cudaStream_t st, Stamps& sp, fsx::Flags* flags_at = nullptr, const float* fin = nullptr,
-              float* fout = nullptr) {
+              float* fout = nullptr, bool cut = false) {
     fsx::Flags* flags = flags_at ? flags_at : dev.flags.as<fsx::Flags>();
     const double2* tw = dev.tw_all.as<double2>();
     const int r = (int)p.dims.size();
     sp.mark();
     if (p.kind == kFusedR2C) {
         double2* H = p.work.as<double2>();
-        const fsx::RowLayout lay{p.P, 0, p.rows};
+        fsx::RowLayout lay{p.P, 0, p.rows};
+        const i64 kcut = (cut && !q) ? plan_kcut(p, taps, T) : -1;
+        lay.kcut = kcut;
+        fsx::AxisGeom ax0 = p.ax0;  // the fused pass covers columns 0..kcut only
+        if (kcut >= 0) ax0.ncols = kcut + 1;
         if (fin) FSX_CK(fsx::launch_r2c_rows_f32(fin, H, p.rows, p.L, lay, tw, st));
         else FSX_CK(fsx::launch_r2c_rows(d_a0, H, p.rows, p.L, lay, tw, st));
         fsx::StepTwiddle none;
@@ -856,9 +911,9 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
             FSX_CK(cudaMemsetAsync(p.qmax.p, 0, 8, st));
             FSX_CK(fsx::launch_fused_qmax(sym, p.ax0.ncols, p.qmax.as<unsigned long long>(), tw, st));
         }
-        if (p.halves) FSX_CK(fsx::launch_fused_halves(p.map2, p.ax0, sym, tw, st));
-        else if (p.tma0) FSX_CK(fsx::launch_cols_tma(p.map0, p.ax0, 2, sym, tw, st));
-        else FSX_CK(fsx::launch_fused_r2c(H, p.ax0, sym, tw, st));
+        if (p.halves) FSX_CK(fsx::launch_fused_halves(p.map2, ax0, sym, tw, st));
+        else if (p.tma0) FSX_CK(fsx::launch_cols_tma(p.map0, ax0, 2, sym, tw, st));
+        else FSX_CK(fsx::launch_fused_r2c(H, ax0, sym, tw, st));
         sp.mark();
         if (r == 3) {
             if (p.tma1) FSX_CK(fsx::launch_cols_tma(p.map1, p.ax1, 1, nosym, tw, st));
@@ -1173,17 +1228,18 @@ void evolve_naive(const fsx_shape* shape, const double* a0, const fsx_kernel* k,
 // writes the floats in its row passes; the other plans widen into / narrow out
 // of their fp64 buffers (the narrowing flags values outside the float range).
 void run_plan_f32(Plan& p, Device& dev, const Taps& taps, u64 T, const float* fin, float* fout, cudaStream_t st,
-                  Stamps& sp, fsx::Flags* flags_at = nullptr) {
+                  Stamps& sp, fsx::Flags* flags_at = nullptr, bool cut = false) {
     const auto a16 = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 15) == 0; };
     if (p.kind == kFusedR2C && fsx::rows_f32_ok(p.L) && a16(fin) && a16(fout)) {
-        run_plan(p, dev, taps, nullptr, T, nullptr, nullptr, st, sp, flags_at, fin, fout);
+        run_plan(p, dev, taps, nullptr, T, nullptr, nullptr, st, sp, flags_at, fin, fout, cut);
         return;
     }
     const i64 n = p.cells * p.m;
     p.d_in.ensure((size_t)n * 8);
     p.d_out.ensure((size_t)n * 8);
     FSX_CK(fsx::launch_widen(fin, p.d_in.as<double>(), n, st));
-    run_plan(p, dev, taps, nullptr, T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp, flags_at);
+    run_plan(p, dev, taps, nullptr, T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp, flags_at, nullptr, nullptr,
+             cut);
     FSX_CK(fsx::launch_narrow(p.d_out.as<double>(), fout, n, flags_at ? flags_at : dev.flags.as<fsx::Flags>(), st));
 }
 
@@ -1242,14 +1298,15 @@ void solve(const SolveReq& rq) {
         return;
     }
     const int force_general = rq.opt && rq.opt->path == 1;
+    const bool cut = rq.opt && rq.opt->spectral_cut;
     Plan* pp = &get_plan(dev, s, taps, force_general);
     if (rq.q && !implicit_fusable(*pp, taps, qtaps)) pp = &get_plan(dev, s, taps, 1);
     Plan& p = *pp;
     if (rq.q && p.kind == kFusedR2C) p.qmax.ensure(8);
     Stamps sp{&dev, rq.st != nullptr || (rq.device_ptrs && rq.opt && rq.opt->stage_events), st};
     if (rq.device_ptrs) {
-        if (f32) run_plan_f32(p, dev, taps, rq.T, rq.a0f, rq.outf, st, sp);
-        else run_plan(p, dev, taps, rq.q ? &qtaps : nullptr, rq.T, rq.a0, rq.out, st, sp);
+        if (f32) run_plan_f32(p, dev, taps, rq.T, rq.a0f, rq.outf, st, sp, nullptr, cut);
+        else run_plan(p, dev, taps, rq.q ? &qtaps : nullptr, rq.T, rq.a0, rq.out, st, sp, nullptr, nullptr, nullptr, cut);
         return;
     }
     DevBuf& bin = f32 ? p.f_in : p.d_in;
@@ -1259,8 +1316,9 @@ void solve(const SolveReq& rq) {
     cudaEvent_t h0 = dev.ev[6], h1 = dev.ev[7];
     if (sp.on) FSX_CK(cudaEventRecord(h0, st));
     FSX_CK(cudaMemcpyAsync(bin.p, in, bytes, cudaMemcpyHostToDevice, st));
-    if (f32) run_plan_f32(p, dev, taps, rq.T, p.f_in.as<float>(), p.f_out.as<float>(), st, sp);
-    else run_plan(p, dev, taps, rq.q ? &qtaps : nullptr, rq.T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp);
+    if (f32) run_plan_f32(p, dev, taps, rq.T, p.f_in.as<float>(), p.f_out.as<float>(), st, sp, nullptr, cut);
+    else run_plan(p, dev, taps, rq.q ? &qtaps : nullptr, rq.T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp,
+                  nullptr, nullptr, nullptr, cut);
     FSX_CK(cudaMemcpyAsync(out, bout.p, bytes, cudaMemcpyDeviceToHost, st));
     if (sp.on) FSX_CK(cudaEventRecord(h1, st));
     check_flags(dev, p.kind, st);
@@ -1307,6 +1365,7 @@ void solve_batch(const fsx_shape* shape, i64 nb, const TE* const* a0s, const fsx
     std::lock_guard<std::mutex> lk(g_mu);
     Device& dev = device_for(opt ? opt->device : 0);
     const int force_general = opt && opt->path == 1;
+    const bool cut = opt && opt->spectral_cut;
     Plan* pl[2];
     for (int l = 0; l < 2; ++l) {
         if (!dev.lanes[l]) {
@@ -1335,8 +1394,9 @@ void solve_batch(const fsx_shape* shape, i64 nb, const TE* const* a0s, const fsx
         DevBuf& bin = f32 ? p.f_in : p.d_in;
         DevBuf& bout = f32 ? p.f_out : p.d_out;
         FSX_CK(cudaMemcpyAsync(bin.p, a0s[i], bytes, cudaMemcpyHostToDevice, st));
-        if constexpr (f32) run_plan_f32(p, dev, taps, T, p.f_in.as<float>(), p.f_out.as<float>(), st, sp, fl + i);
-        else run_plan(p, dev, taps, nullptr, T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp, fl + i);
+        if constexpr (f32) run_plan_f32(p, dev, taps, T, p.f_in.as<float>(), p.f_out.as<float>(), st, sp, fl + i, cut);
+        else run_plan(p, dev, taps, nullptr, T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp, fl + i, nullptr,
+                      nullptr, cut);
         FSX_CK(cudaMemcpyAsync(outs[i], bout.p, bytes, cudaMemcpyDeviceToHost, st));
     }
     std::vector<fsx::Flags> h((size_t)nb);
@@ -1607,6 +1667,22 @@ fsx_status fsx_slab_inverse_p2p(const fsx_shape* global, int32_t nranks, int32_t
         fsx::RowLayout lay{0, sp.CB, sp.n0l, reinterpret_cast<double2* const*>(d_recv_peers), (i64)rank * sp.n0l};
         FSX_CK(fsx::launch_c2r_rows(nullptr, d_local_out, sp.n0l, sp.L, lay, dev.tw_all.as<double2>(),
                                     dev.flags.as<fsx::Flags>(), stream_of(dev, opt)));
+    });
+}
+
+fsx_status fsx_spectral_cut_columns(const fsx_shape* shape, const fsx_kernel* k, uint64_t T, int64_t* kept,
+                                    int64_t* total) {
+    return guarded([&] {
+        const Shape s = parse_shape(shape);
+        const Taps taps = parse_kernel(k);
+        require_fits(taps, s);
+        std::lock_guard<std::mutex> lk(g_mu);
+        Device& dev = device_for(0);
+        Plan& p = get_plan(dev, s, taps, 0);
+        const i64 all = p.kind == kFusedR2C ? p.M + 1 : 0;
+        const i64 kc = T == 0 ? -1 : plan_kcut(p, taps, T);
+        if (kept) *kept = kc >= 0 ? kc + 1 : all;
+        if (total) *total = all;
     });
 }
 

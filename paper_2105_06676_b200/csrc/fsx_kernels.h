@@ -112,6 +112,7 @@ struct RowLayout {
     i64 nrows = 0;
     double2* const* peers = nullptr;
     i64 row_off = 0;
+    i64 kcut = -1;  // exact spectral cut: only columns k <= kcut are stored / loaded (-1: all)
     // (k and blk < 2^31: 32-bit division, the 64-bit one is a long software sequence)
     __host__ __device__ i64 at(i64 row, i64 k) const {
         if (blk == 0) return row * P + k;

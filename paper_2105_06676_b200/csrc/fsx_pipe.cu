@@ -229,8 +229,8 @@ k_r2c_bulk(const TI* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, 
                     const double2 zm = cconj(t == 0 ? v[qz] : v[qp]);
                     const double2 e = cscale(cadd(zk, zm), 0.5);
                     const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
-                    h(j + u * (M / 8)) = cadd(e, cmul(cmul_const<u, 16, -1>(wj), od));
-                    if (i == 0 && u == 0 && t == 0) h(M) = make_double2(zk.x - zk.y, 0.0);
+                    if (lay.kcut < 0 || j + u * (M / 8) <= lay.kcut) h(j + u * (M / 8)) = cadd(e, cmul(cmul_const<u, 16, -1>(wj), od));
+                    if (i == 0 && u == 0 && t == 0 && (lay.kcut < 0 || lay.kcut >= M)) h(M) = make_double2(zk.x - zk.y, 0.0);
                 });
             }
         } else {
@@ -246,8 +246,8 @@ k_r2c_bulk(const TI* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, 
                 const double2 zm = cconj(line[swz((M - k) & (M - 1))]);
                 const double2 e = cscale(cadd(zk, zm), 0.5);
                 const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
-                h(k) = cadd(e, cmul(cmul_const<q, 32, -1>(wt), od));
-                if (k == 0) h(M) = make_double2(zk.x - zk.y, 0.0);
+                if (lay.kcut < 0 || k <= lay.kcut) h(k) = cadd(e, cmul(cmul_const<q, 32, -1>(wt), od));
+                if (k == 0 && (lay.kcut < 0 || lay.kcut >= M)) h(M) = make_double2(zk.x - zk.y, 0.0);
             });
         }
         fence_proxy_async();  // generic writes of this stage before its next bulk fill
@@ -266,9 +266,10 @@ k_r2c_bulk(const TI* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, 
 template <int M, bool BLK>
 __device__ __forceinline__ void load_hrow(double2* dst, const double2* H, const RowLayout& lay, i64 row,
                                           unsigned long long* bar) {
-    mbar_expect_tx(bar, (M + 1) * (unsigned)sizeof(double2));
+    const unsigned nk = (unsigned)(BLK || lay.kcut < 0 || lay.kcut >= M ? M + 1 : lay.kcut + 1);
+    mbar_expect_tx(bar, nk * (unsigned)sizeof(double2));
     if constexpr (!BLK) {
-        bulk_load(dst, H + row * lay.P, (M + 1) * (unsigned)sizeof(double2), bar);
+        bulk_load(dst, H + row * lay.P, nk * (unsigned)sizeof(double2), bar);
     } else {
         for (i64 k0 = 0; k0 <= M; k0 += lay.blk) {
             const i64 len = (M + 1 - k0) < lay.blk ? (M + 1 - k0) : lay.blk;
@@ -308,6 +309,10 @@ k_c2r_bulk(const double2* __restrict__ H, TO* __restrict__ x, i64 nrows, i64 L, 
         mbar_wait(&bar[s], (par >> s) & 1u);
         par ^= 1u << s;
         double2* line = sm + s * SS;
+        if (!BLK && lay.kcut >= 0 && lay.kcut < M) {  // exact spectral cut: the dropped columns are 0
+            for (i64 k = lay.kcut + 1 + t; k <= M; k += TPL) line[k] = make_double2(0.0, 0.0);
+            __syncthreads();
+        }
         double2 v[R];
         // split twiddle W_L^(t + q M/16) = W_L^t * W_32^q: one load per thread
         const double2 wt = __ldg(tw_all + 2 * M + t);

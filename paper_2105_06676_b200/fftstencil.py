@@ -302,15 +302,15 @@ CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the NULL stream's explicit handle
 _OPTS: dict = {}  # option structs are read-only for the library: reuse them
 
 
-def _opts(device: int = 0, path: int = 0, stream: int | None = None, stage_events: int = 0):
+def _opts(device: int = 0, path: int = 0, stream: int | None = None, stage_events: int = 0, spectral_cut: int = 0):
     """fsx_options.  stream None -> the library's own stream; a handle of 0
     (torch's default stream) is passed as cudaStreamLegacy so the work is
     ordered with the caller's NULL-stream work instead of the library stream."""
-    key = (device, path, stream, stage_events)
+    key = (device, path, stream, stage_events, spectral_cut)
     o = _OPTS.get(key)
     if o is None:
         o = _lib.FsxOptions()
-        o.device, o.path, o.stage_events = device, path, stage_events
+        o.device, o.path, o.stage_events, o.spectral_cut = device, path, stage_events, int(bool(spectral_cut))
         o.stream = None if stream is None else (stream or CUDA_STREAM_LEGACY)
         if len(_OPTS) > 256:
             _OPTS.clear()
@@ -319,7 +319,8 @@ def _opts(device: int = 0, path: int = 0, stream: int | None = None, stage_event
 
 
 # ---------------------------------------------------------------- solvers
-def _solve(fn, a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None, path: int, extra=(), out=None):
+def _solve(fn, a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None, path: int, extra=(), out=None,
+           spectral_cut: int = 0):
     L = _lib.load()
     if T < 0 or T >= 1 << 64:
         raise SpecError("T must be a nonnegative 64-bit integer")
@@ -332,7 +333,8 @@ def _solve(fn, a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None,
     stc = st._push() if st is not None else None
     status = getattr(L, fn)(ctypes.byref(shape_c), a0.data.ctypes.data_as(_DP), ctypes.byref(kc),
                             ctypes.c_uint64(int(T)), *extra, out.ctypes.data_as(_DP),
-                            ctypes.byref(_opts(path=path)), ctypes.byref(stc) if stc is not None else None)
+                            ctypes.byref(_opts(path=path, spectral_cut=spectral_cut)),
+                            ctypes.byref(stc) if stc is not None else None)
     del keep
     _lib.check(status)
     if st is not None:
@@ -341,10 +343,11 @@ def _solve(fn, a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None,
 
 
 def solve_periodic(a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None = None, *, path: int = 0,
-                   out: np.ndarray | None = None):
+                   out: np.ndarray | None = None, spectral_cut: int = 0):
     """proj/src/periodic.cpp:76-86 on the B200 path (fsx_solve_periodic).
-    ``out`` optionally supplies the (e.g. pinned) host array the result is written to."""
-    return _solve("fsx_solve_periodic", a0, k, T, st, path, out=out)
+    ``out`` optionally supplies the (e.g. pinned) host array the result is written to.
+    ``spectral_cut=1``: the exact spectral cut (fsx_options.spectral_cut; same result)."""
+    return _solve("fsx_solve_periodic", a0, k, T, st, path, out=out, spectral_cut=spectral_cut)
 
 
 def solve_periodic_vector(a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None = None, *, path: int = 0):
@@ -389,7 +392,7 @@ def solve_periodic_implicit(q: StencilKernel, s: StencilKernel, a0: FieldGrid, T
     return FieldGrid(a0.shape, out)
 
 
-def solve_periodic_batch(a0s, k: StencilKernel, T: int, outs=None) -> list:
+def solve_periodic_batch(a0s, k: StencilKernel, T: int, outs=None, spectral_cut: int = 0) -> list:
     """Pipelined batch of independent solves (fsx_solve_periodic_batch): one
     shape, kernel and T for every grid.  ``a0s`` are FieldGrids; ``outs``
     optionally supplies the host result arrays (pinned for full H2D/D2H
@@ -417,14 +420,15 @@ def solve_periodic_batch(a0s, k: StencilKernel, T: int, outs=None) -> list:
     L = _lib.load()
     kc, keep = k._c()
     status = L.fsx_solve_periodic_batch(ctypes.byref(shape._c()), ctypes.c_int64(n), ins, ctypes.byref(kc),
-                                        ctypes.c_uint64(int(T)), ous, ctypes.byref(_opts()))
+                                        ctypes.c_uint64(int(T)), ous, ctypes.byref(_opts(spectral_cut=spectral_cut)))
     del keep
     _lib.check(status)
     return outs
 
 
 def solve_periodic_device(shape: GridShape, d_a0: int, k: StencilKernel, T: int, d_out: int,
-                          stream: int | None = None, device: int = 0, path: int = 0, stage_events: int = 0) -> None:
+                          stream: int | None = None, device: int = 0, path: int = 0, stage_events: int = 0,
+                          spectral_cut: int = 0) -> None:
     """Device-resident solve (fsx_solve_periodic_device): pointers are CUDA
     device addresses (e.g. ``tensor.data_ptr()``); enqueued on ``stream``.
     Call :func:`device_check` to synchronize and surface NumericError."""
@@ -433,7 +437,7 @@ def solve_periodic_device(shape: GridShape, d_a0: int, k: StencilKernel, T: int,
     kc, keep = k._c()
     status = L.fsx_solve_periodic_device(ctypes.byref(shape_c), ctypes.c_void_p(d_a0), ctypes.byref(kc),
                                          ctypes.c_uint64(int(T)), ctypes.c_void_p(d_out),
-                                         ctypes.byref(_opts(device, path, stream, stage_events)))
+                                         ctypes.byref(_opts(device, path, stream, stage_events, spectral_cut)))
     del keep
     _lib.check(status)
 
@@ -551,6 +555,17 @@ def last_stage_ms(device: int = 0) -> list:
 
 def device_check(stream: int | None = None, device: int = 0) -> None:
     _lib.check(_lib.load().fsx_device_check(ctypes.byref(_opts(device, 0, stream))))
+
+
+def spectral_cut_columns(shape: GridShape, k: StencilKernel, T: int) -> tuple:
+    """(kept, total) half-spectrum columns of the exact spectral cut for this solve
+    (fsx_spectral_cut_columns; kept == total where the cut does not apply)."""
+    kc, keep = k._c()
+    kept, total = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.load().fsx_spectral_cut_columns(ctypes.byref(shape._c()), ctypes.byref(kc), ctypes.c_uint64(int(T)),
+                                                    ctypes.byref(kept), ctypes.byref(total)))
+    del keep
+    return kept.value, total.value
 
 
 def plan_describe(shape: GridShape, k: StencilKernel, path: int = 0) -> dict:
