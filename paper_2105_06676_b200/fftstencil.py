@@ -453,7 +453,7 @@ def _f32(a, n: int, what: str) -> np.ndarray:
 
 
 def solve_periodic_f32(shape: GridShape, a0: np.ndarray, k: StencilKernel, T: int, st: StageTimings | None = None,
-                       *, path: int = 0, out: np.ndarray | None = None) -> np.ndarray:
+                       *, path: int = 0, out: np.ndarray | None = None, spectral_cut: int = 0) -> np.ndarray:
     """fp32 storage mode (fsx_solve_periodic_f32): float32 grid in and out,
     fp64 arithmetic inside; the north star's optional fp32 mode (<= 1e-4
     relative L2 vs the fp64 reference; the result is the fp64 solve of the
@@ -467,7 +467,8 @@ def solve_periodic_f32(shape: GridShape, a0: np.ndarray, k: StencilKernel, T: in
     kc, keep = k._c()
     stc = st._push() if st is not None else None
     status = L.fsx_solve_periodic_f32(ctypes.byref(shape._c()), a0.ctypes.data_as(_FP), ctypes.byref(kc),
-                                      ctypes.c_uint64(int(T)), out.ctypes.data_as(_FP), ctypes.byref(_opts(path=path)),
+                                      ctypes.c_uint64(int(T)), out.ctypes.data_as(_FP),
+                                      ctypes.byref(_opts(path=path, spectral_cut=spectral_cut)),
                                       ctypes.byref(stc) if stc is not None else None)
     del keep
     _lib.check(status)
@@ -476,7 +477,7 @@ def solve_periodic_f32(shape: GridShape, a0: np.ndarray, k: StencilKernel, T: in
     return out
 
 
-def solve_periodic_batch_f32(shape: GridShape, a0s, k: StencilKernel, T: int, outs=None) -> list:
+def solve_periodic_batch_f32(shape: GridShape, a0s, k: StencilKernel, T: int, outs=None, spectral_cut: int = 0) -> list:
     """Pipelined batch in the fp32 storage mode (fsx_solve_periodic_batch_f32)."""
     if T < 0 or T >= 1 << 64:
         raise SpecError("T must be a nonnegative 64-bit integer")
@@ -493,21 +494,22 @@ def solve_periodic_batch_f32(shape: GridShape, a0s, k: StencilKernel, T: int, ou
     L = _lib.load()
     kc, keep = k._c()
     status = L.fsx_solve_periodic_batch_f32(ctypes.byref(shape._c()), ctypes.c_int64(m), pi, ctypes.byref(kc),
-                                            ctypes.c_uint64(int(T)), po, ctypes.byref(_opts()))
+                                            ctypes.c_uint64(int(T)), po, ctypes.byref(_opts(spectral_cut=spectral_cut)))
     del keep
     _lib.check(status)
     return outs
 
 
 def solve_periodic_device_f32(shape: GridShape, d_a0: int, k: StencilKernel, T: int, d_out: int,
-                              stream: int | None = None, device: int = 0, path: int = 0, stage_events: int = 0) -> None:
+                              stream: int | None = None, device: int = 0, path: int = 0, stage_events: int = 0,
+                              spectral_cut: int = 0) -> None:
     """Device-resident fp32 storage mode (fsx_solve_periodic_device_f32):
     float32 device buffers; asynchronous like :func:`solve_periodic_device`."""
     L = _lib.load()
     kc, keep = k._c()
     status = L.fsx_solve_periodic_device_f32(ctypes.byref(shape._c()), ctypes.c_void_p(d_a0), ctypes.byref(kc),
                                              ctypes.c_uint64(int(T)), ctypes.c_void_p(d_out),
-                                             ctypes.byref(_opts(device, path, stream, stage_events)))
+                                             ctypes.byref(_opts(device, path, stream, stage_events, spectral_cut)))
     del keep
     _lib.check(status)
 

@@ -97,3 +97,14 @@ def test_cut_nonfinite_and_batch(orc):
     outs = fs.solve_periodic_batch([g, g, g], k, 10000, spectral_cut=1)
     for o in outs:
         assert np.array_equal(o, one)
+
+
+def test_cut_f32_storage_mode(orc):
+    """The cut composes with the fp32 storage mode (float rows, same columns)."""
+    dims = [1024, 2048]
+    k = K(R.kern_from(JACOBI, 2))
+    a32 = orc.splitmix_fill(9, 1024 * 2048, False).astype(np.float32)
+    full = fs.solve_periodic_f32(fs.GridShape(dims), a32, k, 20000)
+    cut = fs.solve_periodic_f32(fs.GridShape(dims), a32, k, 20000, spectral_cut=1)
+    assert np.array_equal(full, cut)
+    assert fs.spectral_cut_columns(fs.GridShape(dims), k, 20000)[0] < 1025
