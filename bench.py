@@ -430,7 +430,7 @@ def run_gpu(args, cfg):
     # headline, which keeps the reference's full work.  Same steps, same flush;
     # the result must equal the full solve bit for bit.
     cut_line = None
-    if info["path"] == 1 and len(cfg.dims) == 2 and not f32 and ws == 1:
+    if info["path"] == 1 and len(cfg.dims) == 2 and not f32 and ws == 1 and not args.no_cut:
         kept, total = fs.spectral_cut_columns(shape, kern, cfg.T)
         full_out = d_out.clone()
         with torch.cuda.stream(stream):
@@ -595,6 +595,7 @@ def main():
                     help="slab exchange for N > 1: p2p = fused into the row kernels over NVLink peer memory "
                          "(2D; auto falls back to nccl if symmetric memory is unavailable)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cut", action="store_true", help="skip the spectral_cut measurement (profiling runs)")
     ap.add_argument("--precision", type=int, choices=[64, 32], default=64,
                     help="32: the fp32 storage mode (float grids in/out, fp64 arithmetic; single GPU)")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of slabs")
