@@ -946,10 +946,12 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
             tB.kmul = p.N1a;
             tB.omul = 1;
             tB.tab = p.tables.get(p.t_M);
-            FSX_CK(fsx::launch_axis_pow2(z0, z, gA, -1, tA, tw, st));
+            if (fin) FSX_CK(fsx::launch_axis_f32(fin, z, gA, -1, tA, tw, st, nullptr));
+            else FSX_CK(fsx::launch_axis_pow2(z0, z, gA, -1, tA, tw, st));
             FSX_CK(fsx::launch_axis_pow2(z, z, gB, -1, tB, tw, st));
         } else if (p.N1 > 1) {
-            FSX_CK(fsx::launch_axis_pow2(z0, z, p.colg, -1, tf, tw, st));
+            if (fin) FSX_CK(fsx::launch_axis_f32(fin, z, p.colg, -1, tf, tw, st, nullptr));
+            else FSX_CK(fsx::launch_axis_pow2(z0, z, p.colg, -1, tf, tw, st));
         }
         sp.mark();
         const fsx::RowPairArgs a = rowpair_args(p, taps, T, z, dev);
@@ -962,9 +964,11 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
             tA.mode = 2;
             tB.mode = 2;
             FSX_CK(fsx::launch_axis_pow2(z, z, gB, +1, tB, tw, st));
-            FSX_CK(fsx::launch_axis_pow2(z, z, gA, +1, tA, tw, st, flags));
+            if (fout) FSX_CK(fsx::launch_axis_f32(z, fout, gA, +1, tA, tw, st, flags));
+            else FSX_CK(fsx::launch_axis_pow2(z, z, gA, +1, tA, tw, st, flags));
         } else if (p.N1 > 1) {
-            FSX_CK(fsx::launch_axis_pow2(z, z, p.colg, +1, ti, tw, st, flags));
+            if (fout) FSX_CK(fsx::launch_axis_f32(z, fout, p.colg, +1, ti, tw, st, flags));
+            else FSX_CK(fsx::launch_axis_pow2(z, z, p.colg, +1, ti, tw, st, flags));
         } else {
             FSX_CK(fsx::launch_finite_check(d_out, p.cells * p.m, flags, st));
         }
@@ -1235,6 +1239,17 @@ void run_plan_f32(Plan& p, Device& dev, const Taps& taps, u64 T, const float* fi
         return;
     }
     const i64 n = p.cells * p.m;
+    // 1D plan: the first / last column pass reads / writes the floats (strided
+    // route, column length <= 256: the split passes of the large 1D grids);
+    // the plan's complex work buffer is d_out
+    if (p.kind == kRowPair1D && (reinterpret_cast<uintptr_t>(fin) & 7) == 0 &&
+        (reinterpret_cast<uintptr_t>(fout) & 7) == 0 &&
+        (p.N1a ? fsx::axis_f32_ok(fsx::AxisGeom{p.N1a, p.N1b * p.N2, 1, p.Mc, p.N1b * p.N2})
+               : (p.N1 > 1 && fsx::axis_f32_ok(p.colg)))) {
+        p.d_out.ensure((size_t)n * 8);
+        run_plan(p, dev, taps, nullptr, T, nullptr, p.d_out.as<double>(), st, sp, flags_at, fin, fout, cut);
+        return;
+    }
     p.d_in.ensure((size_t)n * 8);
     p.d_out.ensure((size_t)n * 8);
     FSX_CK(fsx::launch_widen(fin, p.d_in.as<double>(), n, st));

@@ -164,10 +164,21 @@ k_contig(const double2* in, double2* out, i64 nlines, i64 pitch, const double2* 
     }
 }
 
+// fp64 <-> fp32 storage-mode element conversions (widen exactly, narrow to nearest)
+__device__ __forceinline__ double2 to_d2(double2 a) { return a; }
+__device__ __forceinline__ double2 to_d2(float2 a) { return make_double2(a.x, a.y); }
+template <class TO>
+__device__ __forceinline__ TO from_d2(double2 a) {
+    if constexpr (sizeof(TO) == 16) return a;
+    else return make_float2((float)a.x, (float)a.y);
+}
+
 // Strided lines: W adjacent columns per CTA, the axis in shared memory.
-template <int N, int SIGN, int TWM>
+// TI / TO = float2: the fp32 storage mode's first / last pass of the 1D plan
+// (the column pass reads the float grid, or writes it), fp64 arithmetic.
+template <int N, int SIGN, int TWM, class TI = double2, class TO = double2>
 __global__ void __launch_bounds__(Cfg<N>::W * Cfg<N>::TPL, Cfg<N>::MINB_W)
-k_strided(const double2* in, double2* out, AxisGeom g, StepTwiddle st, const double2* __restrict__ tw_all,
+k_strided(const TI* in, TO* out, AxisGeom g, StepTwiddle st, const double2* __restrict__ tw_all,
           Flags* flags) {
     using C = Cfg<N>;
     using F = LineFFT<N, SIGN>;
@@ -181,7 +192,7 @@ k_strided(const double2* in, double2* out, AxisGeom g, StepTwiddle st, const dou
     double2 v[C::R];
 #pragma unroll
     for (int q = 0; q < C::R; ++q)
-        v[q] = ok ? in[base + (i64)(t + q * C::TPL) * g.inner] : make_double2(0.0, 0.0);
+        v[q] = ok ? to_d2(in[base + (i64)(t + q * C::TPL) * g.inner]) : make_double2(0.0, 0.0);
     // four-step twiddle W^(b (k kmul + o omul)) for k = t + q TPL: the
     // exponents of one thread form an arithmetic progression in q, so two
     // table reads (base, ratio) and a running product replace 16 two-level
@@ -208,15 +219,55 @@ k_strided(const double2* in, double2* out, AxisGeom g, StepTwiddle st, const dou
             tq = cmul(tq, tr);
         }
     }
-    if (ok) {
+    bool bad = false;
 #pragma unroll
-        for (int q = 0; q < C::R; ++q) out[base + (i64)(t + q * C::TPL) * g.inner] = v[q];
+    for (int q = 0; q < C::R; ++q) {
+        const TO r = from_d2<TO>(v[q]);
+        if (ok) out[base + (i64)(t + q * C::TPL) * g.inner] = r;
+        bad |= ok && (!isfinite(r.x) || !isfinite(r.y));
     }
-    if (flags) {  // last pass of a solve: the non-finite scan rides along (realize_checked)
-        bool bad = false;
-#pragma unroll
-        for (int q = 0; q < C::R; ++q) bad |= ok && (!isfinite(v[q].x) || !isfinite(v[q].y));
-        flag_nonfinite(bad, flags);
+    if (flags) flag_nonfinite(bad, flags);  // last pass of a solve: the non-finite scan rides along (realize_checked)
+}
+
+// fp32 storage mode, 1D plan: the first forward column pass reading the float
+// grid (SIGN -1, post-twiddle) and the last inverse one writing it (SIGN +1,
+// pre-twiddle, non-finite scan), for the strided route (N <= 256).
+template <int N>
+static cudaError_t axis_f32_n(const void* in, void* out, const AxisGeom& g, int sign, const StepTwiddle& st,
+                              const double2* tw, cudaStream_t s, Flags* flags) {
+    using C = Cfg<N>;
+    const size_t smem = (size_t)C::W * C::LSW * sizeof(double2);
+    const i64 blocks = g.outer * ((g.ncols + C::W - 1) / C::W);
+    if (sign < 0 && st.mode == 1) {
+        auto kf = k_strided<N, -1, 1, float2, double2>;
+        kernel_prepare((const void*)kf, smem);
+        kf<<<(unsigned)blocks, C::W * C::TPL, smem, s>>>(static_cast<const float2*>(in), static_cast<double2*>(out), g,
+                                                        st, tw, flags);
+    } else if (sign > 0 && st.mode == 2) {
+        auto kf = k_strided<N, +1, 2, double2, float2>;
+        kernel_prepare((const void*)kf, smem);
+        kf<<<(unsigned)blocks, C::W * C::TPL, smem, s>>>(static_cast<const double2*>(in), static_cast<float2*>(out), g,
+                                                        st, tw, flags);
+    } else {
+        return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+bool axis_f32_ok(const AxisGeom& g) { return g.inner > 1 && g.n >= 2 && g.n <= 256 && (g.n & (g.n - 1)) == 0; }
+
+cudaError_t launch_axis_f32(const void* in, void* out, const AxisGeom& g, int sign, const StepTwiddle& st,
+                            const double2* tw, cudaStream_t s, Flags* flags) {
+    switch (g.n) {
+        case 2: return axis_f32_n<2>(in, out, g, sign, st, tw, s, flags);
+        case 4: return axis_f32_n<4>(in, out, g, sign, st, tw, s, flags);
+        case 8: return axis_f32_n<8>(in, out, g, sign, st, tw, s, flags);
+        case 16: return axis_f32_n<16>(in, out, g, sign, st, tw, s, flags);
+        case 32: return axis_f32_n<32>(in, out, g, sign, st, tw, s, flags);
+        case 64: return axis_f32_n<64>(in, out, g, sign, st, tw, s, flags);
+        case 128: return axis_f32_n<128>(in, out, g, sign, st, tw, s, flags);
+        case 256: return axis_f32_n<256>(in, out, g, sign, st, tw, s, flags);
+        default: return cudaErrorInvalidValue;
     }
 }
 

@@ -86,3 +86,27 @@ def test_f32_overflow_is_numeric_error(orc):
     a1 = np.ones(1 << 12, np.float32)
     with pytest.raises(fs.NumericError):
         fs.solve_periodic_f32(fs.GridShape([1 << 12]), a1, K(R.kern_from({(0,): 1.5}, 1)), 300)
+
+
+@pytest.mark.parametrize("m", [1, 2])
+def test_f32_rowpair_split_columns(orc, monkeypatch, m):
+    """The 1D plan's float I/O through the split column passes (the cfg5
+    layout, forced small with FSX_COLSPLIT on a fresh [1, 1, n] shape): equal
+    to the fp64 GPU solve of the widened input rounded once."""
+    monkeypatch.setenv("FSX_COLSPLIT", "8")
+    n = 1 << 15
+    k = R.Kern(3, m)
+    if m == 1:
+        for o, c in ((-1, 0.25), (0, 0.5), (1, 0.25)):
+            k.add((0, 0, o), [[c]])
+    else:
+        C2 = 0.25
+        k.add((0, 0, 0), [[2 - 2 * C2, -1.0], [1.0, 0.0]])
+        k.add((0, 0, -1), [[C2, 0.0], [0.0, 0.0]])
+        k.add((0, 0, 1), [[C2, 0.0], [0.0, 0.0]])
+    shape = fs.GridShape([1, 1, n], m)
+    a32 = orc.splitmix_fill(17 + m, n * m, True).astype(np.float32)
+    got = fs.solve_periodic_f32(shape, a32, K(k), 700)
+    g64 = fs.solve_periodic(fs.FieldGrid(shape, a32.astype(np.float64)), K(k), 700).data
+    assert np.max(np.abs(got - g64.astype(np.float32))) <= 2 * np.finfo(np.float32).eps * np.max(np.abs(g64))
+    assert fs.plan_describe(shape, K(k))["path"] == 2
