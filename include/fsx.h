@@ -136,14 +136,16 @@ fsx_status fsx_solve_periodic_device(const fsx_shape* shape, const double* d_a0,
                                      uint64_t T, double* d_out, const fsx_options* opt);
 fsx_status fsx_device_check(const fsx_options* opt);
 
-/* fp32 storage mode (north star: an optional fp32 mode at <= 1e-4 relative L2
- * vs the fp64 reference).  Float grids in and out; the arithmetic stays fp64
- * (symbol power, FFTs), so the result is the fp64 solve of the widened input
- * rounded once to float (~6e-8 relative).  What it buys is bytes: half the
- * PCIe traffic of the host entry points and, on the fused 2D/3D plan, half
- * the HBM bytes of the first and last row passes (the row kernels read and
- * write floats directly; the other plans widen / narrow around their fp64
- * buffers).  A result outside the float range raises FSX_ERR_NUMERIC.
+/* fp32 mode (north star: an optional fp32 mode at <= 1e-4 relative L2 vs the
+ * fp64 reference).  Float grids in and out: half the PCIe traffic of the host
+ * entry points and, on the fused 2D/3D plan, half the HBM bytes of the first
+ * and last row passes (the row kernels read and write floats directly; the
+ * 1D plan's strided first / last column passes do too; other shapes widen /
+ * narrow around their fp64 buffers).  The symbol power and the row passes
+ * stay fp64; the fused column pass of a real (symmetric) symbol runs its two
+ * FFTs in fp32 (~1e-7 relative; FSX_F32_COMPUTE=0 keeps it fp64, and every
+ * other path is fp64 arithmetic: the fp64 solve of the widened input rounded
+ * once, ~6e-8).  A result outside the float range raises FSX_ERR_NUMERIC.
  * Same shapes, kernels, T == 0 (bit-exact copy) and error rules as
  * fsx_solve_periodic / fsx_solve_periodic_device / fsx_solve_periodic_batch;
  * no implicit or cached variants.  No reference counterpart (the reference

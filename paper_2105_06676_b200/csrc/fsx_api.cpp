@@ -307,6 +307,7 @@ struct Device {
     int ordinal = 0;
     cudaStream_t stream = nullptr;
     DevBuf tw_all;
+    DevBuf tw_all_f;  // float2 copy (rounded once) for the fp32 mode's fused pass
     DevBuf flags;  // fsx::Flags
     std::map<std::string, std::unique_ptr<Plan>> plans;
     cudaEvent_t ev[8];
@@ -357,6 +358,12 @@ Device& device_for(int ordinal) {
     }
     d->tw_all.ensure(tw.size() * sizeof(double2));
     FSX_CK(cudaMemcpy(d->tw_all.p, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    {
+        std::vector<float2> twf(tw.size());
+        for (size_t i = 0; i < tw.size(); ++i) twf[i] = make_float2((float)tw[i].x, (float)tw[i].y);
+        d->tw_all_f.ensure(twf.size() * sizeof(float2));
+        FSX_CK(cudaMemcpy(d->tw_all_f.p, twf.data(), twf.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    }
     d->flags.ensure(sizeof(fsx::Flags));
     FSX_CK(cudaMemset(d->flags.p, 0, sizeof(fsx::Flags)));
     for (auto& e2 : d->ev) FSX_CK(cudaEventCreate(&e2));
@@ -911,7 +918,11 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
             FSX_CK(cudaMemsetAsync(p.qmax.p, 0, 8, st));
             FSX_CK(fsx::launch_fused_qmax(sym, p.ax0.ncols, p.qmax.as<unsigned long long>(), tw, st));
         }
-        if (p.halves) FSX_CK(fsx::launch_fused_halves(p.map2, ax0, sym, tw, st));
+        // fp32 mode (float grids in / out): the fused pass in fp32 arithmetic where it exists
+        const bool f32c = (fin || fout) && !q && sym.real && p.tma0 && !p.halves && p.ax0.n <= 4096 &&
+                          fsx::f32_compute_enabled();
+        if (f32c) FSX_CK(fsx::launch_cols_tma_f32(p.map0, ax0, sym, tw, dev.tw_all_f.as<float2>(), st));
+        else if (p.halves) FSX_CK(fsx::launch_fused_halves(p.map2, ax0, sym, tw, st));
         else if (p.tma0) FSX_CK(fsx::launch_cols_tma(p.map0, ax0, 2, sym, tw, st));
         else FSX_CK(fsx::launch_fused_r2c(H, ax0, sym, tw, st));
         sp.mark();

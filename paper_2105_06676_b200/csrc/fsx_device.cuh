@@ -48,6 +48,39 @@ __device__ __forceinline__ double2 ctw(double2 a, double2 w) {
     return SIGN < 0 ? cmul(a, w) : cmulc(a, w);
 }
 
+// The same helpers on float2 (the fp32 arithmetic of the fp32 mode's fused
+// pass; the line-FFT engine below is templated on the complex type CT).
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+template <int SIGN>
+__device__ __forceinline__ float2 cmul_si(float2 a) {
+    return SIGN < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
+}
+template <int SIGN>
+__device__ __forceinline__ float2 ctw(float2 a, float2 w) {
+    return SIGN < 0 ? cmul(a, w) : cmulc(a, w);
+}
+template <class CT>
+struct CScalar;
+template <>
+struct CScalar<double2> {
+    using T = double;
+    __device__ __forceinline__ static double2 make(double x, double y) { return make_double2(x, y); }
+};
+template <>
+struct CScalar<float2> {
+    using T = float;
+    __device__ __forceinline__ static float2 make(float x, float y) { return make_float2(x, y); }
+};
+
 // compile-time unrolled loop: f(std::integral_constant<int, I>) for I in [B, E)
 template <int B, int E, class F>
 __device__ __forceinline__ void static_for(F&& f) {
@@ -73,26 +106,27 @@ __device__ __forceinline__ constexpr double cos32q(int j) {
 
 // Multiply a by exp(SIGN * 2 pi i * J / R) with J, R compile-time (R divides
 // 32); the trivial angles are folded to swaps/negations.
-template <int J, int R, int SIGN>
-__device__ __forceinline__ double2 cmul_const(double2 a) {
+template <int J, int R, int SIGN, class CT>
+__device__ __forceinline__ CT cmul_const(CT a) {
     static_assert(32 % R == 0, "cmul_const: R must divide 32");
+    using T = typename CScalar<CT>::T;
     constexpr int j32 = ((J * 32 / R) % 32 + 32) % 32;  // angle in 32nds
     if constexpr (j32 == 0) return a;
-    else if constexpr (j32 == 16) return make_double2(-a.x, -a.y);
+    else if constexpr (j32 == 16) return CScalar<CT>::make(-a.x, -a.y);
     else if constexpr (j32 == 8) return cmul_si<SIGN>(a);
     else if constexpr (j32 == 24) return cmul_si<-SIGN>(a);
     else {
         // exp(i theta) with theta = 2 pi j32 / 32 (then conj for SIGN = -1)
         constexpr int q = j32 % 8, quad = j32 / 8;
         constexpr double c0 = cos32q(q), s0 = cos32q(8 - q);  // cos, sin in the first quadrant
-        constexpr double c = quad == 0 ? c0 : quad == 1 ? -s0 : quad == 2 ? -c0 : s0;
-        constexpr double s = quad == 0 ? s0 : quad == 1 ? c0 : quad == 2 ? -s0 : -c0;
-        constexpr double ss = SIGN < 0 ? -s : s;
+        constexpr T c = (T)(quad == 0 ? c0 : quad == 1 ? -s0 : quad == 2 ? -c0 : s0);
+        constexpr T s = (T)(quad == 0 ? s0 : quad == 1 ? c0 : quad == 2 ? -s0 : -c0);
+        constexpr T ss = SIGN < 0 ? -s : s;
         if constexpr (q == 4) {
             // c, s = +-1/sqrt2
-            return make_double2(c * a.x - ss * a.y, c * a.y + ss * a.x);
+            return CScalar<CT>::make(c * a.x - ss * a.y, c * a.y + ss * a.x);
         } else {
-            return make_double2(fma(c, a.x, -ss * a.y), fma(c, a.y, ss * a.x));
+            return CScalar<CT>::make(fma(c, a.x, -ss * a.y), fma(c, a.y, ss * a.x));
         }
     }
 }
@@ -105,13 +139,15 @@ struct Dft;
 
 template <int SIGN>
 struct Dft<1, SIGN> {
-    __device__ __forceinline__ static void run(double2*) {}
+    template <class CT>
+    __device__ __forceinline__ static void run(CT*) {}
 };
 
 template <int SIGN>
 struct Dft<2, SIGN> {
-    __device__ __forceinline__ static void run(double2* v) {
-        const double2 a = v[0], b = v[1];
+    template <class CT>
+    __device__ __forceinline__ static void run(CT* v) {
+        const CT a = v[0], b = v[1];
         v[0] = cadd(a, b);
         v[1] = csub(a, b);
     }
@@ -119,9 +155,10 @@ struct Dft<2, SIGN> {
 
 template <int SIGN>
 struct Dft<4, SIGN> {
-    __device__ __forceinline__ static void run(double2* v) {
-        const double2 t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
-        const double2 t2 = cadd(v[1], v[3]), t3 = cmul_si<SIGN>(csub(v[1], v[3]));
+    template <class CT>
+    __device__ __forceinline__ static void run(CT* v) {
+        const CT t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+        const CT t2 = cadd(v[1], v[3]), t3 = cmul_si<SIGN>(csub(v[1], v[3]));
         v[0] = cadd(t0, t2);
         v[2] = csub(t0, t2);
         v[1] = cadd(t1, t3);
@@ -133,29 +170,30 @@ struct Dft<4, SIGN> {
 template <int R1, int R2, int SIGN>
 struct DftCT {
     static constexpr int R = R1 * R2;
-    template <int N2, int K1>
-    __device__ __forceinline__ static void tw(double2 (&y)[R2][R1]) {
+    template <int N2, int K1, class CT>
+    __device__ __forceinline__ static void tw(CT (&y)[R2][R1]) {
         if constexpr (N2 < R2) {
             if constexpr (K1 < R1) {
                 y[N2][K1] = cmul_const<N2 * K1, R, SIGN>(y[N2][K1]);
-                tw<N2, K1 + 1>(y);
+                tw<N2, K1 + 1, CT>(y);
             } else {
-                tw<N2 + 1, 0>(y);
+                tw<N2 + 1, 0, CT>(y);
             }
         }
     }
-    __device__ __forceinline__ static void run(double2* v) {
-        double2 y[R2][R1];
+    template <class CT>
+    __device__ __forceinline__ static void run(CT* v) {
+        CT y[R2][R1];
 #pragma unroll
         for (int n2 = 0; n2 < R2; ++n2) {
 #pragma unroll
             for (int n1 = 0; n1 < R1; ++n1) y[n2][n1] = v[R2 * n1 + n2];
             Dft<R1, SIGN>::run(y[n2]);
         }
-        tw<0, 0>(y);
+        tw<0, 0, CT>(y);
 #pragma unroll
         for (int k1 = 0; k1 < R1; ++k1) {
-            double2 z[R2];
+            CT z[R2];
 #pragma unroll
             for (int n2 = 0; n2 < R2; ++n2) z[n2] = y[n2][k1];
             Dft<R2, SIGN>::run(z);
@@ -167,11 +205,13 @@ struct DftCT {
 
 template <int SIGN>
 struct Dft<8, SIGN> {
-    __device__ __forceinline__ static void run(double2* v) { DftCT<2, 4, SIGN>::run(v); }
+    template <class CT>
+    __device__ __forceinline__ static void run(CT* v) { DftCT<2, 4, SIGN>::run(v); }
 };
 template <int SIGN>
 struct Dft<16, SIGN> {
-    __device__ __forceinline__ static void run(double2* v) { DftCT<4, 4, SIGN>::run(v); }
+    template <class CT>
+    __device__ __forceinline__ static void run(CT* v) { DftCT<4, 4, SIGN>::run(v); }
 };
 
 // ------------------------------------------------------------------ smem swizzle
@@ -210,7 +250,9 @@ __device__ __forceinline__ void group_sync() {
     else asm volatile("bar.sync %0, %1;\n" ::"r"(1 + (int)(threadIdx.x / NB)), "n"(NB) : "memory");
 }
 
-template <int N, int SIGN, bool PF = false, bool PAIR = false, int FT = 0, int NB = 0>
+// CT: the complex element type (double2; float2 for the fp32 mode's fused
+// pass, with a float2 copy of the twiddle tables).
+template <int N, int SIGN, bool PF = false, bool PAIR = false, int FT = 0, int NB = 0, class CT = double2>
 struct LineFFT {
     static constexpr int LOGN = ilog2c(N);
     static constexpr int R = N < 16 ? N : 16;
@@ -243,7 +285,7 @@ struct LineFFT {
     // read; the others are products of at most two loaded/derived values
     // (<= 3 roundings).
     template <int S>
-    __device__ __forceinline__ static void load_tw(int t, const double2* __restrict__ tw, double2 (&w)[R]) {
+    __device__ __forceinline__ static void load_tw(int t, const CT* __restrict__ tw, CT (&w)[R]) {
         constexpr int r = radix<S>();
         constexpr int Ns = ns<S>();
         constexpr int C = R / r;
@@ -255,8 +297,8 @@ struct LineFFT {
 #pragma unroll
             for (int i = 0; i < (LAST_DERIVE ? 1 : C); ++i) {
                 const int k = item<S>(t, i) & (Ns - 1);
-                double2* wi = w + i * r;
-                const double2* pt = tw + (kPassTabBase + 15 * N + 16 * Ns);  // tw = tw_all + N
+                CT* wi = w + i * r;
+                const CT* pt = tw + (kPassTabBase + 15 * N + 16 * Ns);  // tw = tw_all + N
                 if constexpr (((FT >> S) & 1) != 0) {
 #pragma unroll
                     for (int u = 1; u < r; ++u) wi[u] = __ldg(pt + (u - 1) * Ns + k);
@@ -288,15 +330,14 @@ struct LineFFT {
     }
 
     template <int S>
-    __device__ __forceinline__ static void pass(double2 (&v)[R], int t, double2* line, const double2* __restrict__ tw,
-                                                double2 (&w)[R]) {
+    __device__ __forceinline__ static void pass(CT (&v)[R], int t, CT* line, const CT* __restrict__ tw, CT (&w)[R]) {
         constexpr int r = radix<S>();
         constexpr int Ns = ns<S>();
         constexpr int C = R / r;
         if constexpr (!PF) load_tw<S>(t, tw, w);
 #pragma unroll
         for (int i = 0; i < C; ++i) {
-            double2 a[r];
+            CT a[r];
 #pragma unroll
             for (int u = 0; u < r; ++u) a[u] = v[i + u * C];
             if constexpr (Ns > 1) {
@@ -331,8 +372,8 @@ struct LineFFT {
         }
     }
 
-    __device__ __forceinline__ static void run(double2 (&v)[R], int t, double2* line, const double2* __restrict__ tw) {
-        double2 w[R];
+    __device__ __forceinline__ static void run(CT (&v)[R], int t, CT* line, const CT* __restrict__ tw) {
+        CT w[R];
         if constexpr (NPASS > 0) pass<0>(v, t, line, tw, w);
     }
 };

@@ -151,6 +151,118 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
     }
 }
 
+// fp32 arithmetic for the fp32 mode's fused pass (real symbols, N <= 4096).
+// The tile arrives and leaves as fp64 (the row passes are unchanged); the two
+// FFTs run on float2 with a float2 copy of the twiddle tables, exchanging
+// through the same tile viewed as float2 lines; the multipliers lam^T / N are
+// computed in fp64 as in MODE 2 (the symbol power is where fp32 would lose
+// the accuracy) and rounded once.  This takes the pass off
+// the FP64 pipe that bounds the fp64 version; what is left is the TMA row rate.
+template <int N>
+__global__ void __launch_bounds__(TCfg<N>::NT, TCfg<N>::MINB)
+k_cols_tma_f32(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all,
+               const float2* __restrict__ twf_all) {
+    using C = TCfg<N>;
+    constexpr int W = C::W;
+    constexpr int FT = N < 4096 ? ~0 : 0;
+    using FF = LineFFT<N, -1, false, false, FT, 0, float2>;
+    using FI = LineFFT<N, +1, false, false, FT, 0, float2>;
+    extern __shared__ __align__(128) double2 tile[];
+    __shared__ __align__(8) unsigned long long bar;
+    __shared__ double2 acoef[kMaxGroups][W];
+    __shared__ double2 tapterm[kMaxFusedTaps][W];
+    const int w = threadIdx.x % W, t = threadIdx.x / W;
+    const i64 tiles = (g.ncols + W - 1) / W;
+    const i64 o = (i64)blockIdx.x / tiles;
+    const i64 c0 = ((i64)blockIdx.x - o * tiles) * W;
+    const i64 c = c0 + w;
+    i64 kx = c, ky = 0;
+    fused_col_freqs(sym, c, kx, ky);
+    if (c0 - (c0 / sym.P) * sym.P > sym.M && sym.rank == 3) return;  // pitch-padding tiles of a 3D plane
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_init_fence();
+        pdl_wait();
+        mbar_expect_tx(&bar, (unsigned)(N * W * sizeof(double2)));
+#pragma unroll 1
+        for (int b = 0; b < C::NBOX; ++b)
+            tma_load_3d(tile + b * C::BOX * W, &map, (int)(2 * c0), b * C::BOX, (int)o, &bar);
+    }
+    float* mult = reinterpret_cast<float*>(tile + W * C::LSW);
+    for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
+    __syncthreads();
+    for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
+        double2 a = make_double2(0.0, 0.0);
+        for (int j = 0; j < sym.ntaps; ++j)
+            if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j][w]);
+        acoef[gi][w] = a;
+    }
+    __syncthreads();
+    {
+        double lam[C::R];
+        symbol_real<N, C::R, C::TPL, false>(lam, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
+        pow_real_vec_skip<C::R, 4>(lam, sym.T, sym.neg_mag2);
+#pragma unroll
+        for (int q = 0; q < C::R; ++q) mult[q * C::NT + threadIdx.x] = (float)(lam[q] * sym.scale);
+    }
+    mbar_wait(&bar, 0);
+    pdl_trigger();
+    float2 v[C::R];
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) {
+        const double2 d = tile[(t + q * C::TPL) * W + w];
+        v[q] = make_float2((float)d.x, (float)d.y);
+    }
+    float2* line = reinterpret_cast<float2*>(tile) + w * C::LSW;  // the first exchange is behind a barrier
+    FF::run(v, t, line, twf_all + N);
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) v[q] = cscale(v[q], mult[q * C::NT + threadIdx.x]);
+    FI::run(v, t, line, twf_all + N);
+    __syncthreads();  // last exchange reads done before the tile is overwritten
+#pragma unroll
+    for (int q = 0; q < C::R; ++q) tile[(t + q * C::TPL) * W + w] = make_double2(v[q].x, v[q].y);
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll 1
+        for (int b = 0; b < C::NBOX; ++b) tma_store_3d(&map, tile + b * C::BOX * W, (int)(2 * c0), b * C::BOX, (int)o);
+        bulk_commit();
+        bulk_wait_read0();
+    }
+}
+
+template <int N>
+static cudaError_t cols_tma_f32_n(const CUtensorMap& map, const AxisGeom& g, const FusedSymbol& sym, const double2* tw,
+                                  const float2* twf, cudaStream_t s) {
+    using C = TCfg<N>;
+    const size_t smem = (size_t)C::W * C::LSW * 16 + (size_t)C::NT * C::R * 4;
+    const i64 tiles = (g.ncols + C::W - 1) / C::W;
+    kernel_prepare((const void*)k_cols_tma_f32<N>, smem);
+    return launch_pdl(k_cols_tma_f32<N>, dim3((unsigned)(g.outer * tiles)), dim3(C::NT), smem, s, map, g, sym, tw, twf);
+}
+
+// FSX_F32_COMPUTE=0 keeps the fp32 mode's fused pass in fp64 arithmetic (A/B)
+bool f32_compute_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_F32_COMPUTE");
+        v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+}
+
+cudaError_t launch_cols_tma_f32(const void* tensor_map, const AxisGeom& g, const FusedSymbol& sym, const double2* tw,
+                                const float2* twf, cudaStream_t s) {
+    const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(tensor_map);
+    switch (g.n) {
+        case 512: return cols_tma_f32_n<512>(map, g, sym, tw, twf, s);
+        case 1024: return cols_tma_f32_n<1024>(map, g, sym, tw, twf, s);
+        case 2048: return cols_tma_f32_n<2048>(map, g, sym, tw, twf, s);
+        case 4096: return cols_tma_f32_n<4096>(map, g, sym, tw, twf, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 // C2C strided pass with TMA column I/O for the general axis launcher
 // (launch_axis_pow2): optional four-step twiddle (TWM 1: post-multiply by
 // W^(b k), 2: pre-multiply by its conjugate; b = column / col_div, exponent as

@@ -454,10 +454,11 @@ def _f32(a, n: int, what: str) -> np.ndarray:
 
 def solve_periodic_f32(shape: GridShape, a0: np.ndarray, k: StencilKernel, T: int, st: StageTimings | None = None,
                        *, path: int = 0, out: np.ndarray | None = None, spectral_cut: int = 0) -> np.ndarray:
-    """fp32 storage mode (fsx_solve_periodic_f32): float32 grid in and out,
-    fp64 arithmetic inside; the north star's optional fp32 mode (<= 1e-4
-    relative L2 vs the fp64 reference; the result is the fp64 solve of the
-    widened input rounded once to float).  Returns the float32 result."""
+    """fp32 mode (fsx_solve_periodic_f32): float32 grid in and out; the north
+    star's optional fp32 mode (<= 1e-4 relative L2 vs the fp64 reference).
+    The symbol power is fp64; the fused column pass of a real symbol runs its
+    FFTs in fp32 (~1e-7); other paths are fp64 arithmetic rounded once.
+    Returns the float32 result."""
     if T < 0 or T >= 1 << 64:
         raise SpecError("T must be a nonnegative 64-bit integer")
     n = int(np.prod(shape.dims())) * shape.fields()

@@ -1,7 +1,8 @@
-"""fp32 storage mode (north star: an optional fp32 mode within 1e-4 relative
-L2 of the reference's fp64 result).  Float32 grids in and out, fp64 arithmetic
-inside: the result must be the fp64 solve of the widened input rounded once
-to float, so the bar here is far tighter than 1e-4.  Covers the fused plan
+"""fp32 mode (north star: an optional fp32 mode within 1e-4 relative L2 of
+the reference's fp64 result).  Float32 grids in and out.  Where the fused
+pass runs in fp32 arithmetic (plan 1, real symbol) the bar is 2e-6; elsewhere
+the arithmetic is fp64 and the result must be the fp64 solve of the widened
+input rounded once to float.  Covers the fused plan
 (float row kernels), the 1D and general plans (widen / narrow around the fp64
 buffers), the batch and device entry points, T = 0 and the overflow check."""
 import numpy as np
@@ -35,17 +36,22 @@ def K(k):
     return out
 
 
+HEAT7 = {(0, 0, 0): 0.4, (1, 0, 0): 0.1, (-1, 0, 0): 0.1, (0, 1, 0): 0.1, (0, -1, 0): 0.1, (0, 0, 1): 0.1,
+         (0, 0, -1): 0.1}
 CASES = [
-    ([1024, 1024], 1, {(0, 0): 0.2, (1, 0): 0.2, (-1, 0): 0.2, (0, 1): 0.2, (0, -1): 0.2}, 10000),  # fused 2D
-    ([64, 32, 128], 1, None, 50),       # fused 3D, random kernel
-    ([1 << 16], 1, {(-1,): 0.25, (0,): 0.5, (1,): 0.25}, 1000),  # 1D row-pair plan (widen / narrow)
-    ([96, 40], 1, None, 11),            # general plan
-    ([256, 64], 2, None, 7),            # vector cells, general plan
+    # (dims, m, taps, T, fp32 arithmetic in the fused pass)
+    ([1024, 1024], 1, {(0, 0): 0.2, (1, 0): 0.2, (-1, 0): 0.2, (0, 1): 0.2, (0, -1): 0.2}, 10000, True),  # fused 2D
+    ([64, 64, 64], 1, HEAT7, 1000, True),     # fused 3D, real symbol
+    ([64, 32, 128], 1, None, 50, False),      # fused 3D, random kernel: complex symbol -> fp64 pass
+    ([1 << 16], 1, {(-1,): 0.25, (0,): 0.5, (1,): 0.25}, 1000, False),  # 1D row-pair plan
+    ([96, 40], 1, None, 11, False),           # general plan
+    ([256, 64], 2, None, 7, False),           # vector cells, general plan
 ]
+F32_ARITH = 2e-6     # float FFTs in the fused pass, fp64 symbol power: measured ~1e-7
 
 
-@pytest.mark.parametrize("dims,m,taps,T", CASES)
-def test_f32_vs_oracle(orc, dims, m, taps, T):
+@pytest.mark.parametrize("dims,m,taps,T,f32c", CASES)
+def test_f32_vs_oracle(orc, dims, m, taps, T, f32c):
     k = R.kern_from(taps, len(dims)) if taps else R.random_kernel(Rng(500 + T), len(dims), 1, m, 0.95)
     n = int(np.prod(dims)) * m
     a32 = orc.splitmix_fill(40 + len(dims), n, True).astype(np.float32)
@@ -53,10 +59,14 @@ def test_f32_vs_oracle(orc, dims, m, taps, T):
     got = fs.solve_periodic_f32(fs.GridShape(dims, m), a32, K(k), T)
     assert got.dtype == np.float32
     e = rel_l2(got, want)
-    assert e <= TOL and e <= TIGHT, (dims, m, e)
-    # equals the fp64 GPU solve of the widened input, rounded once
+    assert e <= TOL, (dims, m, e)
     g64 = fs.solve_periodic(fs.FieldGrid(fs.GridShape(dims, m), a32.astype(np.float64)), K(k), T).data
-    assert np.max(np.abs(got - g64.astype(np.float32))) <= 2 * np.finfo(np.float32).eps * np.max(np.abs(g64))
+    if f32c:
+        assert e <= F32_ARITH, (dims, m, e)
+    else:
+        # fp64 arithmetic: the fp64 GPU solve of the widened input, rounded once
+        assert e <= TIGHT, (dims, m, e)
+        assert np.max(np.abs(got - g64.astype(np.float32))) <= 2 * np.finfo(np.float32).eps * np.max(np.abs(g64))
 
 
 def test_f32_T0_bit_exact_and_batch_and_device(orc):
