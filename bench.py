@@ -547,7 +547,7 @@ def run_gpu(args, cfg):
             "alg_bytes_per_launch": info["fused_bytes"],
             "kernel_ms": fms,
             "peak_source": peak_src,
-            "fp64": load_fp64(cfg.name, fms),
+            "fp64": None if f32 else load_fp64(cfg.name, fms),  # the fp32 mode's fused pass has its own counts
         },
         "pipeline": {"alg_bytes_per_step": alg_step, "achieved_gbs": pipe_gbs, "frac": pipe_gbs / peak,
                      "frac_vs_nominal_8tbs": pipe_gbs / NOMINAL_HBM_GBS},
