@@ -1,0 +1,105 @@
+"""Randomized parity sweep on the GPU (not part of the test suite): random
+shapes (rank 1-3, pow2 and not, length-1 axes), random kernels (m = 1, 2,
+symmetric or not), random T, each solved through the fp64 host API, the fp32
+mode and the spectral cut, checked against the CPU oracle.
+    python scripts/stress_parity.py [cases] [seed]"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import paper_2105_06676_b200 as fs  # noqa: E402
+import refutil as R  # noqa: E402
+from oracle import oracle as orc  # noqa: E402
+
+
+def K(k):
+    out = fs.StencilKernel(k.rank, k.fields)
+    for off in sorted(k.taps):
+        out.add_tap(off, k.taps[off] if k.fields > 1 else float(k.taps[off][0, 0]))
+    return out
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / (nb if nb > 0 else 1.0))
+
+
+def main():
+    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+    pow2 = [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096]
+    other = [3, 5, 6, 7, 12, 15, 24, 100, 255, 300]
+    worst = {"f64": 0.0, "f32": 0.0, "cut": 0.0}
+    fails = 0
+    for i in range(cases):
+        rank = int(rng.integers(1, 4))
+        m = 2 if (rank == 1 and rng.random() < 0.25) else 1
+        dims = []
+        budget = 1 << 18
+        for a in range(rank):
+            choices = pow2 if rng.random() < 0.8 else other
+            if rng.random() < 0.1:
+                choices = [1]
+            d = int(rng.choice([c for c in choices if c <= budget] or [1]))
+            dims.append(d)
+            budget = max(1, budget // max(d, 1))
+        if rank == 1 and dims[0] < 2:
+            dims = [64]
+        k = R.random_kernel(R.Rng(1000 + i), rank, int(rng.integers(1, 3)), m, 0.95)
+        # symmetric half the time (real symbols: the fused multiplier / fp32 paths)
+        if rng.random() < 0.5:
+            sym = R.Kern(rank, m)
+            for off, b in k.taps.items():
+                if all(abs(o) < max(d, 1) for o, d in zip(off, dims)):
+                    sym.add(off, b / 2)
+                    sym.add(tuple(-o for o in off), b / 2)
+            k = sym
+        if not k.taps or any(any(abs(o) >= d for o, d in zip(off, dims)) for off in k.taps):
+            continue
+        T = int(rng.choice([1, 2, 7, 100, 1000, 10000]))
+        n = int(np.prod(dims)) * m
+        a0 = orc.splitmix_fill(5000 + i, n, True)
+        try:
+            want = orc.solve_periodic(a0, dims, m, *k.arrays(), T)
+        except Exception as e:  # the reference raises too (NumericError): ours must as well
+            try:
+                fs.solve_periodic(fs.FieldGrid(fs.GridShape(dims, m), a0), K(k), T)
+                print("MISSING ERROR", dims, m, T, e)
+                fails += 1
+            except fs.Error:
+                pass
+            continue
+        g = fs.FieldGrid(fs.GridShape(dims, m), a0)
+        tag = f"{dims} m={m} T={T} taps={len(k.taps)}"
+        try:
+            e64 = rel(fs.solve_periodic(g, K(k), T).data, want)
+            ecut = rel(fs.solve_periodic(g, K(k), T, spectral_cut=1).data, want)
+            e32 = rel(fs.solve_periodic_f32(fs.GridShape(dims, m), a0.astype(np.float32), K(k), T),
+                      orc.solve_periodic(a0.astype(np.float32).astype(np.float64), dims, m, *k.arrays(), T))
+        except fs.NumericError as e:
+            # residue / non-finite limits can trip where the oracle's stricter-typed path did not
+            print("numeric", tag, e)
+            continue
+        worst["f64"] = max(worst["f64"], e64)
+        worst["cut"] = max(worst["cut"], ecut)
+        # the fp32 mode cannot represent results below the float range (they round to 0 or to
+        # subnormals): judge it only where the result is comfortably inside that range
+        f32_ok_range = np.max(np.abs(want)) > 1e-30
+        if not f32_ok_range:
+            e32 = 0.0
+        bad = e64 > 1e-10 or ecut > 1e-10 or e32 > 1e-4
+        worst["f32"] = max(worst["f32"], e32)
+        if bad:
+            fails += 1
+            print("FAIL", tag, f"f64 {e64:.2e} cut {ecut:.2e} f32 {e32:.2e} max|want| {np.max(np.abs(want)):.2e}")
+    print(f"{cases} cases, {fails} failures, worst: " + ", ".join(f"{k} {v:.2e}" for k, v in worst.items()))
+    return 1 if fails else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
