@@ -1,7 +1,9 @@
 """Randomized parity sweep on the GPU (not part of the test suite): random
 shapes (rank 1-3, pow2 and not, length-1 axes), random kernels (m = 1, 2,
 symmetric or not), random T, each solved through the fp64 host API, the fp32
-mode and the spectral cut, checked against the CPU oracle.
+mode and the spectral cut, checked against the CPU oracle; then random
+implicit (Crank-Nicolson-like) solves against the oracle and batches against
+single calls (bitwise).
     python scripts/stress_parity.py [cases] [seed]"""
 import os
 import sys
@@ -97,7 +99,43 @@ def main():
         if bad:
             fails += 1
             print("FAIL", tag, f"f64 {e64:.2e} cut {ecut:.2e} f32 {e32:.2e} max|want| {np.max(np.abs(want)):.2e}")
-    print(f"{cases} cases, {fails} failures, worst: " + ", ".join(f"{k} {v:.2e}" for k, v in worst.items()))
+    # implicit solves (Crank-Nicolson-like q = (1 + b) I - b S', s = I + ...) and batches
+    worst_i = worst_b = 0.0
+    for i in range(cases // 4):
+        rank = int(rng.integers(1, 4))
+        dims = [int(rng.choice([8, 16, 32, 64, 128, 256, 12, 100])) for _ in range(rank)]
+        while int(np.prod(dims)) > (1 << 18):
+            dims[0] //= 2
+        b = float(rng.uniform(0.05, 0.4))
+        qd, sd = {(0,) * rank: 1.0 + b * rank}, {(0,) * rank: 1.0 - b * rank}
+        for a in range(rank):
+            for sg in (-1, 1):
+                off = tuple(sg if j == a else 0 for j in range(rank))
+                if dims[a] > 1:
+                    qd[off] = qd.get(off, 0.0) - b / 2
+                    sd[off] = sd.get(off, 0.0) + b / 2
+        q, sk = R.kern_from(qd, rank), R.kern_from(sd, rank)
+        T = int(rng.choice([1, 10, 100, 1000]))
+        n = int(np.prod(dims))
+        a0 = orc.splitmix_fill(9000 + i, n, True)
+        want = orc.solve_periodic_implicit(a0, dims, q.arrays(), sk.arrays(), T)
+        got = fs.solve_periodic_implicit(K(q), K(sk), fs.FieldGrid(fs.GridShape(dims), a0), T).data
+        e = rel(got, want)
+        worst_i = max(worst_i, e)
+        if e > 1e-10:
+            fails += 1
+            print("FAIL implicit", dims, T, f"{e:.2e}")
+        g = fs.FieldGrid(fs.GridShape(dims), a0)
+        outs = fs.solve_periodic_batch([g, g], K(sk), T)
+        one = fs.solve_periodic(g, K(sk), T).data
+        eb = max(rel(o, one) for o in outs)
+        worst_b = max(worst_b, eb)
+        if eb != 0.0:
+            fails += 1
+            print("FAIL batch", dims, T, f"{eb:.2e}")
+    worst["implicit"] = worst_i
+    worst["batch_vs_single"] = worst_b
+    print(f"{cases} + {cases // 4} cases, {fails} failures, worst: " + ", ".join(f"{k} {v:.2e}" for k, v in worst.items()))
     return 1 if fails else 0
 
 
