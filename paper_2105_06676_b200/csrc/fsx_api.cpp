@@ -904,7 +904,10 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
         lay.kcut = kcut;
         fsx::AxisGeom ax0 = p.ax0;  // the fused pass covers columns 0..kcut only
         if (kcut >= 0) ax0.ncols = kcut + 1;
-        if (fin) FSX_CK(fsx::launch_r2c_rows_f32(fin, H, p.rows, p.L, lay, tw, st));
+        // fp32 mode: fp32 arithmetic in the row FFTs too (FSX_F32_COMPUTE, real symbols as the fused pass)
+        const bool f32rows = (fin || fout) && !q && symmetric_taps(taps) && fsx::f32_compute_enabled();
+        const float2* twf = f32rows ? dev.tw_all_f.as<float2>() : nullptr;
+        if (fin) FSX_CK(fsx::launch_r2c_rows_f32(fin, H, p.rows, p.L, lay, tw, twf, st));
         else FSX_CK(fsx::launch_r2c_rows(d_a0, H, p.rows, p.L, lay, tw, st));
         fsx::StepTwiddle none;
         const fsx::FusedSymbol sym = fused_symbol(p, taps, T, q, q ? p.qmax.as<unsigned long long>() : nullptr);
@@ -930,7 +933,7 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
             if (p.tma1) FSX_CK(fsx::launch_cols_tma(p.map1, p.ax1, 1, nosym, tw, st));
             else FSX_CK(fsx::launch_axis_pow2(H, H, p.ax1, +1, none, tw, st));
         }
-        if (fout) FSX_CK(fsx::launch_c2r_rows_f32(H, fout, p.rows, p.L, lay, tw, flags, st));
+        if (fout) FSX_CK(fsx::launch_c2r_rows_f32(H, fout, p.rows, p.L, lay, tw, twf, flags, st));
         else FSX_CK(fsx::launch_c2r_rows(H, d_out, p.rows, p.L, lay, tw, flags, st));
         sp.mark();
     } else if (p.kind == kRowPair1D) {

@@ -68,6 +68,15 @@ template <int SIGN>
 __device__ __forceinline__ float2 ctw(float2 a, float2 w) {
     return SIGN < 0 ? cmul(a, w) : cmulc(a, w);
 }
+// fp64 <-> fp32 complex conversions (widen exactly, narrow to nearest)
+__device__ __forceinline__ double2 to_d2(double2 a) { return a; }
+__device__ __forceinline__ double2 to_d2(float2 a) { return make_double2(a.x, a.y); }
+template <class TO>
+__device__ __forceinline__ TO from_d2(double2 a) {
+    if constexpr (sizeof(TO) == 16) return a;
+    else return make_float2((float)a.x, (float)a.y);
+}
+
 template <class CT>
 struct CScalar;
 template <>

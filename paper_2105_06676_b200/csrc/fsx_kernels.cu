@@ -164,15 +164,6 @@ k_contig(const double2* in, double2* out, i64 nlines, i64 pitch, const double2* 
     }
 }
 
-// fp64 <-> fp32 storage-mode element conversions (widen exactly, narrow to nearest)
-__device__ __forceinline__ double2 to_d2(double2 a) { return a; }
-__device__ __forceinline__ double2 to_d2(float2 a) { return make_double2(a.x, a.y); }
-template <class TO>
-__device__ __forceinline__ TO from_d2(double2 a) {
-    if constexpr (sizeof(TO) == 16) return a;
-    else return make_float2((float)a.x, (float)a.y);
-}
-
 // Strided lines: W adjacent columns per CTA, the axis in shared memory.
 // TI / TO = float2: the fp32 storage mode's first / last pass of the 1D plan
 // (the column pass reads the float grid, or writes it), fp64 arithmetic.

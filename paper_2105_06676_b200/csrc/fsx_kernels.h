@@ -229,10 +229,11 @@ cudaError_t launch_cols_tma_f32(const void* tensor_map, const AxisGeom& g, const
                                 const double2* tw_all, const float2* twf_all, cudaStream_t s);
 cudaError_t launch_axis_f32(const void* in, void* out, const AxisGeom& g, int sign, const StepTwiddle& st,
                             const double2* tw_all, cudaStream_t s, Flags* flags);
+// (twf_all: the float twiddle copy -> the row FFTs in fp32 arithmetic; nullptr -> fp64)
 cudaError_t launch_r2c_rows_f32(const float* x, double2* H, i64 nrows, i64 L, const RowLayout& lay,
-                                const double2* tw_all, cudaStream_t s);
+                                const double2* tw_all, const float2* twf_all, cudaStream_t s);
 cudaError_t launch_c2r_rows_f32(const double2* H, float* x, i64 nrows, i64 L, const RowLayout& lay,
-                                const double2* tw_all, Flags* flags, cudaStream_t s);
+                                const double2* tw_all, const float2* twf_all, Flags* flags, cudaStream_t s);
 // Bluestein stages for non-pow2 axes (fsx_kernels.cu): gather * chirp into [lines][P],
 // pointwise * Bhat, scatter * chirp * scale (conj in / out for the inverse)
 cudaError_t launch_blue_pre(const double2* Z, double2* buf, const AxisGeom& g, i64 P, const double2* chirp, int conj_in,

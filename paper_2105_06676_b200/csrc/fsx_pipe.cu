@@ -163,13 +163,14 @@ struct BulkCfg {
 
 // BLK: the output goes to the slab exchange layout (blocked, or straight
 // into the peers' buffers over NVLink, RowLayout::ptr); otherwise pitch rows.
-// TI = float: fp32 storage mode (the row lands as floats, half the bytes, and
-// is widened to fp64 as it is read into registers; the arithmetic is fp64).
-template <int M, int ST, bool BLK, class TI = double>
+// TI = float: fp32 mode (the row lands as floats, half the bytes).  CT is
+// the arithmetic: double2, or float2 for the fp32 mode's fp32 row FFT (with
+// the float twiddle copy); the half spectrum H is fp64 either way.
+template <int M, int ST, bool BLK, class TI = double, class CT = double2>
 __global__ void __launch_bounds__(PCfg<M>::TPL, BulkCfg<M, ST>::MINB)
 k_r2c_bulk(const TI* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, RowLayout lay,
-           const double2* __restrict__ tw_all) {
-    using F = LineFFT<M, -1, true, true>;
+           const CT* __restrict__ tw_all) {
+    using F = LineFFT<M, -1, true, true, 0, 0, CT>;
     constexpr int TPL = PCfg<M>::TPL, R = 16;
     constexpr unsigned BYTES = 2 * M * sizeof(TI);
     extern __shared__ __align__(128) double2 sm[];
@@ -198,17 +199,18 @@ k_r2c_bulk(const TI* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, 
         if (nxt >= nrows) pdl_trigger();  // last row of this CTA: let the successor launch
         mbar_wait(&bar[s], (par >> s) & 1u);
         par ^= 1u << s;
-        double2* line = sm + s * M;
-        double2 v[R];
+        CT* line = reinterpret_cast<CT*>(sm + s * M);
+        CT v[R];
         if constexpr (sizeof(TI) == 8) {
 #pragma unroll
-            for (int q = 0; q < R; ++q) v[q] = line[t + q * TPL];
+            for (int q = 0; q < R; ++q) v[q] = from_d2<CT>(sm[s * M + t + q * TPL]);
         } else {
-            const float2* lf = reinterpret_cast<const float2*>(line);
+            const float2* lf = reinterpret_cast<const float2*>(sm + s * M);
 #pragma unroll
             for (int q = 0; q < R; ++q) {
                 const float2 f = lf[t + q * TPL];
-                v[q] = make_double2(f.x, f.y);
+                if constexpr (sizeof(CT) == 8) v[q] = f;
+                else v[q] = make_double2(f.x, f.y);
             }
         }
         F::run(v, t, line, tw_all + M);
@@ -220,17 +222,19 @@ k_r2c_bulk(const TI* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, 
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
                 const int j = i == 0 ? t : j1;
-                const double2 wj = __ldg(tw_all + 2 * M + j);
+                const CT wj = __ldg(tw_all + 2 * M + j);
                 static_for<0, 8>([&](auto U) {
                     constexpr int u = decltype(U)::value;
                     const int qp = (1 - i) + 2 * (7 - u);                        // partner slot, t != 0
                     const int qz = i == 0 ? 2 * ((8 - u) & 7) : 1 + 2 * (7 - u);  // partner slot, t == 0
-                    const double2 zk = v[i + 2 * u];
-                    const double2 zm = cconj(t == 0 ? v[qz] : v[qp]);
-                    const double2 e = cscale(cadd(zk, zm), 0.5);
-                    const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
-                    if (lay.kcut < 0 || j + u * (M / 8) <= lay.kcut) h(j + u * (M / 8)) = cadd(e, cmul(cmul_const<u, 16, -1>(wj), od));
-                    if (i == 0 && u == 0 && t == 0 && (lay.kcut < 0 || lay.kcut >= M)) h(M) = make_double2(zk.x - zk.y, 0.0);
+                    const CT zk = v[i + 2 * u];
+                    const CT zm = cconj(t == 0 ? v[qz] : v[qp]);
+                    const CT e = cscale(cadd(zk, zm), 0.5);
+                    const CT od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
+                    if (lay.kcut < 0 || j + u * (M / 8) <= lay.kcut)
+                        h(j + u * (M / 8)) = to_d2(cadd(e, cmul(cmul_const<u, 16, -1>(wj), od)));
+                    if (i == 0 && u == 0 && t == 0 && (lay.kcut < 0 || lay.kcut >= M))
+                        h(M) = make_double2((double)zk.x - (double)zk.y, 0.0);
                 });
             }
         } else {
@@ -238,16 +242,16 @@ k_r2c_bulk(const TI* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, 
 #pragma unroll
             for (int q = 0; q < R; ++q) line[swz(t + q * TPL)] = v[q];
             __syncthreads();
-            const double2 wt = __ldg(tw_all + 2 * M + t);  // W_L^(t + q M/16) = W_L^t * W_32^q
+            const CT wt = __ldg(tw_all + 2 * M + t);  // W_L^(t + q M/16) = W_L^t * W_32^q
             static_for<0, R>([&](auto Q) {
                 constexpr int q = decltype(Q)::value;
                 const int k = t + q * TPL;
-                const double2 zk = v[q];
-                const double2 zm = cconj(line[swz((M - k) & (M - 1))]);
-                const double2 e = cscale(cadd(zk, zm), 0.5);
-                const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
-                if (lay.kcut < 0 || k <= lay.kcut) h(k) = cadd(e, cmul(cmul_const<q, 32, -1>(wt), od));
-                if (k == 0 && (lay.kcut < 0 || lay.kcut >= M)) h(M) = make_double2(zk.x - zk.y, 0.0);
+                const CT zk = v[q];
+                const CT zm = cconj(line[swz((M - k) & (M - 1))]);
+                const CT e = cscale(cadd(zk, zm), 0.5);
+                const CT od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
+                if (lay.kcut < 0 || k <= lay.kcut) h(k) = to_d2(cadd(e, cmul(cmul_const<q, 32, -1>(wt), od)));
+                if (k == 0 && (lay.kcut < 0 || lay.kcut >= M)) h(M) = make_double2((double)zk.x - (double)zk.y, 0.0);
             });
         }
         fence_proxy_async();  // generic writes of this stage before its next bulk fill
@@ -278,13 +282,14 @@ __device__ __forceinline__ void load_hrow(double2* dst, const double2* H, const 
     }
 }
 
-// TO = float: fp32 storage mode (rounded to nearest on the store; a value
-// outside the float range becomes inf and raises the non-finite flag).
-template <int M, int ST, bool BLK, class TO = double>
+// TO = float: fp32 mode (rounded to nearest on the store; a value outside the
+// float range becomes inf and raises the non-finite flag).  CT: the
+// arithmetic, as in k_r2c_bulk.
+template <int M, int ST, bool BLK, class TO = double, class CT = double2>
 __global__ void __launch_bounds__(PCfg<M>::TPL, BulkCfg<M, ST>::MINB)
 k_c2r_bulk(const double2* __restrict__ H, TO* __restrict__ x, i64 nrows, i64 L, RowLayout lay,
-           const double2* __restrict__ tw_all, Flags* flags) {
-    using F = LineFFT<M, +1, true>;
+           const CT* __restrict__ tw_all, Flags* flags) {
+    using F = LineFFT<M, +1, true, false, 0, 0, CT>;
     constexpr int TPL = PCfg<M>::TPL, R = 16;
     constexpr int SS = M + 8;  // stage stride: M + 1 elements, 128 B aligned
     extern __shared__ __align__(128) double2 sm[];
@@ -313,25 +318,26 @@ k_c2r_bulk(const double2* __restrict__ H, TO* __restrict__ x, i64 nrows, i64 L, 
             for (i64 k = lay.kcut + 1 + t; k <= M; k += TPL) line[k] = make_double2(0.0, 0.0);
             __syncthreads();
         }
-        double2 v[R];
+        CT v[R];
         // split twiddle W_L^(t + q M/16) = W_L^t * W_32^q: one load per thread
-        const double2 wt = __ldg(tw_all + 2 * M + t);
+        const CT wt = __ldg(tw_all + 2 * M + t);
         static_for<0, R>([&](auto Q) {
             constexpr int q = decltype(Q)::value;
             const int k = t + q * TPL;
-            const double2 xk = line[k];
-            const double2 xm = cconj(line[M - k]);
-            const double2 e = cadd(xk, xm);
-            const double2 od = cmulc(csub(xk, xm), cmul_const<q, 32, -1>(wt));
+            const CT xk = from_d2<CT>(line[k]);
+            const CT xm = cconj(from_d2<CT>(line[M - k]));
+            const CT e = cadd(xk, xm);
+            const CT od = cmulc(csub(xk, xm), cmul_const<q, 32, -1>(wt));
             v[q] = cadd(e, cmul_si<+1>(od));
         });
-        F::run(v, t, line, tw_all + M);
+        F::run(v, t, reinterpret_cast<CT*>(line), tw_all + M);
         if constexpr (sizeof(TO) == 8) {
             double2* dst = reinterpret_cast<double2*>(x + row * L);
 #pragma unroll
             for (int q = 0; q < R; ++q) {
-                dst[t + q * TPL] = v[q];
-                bad |= !isfinite(v[q].x) || !isfinite(v[q].y);
+                const double2 d = to_d2(v[q]);
+                dst[t + q * TPL] = d;
+                bad |= !isfinite(d.x) || !isfinite(d.y);
             }
         } else {
             float2* dst = reinterpret_cast<float2*>(x + row * L);
@@ -603,10 +609,17 @@ cudaError_t launch_c2r_bulk(const double2* H, double* x, i64 nrows, i64 L, const
 }
 
 // fp32 storage mode rows (pitch layout, two stages as the fp64 default)
+// (twf: the float twiddle copy -> fp32 row FFTs; nullptr -> fp64 arithmetic)
 template <int M>
 static cudaError_t r2c_bulk_f32_m(const float* x, double2* H, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
-                                  cudaStream_t s) {
+                                  const float2* twf, cudaStream_t s) {
     const size_t smem = (size_t)2 * M * sizeof(double2);
+    if (twf) {
+        auto kf = k_r2c_bulk<M, 2, false, float, float2>;
+        kernel_prepare((const void*)kf, smem);
+        const int grid = persistent_grid(kf, PCfg<M>::TPL, smem, nrows);
+        return launch_pdl(kf, dim3(grid), dim3(PCfg<M>::TPL), smem, s, x, H, nrows, L, lay, twf);
+    }
     auto kf = k_r2c_bulk<M, 2, false, float>;
     kernel_prepare((const void*)kf, smem);
     const int grid = persistent_grid(kf, PCfg<M>::TPL, smem, nrows);
@@ -615,8 +628,14 @@ static cudaError_t r2c_bulk_f32_m(const float* x, double2* H, i64 nrows, i64 L, 
 
 template <int M>
 static cudaError_t c2r_bulk_f32_m(const double2* H, float* x, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
-                                  Flags* f, cudaStream_t s) {
+                                  const float2* twf, Flags* f, cudaStream_t s) {
     const size_t smem = (size_t)2 * (M + 8) * sizeof(double2);
+    if (twf) {
+        auto kf = k_c2r_bulk<M, 2, false, float, float2>;
+        kernel_prepare((const void*)kf, smem);
+        const int grid = persistent_grid(kf, PCfg<M>::TPL, smem, nrows);
+        return launch_pdl(kf, dim3(grid), dim3(PCfg<M>::TPL), smem, s, H, x, nrows, L, lay, twf, f);
+    }
     auto kf = k_c2r_bulk<M, 2, false, float>;
     kernel_prepare((const void*)kf, smem);
     const int grid = persistent_grid(kf, PCfg<M>::TPL, smem, nrows);
@@ -626,25 +645,25 @@ static cudaError_t c2r_bulk_f32_m(const double2* H, float* x, i64 nrows, i64 L, 
 bool rows_f32_ok(i64 L) { return pipe_enabled() && pipe_rows_ok(L / 2) && rows_variant() == 3; }
 
 cudaError_t launch_r2c_rows_f32(const float* x, double2* H, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
-                                cudaStream_t s) {
+                                const float2* twf, cudaStream_t s) {
     if (lay.blk) return cudaErrorInvalidValue;
     switch (L / 2) {
-        case 512: return r2c_bulk_f32_m<512>(x, H, nrows, L, lay, tw, s);
-        case 1024: return r2c_bulk_f32_m<1024>(x, H, nrows, L, lay, tw, s);
-        case 2048: return r2c_bulk_f32_m<2048>(x, H, nrows, L, lay, tw, s);
-        case 4096: return r2c_bulk_f32_m<4096>(x, H, nrows, L, lay, tw, s);
+        case 512: return r2c_bulk_f32_m<512>(x, H, nrows, L, lay, tw, twf, s);
+        case 1024: return r2c_bulk_f32_m<1024>(x, H, nrows, L, lay, tw, twf, s);
+        case 2048: return r2c_bulk_f32_m<2048>(x, H, nrows, L, lay, tw, twf, s);
+        case 4096: return r2c_bulk_f32_m<4096>(x, H, nrows, L, lay, tw, twf, s);
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t launch_c2r_rows_f32(const double2* H, float* x, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
-                                Flags* f, cudaStream_t s) {
+                                const float2* twf, Flags* f, cudaStream_t s) {
     if (lay.blk) return cudaErrorInvalidValue;
     switch (L / 2) {
-        case 512: return c2r_bulk_f32_m<512>(H, x, nrows, L, lay, tw, f, s);
-        case 1024: return c2r_bulk_f32_m<1024>(H, x, nrows, L, lay, tw, f, s);
-        case 2048: return c2r_bulk_f32_m<2048>(H, x, nrows, L, lay, tw, f, s);
-        case 4096: return c2r_bulk_f32_m<4096>(H, x, nrows, L, lay, tw, f, s);
+        case 512: return c2r_bulk_f32_m<512>(H, x, nrows, L, lay, tw, twf, f, s);
+        case 1024: return c2r_bulk_f32_m<1024>(H, x, nrows, L, lay, tw, twf, f, s);
+        case 2048: return c2r_bulk_f32_m<2048>(H, x, nrows, L, lay, tw, twf, f, s);
+        case 4096: return c2r_bulk_f32_m<4096>(H, x, nrows, L, lay, tw, twf, f, s);
         default: return cudaErrorInvalidValue;
     }
 }
