@@ -141,11 +141,11 @@ fsx_status fsx_device_check(const fsx_options* opt);
  * entry points and, on the fused 2D/3D plan, half the HBM bytes of the first
  * and last row passes (the row kernels read and write floats directly; the
  * 1D plan's strided first / last column passes do too; other shapes widen /
- * narrow around their fp64 buffers).  The symbol power and the row passes
- * stay fp64; the fused column pass of a real (symmetric) symbol runs its two
- * FFTs in fp32 (~1e-7 relative; FSX_F32_COMPUTE=0 keeps it fp64, and every
- * other path is fp64 arithmetic: the fp64 solve of the widened input rounded
- * once, ~6e-8).  A result outside the float range raises FSX_ERR_NUMERIC.
+ * narrow around their fp64 buffers).  The symbol power and the half spectrum
+ * stay fp64; for a real (symmetric) symbol on that plan the row FFTs and the
+ * fused column pass's FFTs run in fp32 (~1e-7 relative; FSX_F32_COMPUTE=0
+ * keeps them fp64, and every other path is fp64 arithmetic: the fp64 solve of
+ * the widened input rounded once, ~6e-8).  A result outside the float range raises FSX_ERR_NUMERIC.
  * Same shapes, kernels, T == 0 (bit-exact copy) and error rules as
  * fsx_solve_periodic / fsx_solve_periodic_device / fsx_solve_periodic_batch;
  * no implicit or cached variants.  No reference counterpart (the reference
