@@ -913,7 +913,8 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
         const fsx::FusedSymbol sym = fused_symbol(p, taps, T, q, q ? p.qmax.as<unsigned long long>() : nullptr);
         fsx::FusedSymbol nosym;
         if (r == 3) {
-            if (p.tma1) FSX_CK(fsx::launch_cols_tma(p.map1, p.ax1, 0, nosym, tw, st));
+            if (p.tma1 && twf && p.ax1.n <= 4096) FSX_CK(fsx::launch_cols_tma_f32(p.map1, p.ax1, 0, nosym, tw, twf, st));
+            else if (p.tma1) FSX_CK(fsx::launch_cols_tma(p.map1, p.ax1, 0, nosym, tw, st));
             else FSX_CK(fsx::launch_axis_pow2(H, H, p.ax1, -1, none, tw, st));
         }
         sp.mark();
@@ -924,13 +925,14 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
         // fp32 mode (float grids in / out): the fused pass in fp32 arithmetic where it exists
         const bool f32c = (fin || fout) && !q && sym.real && p.tma0 && !p.halves && p.ax0.n <= 4096 &&
                           fsx::f32_compute_enabled();
-        if (f32c) FSX_CK(fsx::launch_cols_tma_f32(p.map0, ax0, sym, tw, dev.tw_all_f.as<float2>(), st));
+        if (f32c) FSX_CK(fsx::launch_cols_tma_f32(p.map0, ax0, 2, sym, tw, dev.tw_all_f.as<float2>(), st));
         else if (p.halves) FSX_CK(fsx::launch_fused_halves(p.map2, ax0, sym, tw, st));
         else if (p.tma0) FSX_CK(fsx::launch_cols_tma(p.map0, ax0, 2, sym, tw, st));
         else FSX_CK(fsx::launch_fused_r2c(H, ax0, sym, tw, st));
         sp.mark();
         if (r == 3) {
-            if (p.tma1) FSX_CK(fsx::launch_cols_tma(p.map1, p.ax1, 1, nosym, tw, st));
+            if (p.tma1 && twf && p.ax1.n <= 4096) FSX_CK(fsx::launch_cols_tma_f32(p.map1, p.ax1, 1, nosym, tw, twf, st));
+            else if (p.tma1) FSX_CK(fsx::launch_cols_tma(p.map1, p.ax1, 1, nosym, tw, st));
             else FSX_CK(fsx::launch_axis_pow2(H, H, p.ax1, +1, none, tw, st));
         }
         if (fout) FSX_CK(fsx::launch_c2r_rows_f32(H, fout, p.rows, p.L, lay, tw, twf, flags, st));

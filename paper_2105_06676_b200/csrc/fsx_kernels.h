@@ -223,9 +223,9 @@ cudaError_t launch_widen(const float* x, double* y, i64 n, cudaStream_t s);
 cudaError_t launch_narrow(const double* x, float* y, i64 n, Flags* flags, cudaStream_t s);
 bool rows_f32_ok(i64 L);
 bool axis_f32_ok(const AxisGeom& g);
-// fp32 mode: the plan-1 fused pass in fp32 arithmetic (real symbols, N <= 4096)
+// fp32 mode: plan-1 column passes in fp32 arithmetic (mode 2 fused, real symbols; 0 / 1 the 3D y passes)
 bool f32_compute_enabled();
-cudaError_t launch_cols_tma_f32(const void* tensor_map, const AxisGeom& g, const FusedSymbol& sym,
+cudaError_t launch_cols_tma_f32(const void* tensor_map, const AxisGeom& g, int mode, const FusedSymbol& sym,
                                 const double2* tw_all, const float2* twf_all, cudaStream_t s);
 cudaError_t launch_axis_f32(const void* in, void* out, const AxisGeom& g, int sign, const StepTwiddle& st,
                             const double2* tw_all, cudaStream_t s, Flags* flags);

@@ -158,7 +158,8 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
 // computed in fp64 as in MODE 2 (the symbol power is where fp32 would lose
 // the accuracy) and rounded once.  This takes the pass off
 // the FP64 pipe that bounds the fp64 version; what is left is the TMA row rate.
-template <int N>
+// MODE 2: the fused pass; 0 / 1: a forward / inverse C2C pass (the 3D y passes).
+template <int N, int MODE>
 __global__ void __launch_bounds__(TCfg<N>::NT, TCfg<N>::MINB)
 k_cols_tma_f32(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all,
                const float2* __restrict__ twf_all) {
@@ -177,8 +178,10 @@ k_cols_tma_f32(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol 
     const i64 c0 = ((i64)blockIdx.x - o * tiles) * W;
     const i64 c = c0 + w;
     i64 kx = c, ky = 0;
-    fused_col_freqs(sym, c, kx, ky);
-    if (c0 - (c0 / sym.P) * sym.P > sym.M && sym.rank == 3) return;  // pitch-padding tiles of a 3D plane
+    if constexpr (MODE == 2) {
+        fused_col_freqs(sym, c, kx, ky);
+        if (c0 - (c0 / sym.P) * sym.P > sym.M && sym.rank == 3) return;  // pitch-padding tiles of a 3D plane
+    }
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
         mbar_init_fence();
@@ -189,16 +192,18 @@ k_cols_tma_f32(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol 
             tma_load_3d(tile + b * C::BOX * W, &map, (int)(2 * c0), b * C::BOX, (int)o, &bar);
     }
     float* mult = reinterpret_cast<float*>(tile + W * C::LSW);
-    for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
-    __syncthreads();
-    for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
-        double2 a = make_double2(0.0, 0.0);
-        for (int j = 0; j < sym.ntaps; ++j)
-            if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j][w]);
-        acoef[gi][w] = a;
+    if constexpr (MODE == 2) {
+        for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
     }
     __syncthreads();
-    {
+    if constexpr (MODE == 2) {
+        for (int gi = t; gi < sym.ngroups; gi += C::TPL) {
+            double2 a = make_double2(0.0, 0.0);
+            for (int j = 0; j < sym.ntaps; ++j)
+                if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j][w]);
+            acoef[gi][w] = a;
+        }
+        __syncthreads();
         double lam[C::R];
         symbol_real<N, C::R, C::TPL, false>(lam, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
         pow_real_vec_skip<C::R, 4>(lam, sym.T, sym.neg_mag2);
@@ -214,10 +219,16 @@ k_cols_tma_f32(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol 
         v[q] = make_float2((float)d.x, (float)d.y);
     }
     float2* line = reinterpret_cast<float2*>(tile) + w * C::LSW;  // the first exchange is behind a barrier
-    FF::run(v, t, line, twf_all + N);
+    if constexpr (MODE == 1) {
+        FI::run(v, t, line, twf_all + N);
+    } else {
+        FF::run(v, t, line, twf_all + N);
+    }
+    if constexpr (MODE == 2) {
 #pragma unroll
-    for (int q = 0; q < C::R; ++q) v[q] = cscale(v[q], mult[q * C::NT + threadIdx.x]);
-    FI::run(v, t, line, twf_all + N);
+        for (int q = 0; q < C::R; ++q) v[q] = cscale(v[q], mult[q * C::NT + threadIdx.x]);
+        FI::run(v, t, line, twf_all + N);
+    }
     __syncthreads();  // last exchange reads done before the tile is overwritten
 #pragma unroll
     for (int q = 0; q < C::R; ++q) tile[(t + q * C::TPL) * W + w] = make_double2(v[q].x, v[q].y);
@@ -231,14 +242,15 @@ k_cols_tma_f32(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol 
     }
 }
 
-template <int N>
+template <int N, int MODE>
 static cudaError_t cols_tma_f32_n(const CUtensorMap& map, const AxisGeom& g, const FusedSymbol& sym, const double2* tw,
                                   const float2* twf, cudaStream_t s) {
     using C = TCfg<N>;
-    const size_t smem = (size_t)C::W * C::LSW * 16 + (size_t)C::NT * C::R * 4;
+    const size_t smem = (size_t)C::W * C::LSW * 16 + (MODE == 2 ? (size_t)C::NT * C::R * 4 : 0);
     const i64 tiles = (g.ncols + C::W - 1) / C::W;
-    kernel_prepare((const void*)k_cols_tma_f32<N>, smem);
-    return launch_pdl(k_cols_tma_f32<N>, dim3((unsigned)(g.outer * tiles)), dim3(C::NT), smem, s, map, g, sym, tw, twf);
+    auto kf = k_cols_tma_f32<N, MODE>;
+    kernel_prepare((const void*)kf, smem);
+    return launch_pdl(kf, dim3((unsigned)(g.outer * tiles)), dim3(C::NT), smem, s, map, g, sym, tw, twf);
 }
 
 // FSX_F32_COMPUTE=0 keeps the fp32 mode's fused pass in fp64 arithmetic (A/B)
@@ -251,16 +263,22 @@ bool f32_compute_enabled() {
     return v != 0;
 }
 
-cudaError_t launch_cols_tma_f32(const void* tensor_map, const AxisGeom& g, const FusedSymbol& sym, const double2* tw,
-                                const float2* twf, cudaStream_t s) {
+cudaError_t launch_cols_tma_f32(const void* tensor_map, const AxisGeom& g, int mode, const FusedSymbol& sym,
+                                const double2* tw, const float2* twf, cudaStream_t s) {
     const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(tensor_map);
+#define FSX_TMAF(N)                                                                  \
+    case N:                                                                          \
+        return mode == 0 ? cols_tma_f32_n<N, 0>(map, g, sym, tw, twf, s)             \
+             : mode == 1 ? cols_tma_f32_n<N, 1>(map, g, sym, tw, twf, s)             \
+                         : cols_tma_f32_n<N, 2>(map, g, sym, tw, twf, s);
     switch (g.n) {
-        case 512: return cols_tma_f32_n<512>(map, g, sym, tw, twf, s);
-        case 1024: return cols_tma_f32_n<1024>(map, g, sym, tw, twf, s);
-        case 2048: return cols_tma_f32_n<2048>(map, g, sym, tw, twf, s);
-        case 4096: return cols_tma_f32_n<4096>(map, g, sym, tw, twf, s);
+        FSX_TMAF(512)
+        FSX_TMAF(1024)
+        FSX_TMAF(2048)
+        FSX_TMAF(4096)
         default: return cudaErrorInvalidValue;
     }
+#undef FSX_TMAF
 }
 
 // C2C strided pass with TMA column I/O for the general axis launcher

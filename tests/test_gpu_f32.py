@@ -42,6 +42,7 @@ CASES = [
     # (dims, m, taps, T, fp32 arithmetic in the fused pass)
     ([1024, 1024], 1, {(0, 0): 0.2, (1, 0): 0.2, (-1, 0): 0.2, (0, 1): 0.2, (0, -1): 0.2}, 10000, True),  # fused 2D
     ([64, 64, 64], 1, HEAT7, 1000, True),     # fused 3D, real symbol
+    ([16, 512, 1024], 1, HEAT7, 300, True),   # 3D with fp32 TMA y passes (n1 = 512)
     ([64, 32, 128], 1, None, 50, False),      # fused 3D, random kernel: complex symbol -> fp64 pass
     ([1 << 16], 1, {(-1,): 0.25, (0,): 0.5, (1,): 0.25}, 1000, False),  # 1D row-pair plan
     ([96, 40], 1, None, 11, False),           # general plan
