@@ -287,6 +287,7 @@ cudaError_t launch_fused_halves(const void* tensor_map2, const AxisGeom& g, cons
 bool tma_cols_ok(i64 N);
 int tma_cols_width(i64 N);  // columns per TMA tile (the box width the host encodes)
 int make_cols_tensor_map(void* out_map, void* base, const AxisGeom& g);
+int make_cols_tensor_map_w(void* out_map, void* base, const AxisGeom& g, int W);  // explicit tile width
 cudaError_t launch_cols_tma(const void* tensor_map, const AxisGeom& g, int mode, const FusedSymbol& sym,
                             const double2* tw_all, cudaStream_t s);
 cudaError_t launch_transpose_split(const double2* in, double2* out, i64 outer, i64 n1, i64 n2, i64 inner,

@@ -287,11 +287,13 @@ cudaError_t launch_cols_tma_f32(const void* tensor_map, const AxisGeom& g, int m
 // StepTwiddle), out of place (separate load / store maps), and the solve's
 // non-finite scan on its output when `flags` is set.  Used by the 1D plan's
 // column FFTs (128-point columns for cfg5, 512 for cfg1).
-template <int N, int SIGN, int TWM>
-__global__ void __launch_bounds__(TCfg<N>::NT, TCfg<N>::MINB)
+// WW: columns per tile (0: the 64 KB default, 4096 / N; a narrower tile gives
+// small problems more CTAs than SMs, see launch_axis_tma).
+template <int N, int SIGN, int TWM, int WW = 0>
+__global__ void __launch_bounds__(TCfg<N, WW>::NT, TCfg<N, WW>::MINB)
 k_axis_tma(const __grid_constant__ CUtensorMap map_in, const __grid_constant__ CUtensorMap map_out, AxisGeom g,
            StepTwiddle st, const double2* __restrict__ tw_all, Flags* flags) {
-    using C = TCfg<N>;
+    using C = TCfg<N, WW>;
     constexpr int W = C::W;
     using F = LineFFT<N, SIGN, false, false, (N < 4096 ? ~0 : 0)>;
     extern __shared__ __align__(128) double2 tile[];
@@ -366,27 +368,38 @@ static int axis_tma_enabled() {
     return v;
 }
 
-template <int N, int SIGN, int TWM>
+template <int N, int SIGN, int TWM, int WW>
 static cudaError_t axis_tma_nst(const CUtensorMap& mi, const CUtensorMap& mo, const AxisGeom& g, const StepTwiddle& st,
                                 const double2* tw, Flags* f, cudaStream_t s) {
-    using C = TCfg<N>;
+    using C = TCfg<N, WW>;
     const size_t smem = (size_t)C::W * C::LSW * sizeof(double2);
     const i64 tiles = (g.ncols + C::W - 1) / C::W;
-    auto kf = k_axis_tma<N, SIGN, TWM>;
+    auto kf = k_axis_tma<N, SIGN, TWM, WW>;
     kernel_prepare((const void*)kf, smem);
     return launch_pdl(kf, dim3((unsigned)(g.outer * tiles)), dim3(C::NT), smem, s, mi, mo, g, st, tw, f);
 }
 
-template <int N>
+template <int N, int WW = 0>
 static cudaError_t axis_tma_n(const CUtensorMap& mi, const CUtensorMap& mo, const AxisGeom& g, int sign,
                               const StepTwiddle& st, const double2* tw, Flags* f, cudaStream_t s) {
     if (sign < 0)
-        return st.mode == 1 ? axis_tma_nst<N, -1, 1>(mi, mo, g, st, tw, f, s)
-             : st.mode == 2 ? axis_tma_nst<N, -1, 2>(mi, mo, g, st, tw, f, s)
-                            : axis_tma_nst<N, -1, 0>(mi, mo, g, st, tw, f, s);
-    return st.mode == 1 ? axis_tma_nst<N, +1, 1>(mi, mo, g, st, tw, f, s)
-         : st.mode == 2 ? axis_tma_nst<N, +1, 2>(mi, mo, g, st, tw, f, s)
-                        : axis_tma_nst<N, +1, 0>(mi, mo, g, st, tw, f, s);
+        return st.mode == 1 ? axis_tma_nst<N, -1, 1, WW>(mi, mo, g, st, tw, f, s)
+             : st.mode == 2 ? axis_tma_nst<N, -1, 2, WW>(mi, mo, g, st, tw, f, s)
+                            : axis_tma_nst<N, -1, 0, WW>(mi, mo, g, st, tw, f, s);
+    return st.mode == 1 ? axis_tma_nst<N, +1, 1, WW>(mi, mo, g, st, tw, f, s)
+         : st.mode == 2 ? axis_tma_nst<N, +1, 2, WW>(mi, mo, g, st, tw, f, s)
+                        : axis_tma_nst<N, +1, 0, WW>(mi, mo, g, st, tw, f, s);
+}
+
+// FSX_AXIS_NARROW (default 2; 0 = off): with fewer than two default tiles per
+// SM, 512- and 1024-point columns use this many columns per tile instead
+static int axis_narrow() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_AXIS_NARROW");
+        v = e ? atoi(e) : 2;
+    }
+    return v;
 }
 
 // Returns cudaErrorNotSupported when the TMA path does not apply (the caller
@@ -396,14 +409,30 @@ cudaError_t launch_axis_tma(const double2* in, double2* out, const AxisGeom& g, 
     // FSX_TMA_AXIS (default 512): the shortest column length taken by this path
     const int nmin = axis_tma_enabled();
     if (!nmin || g.inner <= 1 || g.n < nmin || g.n > 4096) return cudaErrorNotSupported;
-    const int W = tma_cols_width(g.n);
+    int W = tma_cols_width(g.n);
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const int nw = axis_narrow();
+    const bool narrow = (g.n == 512 || g.n == 1024) && (nw == 2 || nw == 4) && nw < W &&
+                        g.outer * (g.ncols / W) < 2 * (i64)sms && g.ncols % nw == 0;
+    if (narrow) W = nw;
     if (g.ncols % W || (reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) % 16) return cudaErrorNotSupported;
     alignas(64) unsigned char mi[128], mo[128];
-    if (make_cols_tensor_map(mi, const_cast<double2*>(in), g) != 0) return cudaErrorNotSupported;
+    if (make_cols_tensor_map_w(mi, const_cast<double2*>(in), g, W) != 0) return cudaErrorNotSupported;
     if (out == in) std::memcpy(mo, mi, sizeof mo);
-    else if (make_cols_tensor_map(mo, out, g) != 0) return cudaErrorNotSupported;
+    else if (make_cols_tensor_map_w(mo, out, g, W) != 0) return cudaErrorNotSupported;
     const CUtensorMap& MI = *reinterpret_cast<const CUtensorMap*>(mi);
     const CUtensorMap& MO = *reinterpret_cast<const CUtensorMap*>(mo);
+    if (narrow) {
+        if (g.n == 512) return W == 2 ? axis_tma_n<512, 2>(MI, MO, g, sign, st, tw, flags, s)
+                                      : axis_tma_n<512, 4>(MI, MO, g, sign, st, tw, flags, s);
+        return axis_tma_n<1024, 2>(MI, MO, g, sign, st, tw, flags, s);
+    }
     switch (g.n) {
         case 128: return axis_tma_n<128>(MI, MO, g, sign, st, tw, flags, s);
         case 256: return axis_tma_n<256>(MI, MO, g, sign, st, tw, flags, s);
@@ -638,6 +667,10 @@ int make_cols_tensor_map_par(void* out_map, void* base, const AxisGeom& g) {
 }
 
 int make_cols_tensor_map(void* out_map, void* base, const AxisGeom& g) {
+    return make_cols_tensor_map_w(out_map, base, g, tma_cols_width(g.n));
+}
+
+int make_cols_tensor_map_w(void* out_map, void* base, const AxisGeom& g, int W) {
     static EncodeTiledFn encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -650,7 +683,7 @@ int make_cols_tensor_map(void* out_map, void* base, const AxisGeom& g) {
     if (g.outer > 1 && g.block != g.n * g.inner) return -2;  // contiguous outer blocks only
     const cuuint64_t dims[3] = {(cuuint64_t)(2 * g.inner), (cuuint64_t)g.n, (cuuint64_t)g.outer};
     const cuuint64_t strides[2] = {(cuuint64_t)(g.inner * 16), (cuuint64_t)(g.block * 16)};
-    const cuuint32_t box[3] = {(cuuint32_t)(2 * tma_cols_width(g.n)), (cuuint32_t)(g.n < 256 ? g.n : 256), 1};
+    const cuuint32_t box[3] = {(cuuint32_t)(2 * W), (cuuint32_t)(g.n < 256 ? g.n : 256), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = encode(reinterpret_cast<CUtensorMap*>(out_map), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides,
                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
