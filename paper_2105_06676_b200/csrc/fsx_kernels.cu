@@ -477,12 +477,19 @@ __device__ __forceinline__ void pair_mode0_real_x4(const RowPairArgs& a, double2
         wk[i] = phase_at(a.wk, k[i]);
         x[i] = x[4 + i] = 0.0;
     }
+    int last = 0;  // cos is even in o: offset 0 reads nothing, +-o share one read (see real_block_symbol)
+    double lastc[4] = {1.0, 1.0, 1.0, 1.0};
     for (int j = 0; j < a.ntaps; ++j) {
-        const int o = a.tap_off[j];
+        const int o = a.tap_off[j], ao = o < 0 ? -o : o;
         const double b = a.tap_b[j][0], bp = (o & 1) ? -b : b;
+        if (ao != 0 && ao != last) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) lastc[i] = phase_at(a.wk, modp(k[i] * (i64)ao, L)).x;
+            last = ao;
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const double c = phase_at(a.wk, modp(k[i] * (i64)o, L)).x;
+            const double c = ao == 0 ? 1.0 : lastc[i];
             x[i] = fma(b, c, x[i]);
             x[4 + i] = fma(bp, c, x[4 + i]);
         }
@@ -569,10 +576,21 @@ __device__ __forceinline__ void pair_mode1(const RowPairArgs& a, double2& zk, do
 // Real 2x2 symbols of two frequencies at once: the two binary-exponentiation
 // chains are independent, so interleaving them doubles the FP64 ILP of the
 // power (the row-pair pass of cfg5 is bound by this loop at T = 1e6).
+// cos(2 pi k o / N) is even in o: offset 0 needs no table read, and +-o share
+// one (the taps come in sorted order, so the two of a pair are looked up by
+// |o| from a one-entry cache of the last nonzero |o|; a symmetric 3-point
+// stencil reads one two-level phase per frequency instead of three).
 __device__ __forceinline__ void real_block_symbol(const RowPairArgs& a, i64 k, i64 N, double (&l)[4]) {
     l[0] = l[1] = l[2] = l[3] = 0.0;
+    int last = 0;
+    double lastc = 1.0;
     for (int j = 0; j < a.ntaps; ++j) {
-        const double c = phase_at(a.wk, modp(k * (i64)a.tap_off[j], N)).x;
+        const int o = a.tap_off[j] < 0 ? -a.tap_off[j] : a.tap_off[j];
+        if (o != 0 && o != last) {
+            lastc = phase_at(a.wk, modp(k * (i64)o, N)).x;
+            last = o;
+        }
+        const double c = o == 0 ? 1.0 : lastc;
 #pragma unroll
         for (int e = 0; e < 4; ++e) l[e] = fma(a.tap_b[j][e], c, l[e]);
     }
