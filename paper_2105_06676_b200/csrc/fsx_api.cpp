@@ -689,6 +689,15 @@ fsx::FusedSymbol fused_symbol(const Plan& p, const Taps& taps, u64 T, const Taps
     s.ntaps = j;
     s.ngroups = (int)gid.size();
     s.real = symmetric_taps(taps) && (!q || symmetric_taps(*q)) ? 1 : 0;
+    // +-og partner groups of one tap set (complex symbols share their phase reads)
+    for (int g = 0; g < s.ngroups; ++g) {
+        if (s.group_off[g] <= 0) continue;
+        for (int h = 0; h < s.ngroups; ++h)
+            if (s.group_off[h] == -s.group_off[g] && s.group_set[h] == s.group_set[g]) {
+                s.group_partner[g] = 1 + h;
+                s.group_partner[h] = -1;
+            }
+    }
     return s;
 }
 

@@ -66,6 +66,8 @@ struct FusedSymbol {
     i64 P = 1;                   // half-spectrum row pitch (complex)
     i64 M = 1;                   // L / 2
     int group_off[kMaxGroups];   // axis-0 offset of each group
+    int group_partner[kMaxGroups] = {};  // complex symbols: for og > 0, 1 + the group of -og (0: none);
+                                         // -1: an -og group folded into its partner
     int tap_group[kMaxFusedTaps];
     int tap_o1[kMaxFusedTaps];   // axis-1 offset (rank 3)
     int tap_olast[kMaxFusedTaps];

@@ -317,16 +317,28 @@ __device__ __forceinline__ void spectral_regs_at(double2 (&v)[R], int kbase, int
 #pragma unroll
         for (int q = 0; q < R; ++q) v[q] = cscale(v[q], lam[q] * sym.scale);
     } else {
+        // complex symbol: offset 0 needs no phase (a * 1 = a exactly), and a group
+        // with offset -og shares the phase read of its partner +og
+        // (exp(-i phi) = conj(exp(i phi)); FusedSymbol::group_partner)
         double2 lam[R];
 #pragma unroll
         for (int q = 0; q < R; ++q) lam[q] = make_double2(0.0, 0.0);
         for (int gi = 0; gi < sym.ngroups; ++gi) {
+            const int pg = sym.group_partner[gi] - 1;  // -1: none
+            if (pg == -2) continue;                     // folded into its +og partner
             const double2 a = acoef(gi);
             const i64 og = sym.group_off[gi];
+            if (og == 0) {
+#pragma unroll
+                for (int q = 0; q < R; ++q) lam[q] = cadd(lam[q], a);
+                continue;
+            }
+            const double2 am = pg >= 0 ? acoef(pg) : make_double2(0.0, 0.0);
 #pragma unroll
             for (int q = 0; q < R; ++q) {
                 const double2 e = eplus_tab(tw_all, N, (i64)(kbase + q * kstride) * og);
                 lam[q] = cadd(lam[q], cmul(a, e));
+                if (pg >= 0) lam[q] = cadd(lam[q], cmul(am, cconj(e)));
             }
         }
 #pragma unroll
