@@ -240,13 +240,17 @@ __device__ __forceinline__ void symbol_real_set(double (&lam)[R], int t, const F
     for (int q = 0; q < R; ++q) lam[q] = 0.0;
     for (int gi = 0; gi < sym.ngroups; ++gi) {
         if (sym.group_set[gi] != set) continue;
-        const double2 a = acoef(gi);
+        if (sym.group_partner[gi] < 0) continue;  // -og of a symmetric pair: counted with +og below
+        double2 a = acoef(gi);
         const i64 og = sym.group_off[gi];
         if (og == 0) {  // exp(0) = 1: no table read
 #pragma unroll
             for (int q = 0; q < R; ++q) lam[q] += a.x;
             continue;
         }
+        // symmetric taps: A_{-og} = conj(A_og) and exp(-i phi) = conj(exp(i phi)), so the pair
+        // contributes 2 Re(A_og exp(i phi)) -- one set of phase reads for both
+        if (sym.group_partner[gi] > 0) a = make_double2(2.0 * a.x, 2.0 * a.y);
         if constexpr (R == 16 && TPL * 16 == N) {
             eplus16<N>(tw_all, t, og, [&](int q, double2 e) { lam[q] = fma(a.x, e.x, fma(-a.y, e.y, lam[q])); });
         } else {
