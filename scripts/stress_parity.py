@@ -4,7 +4,7 @@ symmetric or not), random T, each solved through the fp64 host API, the fp32
 mode and the spectral cut, checked against the CPU oracle; then random
 implicit (Crank-Nicolson-like) solves against the oracle and batches against
 single calls (bitwise).
-    python scripts/stress_parity.py [cases] [seed]"""
+    python scripts/stress_parity.py [cases] [seed] [max cells]"""
 import os
 import sys
 
@@ -34,7 +34,7 @@ def rel(a, b):
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
-    pow2 = [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096]
+    pow2 = [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096, 8192]
     other = [3, 5, 6, 7, 12, 15, 24, 100, 255, 300]
     worst = {"f64": 0.0, "f32": 0.0, "cut": 0.0}
     fails = 0
@@ -42,7 +42,7 @@ def main():
         rank = int(rng.integers(1, 4))
         m = 2 if (rank == 1 and rng.random() < 0.25) else 1
         dims = []
-        budget = 1 << 18
+        budget = int(sys.argv[3]) if len(sys.argv) > 3 else 1 << 18
         for a in range(rank):
             choices = pow2 if rng.random() < 0.8 else other
             if rng.random() < 0.1:
