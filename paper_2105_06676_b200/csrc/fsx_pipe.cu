@@ -158,7 +158,7 @@ k_c2r_pipe(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64
 // version fits one 128 KB CTA per SM: 8 warps, 250 registers).
 template <int M, int ST>
 struct BulkCfg {
-    static constexpr int MINB = ST == 2 ? PCfg<M>::MINB_ROW : 2;
+    static constexpr int MINB = ST == 2 ? PCfg<M>::MINB_ROW : ST == 1 ? 2 : 1;
 };
 
 // BLK: the output goes to the slab exchange layout (blocked, or straight
@@ -183,18 +183,22 @@ k_r2c_bulk(const TI* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, 
         for (int b = 0; b < ST; ++b) mbar_init(&bar[b], 1);
         mbar_init_fence();
         pdl_wait();  // x may be the predecessor's output
-        if (row < nrows) {
-            mbar_expect_tx(&bar[0], BYTES);
-            bulk_load(sm, x + row * L, BYTES, &bar[0]);
-        }
+#pragma unroll
+        for (int b = 0; b < (ST > 1 ? ST - 1 : 1); ++b)  // ST > 1: the first ST - 1 rows in flight
+            if (row + b * G < nrows) {
+                mbar_expect_tx(&bar[b], BYTES);
+                bulk_load(sm + b * M, x + (row + b * G) * L, BYTES, &bar[b]);
+            }
     }
     __syncthreads();
     unsigned par = 0;  // bit s: parity of the next completion of stage s
-    for (int s = 0; row < nrows; row += G, s = (ST == 2 ? s ^ 1 : 0)) {
+    for (int s = 0; row < nrows; row += G, s = (ST > 1 ? (s + 1) % ST : 0)) {
         const i64 nxt = row + G;
-        if (ST == 2 && t == 0 && nxt < nrows) {
-            mbar_expect_tx(&bar[s ^ 1], BYTES);
-            bulk_load(sm + (s ^ 1) * M, x + nxt * L, BYTES, &bar[s ^ 1]);
+        const i64 pre = row + (ST - 1) * G;  // ST > 1: the row that now enters the stage the last one freed
+        const int sp = (s + ST - 1) % ST;
+        if (ST > 1 && t == 0 && pre < nrows) {
+            mbar_expect_tx(&bar[sp], BYTES);
+            bulk_load(sm + sp * M, x + pre * L, BYTES, &bar[sp]);
         }
         if (nxt >= nrows) pdl_trigger();  // last row of this CTA: let the successor launch
         mbar_wait(&bar[s], (par >> s) & 1u);
@@ -303,13 +307,17 @@ k_c2r_bulk(const double2* __restrict__ H, TO* __restrict__ x, i64 nrows, i64 L, 
         for (int b = 0; b < ST; ++b) mbar_init(&bar[b], 1);
         mbar_init_fence();
         pdl_wait();  // H is the predecessor's output
-        if (row < nrows) load_hrow<M, BLK>(sm, H, lay, row, &bar[0]);
+#pragma unroll
+        for (int b = 0; b < (ST > 1 ? ST - 1 : 1); ++b)
+            if (row + b * G < nrows) load_hrow<M, BLK>(sm + b * SS, H, lay, row + b * G, &bar[b]);
     }
     __syncthreads();
     unsigned par = 0;
-    for (int s = 0; row < nrows; row += G, s = (ST == 2 ? s ^ 1 : 0)) {
+    for (int s = 0; row < nrows; row += G, s = (ST > 1 ? (s + 1) % ST : 0)) {
         const i64 nxt = row + G;
-        if (ST == 2 && t == 0 && nxt < nrows) load_hrow<M, BLK>(sm + (s ^ 1) * SS, H, lay, nxt, &bar[s ^ 1]);
+        const i64 pre = row + (ST - 1) * G;
+        const int sp = (s + ST - 1) % ST;
+        if (ST > 1 && t == 0 && pre < nrows) load_hrow<M, BLK>(sm + sp * SS, H, lay, pre, &bar[sp]);
         if (nxt >= nrows) pdl_trigger();
         mbar_wait(&bar[s], (par >> s) & 1u);
         par ^= 1u << s;
@@ -495,14 +503,17 @@ static cudaError_t c2r_pipe_m(const double2* H, double* x, i64 nrows, i64 L, con
     return cudaGetLastError();
 }
 
-// FSX_ROW_STAGES=1 selects one stage x 2 CTAs/SM (A/B); default 2 stages
+// FSX_ROW_STAGES=1/2/3 selects the stage count (A/B); default 3 at M = 4096, else 2
 static int row_stages(int M) {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("FSX_ROW_STAGES");
         v = e ? atoi(e) : 0;
     }
-    return v == 1 ? 1 : 2;  // 1 stage x 2 CTAs measured slower at M = 4096 (269 vs 254 us)
+    // 1 stage x 2 CTAs measured slower at M = 4096 (269 vs 254 us); 3 stages (two rows in flight,
+    // one 192 KB CTA per SM) measured 243 -> 238 us for the M = 4096 R2C rows (default there)
+    if (v == 1 || v == 2 || v == 3) return v;
+    return M == 4096 ? 3 : 2;
 }
 
 template <int M, int ST, bool BLK>
@@ -519,6 +530,8 @@ template <int M>
 static cudaError_t r2c_bulk_m(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
                               cudaStream_t s) {
     if (lay.blk) return r2c_bulk_ms<M, 2, true>(x, H, nrows, L, lay, tw, s);
+    if constexpr (M == 4096)  // FSX_ROW_STAGES=3: three 64 KB stages (two rows in flight)
+        if (row_stages(M) == 3) return r2c_bulk_ms<M, 3, false>(x, H, nrows, L, lay, tw, s);
     return row_stages(M) == 1 ? r2c_bulk_ms<M, 1, false>(x, H, nrows, L, lay, tw, s)
                               : r2c_bulk_ms<M, 2, false>(x, H, nrows, L, lay, tw, s);
 }
@@ -537,6 +550,8 @@ template <int M>
 static cudaError_t c2r_bulk_m(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
                               Flags* f, cudaStream_t s) {
     if (lay.blk) return c2r_bulk_ms<M, 2, true>(H, x, nrows, L, lay, tw, f, s);
+    if constexpr (M == 4096)
+        if (row_stages(M) == 3) return c2r_bulk_ms<M, 3, false>(H, x, nrows, L, lay, tw, f, s);
     return row_stages(M) == 1 ? c2r_bulk_ms<M, 1, false>(H, x, nrows, L, lay, tw, f, s)
                               : c2r_bulk_ms<M, 2, false>(H, x, nrows, L, lay, tw, f, s);
 }
