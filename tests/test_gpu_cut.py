@@ -47,6 +47,7 @@ CASES = [
     ([512, 2048], box9(7), 1000, False),      # 4-column tiles, L = 2048 (T too small: nothing provably 0)
     ([8192, 1024], JACOBI, 5000, True),       # 8192-point columns (parity halves pass)
     ([4096, 4096], JACOBI, 10000, True),      # cfg2 full size
+    ([512, 8192], JACOBI, 20000, True),       # 4096-complex rows (three-stage row kernels)
     ([256, 1024], {(0, 0): 0.5, (0, 1): 0.5}, 300, True),   # complex, |lam| = |cos(theta_x / 2)|: top columns
 ]
 
