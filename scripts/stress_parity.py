@@ -40,7 +40,7 @@ def main():
     fails = 0
     for i in range(cases):
         rank = int(rng.integers(1, 4))
-        m = 2 if (rank == 1 and rng.random() < 0.25) else 1
+        m = 2 if (rank == 1 and rng.random() < 0.25) else (int(rng.integers(2, 4)) if rng.random() < 0.1 else 1)
         dims = []
         budget = int(sys.argv[3]) if len(sys.argv) > 3 else 1 << 18
         for a in range(rank):
