@@ -149,43 +149,73 @@ def dist_env():
     return ws, rank, local
 
 
-def cpu_reference(cfg, steps, warmup, budget_s=150.0):
-    """Times the reference CPU path (oracle restatement of proj/src/periodic.cpp,
-    all host threads) on a bounded sample of the workload.  Returns
-    (cell-updates/s, sample description, cores)."""
-    import numpy as np
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    from oracle import oracle as orc
 
-    orc.build()
-    cores = orc.thread_count()
-    # calibrate on a small square of the same family, extrapolate N log N
+def mem_available_bytes():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def oracle_peak_bytes(cells, m):
+    """Peak host RAM of the reference pipeline (~96 N bytes
+    for m = 1, ~(32 m^2 + 80 m) N for m > 1)."""
+    return cells * (96 if m == 1 else 32 * m * m + 80 * m)
+
+
+def cpu_sample(cfg, budget_s=None):
+    """The CPU reference's workload: the FULL configured grid whenever the
+    host has the RAM for the reference pipeline (and, if `budget_s` is given,
+    one solve fits that budget by an N log N estimate); otherwise the largest
+    halved grid that does.  Returns (sample config, offsets, blocks, a0)."""
     dims = list(cfg.dims)
-    rank = len(dims)
-    small = [max(8, d // (16 if rank > 1 else 64)) for d in dims]
-    sc = cfg.scaled(small)
-    off, blk = sc.kernel().arrays()
-    a = sc.initial()
-    t0 = time.perf_counter()
-    orc.solve_periodic(a, small, cfg.fields, off, blk, cfg.T, vector=cfg.fields > 1)
-    t_small = max(time.perf_counter() - t0, 1e-4)
-    n_s = sc.cells()
+    avail = mem_available_bytes()
 
-    def estimate(d):
-        n = math.prod(d)
-        return t_small * (n / n_s) * (math.log2(n) / max(math.log2(n_s), 1.0))
+    def fits(d):
+        return oracle_peak_bytes(math.prod(d), cfg.fields) < 0.8 * avail if avail else True
 
-    runs = max(1, steps + warmup)
     use = dims
-    while estimate(use) * runs > budget_s and math.prod(use) > 4096:
+    est = None
+    if budget_s is not None:
+        from oracle import oracle as orc
+
+        small = [max(8, d // (16 if len(dims) > 1 else 64)) for d in dims]
+        sc = cfg.scaled(small)
+        off, blk = sc.kernel().arrays()
+        a = sc.initial()
+        t0 = time.perf_counter()
+        orc.solve_periodic(a, small, cfg.fields, off, blk, cfg.T, vector=cfg.fields > 1)
+        t_small, n_s = max(time.perf_counter() - t0, 1e-4), sc.cells()
+
+        def est(d):
+            n = math.prod(d)
+            return t_small * (n / n_s) * (math.log2(n) / max(math.log2(n_s), 1.0))
+    while math.prod(use) > 4096 and (not fits(use) or (est is not None and est(use) > budget_s)):
         use = [max(8, d // 2) for d in use]
     sample = cfg.scaled(use) if use != dims else cfg
     off, blk = sample.kernel().arrays()
-    a = sample.initial()
-    return sample, off, blk, a, cores
+    return sample, off, blk, sample.initial()
 
 
 def run_reference(args, cfg):
+    """--impl reference: the reference's CPU path (the oracle restatement of
+    proj/src/periodic.cpp; the reference itself cannot be built here, DESIGN
+    section 1) on all host threads, on the SAME grid as our arm (no sample
+    shrink unless the host lacks the RAM), K timed solves after W warm-ups."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
@@ -193,7 +223,9 @@ def run_reference(args, cfg):
 
     from oracle import oracle as orc
 
-    sample, off, blk, a, cores = cpu_reference(cfg, args.steps, args.warmup)
+    orc.build()
+    cores = orc.thread_count()
+    sample, off, blk, a = cpu_sample(cfg)
     for _ in range(args.warmup):
         orc.solve_periodic(a, sample.dims, sample.fields, off, blk, sample.T, vector=sample.fields > 1)
     times = []
@@ -204,15 +236,17 @@ def run_reference(args, cfg):
     t = sum(times) / len(times)
     value = sample.cells() * sample.T / t
     desc = (f"oracle (CPU restatement of the reference solve_periodic; radix-2/Bluestein FFT, FFT-of-generator "
-            f"spectrum, std::thread chunks) on grid {sample.dims} x{sample.fields}, T={sample.T}"
-            + ("" if sample.dims == cfg.dims else f" (bounded sample of {cfg.dims})"))
+            f"spectrum, std::thread chunks) on grid {sample.dims} x{sample.fields}, T={sample.T}, "
+            f"{cores} threads on {cpu_model()}; mean of {args.steps} solves (best {min(times):.3f} s)"
+            + ("" if sample.dims == cfg.dims else f" (bounded sample of {cfg.dims}: host RAM)"))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (SplitMix64, reference init)",
         "config": {"workload": cfg.name + ": " + cfg.description, "grid": cfg.dims, "fields": cfg.fields,
-                   "T": cfg.T, "sample_grid": sample.dims},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc},
+                   "T": cfg.T, "sample_grid": sample.dims, "same_grid": sample.dims == cfg.dims},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc,
+                         "cpu_model": cpu_model(), "best_s": min(times), "mean_s": t},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
         "checksum": float(np.abs(out).sum()),
@@ -336,6 +370,42 @@ def run_gpu_slab(args, cfg, ws, rank, local):
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
+
+
+def cpu_baseline(cfg):
+    """The reference CPU path timed on this host (rank 0, N = 1): best of 3
+    solves of the configured grid on all host threads (BASELINE.md section 2;
+    a halved-grid sample only when the host lacks the RAM or one solve would
+    exceed ~30 s by an N log N estimate), plus a 1-thread solve of a bounded sample."""
+    from oracle import oracle as orc
+
+    orc.build()
+    cores = orc.thread_count()
+    sample, off, blk, a = cpu_sample(cfg, budget_s=30.0)
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        orc.solve_periodic(a, sample.dims, sample.fields, off, blk, sample.T, vector=sample.fields > 1)
+        ts.append(time.perf_counter() - t0)
+    tc = min(ts)
+    # 1 thread on a bounded sample (the reference's 1D FFTs are serial anyway, SURVEY 8a)
+    s1, off1, blk1, a1 = cpu_sample(cfg, budget_s=4.0)
+    orc.set_threads(1)
+    try:
+        t0 = time.perf_counter()
+        orc.solve_periodic(a1, s1.dims, s1.fields, off1, blk1, s1.T, vector=s1.fields > 1)
+        t1 = time.perf_counter() - t0
+    finally:
+        orc.set_threads(0)
+    return {
+        "value": sample.cells() * sample.T / tc, "unit": UNIT, "cores": cores, "kind": "port",
+        "cpu_model": cpu_model(),
+        "sample": f"best of 3 oracle solve_periodic on grid {sample.dims} x{sample.fields}, T={sample.T}, "
+                  f"{cores} threads ({', '.join(f'{x:.2f}' for x in ts)} s)"
+                  + ("" if sample.dims == cfg.dims else f" (bounded sample of {cfg.dims})"),
+        "one_thread": {"value": s1.cells() * s1.T / t1, "unit": UNIT, "cores": 1, "grid": s1.dims,
+                       "seconds": t1},
+    }
 
 
 def run_gpu(args, cfg):
@@ -565,22 +635,32 @@ def run_gpu(args, cfg):
                        "single_call_value": e2e_single,
                        "single_call_mode": f"one synchronous fsx_solve_periodic{sfx} per step"}
     if rank == 0 and ws == 1 and not args.no_cpu:
-        from oracle import oracle as orc
-
-        sample, off, blk, a, cores = cpu_reference(cfg, 1, 0, budget_s=30.0)
-        t0 = time.perf_counter()
-        orc.solve_periodic(a, sample.dims, sample.fields, off, blk, sample.T, vector=sample.fields > 1)
-        tc = time.perf_counter() - t0
-        line["cpu_baseline"] = {
-            "value": sample.cells() * sample.T / tc, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"one oracle solve_periodic on grid {sample.dims} x{sample.fields}, T={sample.T}"
-                      + ("" if sample.dims == cfg.dims else f" (bounded sample of {cfg.dims})"),
-        }
+        line["cpu_baseline"] = cpu_baseline(cfg)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(n):
+    """`python bench.py --gpus N` without torchrun: relaunch this command as N
+    ranks (one process per GPU) through torch.distributed.run on 127.0.0.1.
+    Exits non-zero when fewer than N GPUs are visible."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"error": f"--gpus {n} requested but {have} CUDA device(s) visible"}), flush=True)
+        sys.exit(3)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
@@ -589,7 +669,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg3",
+                    help="BASELINE config (default cfg3: 8192^2, T=1e5, one of the metric's 1/2/4/8-GPU configs)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--exchange", choices=["auto", "nccl", "p2p"], default="auto",
                     help="slab exchange for N > 1: p2p = fused into the row kernels over NVLink peer memory "
@@ -601,6 +682,8 @@ def main():
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of slabs")
     ap.add_argument("--slab", action="store_true", help="use the slab-decomposed path even at N=1 (under torchrun)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     from paper_2105_06676_b200.synthetic import configs

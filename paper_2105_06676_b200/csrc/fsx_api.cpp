@@ -301,14 +301,48 @@ struct Plan {
     std::vector<char> taps_host;
     int launches = 0;
     i64 alg_bytes = 0, fused_bytes = 0;
+    const char* kernel = "";  // the dominant (fused) kernel of a solve, for measurement
+    // Cross-stream ordering of the plan's workspaces: `done` is recorded after
+    // every enqueue on `last`; a solve on another stream first waits on it, so
+    // two solves that share this plan's buffers never overlap on the GPU.
+    cudaEvent_t done = nullptr;
+    cudaStream_t last = nullptr;
+    Plan() = default;
+    Plan(const Plan&) = delete;
+    Plan& operator=(const Plan&) = delete;
+    ~Plan() {
+        if (done) cudaEventDestroy(done);
+    }
+};
+
+// Orders a solve on stream `st` after the plan's previous enqueue (on any stream).
+void plan_enter(Plan& p, cudaStream_t st) {
+    if (p.done && p.last != st) FSX_CK(cudaStreamWaitEvent(st, p.done, 0));
+}
+void plan_leave(Plan& p, cudaStream_t st) {
+    if (!p.done) FSX_CK(cudaEventCreateWithFlags(&p.done, cudaEventDisableTiming));
+    FSX_CK(cudaEventRecord(p.done, st));
+    p.last = st;
+}
+
+// direct-stepping verifier buffers (per device)
+struct NaiveBufs {
+    DevBuf s0, s1, off, blk;
 };
 
 struct Device {
+    // Serialises the host-side enqueueing of calls on THIS device; calls on
+    // different devices run concurrently (the reference's solvers are safe to
+    // call concurrently, proj/README.md:165-168).
+    std::mutex mu;
     int ordinal = 0;
     cudaStream_t stream = nullptr;
     DevBuf tw_all;
     DevBuf tw_all_f;  // float2 copy (rounded once) for the fp32 mode's fused pass
-    DevBuf flags;  // fsx::Flags
+    DevBuf flags;  // fsx::Flags of deferred device-mode / slab solves (read by fsx_device_check)
+    DevBuf hflags; // fsx::Flags of synchronous host-pointer solves (checked and reset by each call)
+    int dev_general = 0;  // a device-mode general-plan solve ran since the last fsx_device_check
+    NaiveBufs naive;
     std::map<std::string, std::unique_ptr<Plan>> plans;
     cudaEvent_t ev[8];
     bool events = false;
@@ -319,15 +353,32 @@ struct Device {
     DevBuf bflags;  // per-solve Flags of a batch
 };
 
-std::mutex g_mu;
+std::mutex g_map_mu;  // guards g_devices (lookup and creation only)
 std::map<int, std::unique_ptr<Device>> g_devices;
 
+Device& device_create(int ordinal);
+
+// The device object for an ordinal (created on first use), with that device
+// selected on the calling thread.
 Device& device_for(int ordinal) {
-    auto it = g_devices.find(ordinal);
-    if (it != g_devices.end()) {
-        FSX_CK(cudaSetDevice(ordinal));
-        return *it->second;
+    Device* d = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_map_mu);
+        auto it = g_devices.find(ordinal);
+        d = it != g_devices.end() ? it->second.get() : &device_create(ordinal);
     }
+    FSX_CK(cudaSetDevice(ordinal));
+    return *d;
+}
+
+// RAII: the device selected and its mutex held for one API call.
+struct DevLock {
+    Device& dev;
+    std::unique_lock<std::mutex> lk;
+    explicit DevLock(int ordinal) : dev(device_for(ordinal)), lk(dev.mu) {}
+};
+
+Device& device_create(int ordinal) {
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess || count == 0) {
@@ -366,6 +417,8 @@ Device& device_for(int ordinal) {
     }
     d->flags.ensure(sizeof(fsx::Flags));
     FSX_CK(cudaMemset(d->flags.p, 0, sizeof(fsx::Flags)));
+    d->hflags.ensure(sizeof(fsx::Flags));
+    FSX_CK(cudaMemset(d->hflags.p, 0, sizeof(fsx::Flags)));
     for (auto& e2 : d->ev) FSX_CK(cudaEventCreate(&e2));
     d->events = true;
     auto& ref = *d;
@@ -1028,6 +1081,7 @@ struct SlabPlan {
     fsx::AxisGeom axy;  // 3D local y pass
 };
 
+std::mutex g_slab_mu;  // guards the g_slabs map (entries are per device, used under that device's lock)
 std::map<std::string, std::unique_ptr<SlabPlan>> g_slabs;
 
 // Geometry only (no device work): validates and fills the sizes.
@@ -1063,16 +1117,22 @@ void slab_geom(const fsx_shape* global, int P, int r, SlabPlan& sp) {
     }
 }
 
-// Device plan (call with g_mu held and the device selected).
+// Device plan (call with the device's lock held and the device selected).
 SlabPlan& slab_plan(const fsx_shape* global, int P, int r) {
     const Shape s = parse_shape(global);
     int dev = 0;
     cudaGetDevice(&dev);  // the caller selected the device (device_for): plans hold its buffers
-    std::string key = std::to_string(dev) + "#" + std::to_string(P) + "/" + std::to_string(r);
+    const std::string prefix = std::to_string(dev) + "#";
+    std::string key = prefix + std::to_string(P) + "/" + std::to_string(r);
     for (i64 d : s.dims) key += ":" + std::to_string(d);
+    std::lock_guard<std::mutex> lk(g_slab_mu);
     auto it = g_slabs.find(key);
     if (it != g_slabs.end()) return *it->second;
-    if (g_slabs.size() >= 16) g_slabs.clear();
+    // bounded: drop this device's other slab plans (never another device's, which may be in use)
+    int mine = 0;
+    for (const auto& e : g_slabs) mine += e.first.rfind(prefix, 0) == 0;
+    if (mine >= 16)
+        for (auto e = g_slabs.begin(); e != g_slabs.end();) e = e->first.rfind(prefix, 0) == 0 ? g_slabs.erase(e) : std::next(e);
     auto sp = std::make_unique<SlabPlan>();
     slab_geom(global, P, r, *sp);
     if (sp->dims.size() == 3) {
@@ -1174,11 +1234,11 @@ void judge_flags(const fsx::Flags& h, int kind, const std::string& where = "") {
     }
 }
 
-void check_flags(Device& dev, int kind, cudaStream_t st) {
+void check_flags(const DevBuf& fl, int kind, cudaStream_t st) {
     fsx::Flags h;
-    FSX_CK(cudaMemcpyAsync(&h, dev.flags.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    FSX_CK(cudaMemcpyAsync(&h, fl.p, sizeof(h), cudaMemcpyDeviceToHost, st));
     FSX_CK(cudaStreamSynchronize(st));
-    FSX_CK(cudaMemsetAsync(dev.flags.p, 0, sizeof(fsx::Flags), st));
+    FSX_CK(cudaMemsetAsync(fl.p, 0, sizeof(fsx::Flags), st));
     judge_flags(h, kind);
 }
 
@@ -1190,10 +1250,6 @@ cudaStream_t stream_of(Device& dev, const fsx_options* opt) {
 // evolve_periodic_naive / step_periodic (proj/src/oracle.cpp:90-115) on the
 // GPU: T direct stencil steps, bitwise equal to the reference loop.  Not on
 // the solve path; a full-size independent check of the FFT solver.
-struct NaiveBufs {
-    DevBuf s0, s1, off, blk;
-};
-std::map<int, std::unique_ptr<NaiveBufs>> g_naive;
 
 void evolve_naive(const fsx_shape* shape, const double* a0, const fsx_kernel* k, u64 T, double* out,
                   const fsx_options* opt, bool device_ptrs) {
@@ -1210,16 +1266,14 @@ void evolve_naive(const fsx_shape* shape, const double* a0, const fsx_kernel* k,
     const int rk = s.rank();
     if (rk <= 3 && ((rk == 3 && s.dims[0] > 65535) || (rk >= 2 && s.dims[rk - 2] > 65535)))
         throw SpecErr("evolve_periodic_naive: leading axes must be <= 65535");
-    std::lock_guard<std::mutex> lk(g_mu);
-    Device& dev = device_for(opt ? opt->device : 0);
+    DevLock dlk(opt ? opt->device : 0);
+    Device& dev = dlk.dev;
     cudaStream_t st = stream_of(dev, opt);
     if (T == 0) {
         if (out != a0) FSX_CK(cudaMemcpyAsync(out, a0, bytes, cudaMemcpyDeviceToDevice, st));
         return;
     }
-    auto& slot = g_naive[dev.ordinal];
-    if (!slot) slot = std::make_unique<NaiveBufs>();
-    NaiveBufs& nb = *slot;
+    NaiveBufs& nb = dev.naive;
     fsx::NaiveGeom g;
     g.rank = rk;
     g.m = s.fields;
@@ -1330,8 +1384,8 @@ void solve(const SolveReq& rq) {
         if (out != in) std::memmove(out, in, bytes);
         return;
     }
-    std::lock_guard<std::mutex> lk(g_mu);
-    Device& dev = device_for(ordinal);
+    DevLock dlk(ordinal);
+    Device& dev = dlk.dev;
     cudaStream_t st = stream_of(dev, rq.opt);
     if (rq.T == 0) {
         if (out != in) FSX_CK(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, st));
@@ -1344,11 +1398,17 @@ void solve(const SolveReq& rq) {
     Plan& p = *pp;
     if (rq.q && p.kind == kFusedR2C) p.qmax.ensure(8);
     Stamps sp{&dev, rq.st != nullptr || (rq.device_ptrs && rq.opt && rq.opt->stage_events), st};
+    plan_enter(p, st);
     if (rq.device_ptrs) {
         if (f32) run_plan_f32(p, dev, taps, rq.T, rq.a0f, rq.outf, st, sp, nullptr, cut);
         else run_plan(p, dev, taps, rq.q ? &qtaps : nullptr, rq.T, rq.a0, rq.out, st, sp, nullptr, nullptr, nullptr, cut);
+        plan_leave(p, st);
+        if (p.kind == kGeneral) dev.dev_general = 1;  // fsx_device_check applies the residue test
         return;
     }
+    // host solves: their own flags slot (a deferred device-mode solve's flags
+    // must neither fail nor mask this call's check)
+    fsx::Flags* hfl = dev.hflags.as<fsx::Flags>();
     DevBuf& bin = f32 ? p.f_in : p.d_in;
     DevBuf& bout = f32 ? p.f_out : p.d_out;
     bin.ensure(bytes);
@@ -1356,12 +1416,13 @@ void solve(const SolveReq& rq) {
     cudaEvent_t h0 = dev.ev[6], h1 = dev.ev[7];
     if (sp.on) FSX_CK(cudaEventRecord(h0, st));
     FSX_CK(cudaMemcpyAsync(bin.p, in, bytes, cudaMemcpyHostToDevice, st));
-    if (f32) run_plan_f32(p, dev, taps, rq.T, p.f_in.as<float>(), p.f_out.as<float>(), st, sp, nullptr, cut);
+    if (f32) run_plan_f32(p, dev, taps, rq.T, p.f_in.as<float>(), p.f_out.as<float>(), st, sp, hfl, cut);
     else run_plan(p, dev, taps, rq.q ? &qtaps : nullptr, rq.T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp,
-                  nullptr, nullptr, nullptr, cut);
+                  hfl, nullptr, nullptr, cut);
     FSX_CK(cudaMemcpyAsync(out, bout.p, bytes, cudaMemcpyDeviceToHost, st));
     if (sp.on) FSX_CK(cudaEventRecord(h1, st));
-    check_flags(dev, p.kind, st);
+    plan_leave(p, st);
+    check_flags(dev.hflags, p.kind, st);
     if (sp.on) {
         float t[4] = {0, 0, 0, 0}, pre = 0, post = 0;
         for (int i = 0; i < 3; ++i) FSX_CK(cudaEventElapsedTime(&t[i], dev.ev[i], dev.ev[i + 1]));
@@ -1402,8 +1463,8 @@ void solve_batch(const fsx_shape* shape, i64 nb, const TE* const* a0s, const fsx
         return;
     }
     if (nb == 0) return;
-    std::lock_guard<std::mutex> lk(g_mu);
-    Device& dev = device_for(opt ? opt->device : 0);
+    DevLock dlk(opt ? opt->device : 0);
+    Device& dev = dlk.dev;
     const int force_general = opt && opt->path == 1;
     const bool cut = opt && opt->spectral_cut;
     Plan* pl[2];
@@ -1424,6 +1485,8 @@ void solve_batch(const fsx_shape* shape, i64 nb, const TE* const* a0s, const fsx
         FSX_CK(cudaEventRecord(dev.lane_ev[1], reinterpret_cast<cudaStream_t>(opt->stream)));
         FSX_CK(cudaStreamWaitEvent(dev.lanes[0], dev.lane_ev[1], 0));
     }
+    plan_enter(*pl[0], dev.lanes[0]);
+    plan_enter(*pl[1], dev.lanes[0]);
     FSX_CK(cudaEventRecord(dev.lane_ev[0], dev.lanes[0]));
     FSX_CK(cudaStreamWaitEvent(dev.lanes[1], dev.lane_ev[0], 0));
     for (i64 i = 0; i < nb; ++i) {
@@ -1439,6 +1502,8 @@ void solve_batch(const fsx_shape* shape, i64 nb, const TE* const* a0s, const fsx
                       nullptr, cut);
         FSX_CK(cudaMemcpyAsync(outs[i], bout.p, bytes, cudaMemcpyDeviceToHost, st));
     }
+    plan_leave(*pl[1], dev.lanes[1]);
+    plan_leave(*pl[0], dev.lanes[0]);
     std::vector<fsx::Flags> h((size_t)nb);
     FSX_CK(cudaStreamSynchronize(dev.lanes[1]));
     FSX_CK(cudaMemcpyAsync(h.data(), fl, (size_t)nb * sizeof(fsx::Flags), cudaMemcpyDeviceToHost, dev.lanes[0]));
@@ -1478,7 +1543,7 @@ fsx_status guarded(F&& f) {
 // The spectrum itself is analytic on the GPU, so the cache keeps the kernel.
 struct fsx_spectrum_cache {
     std::mutex mu;
-    std::map<std::vector<i64>, Taps> by_dims;
+    std::map<std::vector<i64>, Taps> by_dims;  // the first kernel seen for a dims vector (Taps::m = its fields)
 };
 
 extern "C" {
@@ -1527,6 +1592,9 @@ fsx_status fsx_solve_periodic_cached(const fsx_shape* shape, const double* a0, c
             if (it == cache->by_dims.end()) it = cache->by_dims.emplace(sh.dims, taps).first;
             cached = it->second;
         }
+        // the cached spectrum keeps its own block size: a grid with another
+        // field count fails in hadamard, as in the reference (spectrum.cpp:111-116)
+        if (cached.m != sh.fields) throw SpecErr("hadamard: shape mismatch");
         SolveReq rq{shape, a0, k, nullptr, T, out, opt, st};
         rq.cached = &cached;
         solve(rq);
@@ -1600,17 +1668,21 @@ fsx_status fsx_solve_periodic_batch_f32(const fsx_shape* shape, int64_t nbatch, 
 
 fsx_status fsx_device_check(const fsx_options* opt) {
     return guarded([&] {
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(opt ? opt->device : 0);
-        check_flags(dev, kFusedR2C, stream_of(dev, opt));
+        DevLock dlk(opt ? opt->device : 0);
+        Device& dev = dlk.dev;
+        // the reference's imaginary-residue test applies when a complex
+        // (general-plan) solve was enqueued since the last check
+        const int kind = dev.dev_general ? kGeneral : kFusedR2C;
+        dev.dev_general = 0;
+        check_flags(dev.flags, kind, stream_of(dev, opt));
     });
 }
 
 fsx_status fsx_last_stage_ms(const fsx_options* opt, double* ms) {
     return guarded([&] {
         if (!ms) throw SpecErr("fsx_last_stage_ms: null output");
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(opt ? opt->device : 0);
+        DevLock dlk(opt ? opt->device : 0);
+        Device& dev = dlk.dev;
         FSX_CK(cudaEventSynchronize(dev.ev[3]));
         for (int i = 0; i < 3; ++i) {
             float t = 0;
@@ -1640,8 +1712,8 @@ fsx_status fsx_slab_forward(const fsx_shape* global, int32_t nranks, int32_t ran
                             double* d_send, const fsx_options* opt) {
     return guarded([&] {
         if (!d_local_in || !d_send) throw SpecErr("fsx_slab_forward: null pointer");
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(opt ? opt->device : 0);
+        DevLock dlk(opt ? opt->device : 0);
+        Device& dev = dlk.dev;
         SlabPlan& sp = slab_plan(global, nranks, rank);
         slab_forward(sp, dev, d_local_in, reinterpret_cast<double2*>(d_send), stream_of(dev, opt));
     });
@@ -1655,8 +1727,8 @@ fsx_status fsx_slab_spectral(const fsx_shape* global, const fsx_kernel* k, uint6
         const Taps taps = parse_kernel(k);
         require_fits(taps, s);
         if ((i64)taps.map.size() > fsx::kMaxFusedTaps) throw SpecErr("slab: at most 64 taps");
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(opt ? opt->device : 0);
+        DevLock dlk(opt ? opt->device : 0);
+        Device& dev = dlk.dev;
         SlabPlan& sp = slab_plan(global, nranks, rank);
         slab_spectral(sp, dev, taps, T, reinterpret_cast<double2*>(d_recv), stream_of(dev, opt));
     });
@@ -1666,8 +1738,8 @@ fsx_status fsx_slab_inverse(const fsx_shape* global, int32_t nranks, int32_t ran
                             double* d_local_out, const fsx_options* opt) {
     return guarded([&] {
         if (!d_send || !d_local_out) throw SpecErr("fsx_slab_inverse: null pointer");
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(opt ? opt->device : 0);
+        DevLock dlk(opt ? opt->device : 0);
+        Device& dev = dlk.dev;
         SlabPlan& sp = slab_plan(global, nranks, rank);
         slab_inverse(sp, dev, reinterpret_cast<const double2*>(d_send), d_local_out, stream_of(dev, opt));
     });
@@ -1689,8 +1761,8 @@ fsx_status fsx_slab_forward_p2p(const fsx_shape* global, int32_t nranks, int32_t
                                 void* const* d_recv_peers, const fsx_options* opt) {
     return guarded([&] {
         if (!d_local_in) throw SpecErr("fsx_slab_forward_p2p: null pointer");
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(opt ? opt->device : 0);
+        DevLock dlk(opt ? opt->device : 0);
+        Device& dev = dlk.dev;
         SlabPlan& sp = slab_p2p_plan(global, nranks, rank, d_recv_peers);
         fsx::RowLayout lay{0, sp.CB, sp.n0l, reinterpret_cast<double2* const*>(d_recv_peers), (i64)rank * sp.n0l};
         FSX_CK(fsx::launch_r2c_rows(d_local_in, nullptr, sp.n0l, sp.L, lay, dev.tw_all.as<double2>(), stream_of(dev, opt)));
@@ -1701,8 +1773,8 @@ fsx_status fsx_slab_inverse_p2p(const fsx_shape* global, int32_t nranks, int32_t
                                 double* d_local_out, const fsx_options* opt) {
     return guarded([&] {
         if (!d_local_out) throw SpecErr("fsx_slab_inverse_p2p: null pointer");
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(opt ? opt->device : 0);
+        DevLock dlk(opt ? opt->device : 0);
+        Device& dev = dlk.dev;
         SlabPlan& sp = slab_p2p_plan(global, nranks, rank, d_recv_peers);
         fsx::RowLayout lay{0, sp.CB, sp.n0l, reinterpret_cast<double2* const*>(d_recv_peers), (i64)rank * sp.n0l};
         FSX_CK(fsx::launch_c2r_rows(nullptr, d_local_out, sp.n0l, sp.L, lay, dev.tw_all.as<double2>(),
@@ -1716,8 +1788,8 @@ fsx_status fsx_spectral_cut_columns(const fsx_shape* shape, const fsx_kernel* k,
         const Shape s = parse_shape(shape);
         const Taps taps = parse_kernel(k);
         require_fits(taps, s);
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(0);
+        DevLock dlk(0);
+        Device& dev = dlk.dev;
         Plan& p = get_plan(dev, s, taps, 0);
         const i64 all = p.kind == kFusedR2C ? p.M + 1 : 0;
         const i64 kc = T == 0 ? -1 : plan_kcut(p, taps, T);
@@ -1733,8 +1805,8 @@ fsx_status fsx_plan_describe(const fsx_shape* shape, const fsx_kernel* k, const 
         const Shape s = parse_shape(shape);
         const Taps taps = parse_kernel(k);
         require_fits(taps, s);
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(opt ? opt->device : 0);
+        DevLock dlk(opt ? opt->device : 0);
+        Device& dev = dlk.dev;
         Plan& p = get_plan(dev, s, taps, opt && opt->path == 1);
         info->path = p.kind;
         info->launches = p.launches;
@@ -1749,8 +1821,8 @@ fsx_status fsx_multi_fft(const fsx_shape* shape, const double* in, double* out, 
     return guarded([&] {
         const Shape s = parse_shape(shape);
         if (!in || !out) throw SpecErr("multi_fft: null pointer");
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(0);
+        DevLock dlk(0);
+        Device& dev = dlk.dev;
         cudaStream_t st = dev.stream;
         Taps dummy;
         dummy.rank = s.rank();
@@ -1791,8 +1863,8 @@ fsx_status fsx_spectrum_from_kernel(const fsx_shape* shape, const fsx_kernel* k,
         require_fits(taps, s);
         if (!out) throw SpecErr("spectrum_from_kernel: null output");
         if (s.fields > 8) throw SpecErr("spectrum_from_kernel: fields > 8 not supported on the GPU path");
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(0);
+        DevLock dlk(0);
+        Device& dev = dlk.dev;
         cudaStream_t st = dev.stream;
         Plan& p = get_plan(dev, s, taps, 1);
         fsx::GeneralSymbol sym = general_symbol(p, taps, nullptr, 1, st);
@@ -1817,8 +1889,8 @@ fsx_status fsx_pow_spectrum(const fsx_shape* shape, const double* blocks, uint64
         Shape s;
         size_t bytes;
         spectral_io(shape, s, bytes);
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(0);
+        DevLock dlk(0);
+        Device& dev = dlk.dev;
         cudaStream_t st = dev.stream;
         DevBuf a, b;
         a.ensure(bytes);
@@ -1836,8 +1908,8 @@ fsx_status fsx_pseudo_inverse_spectrum(const fsx_shape* shape, const double* blo
         size_t bytes;
         spectral_io(shape, s, bytes);
         if (s.fields != 1) throw SpecErr("pseudo_inverse_spectrum: scalar spectra only");
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(0);
+        DevLock dlk(0);
+        Device& dev = dlk.dev;
         cudaStream_t st = dev.stream;
         DevBuf a, b, mx;
         a.ensure(bytes);
@@ -1857,8 +1929,8 @@ fsx_status fsx_multiply_spectra(const fsx_shape* shape, const double* a, const d
         Shape s;
         size_t bytes;
         spectral_io(shape, s, bytes);
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(0);
+        DevLock dlk(0);
+        Device& dev = dlk.dev;
         cudaStream_t st = dev.stream;
         DevBuf da, db, dc;
         da.ensure(bytes);
@@ -1878,8 +1950,8 @@ fsx_status fsx_hadamard(const fsx_shape* shape, const double* lam, const double*
         size_t bytes;
         spectral_io(shape, s, bytes);
         const size_t xb = (size_t)s.values() * 16;
-        std::lock_guard<std::mutex> lk(g_mu);
-        Device& dev = device_for(0);
+        DevLock dlk(0);
+        Device& dev = dlk.dev;
         cudaStream_t st = dev.stream;
         DevBuf dl, dx, dy;
         dl.ensure(bytes);

@@ -203,6 +203,17 @@ class StencilKernel:
         return self._cc
 
 
+
+def _u64_T(T) -> "ctypes.c_uint64":
+    """T as the C ABI's uint64_t; the reference's T is uint64_t
+    (proj/include/fftstencil/periodic.hpp:43): outside [0, 2^64) is a SpecError
+    (never a silent wrap-around)."""
+    T = int(T)
+    if T < 0 or T >= 1 << 64:
+        raise SpecError(f"T must be in [0, 2^64), got {T}")
+    return ctypes.c_uint64(T)
+
+
 def fold_kernels(kset) -> StencilKernel:
     """proj/src/kernel.cpp:51-81: m x m matrix of scalar kernels -> one m x m-block kernel."""
     m = len(kset)
@@ -332,7 +343,7 @@ def _solve(fn, a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None,
         raise SpecError("out must be a contiguous float64 array of the grid's size")
     stc = st._push() if st is not None else None
     status = getattr(L, fn)(ctypes.byref(shape_c), a0.data.ctypes.data_as(_DP), ctypes.byref(kc),
-                            ctypes.c_uint64(int(T)), *extra, out.ctypes.data_as(_DP),
+                            _u64_T(T), *extra, out.ctypes.data_as(_DP),
                             ctypes.byref(_opts(path=path, spectral_cut=spectral_cut)),
                             ctypes.byref(stc) if stc is not None else None)
     del keep
@@ -364,7 +375,7 @@ def solve_periodic_cached(a0: FieldGrid, k: StencilKernel, T: int, cache: Spectr
     out = np.empty_like(a0.data)
     stc = st._push() if st is not None else None
     status = L.fsx_solve_periodic_cached(ctypes.byref(shape_c), a0.data.ctypes.data_as(_DP), ctypes.byref(kc),
-                                         ctypes.c_uint64(int(T)), cache._h, out.ctypes.data_as(_DP),
+                                         _u64_T(T), cache._h, out.ctypes.data_as(_DP),
                                          ctypes.byref(_opts()), ctypes.byref(stc) if stc is not None else None)
     del keep
     _lib.check(status)
@@ -383,7 +394,7 @@ def solve_periodic_implicit(q: StencilKernel, s: StencilKernel, a0: FieldGrid, T
     out = np.empty_like(a0.data)
     stc = st._push() if st is not None else None
     status = L.fsx_solve_periodic_implicit(ctypes.byref(shape_c), a0.data.ctypes.data_as(_DP), ctypes.byref(qc),
-                                           ctypes.byref(sc), ctypes.c_uint64(int(T)), out.ctypes.data_as(_DP),
+                                           ctypes.byref(sc), _u64_T(T), out.ctypes.data_as(_DP),
                                            ctypes.byref(_opts()), ctypes.byref(stc) if stc is not None else None)
     del kq, ks
     _lib.check(status)
@@ -420,7 +431,7 @@ def solve_periodic_batch(a0s, k: StencilKernel, T: int, outs=None, spectral_cut:
     L = _lib.load()
     kc, keep = k._c()
     status = L.fsx_solve_periodic_batch(ctypes.byref(shape._c()), ctypes.c_int64(n), ins, ctypes.byref(kc),
-                                        ctypes.c_uint64(int(T)), ous, ctypes.byref(_opts(spectral_cut=spectral_cut)))
+                                        _u64_T(T), ous, ctypes.byref(_opts(spectral_cut=spectral_cut)))
     del keep
     _lib.check(status)
     return outs
@@ -436,7 +447,7 @@ def solve_periodic_device(shape: GridShape, d_a0: int, k: StencilKernel, T: int,
     shape_c = shape._c()
     kc, keep = k._c()
     status = L.fsx_solve_periodic_device(ctypes.byref(shape_c), ctypes.c_void_p(d_a0), ctypes.byref(kc),
-                                         ctypes.c_uint64(int(T)), ctypes.c_void_p(d_out),
+                                         _u64_T(T), ctypes.c_void_p(d_out),
                                          ctypes.byref(_opts(device, path, stream, stage_events, spectral_cut)))
     del keep
     _lib.check(status)
@@ -468,7 +479,7 @@ def solve_periodic_f32(shape: GridShape, a0: np.ndarray, k: StencilKernel, T: in
     kc, keep = k._c()
     stc = st._push() if st is not None else None
     status = L.fsx_solve_periodic_f32(ctypes.byref(shape._c()), a0.ctypes.data_as(_FP), ctypes.byref(kc),
-                                      ctypes.c_uint64(int(T)), out.ctypes.data_as(_FP),
+                                      _u64_T(T), out.ctypes.data_as(_FP),
                                       ctypes.byref(_opts(path=path, spectral_cut=spectral_cut)),
                                       ctypes.byref(stc) if stc is not None else None)
     del keep
@@ -495,7 +506,7 @@ def solve_periodic_batch_f32(shape: GridShape, a0s, k: StencilKernel, T: int, ou
     L = _lib.load()
     kc, keep = k._c()
     status = L.fsx_solve_periodic_batch_f32(ctypes.byref(shape._c()), ctypes.c_int64(m), pi, ctypes.byref(kc),
-                                            ctypes.c_uint64(int(T)), po, ctypes.byref(_opts(spectral_cut=spectral_cut)))
+                                            _u64_T(T), po, ctypes.byref(_opts(spectral_cut=spectral_cut)))
     del keep
     _lib.check(status)
     return outs
@@ -509,7 +520,7 @@ def solve_periodic_device_f32(shape: GridShape, d_a0: int, k: StencilKernel, T: 
     L = _lib.load()
     kc, keep = k._c()
     status = L.fsx_solve_periodic_device_f32(ctypes.byref(shape._c()), ctypes.c_void_p(d_a0), ctypes.byref(kc),
-                                             ctypes.c_uint64(int(T)), ctypes.c_void_p(d_out),
+                                             _u64_T(T), ctypes.c_void_p(d_out),
                                              ctypes.byref(_opts(device, path, stream, stage_events, spectral_cut)))
     del keep
     _lib.check(status)
@@ -531,7 +542,7 @@ def evolve_periodic_naive(a0: FieldGrid, k: StencilKernel, T: int) -> FieldGrid:
     kc, keep = k._c()
     out = np.empty_like(a0.data)
     status = L.fsx_evolve_periodic_naive(ctypes.byref(a0.shape._c()), a0.data.ctypes.data_as(_DP), ctypes.byref(kc),
-                                         ctypes.c_uint64(int(T)), out.ctypes.data_as(_DP), ctypes.byref(_opts()))
+                                         _u64_T(T), out.ctypes.data_as(_DP), ctypes.byref(_opts()))
     del keep
     _lib.check(status)
     return FieldGrid(a0.shape, out)
@@ -543,7 +554,7 @@ def evolve_periodic_naive_device(shape: GridShape, d_a0: int, k: StencilKernel, 
     L = _lib.load()
     kc, keep = k._c()
     status = L.fsx_evolve_periodic_naive_device(ctypes.byref(shape._c()), ctypes.c_void_p(d_a0), ctypes.byref(kc),
-                                                ctypes.c_uint64(int(T)), ctypes.c_void_p(d_out),
+                                                _u64_T(T), ctypes.c_void_p(d_out),
                                                 ctypes.byref(_opts(device, 0, stream)))
     del keep
     _lib.check(status)
@@ -565,7 +576,7 @@ def spectral_cut_columns(shape: GridShape, k: StencilKernel, T: int) -> tuple:
     (fsx_spectral_cut_columns; kept == total where the cut does not apply)."""
     kc, keep = k._c()
     kept, total = ctypes.c_int64(), ctypes.c_int64()
-    _lib.check(_lib.load().fsx_spectral_cut_columns(ctypes.byref(shape._c()), ctypes.byref(kc), ctypes.c_uint64(int(T)),
+    _lib.check(_lib.load().fsx_spectral_cut_columns(ctypes.byref(shape._c()), ctypes.byref(kc), _u64_T(T),
                                                     ctypes.byref(kept), ctypes.byref(total)))
     del keep
     return kept.value, total.value
@@ -629,7 +640,7 @@ def pow_spectrum(lam: DiagonalSpectrum, T: int) -> DiagonalSpectrum:
     """proj/src/spectrum.cpp:47-83"""
     out = np.empty_like(lam.blocks)
     _lib.check(_lib.load().fsx_pow_spectrum(ctypes.byref(lam.shape._c()), lam.blocks.ctypes.data_as(_DP),
-                                            ctypes.c_uint64(int(T)), out.ctypes.data_as(_DP)))
+                                            _u64_T(T), out.ctypes.data_as(_DP)))
     return DiagonalSpectrum(lam.shape, out)
 
 

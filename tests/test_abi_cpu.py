@@ -107,3 +107,22 @@ def test_fold_kernels_and_value_types():
     lam = fs.DiagonalSpectrum(fs.GridShape([3], 2))
     lam.set_block(1, [[1, 2], [3, 4]])
     assert lam.entry(1, 1, 0) == 3
+
+
+def test_T_out_of_range_is_spec_error_on_every_wrapper():
+    """T is the reference's uint64_t (periodic.hpp:43): a negative or >= 2^64 T
+    raises SpecError in every wrapper, before any device work (no wrap-around)."""
+    k = fs.StencilKernel(1).add_tap([0], 0.5).add_tap([1], 0.5)
+    sh = fs.GridShape([16])
+    g = fs.FieldGrid(sh, np.zeros(16))
+    for bad in (-1, 1 << 64):
+        with pytest.raises(fs.SpecError):
+            fs.solve_periodic_cached(g, k, bad, fs.SpectrumCache())
+        with pytest.raises(fs.SpecError):
+            fs.solve_periodic_implicit(k, k, g, bad)
+        with pytest.raises(fs.SpecError):
+            fs.solve_periodic_device(sh, 0, k, bad, 0)
+        with pytest.raises(fs.SpecError):
+            fs.evolve_periodic_naive_device(sh, 0, k, bad, 0)
+        with pytest.raises(fs.SpecError):
+            fs.spectral_cut_columns(sh, k, bad)
