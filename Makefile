@@ -25,7 +25,10 @@ $(CSRC)/fsx_api.o: $(CSRC)/fsx_api.cpp $(CSRC)/fsx_kernels.h include/fsx.h
 $(CSRC)/fsx_naive.o: $(CSRC)/fsx_naive.cu $(CSRC)/fsx_kernels.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@ > build_ptxas_naive.log 2>&1 || (cat build_ptxas_naive.log; false)
 
-$(LIB): $(CSRC)/fsx_kernels.o $(CSRC)/fsx_pipe.o $(CSRC)/fsx_tma.o $(CSRC)/fsx_naive.o $(CSRC)/fsx_api.o
+$(CSRC)/fsx_io.o: $(CSRC)/fsx_io.cpp include/fsx.h
+	g++ -std=c++20 -O2 -fPIC -Wall -Iinclude -I/usr/local/cuda/include -c $< -o $@
+
+$(LIB): $(CSRC)/fsx_kernels.o $(CSRC)/fsx_pipe.o $(CSRC)/fsx_tma.o $(CSRC)/fsx_naive.o $(CSRC)/fsx_api.o $(CSRC)/fsx_io.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart_static -lrt -lpthread -ldl
 
 oracle:

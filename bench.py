@@ -1,10 +1,12 @@
 """Benchmark: StencilFFT-P periodic solve on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl reference]
 
 A step is one full periodic solve a_T = IFFT(FFT(s)^T . FFT(a_0)) of the
-configured synthetic grid.  The default workload is BASELINE configs[1]
-(cfg2: 2D 5-point Jacobi, 4096^2 fp64, T = 1e4).
+configured synthetic grid.  The default workload is BASELINE configs[2]
+(cfg3: 2D 9-point box, 8192^2 fp64, T = 1e5), one of the configs the
+metric is quoted on at 1/2/4/8 GPUs and the largest 2D one that fits a B200;
+`--impl reference` times the reference's CPU path on the same full grid.
 
 `value`  cell-updates/s (cells * T / device time) with a_0 resident in HBM,
          the step timed with CUDA events on the solve's stream, L2 flushed
@@ -57,7 +59,7 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def load_fp64(cfg_name, kernel_ms):
+def load_fp64(cfg_name, kernel_ms, kernel=""):
     """FP64 roofline of the dominant kernel: its per-launch FP64 pipe
     instructions (committed ncu count) over its live CUDA-event time, against
     the measured DFMA instruction rate (profiles/fp64_peak.json)."""
@@ -68,6 +70,8 @@ def load_fp64(cfg_name, kernel_ms):
         return None
     if not cnt or not kernel_ms:
         return None
+    if kernel and kernel.split()[0].split("<")[0] not in cnt.get("kernel", ""):
+        return None  # the committed count is of another kernel than this build's
     peak_ops = peak["fp64_fma_tflops"] / 2.0  # DFMA instructions (tera) per second
     ach = cnt["pipe_ops"] / (kernel_ms * 1e-3) / 1e12
     return {"bound": "fp64 pipe", "achieved_tops": ach, "peak_tops": peak_ops, "frac": ach / peak_ops,
@@ -77,14 +81,31 @@ def load_fp64(cfg_name, kernel_ms):
                       "scripts/micro/fp64_peak.cu (profiles/fp64_peak.json)"}
 
 
-def load_traffic(cfg_name):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+def load_traffic(cfg_name, kernel):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/ncu_traffic.json, stamped with the kernel it measured and
+    the commit it was taken at).  None when the capture is of another kernel
+    than the one this build launches (a stale count is not reported)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(cfg_name)
+            t = json.load(f)
     except Exception:
-        return None
+        return None, None
+    name = t.get(cfg_name + "_kernel", "")
+    if t.get(cfg_name) is None or not kernel.startswith(name.split("<")[0]) or name.split("<")[0] == "":
+        return None, f"no capture of {kernel} in profiles/ncu_traffic.json"
+    return t.get(cfg_name), f"ncu --set full of {name} at {t.get(cfg_name + '_head', 'round-1 HEAD')}"
+
+
+def dominant_kernel(info, cfg):
+    """The kernel bench.py's roofline times (the plan's fused spectral pass)."""
+    if info["path"] == 1:
+        n0 = cfg.dims[0]
+        if n0 == 8192 and len(cfg.dims) == 2:
+            return "k_fused8192c (8192-point columns, 2-CTA cluster)"
+        return f"k_cols_tma<{n0}, 2>"
+    return {2: "k_rowpair", 3: "k_spectral_general"}[info["path"]]
 
 
 class ClockSampler:
@@ -582,7 +603,8 @@ def run_gpu(args, cfg):
     if f32:  # plan 1 reads / writes the grid as floats; the others widen (R/2 + R) and narrow (R + R/2)
         alg_step += -n * 8 if info["path"] == 1 else 3 * n * 8
     pipe_gbs = alg_step / (ms * 1e-3) / 1e9
-    kernel_name = {1: "k_cols_tma", 2: "k_rowpair", 3: "k_spectral_general"}[info["path"]]
+    kernel_name = dominant_kernel(info, cfg)
+    traffic, traffic_src = load_traffic(cfg.name, kernel_name)
     line = {
         "metric": METRIC,
         "value": value,
@@ -613,11 +635,12 @@ def run_gpu(args, cfg):
             "unit": "GB/s",
             "frac": (fused_gbs / peak) if fused_gbs else None,
             "frac_vs_nominal_8tbs": (fused_gbs / NOMINAL_HBM_GBS) if fused_gbs else None,
-            "traffic": load_traffic(cfg.name),
+            "traffic": traffic,
+            "traffic_source": traffic_src,
             "alg_bytes_per_launch": info["fused_bytes"],
             "kernel_ms": fms,
             "peak_source": peak_src,
-            "fp64": None if f32 else load_fp64(cfg.name, fms),  # the fp32 mode's fused pass has its own counts
+            "fp64": None if f32 else load_fp64(cfg.name, fms, kernel_name),  # the fp32 mode's fused pass has its own counts
         },
         "pipeline": {"alg_bytes_per_step": alg_step, "achieved_gbs": pipe_gbs, "frac": pipe_gbs / peak,
                      "frac_vs_nominal_8tbs": pipe_gbs / NOMINAL_HBM_GBS},

@@ -34,7 +34,8 @@ typedef enum fsx_status {
     FSX_ERR_NUMERIC = 2,   /* reference NumericError: non-finite result / residue blow-up */
     FSX_ERR_CUDA = 3,      /* CUDA runtime failure (no device, launch error, ...) */
     FSX_ERR_NCCL = 4,      /* reserved for the multi-GPU path */
-    FSX_ERR_OOM = 5        /* device allocation failed */
+    FSX_ERR_OOM = 5,       /* device allocation failed */
+    FSX_ERR_IO = 6         /* reference IoError: file parsing / reading / writing (errors.hpp:20-24) */
 } fsx_status;
 
 #define FSX_MAX_RANK 8
@@ -245,6 +246,30 @@ fsx_status fsx_multiply_spectra(const fsx_shape* shape, const double* a, const d
 
 /* hadamard (proj/src/spectrum.cpp:111-134): y = lam x per frequency */
 fsx_status fsx_hadamard(const fsx_shape* shape, const double* lam, const double* x, double* y);
+
+/* ---------------------------------------------------------------- grid I/O and the bench stage table
+ * (proj/include/fftstencil/grid_io.hpp,
+ * proj/src/grid_io.cpp, proj/src/runner.cpp:46-115).
+ * raw: little-endian float64, row-major dims then field, plus "<path>.meta"
+ * ("dims = ...", "fields = m", "dtype = float64", "order = row-major");
+ * csv: one line per (cell, field) "i1,...,id,f,value", shortest round-trip
+ * decimals.  Reading detects raw by the presence of the sidecar.  Malformed
+ * input -> FSX_ERR_IO naming the offending line or byte count. */
+#define FSX_GRID_CSV 0
+#define FSX_GRID_RAW 1
+fsx_status fsx_write_grid(const fsx_shape* shape, const double* data, const char* path, int32_t format);
+/* The grid's shape as stored (raw: from the sidecar, validated against the file size). */
+fsx_status fsx_read_grid_shape(const char* path, fsx_shape* shape);
+/* Host read; `shape` (may be NULL) must equal the stored shape. */
+fsx_status fsx_read_grid(const char* path, const fsx_shape* shape, double* out);
+/* Raw grid straight into device memory d_out (opt->device): chunked reads into
+ * two pinned staging buffers, each chunk's H2D overlapping the next read.
+ * Returns after the data is on the device. */
+fsx_status fsx_load_grid_device(const char* path, const fsx_shape* shape, double* d_out, const fsx_options* opt);
+/* run_bench's stage table (runner.cpp:46-62) for accumulated StageTimings,
+ * the call's total seconds and (>= 0) the naive solver's seconds. */
+fsx_status fsx_format_stage_table(const fsx_stage_timings* st, double total, double naive_seconds, char* buf,
+                                  int64_t buflen);
 
 /* ---------------------------------------------------------------- introspection */
 const char* fsx_last_error(void);

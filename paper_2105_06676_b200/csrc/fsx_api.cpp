@@ -1548,6 +1548,9 @@ struct fsx_spectrum_cache {
 
 extern "C" {
 
+// the I/O module's errors (fsx_io.cpp) land in the same thread-local message
+__attribute__((visibility("hidden"))) void fsx_internal_set_error(const char* msg) { g_err = msg ? msg : ""; }
+
 const char* fsx_last_error(void) { return g_err.c_str(); }
 int32_t fsx_version(void) { return 100; }
 

@@ -338,18 +338,55 @@ struct LineFFT {
         }
     }
 
+    // One radix-16 item (C == 1) with derived twiddles, applied as they are
+    // formed: W^1, W^2, W^4, W^8 are read, and every product is consumed right
+    // away, so at most a handful of twiddles are live (the 15-entry w[] array
+    // of the generic path costs 60 registers and spilled at 128).  The products
+    // are the generic path's (w3 = w1 w2, w5 = w1 w4, w6 = w2 w4, w7 = w3 w4,
+    // w(u + 8) = w(u) w8): bitwise the same results.
+    template <int S>
+    __device__ __forceinline__ static void tw16_apply(CT (&a)[16], int t, const CT* __restrict__ tw) {
+        constexpr int Ns = ns<S>();
+        const int k = item<S>(t, 0) & (Ns - 1);
+        const CT* pt = tw + (kPassTabBase + 15 * N + 16 * Ns) + k;
+        const CT w1 = __ldg(pt), w2 = __ldg(pt + Ns), w4 = __ldg(pt + 3 * Ns), w8 = __ldg(pt + 7 * Ns);
+        a[1] = ctw<SIGN>(a[1], w1);
+        a[2] = ctw<SIGN>(a[2], w2);
+        a[4] = ctw<SIGN>(a[4], w4);
+        a[8] = ctw<SIGN>(a[8], w8);
+        a[9] = ctw<SIGN>(a[9], cmul(w1, w8));
+        a[10] = ctw<SIGN>(a[10], cmul(w2, w8));
+        a[12] = ctw<SIGN>(a[12], cmul(w4, w8));
+        const CT w3 = cmul(w1, w2);
+        a[3] = ctw<SIGN>(a[3], w3);
+        a[11] = ctw<SIGN>(a[11], cmul(w3, w8));
+        const CT w5 = cmul(w1, w4);
+        a[5] = ctw<SIGN>(a[5], w5);
+        a[13] = ctw<SIGN>(a[13], cmul(w5, w8));
+        const CT w6 = cmul(w2, w4);
+        a[6] = ctw<SIGN>(a[6], w6);
+        a[14] = ctw<SIGN>(a[14], cmul(w6, w8));
+        const CT w7 = cmul(w3, w4);
+        a[7] = ctw<SIGN>(a[7], w7);
+        a[15] = ctw<SIGN>(a[15], cmul(w7, w8));
+    }
+
     template <int S>
     __device__ __forceinline__ static void pass(CT (&v)[R], int t, CT* line, const CT* __restrict__ tw, CT (&w)[R]) {
         constexpr int r = radix<S>();
         constexpr int Ns = ns<S>();
         constexpr int C = R / r;
-        if constexpr (!PF) load_tw<S>(t, tw, w);
+        // radix-16 items with derived twiddles: formed and applied on the fly
+        constexpr bool INC = !PF && r == 16 && C == 1 && Ns > 1 && ((FT >> S) & 1) == 0 && !(PAIRED && S == NPASS - 1);
+        if constexpr (!PF && !INC) load_tw<S>(t, tw, w);
 #pragma unroll
         for (int i = 0; i < C; ++i) {
             CT a[r];
 #pragma unroll
             for (int u = 0; u < r; ++u) a[u] = v[i + u * C];
-            if constexpr (Ns > 1) {
+            if constexpr (INC) {
+                tw16_apply<S>(a, t, tw);
+            } else if constexpr (Ns > 1) {
 #pragma unroll
                 for (int u = 1; u < r; ++u) a[u] = ctw<SIGN>(a[u], w[i * r + u]);
             }

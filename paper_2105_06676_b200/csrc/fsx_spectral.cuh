@@ -381,6 +381,28 @@ __device__ __forceinline__ void spectral_regs(double2 (&v)[R], int t, const Fuse
         pow_real_vec_skip<R, (R % 4 == 0 ? 4 : R)>(lam, sym.T, sym.neg_mag2);
 #pragma unroll
         for (int q = 0; q < R; ++q) v[q] = cscale(v[q], lam[q] * sym.scale);
+    } else if constexpr (R == 16 && TPL * 16 == N && N >= 4096) {
+        // complex symbol, four elements q = 4 a + b (a = 0..3) per chunk b: one
+        // phase read per group and chunk (e_b; the others are exact quarter
+        // turns), and only four complex multipliers live next to the 16 data
+        // values (the 16-wide multiplier array spilled at 128 registers)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            double2 lam[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) lam[a] = make_double2(0.0, 0.0);
+            for (int gi = 0; gi < sym.ngroups; ++gi) {
+                const double2 c = acoef(gi);
+                const i64 og = sym.group_off[gi];
+                const double2 e = eplus_tab(tw_all, N, (i64)(t + b * (N / 16)) * og);
+                const int mo = (int)(og & 3);
+#pragma unroll
+                for (int a = 0; a < 4; ++a) lam[a] = cadd(lam[a], cmul(c, rot_quarter(e, (mo * a) & 3)));
+            }
+            pow_complex_vec_skip<4, 4>(lam, sym.T, sym.neg_mag2);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) v[4 * a + b] = cscale(cmul(lam[a], v[4 * a + b]), sym.scale);
+        }
     } else {
         double2 lam[R];
 #pragma unroll

@@ -582,6 +582,234 @@ k_fused8192h(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol s
     }
 }
 
+// ------------------------------------------------------------------ 8192-point columns on a CTA pair
+// Cluster primitives (sm_90+): this CTA's rank in the cluster, a peer CTA's
+// shared-memory address, fire-and-forget stores into it, and the split
+// cluster barrier (arrive / wait).
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned peer_smem(const void* local, unsigned rank) {
+    unsigned out;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(out) : "r"(smem_u32(local)), "r"(rank));
+    return out;
+}
+__device__ __forceinline__ void st_peer(unsigned addr, double2 v) {
+    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+
+// Spectral multiply of the CTA-pair layout: u[b + 8 s] = X[k0] with
+// k0 = th + 256 b + 2048 (h + 2 s), h = the CTA's rank, so
+// exp(2 pi i og k0 / 8192) = e_b i^(og (h + 2 s)): eight table reads per group
+// (e_b, b < 8) and exact quarter turns.  Four elements at a time
+// {b, b + 1} x {s = 0, 1}, so only four multipliers are live next to the 16
+// data values (the 16-wide complex multiplier array spilled at 128 registers).
+__device__ __forceinline__ void spectral_pair8192(double2 (&u)[16], int th, int h, const FusedSymbol& sym,
+                                                  const double2* __restrict__ tw_all, const double2* acoef) {
+    constexpr int N = 8192;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int b0 = 2 * c;
+        // element i of the chunk: b = b0 + (i & 1), s = i >> 1 -> u[b + 8 s]
+        if (sym.real) {
+            double lam[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int gi = 0; gi < sym.ngroups; ++gi) {
+                if (sym.group_partner[gi] < 0) continue;  // -og of a symmetric pair: with +og below
+                double2 a = acoef[gi];
+                const i64 og = sym.group_off[gi];
+                if (og == 0) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) lam[i] += a.x;
+                    continue;
+                }
+                if (sym.group_partner[gi] > 0) a = make_double2(2.0 * a.x, 2.0 * a.y);  // 2 Re(A e)
+                const double2 e0 = eplus_tab(tw_all, N, (i64)(th + 256 * b0) * og);
+                const double2 e1 = eplus_tab(tw_all, N, (i64)(th + 256 * (b0 + 1)) * og);
+                const int mo = (int)(og & 3);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const double2 e = rot_quarter((i & 1) ? e1 : e0, (mo * (h + 2 * (i >> 1))) & 3);
+                    lam[i] = fma(a.x, e.x, fma(-a.y, e.y, lam[i]));
+                }
+            }
+            pow_real_vec_skip<4, 4>(lam, sym.T, sym.neg_mag2);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int j = b0 + (i & 1) + 8 * (i >> 1);
+                u[j] = cscale(u[j], lam[i] * sym.scale);
+            }
+        } else {
+            double2 lam[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) lam[i] = make_double2(0.0, 0.0);
+            for (int gi = 0; gi < sym.ngroups; ++gi) {
+                const int pg = sym.group_partner[gi] - 1;  // -1: none
+                if (pg == -2) continue;                     // folded into its +og partner
+                const double2 a = acoef[gi];
+                const i64 og = sym.group_off[gi];
+                if (og == 0) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) lam[i] = cadd(lam[i], a);
+                    continue;
+                }
+                const double2 am = pg >= 0 ? acoef[pg] : make_double2(0.0, 0.0);
+                const double2 e0 = eplus_tab(tw_all, N, (i64)(th + 256 * b0) * og);
+                const double2 e1 = eplus_tab(tw_all, N, (i64)(th + 256 * (b0 + 1)) * og);
+                const int mo = (int)(og & 3);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const double2 e = rot_quarter((i & 1) ? e1 : e0, (mo * (h + 2 * (i >> 1))) & 3);
+                    lam[i] = cadd(lam[i], cmul(a, e));
+                    if (pg >= 0) lam[i] = cadd(lam[i], cmul(am, cconj(e)));
+                }
+            }
+            pow_complex_vec_skip<4, 4>(lam, sym.T, sym.neg_mag2);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int j = b0 + (i & 1) + 8 * (i >> 1);
+                u[j] = cscale(cmul(lam[i], u[j]), sym.scale);
+            }
+        }
+    }
+}
+
+// Fused spectral pass for 8192-point columns on a 2-CTA cluster.  CTA h of
+// the pair owns the samples of parity h (x[2n + h]: the 4-D tensor map view
+// {2 inner, parity, n/2, outer}), i.e. a 4096-point half column of 64 KB, so
+// two pairs share an SM and one CTA's TMA load / store overlaps another's
+// arithmetic (the 128 KB one-CTA-per-column kernel could not overlap them).
+//   1. forward 4096-point FFT of the own half: E (h = 0) or O (h = 1); CTA 1
+//      applies W_8192^k;
+//   2. exchange 1 over DSMEM (fire-and-forget stores, 32 KB each way): CTA 0
+//      keeps k < 2048 and sends E[k >= 2048]; CTA 1 keeps k >= 2048 and sends
+//      W O[k < 2048]; the radix-2 join X[k] = E + W O, X[k + 4096] = E - W O
+//      then runs in registers for the own k;
+//   3. symbol^T / N (spectral_pair8192) and the inverse split
+//      e[k] = X[k] + X[k + 4096], o[k] = (X[k] - X[k + 4096]) W^-k;
+//   4. exchange 2 into the peer's (now idle) tile: CTA 0 collects e, CTA 1 o;
+//   5. inverse 4096-point FFT = the output samples of parity h; TMA store.
+// Three cluster barriers per column: start-up (before the first remote store),
+// after each exchange.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
+k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
+    constexpr int N = 8192, NH = 4096, TH = 256;
+    using FF = LineFFT<NH, -1>;
+    using FI = LineFFT<NH, +1>;
+    extern __shared__ __align__(128) double2 tile[];  // [NH] tile + [NH / 2] exchange-1 landing
+    double2* recv = tile + NH;
+    __shared__ __align__(8) unsigned long long bar;
+    __shared__ double2 acoef[kMaxGroups];
+    __shared__ double2 tapterm[kMaxFusedTaps];
+    const int th = threadIdx.x;
+    const unsigned h = cluster_rank();
+    const i64 c = blockIdx.x >> 1;
+    i64 kx, ky;
+    fused_col_freqs(sym, c, kx, ky);
+    if (sym.rank == 3 && c - (c / sym.P) * sym.P > sym.M) return;  // pitch padding of a 3D plane (both CTAs)
+    cluster_arrive_relaxed();  // (A1) this CTA is running: the peer may store into it after its wait
+    if (th == 0) {
+        mbar_init(&bar, 1);
+        mbar_init_fence();
+        pdl_wait();
+        mbar_expect_tx(&bar, (unsigned)(NH * sizeof(double2)));
+#pragma unroll 1
+        for (int b = 0; b < NH / 256; ++b) tma_load_4d(tile + b * 256, &map2, (int)(2 * c), (int)h, b * 256, 0, &bar);
+    }
+    for (int j = th; j < sym.ntaps; j += TH) tapterm[j] = tap_term(sym, tw_all, j, kx, ky);
+    __syncthreads();
+    for (int gi = th; gi < sym.ngroups; gi += TH) {
+        double2 a = make_double2(0.0, 0.0);
+        for (int j = 0; j < sym.ntaps; ++j)
+            if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j]);
+        acoef[gi] = a;
+    }
+    mbar_wait(&bar, 0);
+    pdl_trigger();
+    double2 v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = tile[th + 256 * q];
+    FF::run(v, th, tile, tw_all + NH);
+    const double2 wt = __ldg(tw_all + N + th);  // W_8192^th; W_8192^(th + 256 q) = wt W_32^q
+    if (h == 1) {
+        static_for<0, 16>([&](auto Q) {
+            constexpr int q = decltype(Q)::value;
+            v[q] = cmul(v[q], cmul_const<q, 32, -1>(wt));
+        });
+    }
+    // exchange 1: the half of the k range the peer keeps
+    cluster_wait();  // (W1) the peer is running
+    {
+        const unsigned dst = peer_smem(recv + th, h ^ 1u);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) st_peer(dst + 256u * 16u * b, h == 0 ? v[8 + b] : v[b]);
+    }
+    cluster_arrive();  // (A2) stores released; this CTA is done with its tile (forward FFT over)
+    cluster_wait();    // (W2) the peer's stores landed in recv
+    double2 u[16];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const double2 r = recv[th + 256 * b];
+        const double2 e = h == 0 ? v[b] : r;
+        const double2 o = h == 0 ? r : v[8 + b];
+        u[b] = cadd(e, o);
+        u[b + 8] = csub(e, o);
+    }
+    spectral_pair8192(u, th, (int)h, sym, tw_all, acoef);
+    // inverse split for the own k = th + 256 b + 2048 h: e into v[8h + b] slots of CTA 0, o of CTA 1
+    double2 keep[8], send[8];
+    static_for<0, 8>([&](auto B) {
+        constexpr int b = decltype(B)::value;
+        const double2 e = cadd(u[b], u[b + 8]);
+        const double2 d = csub(u[b], u[b + 8]);
+        const double2 o = h == 0 ? cmulc(d, cmul_const<b, 32, -1>(wt)) : cmulc(d, cmul_const<b + 8, 32, -1>(wt));
+        keep[b] = h == 0 ? e : o;
+        send[b] = h == 0 ? o : e;
+    });
+    // exchange 2 into the peer's tile (idle since its A2)
+    {
+        const unsigned dst = peer_smem(tile + th, h ^ 1u);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) st_peer(dst + 256u * 16u * b, send[b]);
+    }
+    cluster_arrive();  // (A3)
+    cluster_wait();    // (W3) the peer's half of this CTA's inverse input landed
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const double2 r = tile[th + 256 * b];
+        v[b] = h == 0 ? keep[b] : r;
+        v[8 + b] = h == 0 ? r : keep[b];
+    }
+    FI::run(v, th, tile, tw_all + NH);
+    __syncthreads();  // the last exchange reads are done before the tile is overwritten
+#pragma unroll
+    for (int q = 0; q < 16; ++q) tile[th + 256 * q] = v[q];
+    fence_proxy_async();
+    __syncthreads();
+    if (th == 0) {
+#pragma unroll 1
+        for (int b = 0; b < NH / 256; ++b) tma_store_4d(&map2, tile + b * 256, (int)(2 * c), (int)h, b * 256, 0);
+        bulk_commit();
+        bulk_wait_read0();
+    }
+}
+
+// FSX_F8192: "c" (default) the CTA-pair kernel, "h" the one-CTA parity-halves kernel
+static bool f8192_pair() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_F8192");
+        v = (e && e[0] == 'h') ? 0 : 1;
+    }
+    return v != 0;
+}
+
 static int fused_halves() {
     static int v = -1;
     if (v < 0) {
@@ -596,6 +824,11 @@ bool halves_ok(const AxisGeom& g) { return g.n == 8192 && g.outer == 1 && fused_
 cudaError_t launch_fused_halves(const void* tensor_map2, const AxisGeom& g, const FusedSymbol& sym,
                                 const double2* tw, cudaStream_t s) {
     const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(tensor_map2);
+    if (f8192_pair()) {
+        const size_t smem2 = (4096 + 2048) * sizeof(double2);
+        kernel_prepare((const void*)k_fused8192c, smem2);
+        return launch_pdl(k_fused8192c, dim3((unsigned)(2 * g.ncols)), dim3(256), smem2, s, map, g, sym, tw);
+    }
     const size_t smem = 8192 * sizeof(double2);
     kernel_prepare((const void*)k_fused8192h, smem);
     return launch_pdl(k_fused8192h, dim3((unsigned)g.ncols), dim3(512), smem, s, map, g, sym, tw);
