@@ -17,6 +17,8 @@
 //   * std::thread chunked parallel_for, n < 2048 inline (proj/src/parallel.cpp:11-58)
 //   * naive Theta(NT) stepping                        (proj/src/oracle.cpp:23-113)
 //   * tap accumulation and require_fits               (proj/src/kernel.cpp:7-49)
+//   * modal truth: three Fourier modes amplified by the double-double
+//     lambda^T (accuracy-parity criterion)             (proj/src/modal.cpp:13-145)
 //
 // It is pinned against the reference's own known-answer and property tests
 // (tests/golden/reference_known_answers.json, tests/test_oracle_cpu.py).
@@ -738,6 +740,105 @@ void put_timings(const orc::Timings& t, double* st) {
 
 using cd = std::complex<double>;
 using cl = std::complex<long double>;
+
+// ---------------------------------------------------------------- modal truth
+// proj/src/modal.cpp:13-145: three periodic Fourier modes whose eigenvalues
+// are raised to T in double-double complex arithmetic (relative error ~1e-32
+// per multiply), so the reference grid Re(sum_q A_q lam_q^T e^{i(2 pi k_q.x/n + phi_q)})
+// is exact far below either solver's error.  Used by the accuracy-parity
+// acceptance criterion (proj/tests/acceptance.cpp:298-320).
+namespace modal {
+using orc::i64;
+using orc::Kernel;
+using orc::Shape;
+using orc::SpecError;
+using orc::u64;
+struct DD {
+    double hi = 0, lo = 0;
+};
+static DD two_sum(double a, double b) {
+    const double s = a + b;
+    const double bb = s - a;
+    return {s, (a - (s - bb)) + (b - bb)};
+}
+static DD two_prod(double a, double b) {
+    const double p = a * b;
+    return {p, std::fma(a, b, -p)};
+}
+static DD dd_add(DD a, DD b) {
+    const DD s = two_sum(a.hi, b.hi);
+    return two_sum(s.hi, s.lo + a.lo + b.lo);
+}
+static DD dd_mul(DD a, DD b) {
+    const DD p = two_prod(a.hi, b.hi);
+    return two_sum(p.hi, p.lo + a.hi * b.lo + a.lo * b.hi);
+}
+static DD dd(double x) { return {x, 0.0}; }
+struct DDC {
+    DD re, im;
+};
+static DDC ddc_mul(const DDC& a, const DDC& b) {
+    return {dd_add(dd_mul(a.re, b.re), dd_mul(dd_mul(a.im, b.im), dd(-1.0))),
+            dd_add(dd_mul(a.re, b.im), dd_mul(a.im, b.re))};
+}
+static DDC ddc_pow(DDC base, u64 t) {
+    DDC acc{dd(1.0), dd(0.0)};
+    while (t) {
+        if (t & 1) acc = ddc_mul(acc, base);
+        t >>= 1;
+        if (t) base = ddc_mul(base, base);
+    }
+    return acc;
+}
+struct Mode {
+    std::vector<i64> k;
+    double amplitude, phase;
+};
+static void problem_periodic(const Shape& s, const Kernel& k, u64 T, double* initial, double* reference) {
+    k.require_fits(s);
+    if (s.fields != 1) throw SpecError("accuracy mode: periodic reference needs a scalar field");
+    const int d = s.rank();
+    std::vector<Mode> modes(3);
+    modes[0] = {std::vector<i64>(d, 0), 1.0, 0.0};
+    modes[0].k[0] = 1;
+    modes[1] = {std::vector<i64>(d, 0), 0.6, 0.7};
+    if (d >= 2) modes[1].k[1] = 1;
+    else modes[1].k[0] = 2;
+    modes[2] = {std::vector<i64>(d, 1), 0.3, 1.3};
+    if (d == 1) modes[2].k[0] = 3;
+    std::vector<DDC> amp(modes.size());
+    for (size_t q = 0; q < modes.size(); ++q) {
+        std::complex<double> lam(0, 0);
+        for (const auto& [off, block] : k.taps) {
+            double frac = 0;
+            for (int a = 0; a < d; ++a)
+                frac += static_cast<double>(modes[q].k[a] * off[a]) / static_cast<double>(s.dims[a]);
+            const double angle = 2.0 * std::numbers::pi * frac;
+            lam += block[0] * std::complex<double>(std::cos(angle), std::sin(angle));
+        }
+        amp[q] = ddc_pow({dd(lam.real()), dd(lam.imag())}, T);
+    }
+    std::vector<i64> idx(d, 0);
+    for (i64 cell = 0; cell < s.cells; ++cell) {
+        double init = 0, ref = 0;
+        for (size_t q = 0; q < modes.size(); ++q) {
+            double frac = 0;
+            for (int a = 0; a < d; ++a)
+                frac += static_cast<double>((modes[q].k[a] * idx[a]) % s.dims[a]) / static_cast<double>(s.dims[a]);
+            const double angle = 2.0 * std::numbers::pi * frac + modes[q].phase;
+            const double c = std::cos(angle), sn = std::sin(angle);
+            init += modes[q].amplitude * c;
+            ref += modes[q].amplitude * (amp[q].re.hi * c - amp[q].im.hi * sn);
+        }
+        initial[cell] = init;
+        reference[cell] = ref;
+        for (int a = d - 1; a >= 0; --a) {  // next_index, row-major
+            if (++idx[a] < s.dims[a]) break;
+            idx[a] = 0;
+        }
+    }
+}
+}  // namespace modal
 }  // namespace
 
 extern "C" {
@@ -896,6 +997,17 @@ int orc_dense_stencil_matrix(int rank, const int64_t* dims, int fields, int64_t 
         orc::Shape s(dims, rank, fields);
         orc::Kernel k = orc::kernel_from_arrays(rank, fields, ntaps, offsets, blocks);
         orc::dense_matrix(s, k, mat);
+    });
+}
+
+// modal_problem_periodic (proj/src/modal.cpp:99-145): initial grid and its
+// double-double-amplified exact evolution after T steps (scalar fields).
+int orc_modal_problem_periodic(int rank, const int64_t* dims, int64_t ntaps, const int64_t* offsets,
+                               const double* blocks, uint64_t T, double* initial, double* reference) {
+    return guard([&] {
+        orc::Shape s(dims, rank, 1);
+        orc::Kernel k = orc::kernel_from_arrays(rank, 1, ntaps, offsets, blocks);
+        modal::problem_periodic(s, k, T, initial, reference);
     });
 }
 

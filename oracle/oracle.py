@@ -232,3 +232,16 @@ def splitmix_fill(seed: int, n: int, symmetric: bool) -> np.ndarray:
     lib().orc_splitmix_fill(ctypes.c_uint64(int(seed)), ctypes.c_int64(int(n)), ctypes.c_int(int(symmetric)),
                             _dp(out))
     return out
+
+
+def modal_problem_periodic(dims, offsets, blocks, T):
+    """proj/src/modal.cpp:99-145: (initial grid, exact reference after T steps)
+    with the mode amplification lambda^T in double-double arithmetic."""
+    d = _dims(dims)
+    off, blk = _taps(offsets, blocks, d.size, 1)
+    n = int(np.prod(d))
+    init = np.empty(n)
+    ref = np.empty(n)
+    _check(lib().orc_modal_problem_periodic(ctypes.c_int(d.size), _ip(d), ctypes.c_int64(off.shape[0]), _ip(off),
+                                            _dp(blk), ctypes.c_uint64(int(T)), _dp(init), _dp(ref)))
+    return init, ref

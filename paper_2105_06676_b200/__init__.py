@@ -45,6 +45,15 @@ from .fftstencil import (  # noqa: F401
     spectrum_from_kernel,
     step_periodic,
 )
+from .grid_io import (  # noqa: F401
+    IoError,
+    format_stage_table,
+    load_grid_device,
+    read_grid,
+    read_grid_shape,
+    run_bench,
+    write_grid,
+)
 from . import _lib  # noqa: F401
 
 __all__ = [n for n in dir() if not n.startswith("_")]

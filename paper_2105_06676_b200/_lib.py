@@ -12,7 +12,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfsx.so")
 
-FSX_OK, FSX_ERR_SPEC, FSX_ERR_NUMERIC, FSX_ERR_CUDA, FSX_ERR_NCCL, FSX_ERR_OOM = 0, 1, 2, 3, 4, 5
+FSX_OK, FSX_ERR_SPEC, FSX_ERR_NUMERIC, FSX_ERR_CUDA, FSX_ERR_NCCL, FSX_ERR_OOM, FSX_ERR_IO = 0, 1, 2, 3, 4, 5, 6
+FSX_GRID_CSV, FSX_GRID_RAW = 0, 1
 MAX_RANK = 8
 
 
@@ -30,6 +31,10 @@ class NumericError(Error, ArithmeticError):
 
 class CudaError(Error):
     """CUDA failure (no device, launch error, out of memory)."""
+
+
+class IoError(Error, OSError):
+    """File parsing / reading / writing problems (errors.hpp:20-24)."""
 
 
 class FsxShape(ctypes.Structure):
@@ -111,6 +116,11 @@ EXPORTS = (
     "fsx_device_count",
     "fsx_plan_describe",
     "fsx_spectral_cut_columns",
+    "fsx_write_grid",
+    "fsx_read_grid_shape",
+    "fsx_read_grid",
+    "fsx_load_grid_device",
+    "fsx_format_stage_table",
 )
 
 _lib = None
@@ -143,4 +153,6 @@ def check(status: int) -> None:
         raise SpecError(msg)
     if status == FSX_ERR_NUMERIC:
         raise NumericError(msg)
+    if status == FSX_ERR_IO:
+        raise IoError(msg)
     raise CudaError(f"[fsx status {status}] {msg}")

@@ -596,13 +596,9 @@ __device__ __forceinline__ unsigned peer_smem(const void* local, unsigned rank) 
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(out) : "r"(smem_u32(local)), "r"(rank));
     return out;
 }
-__device__ __forceinline__ void st_peer(unsigned addr, double2 v) {
-    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
-}
 __device__ __forceinline__ void cluster_arrive_relaxed() {
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
 }
-__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
 
 // Spectral multiply of the CTA-pair layout: u[b + 8 s] = X[k0] with
@@ -687,16 +683,40 @@ __device__ __forceinline__ void spectral_pair8192(double2 (&u)[16], int th, int 
 // arithmetic (the 128 KB one-CTA-per-column kernel could not overlap them).
 //   1. forward 4096-point FFT of the own half: E (h = 0) or O (h = 1); CTA 1
 //      applies W_8192^k;
-//   2. exchange 1 over DSMEM (fire-and-forget stores, 32 KB each way): CTA 0
-//      keeps k < 2048 and sends E[k >= 2048]; CTA 1 keeps k >= 2048 and sends
-//      W O[k < 2048]; the radix-2 join X[k] = E + W O, X[k + 4096] = E - W O
-//      then runs in registers for the own k;
+//   2. exchange 1 over DSMEM, 32 KB each way: CTA 0 keeps k < 2048 and sends
+//      E[k >= 2048]; CTA 1 keeps k >= 2048 and sends W O[k < 2048]; the
+//      radix-2 join X[k] = E + W O, X[k + 4096] = E - W O then runs in
+//      registers for the own k;
 //   3. symbol^T / N (spectral_pair8192) and the inverse split
 //      e[k] = X[k] + X[k + 4096], o[k] = (X[k] - X[k + 4096]) W^-k;
-//   4. exchange 2 into the peer's (now idle) tile: CTA 0 collects e, CTA 1 o;
+//   4. exchange 2 into the peer's tile (once the peer reports its forward
+//      FFT done): CTA 0 collects e, CTA 1 o;
 //   5. inverse 4096-point FFT = the output samples of parity h; TMA store.
-// Three cluster barriers per column: start-up (before the first remote store),
-// after each exchange.
+// The exchanges are st.async stores that complete on the RECEIVER's mbarrier
+// (complete_tx, 32 KB expected), and "my tile is free" is one remote mbarrier
+// arrive: the only cluster-wide barrier is the start-up one that publishes the
+// barrier initialisation (a release cluster barrier per exchange costs a
+// GPU-scope fence and an L1 invalidation: ~20 % of the stall samples).
+__device__ __forceinline__ void st_async_peer(unsigned addr, double2 v, unsigned peer_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(addr),
+                 "d"(v.x), "d"(v.y), "r"(peer_bar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_peer(unsigned peer_bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(peer_bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAITC_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAITC_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
 k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
     constexpr int N = 8192, NH = 4096, TH = 256;
@@ -704,24 +724,31 @@ k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol s
     using FI = LineFFT<NH, +1>;
     extern __shared__ __align__(128) double2 tile[];  // [NH] tile + [NH / 2] exchange-1 landing
     double2* recv = tile + NH;
-    __shared__ __align__(8) unsigned long long bar;
+    // bar: TMA load; bx1 / bx2: the peer's exchange-1 / exchange-2 stores
+    // landed here; bok: the peer's tile is free for exchange 2
+    __shared__ __align__(8) unsigned long long bar, bx1, bx2, bok;
     __shared__ double2 acoef[kMaxGroups];
     __shared__ double2 tapterm[kMaxFusedTaps];
     const int th = threadIdx.x;
-    const unsigned h = cluster_rank();
+    const unsigned h = cluster_rank(), peer = h ^ 1u;
     const i64 c = blockIdx.x >> 1;
     i64 kx, ky;
     fused_col_freqs(sym, c, kx, ky);
     if (sym.rank == 3 && c - (c / sym.P) * sym.P > sym.M) return;  // pitch padding of a 3D plane (both CTAs)
-    cluster_arrive_relaxed();  // (A1) this CTA is running: the peer may store into it after its wait
     if (th == 0) {
         mbar_init(&bar, 1);
+        mbar_init(&bx1, 1);
+        mbar_init(&bx2, 1);
+        mbar_init(&bok, 1);
         mbar_init_fence();
+        mbar_expect_tx(&bx1, (unsigned)(NH / 2 * sizeof(double2)));  // (its own arrival; the peer's bytes complete it)
+        mbar_expect_tx(&bx2, (unsigned)(NH / 2 * sizeof(double2)));
         pdl_wait();
         mbar_expect_tx(&bar, (unsigned)(NH * sizeof(double2)));
 #pragma unroll 1
         for (int b = 0; b < NH / 256; ++b) tma_load_4d(tile + b * 256, &map2, (int)(2 * c), (int)h, b * 256, 0, &bar);
     }
+    cluster_arrive_relaxed();  // publishes the barrier initialisation (fence above) to the peer
     for (int j = th; j < sym.ntaps; j += TH) tapterm[j] = tap_term(sym, tw_all, j, kx, ky);
     __syncthreads();
     for (int gi = th; gi < sym.ngroups; gi += TH) {
@@ -730,6 +757,7 @@ k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol s
             if (sym.tap_group[j] == gi) a = cadd(a, tapterm[j]);
         acoef[gi] = a;
     }
+    cluster_wait();  // the peer's barriers exist (and, CTA-wide, acoef is written)
     mbar_wait(&bar, 0);
     pdl_trigger();
     double2 v[16];
@@ -743,15 +771,15 @@ k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol s
             v[q] = cmul(v[q], cmul_const<q, 32, -1>(wt));
         });
     }
-    // exchange 1: the half of the k range the peer keeps
-    cluster_wait();  // (W1) the peer is running
+    // exchange 1: the half of the k range the peer keeps, into its recv
     {
-        const unsigned dst = peer_smem(recv + th, h ^ 1u);
+        const unsigned dst = peer_smem(recv + th, peer), pbar = peer_smem(&bx1, peer);
 #pragma unroll
-        for (int b = 0; b < 8; ++b) st_peer(dst + 256u * 16u * b, h == 0 ? v[8 + b] : v[b]);
+        for (int b = 0; b < 8; ++b) st_async_peer(dst + 256u * 16u * b, h == 0 ? v[8 + b] : v[b], pbar);
     }
-    cluster_arrive();  // (A2) stores released; this CTA is done with its tile (forward FFT over)
-    cluster_wait();    // (W2) the peer's stores landed in recv
+    __syncthreads();  // every thread is past the forward FFT's tile reads
+    if (th == 0) mbar_arrive_peer(peer_smem(&bok, peer));  // the peer may write into this tile
+    mbar_wait(&bx1, 0);
     double2 u[16];
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
@@ -762,7 +790,7 @@ k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol s
         u[b + 8] = csub(e, o);
     }
     spectral_pair8192(u, th, (int)h, sym, tw_all, acoef);
-    // inverse split for the own k = th + 256 b + 2048 h: e into v[8h + b] slots of CTA 0, o of CTA 1
+    // inverse split for the own k = th + 256 b + 2048 h: CTA 0 keeps e and sends o, CTA 1 the reverse
     double2 keep[8], send[8];
     static_for<0, 8>([&](auto B) {
         constexpr int b = decltype(B)::value;
@@ -772,14 +800,14 @@ k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol s
         keep[b] = h == 0 ? e : o;
         send[b] = h == 0 ? o : e;
     });
-    // exchange 2 into the peer's tile (idle since its A2)
+    // exchange 2 into the peer's tile, once the peer's forward FFT is done with it
+    mbar_wait_cluster(&bok, 0);
     {
-        const unsigned dst = peer_smem(tile + th, h ^ 1u);
+        const unsigned dst = peer_smem(tile + th, peer), pbar = peer_smem(&bx2, peer);
 #pragma unroll
-        for (int b = 0; b < 8; ++b) st_peer(dst + 256u * 16u * b, send[b]);
+        for (int b = 0; b < 8; ++b) st_async_peer(dst + 256u * 16u * b, send[b], pbar);
     }
-    cluster_arrive();  // (A3)
-    cluster_wait();    // (W3) the peer's half of this CTA's inverse input landed
+    mbar_wait(&bx2, 0);  // the peer's half of this CTA's inverse input landed
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
         const double2 r = tile[th + 256 * b];
