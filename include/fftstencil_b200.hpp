@@ -156,6 +156,16 @@ private:
     fsx_spectrum_cache* h_;
 };
 
+// Multi-GPU for every later solve_periodic / solve_periodic_cached of an
+// eligible 2D/3D grid in this process (fsx_set_devices): the GPU counterpart
+// of the reference's process-wide set_num_threads (proj/src/parallel.cpp:11-21).
+// An empty list (or one device) returns to a single GPU.
+inline void set_devices(const std::vector<int>& devices) {
+    std::vector<std::int32_t> d(devices.begin(), devices.end());
+    check(fsx_set_devices(d.empty() ? nullptr : d.data(), (std::int32_t)d.size()));
+}
+inline void set_num_gpus(int n) { check(fsx_set_devices(nullptr, n)); }
+
 namespace detail {
 inline fsx_stage_timings to_c(const StageTimings* st) {
     fsx_stage_timings t{};

@@ -33,7 +33,7 @@ typedef enum fsx_status {
     FSX_ERR_SPEC = 1,      /* reference SpecError: invalid shapes, kernels, arguments */
     FSX_ERR_NUMERIC = 2,   /* reference NumericError: non-finite result / residue blow-up */
     FSX_ERR_CUDA = 3,      /* CUDA runtime failure (no device, launch error, ...) */
-    FSX_ERR_NCCL = 4,      /* reserved for the multi-GPU path */
+    FSX_ERR_NCCL = 4,      /* NCCL failure (multi-GPU nccl exchange) */
     FSX_ERR_OOM = 5,       /* device allocation failed */
     FSX_ERR_IO = 6         /* reference IoError: file parsing / reading / writing (errors.hpp:20-24) */
 } fsx_status;
@@ -85,7 +85,36 @@ typedef struct fsx_options {
                              is bitwise the full solve's (those columns are exactly 0 there).
                              Default 0: every column moves (the reference's work). */
     void* stream;       /* cudaStream_t to enqueue on (NULL = library stream) */
+    /* Multi-GPU (single process; host-pointer fsx_solve_periodic /
+     * fsx_solve_periodic_cached of rank-2/3 scalar pow2 grids whose axis 0 (and,
+     * in 3D, axis 1) divides by the device count; other problems run on one
+     * GPU with the same result contract):
+     *   num_gpus  0 = the process default (fsx_set_devices), 1 = one GPU,
+     *             P > 1 = slab-decompose axis 0 over P devices;
+     *   devices   NULL = ordinals 0..P-1, else P ordinals (a repeated ordinal
+     *             runs several ranks on one device: one-GPU emulation);
+     *   exchange  FSX_EXCHANGE_AUTO (p2p when every pair has peer access),
+     *             FSX_EXCHANGE_P2P (NVLink peer memory: fused into the row
+     *             kernels in 2D, chunked copy-engine puts/pulls overlapping
+     *             the y passes in 3D), FSX_EXCHANGE_NCCL (grouped
+     *             ncclSend/ncclRecv all-to-alls; libnccl.so.2 loaded on use). */
+    int32_t num_gpus;
+    int32_t exchange;
+    const int32_t* devices;
 } fsx_options;
+
+#define FSX_EXCHANGE_AUTO 0
+#define FSX_EXCHANGE_P2P 1
+#define FSX_EXCHANGE_NCCL 2
+
+/* Process default device list for host solves whose options leave num_gpus
+ * at 0 (the drop-in C++ header passes no options): n = 0 or 1 -> one GPU.
+ * The multi-GPU counterpart of the reference's process-wide thread budget
+ * (proj/include/fftstencil/parallel.hpp, set_num_threads; parallel.cpp:11-21).
+ * devices NULL = ordinals 0..n-1.  Ordinals are validated against the visible
+ * devices.  fsx_get_devices copies up to cap ordinals and returns the count. */
+fsx_status fsx_set_devices(const int32_t* devices, int32_t n);
+int32_t fsx_get_devices(int32_t* devices, int32_t cap);
 
 /* Opaque spectrum/plan cache (proj/include/fftstencil/periodic.hpp:28-35). */
 typedef struct fsx_spectrum_cache fsx_spectrum_cache;
@@ -285,6 +314,8 @@ typedef struct fsx_plan_info {
     int64_t alg_bytes;       /* algorithmic bytes per solve (all passes) */
     int64_t fused_bytes;     /* algorithmic bytes of the dominant (fused) kernel */
     int64_t work_bytes;      /* device workspace of the plan */
+    int32_t ranks;           /* devices a host solve is decomposed over (1 = single GPU) */
+    int32_t exchange;        /* ranks > 1: FSX_EXCHANGE_P2P or FSX_EXCHANGE_NCCL as resolved */
 } fsx_plan_info;
 /* Columns the exact spectral cut keeps for this solve (kept <= total = L/2 + 1;
  * kept == total when the cut does not apply: other plans, rank 3, T == 1, ...). */

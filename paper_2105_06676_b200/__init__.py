@@ -24,6 +24,7 @@ from .fftstencil import (  # noqa: F401
     evolve_periodic_naive_device,
     fft,
     fold_kernels,
+    get_devices,
     hadamard,
     last_stage_ms,
     multi_fft,
@@ -32,6 +33,7 @@ from .fftstencil import (  # noqa: F401
     plan_describe,
     pow_spectrum,
     pseudo_inverse_spectrum,
+    set_devices,
     solve_periodic,
     solve_periodic_batch,
     solve_periodic_cached,

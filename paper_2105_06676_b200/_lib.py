@@ -10,10 +10,11 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfsx.so")
+LIB_PATH = os.environ.get("FSX_LIB") or os.path.join(HERE, "libfsx.so")  # FSX_LIB: A/B builds
 
 FSX_OK, FSX_ERR_SPEC, FSX_ERR_NUMERIC, FSX_ERR_CUDA, FSX_ERR_NCCL, FSX_ERR_OOM, FSX_ERR_IO = 0, 1, 2, 3, 4, 5, 6
 FSX_GRID_CSV, FSX_GRID_RAW = 0, 1
+FSX_EXCHANGE_AUTO, FSX_EXCHANGE_P2P, FSX_EXCHANGE_NCCL = 0, 1, 2
 MAX_RANK = 8
 
 
@@ -68,6 +69,9 @@ class FsxOptions(ctypes.Structure):
         ("stage_events", ctypes.c_int32),
         ("spectral_cut", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
+        ("num_gpus", ctypes.c_int32),
+        ("exchange", ctypes.c_int32),
+        ("devices", ctypes.POINTER(ctypes.c_int32)),
     ]
 
 
@@ -78,6 +82,8 @@ class FsxPlanInfo(ctypes.Structure):
         ("alg_bytes", ctypes.c_int64),
         ("fused_bytes", ctypes.c_int64),
         ("work_bytes", ctypes.c_int64),
+        ("ranks", ctypes.c_int32),
+        ("exchange", ctypes.c_int32),
     ]
 
 
@@ -114,6 +120,8 @@ EXPORTS = (
     "fsx_last_error",
     "fsx_version",
     "fsx_device_count",
+    "fsx_set_devices",
+    "fsx_get_devices",
     "fsx_plan_describe",
     "fsx_spectral_cut_columns",
     "fsx_write_grid",
@@ -139,6 +147,7 @@ def load():
     L.fsx_last_error.restype = ctypes.c_char_p
     L.fsx_version.restype = ctypes.c_int32
     L.fsx_device_count.restype = ctypes.c_int32
+    L.fsx_get_devices.restype = ctypes.c_int32
     L.fsx_spectrum_cache_create.restype = ctypes.c_void_p
     L.fsx_spectrum_cache_destroy.argtypes = [ctypes.c_void_p]
     _lib = L

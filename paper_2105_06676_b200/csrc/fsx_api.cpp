@@ -28,6 +28,9 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+#include <type_traits>
 
 #include "fsx.h"
 #include "fsx_kernels.h"
@@ -1118,6 +1121,18 @@ void slab_geom(const fsx_shape* global, int P, int r, SlabPlan& sp) {
     }
 }
 
+// A slab plan with its device buffers on the current device.
+std::unique_ptr<SlabPlan> make_slab_plan(const fsx_shape* global, int P, int r) {
+    auto sp = std::make_unique<SlabPlan>();
+    slab_geom(global, P, r, *sp);
+    if (sp->dims.size() == 3) {
+        sp->H.ensure((size_t)sp->n0l * sp->n1 * sp->Pp * 16);
+        sp->tmaH = tma_enabled() && fsx::tma_cols_ok(sp->n1) &&
+                   fsx::make_cols_tensor_map(sp->mapH, sp->H.p, sp->axy) == 0;
+    }
+    return sp;
+}
+
 // Device plan (call with the device's lock held and the device selected).
 SlabPlan& slab_plan(const fsx_shape* global, int P, int r) {
     const Shape s = parse_shape(global);
@@ -1134,13 +1149,7 @@ SlabPlan& slab_plan(const fsx_shape* global, int P, int r) {
     for (const auto& e : g_slabs) mine += e.first.rfind(prefix, 0) == 0;
     if (mine >= 16)
         for (auto e = g_slabs.begin(); e != g_slabs.end();) e = e->first.rfind(prefix, 0) == 0 ? g_slabs.erase(e) : std::next(e);
-    auto sp = std::make_unique<SlabPlan>();
-    slab_geom(global, P, r, *sp);
-    if (sp->dims.size() == 3) {
-        sp->H.ensure((size_t)sp->n0l * sp->n1 * sp->Pp * 16);
-        sp->tmaH = tma_enabled() && fsx::tma_cols_ok(sp->n1) &&
-                   fsx::make_cols_tensor_map(sp->mapH, sp->H.p, sp->axy) == 0;
-    }
+    auto sp = make_slab_plan(global, P, r);
     auto& ref = *sp;
     g_slabs.emplace(key, std::move(sp));
     return ref;
@@ -1166,9 +1175,10 @@ void slab_forward(SlabPlan& sp, Device& dev, const double* in, double2* send, cu
                                  (size_t)sp.n1 * sp.Pp * 16, w, (size_t)sp.n0l, cudaMemcpyDeviceToDevice, st));
 }
 
-void slab_inverse(SlabPlan& sp, Device& dev, const double2* send, double* out, cudaStream_t st) {
+void slab_inverse(SlabPlan& sp, Device& dev, const double2* send, double* out, cudaStream_t st,
+                  fsx::Flags* flags_at = nullptr) {
     const double2* tw = dev.tw_all.as<double2>();
-    fsx::Flags* flags = dev.flags.as<fsx::Flags>();
+    fsx::Flags* flags = flags_at ? flags_at : dev.flags.as<fsx::Flags>();
     if (sp.dims.size() == 2) {
         const fsx::RowLayout lay{0, sp.CB, sp.n0l};
         FSX_CK(fsx::launch_c2r_rows(send, out, sp.n0l, sp.L, lay, tw, flags, st));
@@ -1338,6 +1348,443 @@ void run_plan_f32(Plan& p, Device& dev, const Taps& taps, u64 T, const float* fi
     FSX_CK(fsx::launch_narrow(p.d_out.as<double>(), fout, n, flags_at ? flags_at : dev.flags.as<fsx::Flags>(), st));
 }
 
+// ------------------------------------------------------------------ single-process multi-GPU
+// fsx_options.num_gpus / .devices (or the process default of fsx_set_devices):
+// one host call slab-decomposes a rank-2/3 grid over P devices of this
+// process, like the reference's process-wide thread budget spreads its line
+// FFTs over threads (proj/src/parallel.cpp:11-21).  The exchange is either
+//   p2p   the NVLink peer-memory transpose: 2D -- the R2C row kernel stores
+//         column block d straight into rank d's exchange buffer and the C2R
+//         row kernel loads its blocks from every rank's buffer (the
+//         all-to-all fused into the row passes); 3D -- the R2C rows and the
+//         y pass run in plane chunks and each finished chunk is put into the
+//         owners' buffers by the copy engines while the next chunk computes
+//         (the inverse pulls chunk by chunk ahead of the y pass and C2R rows);
+//   nccl  fsx_slab_forward -> grouped ncclSend/ncclRecv -> fused pass ->
+//         grouped ncclSend/ncclRecv -> fsx_slab_inverse (NCCL loaded with
+//         dlopen on first use).
+// Cross-device ordering is by CUDA events (no device-side spinning): every
+// stream waits on all ranks' "exchange written" events before the fused pass
+// and on all "fused pass done" events before the inverse reads.  Repeated
+// device ordinals run several ranks on one device (the p2p exchange then
+// moves within that device's memory): one-GPU emulation for tests.
+struct NcclErr : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+struct NcclApi {
+    bool tried = false, ok = false;
+    std::string why;
+    decltype(&ncclCommInitAll) CommInitAll = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclGroupStart) GroupStart = nullptr;
+    decltype(&ncclGroupEnd) GroupEnd = nullptr;
+    decltype(&ncclSend) Send = nullptr;
+    decltype(&ncclRecv) Recv = nullptr;
+    decltype(&ncclGetErrorString) ErrStr = nullptr;
+};
+std::mutex g_nccl_mu;
+NcclApi g_nccl;
+
+const NcclApi& nccl_api() {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (g_nccl.tried) return g_nccl;
+    g_nccl.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        g_nccl.why = std::string("dlopen(libnccl.so.2): ") + dlerror();
+        return g_nccl;
+    }
+    auto sym = [&](auto& fn, const char* name) {
+        fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+        return fn != nullptr;
+    };
+    g_nccl.ok = sym(g_nccl.CommInitAll, "ncclCommInitAll") && sym(g_nccl.CommDestroy, "ncclCommDestroy") &&
+                sym(g_nccl.GroupStart, "ncclGroupStart") && sym(g_nccl.GroupEnd, "ncclGroupEnd") &&
+                sym(g_nccl.Send, "ncclSend") && sym(g_nccl.Recv, "ncclRecv") &&
+                sym(g_nccl.ErrStr, "ncclGetErrorString");
+    if (!g_nccl.ok) g_nccl.why = "libnccl.so.2 lacks the point-to-point API";
+    return g_nccl;
+}
+
+#define FSX_NCCL(api, x)                                                                         \
+    do {                                                                                         \
+        ncclResult_t r_ = (x);                                                                   \
+        if (r_ != ncclSuccess) throw NcclErr(std::string(#x) + ": " + (api).ErrStr(r_));         \
+    } while (0)
+
+enum { kExAuto = 0, kExP2P = 1, kExNccl = 2 };
+
+// process default of fsx_set_devices (empty: single GPU)
+std::mutex g_multi_default_mu;
+std::vector<int> g_multi_default;
+
+struct alignas(64) TmaMap {
+    unsigned char b[128];
+};
+
+struct MultiRank {
+    Device* dev = nullptr;
+    int ordinal = 0;
+    cudaStream_t st = nullptr;   // kernels
+    cudaStream_t cst = nullptr;  // 3D p2p: chunk puts / pulls (copy engines)
+    std::unique_ptr<SlabPlan> sp;
+    DevBuf in, out, send, recv, peers, flags;
+    cudaEvent_t ev_fwd = nullptr, ev_spec = nullptr, ev_done = nullptr;
+    std::vector<cudaEvent_t> ev_chunk;  // 3D p2p: per plane chunk
+    std::vector<TmaMap> ymaps;          // 3D: y-pass tensor map per plane chunk
+    std::vector<bool> ytma;
+    ncclComm_t comm = nullptr;
+    ~MultiRank() {
+        cudaSetDevice(ordinal);
+        for (cudaEvent_t e : {ev_fwd, ev_spec, ev_done})
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : ev_chunk) cudaEventDestroy(e);
+        if (st) cudaStreamDestroy(st);
+        if (cst) cudaStreamDestroy(cst);
+        if (comm && g_nccl.ok) g_nccl.CommDestroy(comm);
+    }
+};
+
+struct MultiCtx {
+    std::vector<int> devs;
+    std::vector<i64> dims;
+    int exchange = kExP2P;
+    int P = 1, chunks = 1;
+    i64 local_values = 0;  // real values per rank's slab
+    std::vector<std::unique_ptr<MultiRank>> ranks;
+    bool fresh = true;         // no solve enqueued yet (no ev_done to wait on)
+    cudaEvent_t tev[4] = {};   // stage stamps on rank 0's stream
+    std::mutex mu;             // one solve per context at a time
+    ~MultiCtx() {
+        if (!ranks.empty()) cudaSetDevice(ranks[0]->ordinal);
+        for (cudaEvent_t e : tev)
+            if (e) cudaEventDestroy(e);
+        ranks.clear();
+    }
+};
+
+std::mutex g_multi_mu;
+std::map<std::string, std::unique_ptr<MultiCtx>> g_multi;
+
+// The device list a host solve runs on: opt->devices[0..num_gpus) or
+// 0..num_gpus-1 when opt->num_gpus > 1 (or devices are given); else the
+// process default (fsx_set_devices); empty = single GPU.
+std::vector<int> multi_devices(const fsx_options* opt) {
+    std::vector<int> devs;
+    if (opt && (opt->num_gpus > 1 || (opt->devices && opt->num_gpus >= 1))) {
+        for (int r = 0; r < opt->num_gpus; ++r) devs.push_back(opt->devices ? opt->devices[r] : r);
+        return devs;
+    }
+    if (opt && opt->num_gpus == 1) return devs;  // explicitly one GPU
+    std::lock_guard<std::mutex> lk(g_multi_default_mu);
+    return g_multi_default;
+}
+
+// Whether a problem decomposes into slabs over P ranks (else it runs on one
+// GPU: same result contract, the decomposition is a performance choice).
+bool multi_eligible(const Shape& s, const Taps& taps, int P) {
+    const int rk = s.rank();
+    if ((rk != 2 && rk != 3) || s.fields != 1 || P < 1) return false;
+    for (i64 d : s.dims)
+        if (!is_pow2(d)) return false;
+    const i64 L = s.dims[rk - 1];
+    if (L < 16 || L > 2 * fsx::kMaxLine || s.dims[0] < 8 || s.dims[0] > fsx::kMaxLine || s.dims[0] % P) return false;
+    if (rk == 3 && (s.dims[1] < 2 || s.dims[1] % P || s.dims[1] > fsx::kMaxLine)) return false;
+    if ((i64)taps.map.size() > fsx::kMaxFusedTaps) return false;
+    std::set<i64> groups;
+    for (const auto& kv : taps.map) groups.insert(kv.first[0]);
+    return (int)groups.size() <= fsx::kMaxGroups;
+}
+
+MultiCtx& multi_ctx(const fsx_shape* global, const Shape& s, const std::vector<int>& devs, int exchange) {
+    const int P = (int)devs.size();
+    std::set<int> distinct(devs.begin(), devs.end());
+    if (exchange == kExAuto) {
+        exchange = kExP2P;
+        for (int a : distinct)
+            for (int b : distinct) {
+                int can = 1;
+                if (a != b) FSX_CK(cudaDeviceCanAccessPeer(&can, a, b));
+                if (!can) exchange = kExNccl;
+            }
+    }
+    std::string key = std::to_string(exchange) + "|";
+    for (int d : devs) key += std::to_string(d) + ",";
+    for (i64 d : s.dims) key += ":" + std::to_string(d);
+    std::lock_guard<std::mutex> lk(g_multi_mu);
+    auto it = g_multi.find(key);
+    if (it != g_multi.end()) return *it->second;
+    if (g_multi.size() >= 4) {  // bounded: drop idle contexts
+        for (auto e = g_multi.begin(); e != g_multi.end();) {
+            std::unique_lock<std::mutex> busy(e->second->mu, std::try_to_lock);
+            if (busy.owns_lock()) {
+                busy.unlock();
+                e = g_multi.erase(e);
+            } else {
+                ++e;
+            }
+        }
+    }
+    auto c = std::make_unique<MultiCtx>();
+    c->devs = devs;
+    c->dims = s.dims;
+    c->exchange = exchange;
+    c->P = P;
+    c->local_values = s.cells / P;
+    const bool three = s.rank() == 3;
+    // peer access between every pair of distinct devices (NVLink / NVSwitch)
+    if (exchange == kExP2P)
+        for (int a : distinct)
+            for (int b : distinct) {
+                if (a == b) continue;
+                int can = 0;
+                FSX_CK(cudaDeviceCanAccessPeer(&can, a, b));
+                if (!can) throw SpecErr("multi-GPU p2p exchange: device " + std::to_string(a) + " cannot access device " +
+                                        std::to_string(b) + " (use the nccl exchange)");
+                FSX_CK(cudaSetDevice(a));
+                const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else FSX_CK(e);
+            }
+    for (int r = 0; r < P; ++r) {
+        auto mr = std::make_unique<MultiRank>();
+        mr->ordinal = devs[r];
+        mr->dev = &device_for(devs[r]);  // selects the device
+        FSX_CK(cudaStreamCreateWithFlags(&mr->st, cudaStreamNonBlocking));
+        FSX_CK(cudaStreamCreateWithFlags(&mr->cst, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&mr->ev_fwd, &mr->ev_spec, &mr->ev_done})
+            FSX_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        mr->sp = make_slab_plan(global, P, r);
+        const SlabPlan& sp = *mr->sp;
+        mr->in.ensure((size_t)c->local_values * 8);
+        mr->out.ensure((size_t)c->local_values * 8);
+        mr->recv.ensure((size_t)sp.xcount * 16);
+        if (exchange == kExNccl) mr->send.ensure((size_t)sp.xcount * 16);
+        mr->flags.ensure(sizeof(fsx::Flags));
+        FSX_CK(cudaMemset(mr->flags.p, 0, sizeof(fsx::Flags)));
+        if (three) {
+            // plane chunks of the 3D exchange: up to 4, each >= 1 plane
+            c->chunks = (int)std::min<i64>(4, sp.n0l);
+            const i64 pc = sp.n0l / c->chunks;
+            mr->ymaps.resize(c->chunks);
+            mr->ytma.assign(c->chunks, false);
+            mr->ev_chunk.resize(c->chunks);
+            for (int q = 0; q < c->chunks; ++q) {
+                FSX_CK(cudaEventCreateWithFlags(&mr->ev_chunk[q], cudaEventDisableTiming));
+                fsx::AxisGeom g = sp.axy;
+                g.outer = pc;
+                mr->ytma[q] = tma_enabled() && fsx::tma_cols_ok(sp.n1) &&
+                              fsx::make_cols_tensor_map(mr->ymaps[q].b, sp.H.as<double2>() + q * pc * sp.n1 * sp.Pp,
+                                                        g) == 0;
+            }
+        }
+        c->ranks.push_back(std::move(mr));
+    }
+    if (exchange == kExP2P && !three) {
+        // 2D: each rank's device array of every rank's exchange buffer
+        std::vector<void*> ptrs(P);
+        for (int d = 0; d < P; ++d) ptrs[d] = c->ranks[d]->recv.p;
+        for (auto& mr : c->ranks) {
+            FSX_CK(cudaSetDevice(mr->ordinal));
+            mr->peers.ensure(P * sizeof(void*));
+            FSX_CK(cudaMemcpy(mr->peers.p, ptrs.data(), P * sizeof(void*), cudaMemcpyHostToDevice));
+        }
+    }
+    if (exchange == kExNccl) {
+        const NcclApi& api = nccl_api();
+        if (!api.ok) throw NcclErr("multi-GPU nccl exchange: " + api.why);
+        if ((int)distinct.size() != P)
+            throw SpecErr("multi-GPU nccl exchange: one rank per device (repeated ordinals need the p2p exchange)");
+        std::vector<ncclComm_t> comms(P);
+        FSX_NCCL(api, api.CommInitAll(comms.data(), P, devs.data()));
+        for (int r = 0; r < P; ++r) c->ranks[r]->comm = comms[r];
+    }
+    FSX_CK(cudaSetDevice(devs[0]));
+    for (cudaEvent_t& e : c->tev) FSX_CK(cudaEventCreate(&e));
+    auto& ref = *c;
+    g_multi.emplace(key, std::move(c));
+    return ref;
+}
+
+// One grouped all-to-all of equal blocks: rank r sends src_r block d to rank
+// d, which receives it as dst_d block r (NCCL point-to-point, one group).
+void nccl_all_to_all(MultiCtx& c, bool back) {
+    const NcclApi& api = nccl_api();
+    const size_t blk = (size_t)c.ranks[0]->sp->xcount / c.P * 2;  // doubles per block
+    FSX_NCCL(api, api.GroupStart());
+    for (int r = 0; r < c.P; ++r) {
+        MultiRank& mr = *c.ranks[r];
+        const double* src = (back ? mr.recv : mr.send).as<double>();
+        double* dst = (back ? mr.send : mr.recv).as<double>();
+        for (int d = 0; d < c.P; ++d) {
+            FSX_NCCL(api, api.Send(src + d * blk, blk, ncclDouble, d, mr.comm, mr.st));
+            FSX_NCCL(api, api.Recv(dst + d * blk, blk, ncclDouble, d, mr.comm, mr.st));
+        }
+    }
+    FSX_NCCL(api, api.GroupEnd());
+}
+
+// Every rank's stream st (or cst) waits on event ev of every rank.
+void multi_barrier(MultiCtx& c, cudaEvent_t MultiRank::*ev, bool copy_stream = false) {
+    for (auto& mr : c.ranks) {
+        FSX_CK(cudaSetDevice(mr->ordinal));
+        for (auto& other : c.ranks) FSX_CK(cudaStreamWaitEvent(copy_stream ? mr->cst : mr->st, (*other).*ev, 0));
+    }
+}
+
+// One host-pointer solve over the context's ranks (the caller holds every
+// involved device's lock and the context's).
+void multi_solve(MultiCtx& c, const Taps& taps, u64 T, const double* a0, double* out, fsx_stage_timings* stt,
+                 std::chrono::steady_clock::time_point t_entry) {
+    using clk = std::chrono::steady_clock;
+    const int P = c.P;
+    const bool three = c.dims.size() == 3;
+    const size_t lbytes = (size_t)c.local_values * 8;
+    const auto t_enq = clk::now();
+    // the previous solve's inverse reads every exchange buffer: all of it
+    // must have finished before this solve writes into them
+    if (!c.fresh) multi_barrier(c, &MultiRank::ev_done);
+    FSX_CK(cudaSetDevice(c.ranks[0]->ordinal));
+    if (stt) FSX_CK(cudaEventRecord(c.tev[0], c.ranks[0]->st));
+    for (int r = 0; r < P; ++r) {
+        MultiRank& mr = *c.ranks[r];
+        SlabPlan& sp = *mr.sp;
+        const double2* tw = mr.dev->tw_all.as<double2>();
+        FSX_CK(cudaSetDevice(mr.ordinal));
+        FSX_CK(cudaMemcpyAsync(mr.in.p, a0 + (size_t)r * c.local_values, lbytes, cudaMemcpyHostToDevice, mr.st));
+        if (c.exchange == kExNccl) {
+            slab_forward(sp, *mr.dev, mr.in.as<double>(), mr.send.as<double2>(), mr.st);
+        } else if (!three) {
+            const fsx::RowLayout lay{0, sp.CB, sp.n0l, mr.peers.as<double2* const>(), (i64)r * sp.n0l};
+            FSX_CK(fsx::launch_r2c_rows(mr.in.as<double>(), nullptr, sp.n0l, sp.L, lay, tw, mr.st));
+            FSX_CK(cudaEventRecord(mr.ev_fwd, mr.st));
+        } else {
+            // chunked: R2C rows + y pass of a plane chunk, then its puts on the copy stream
+            const i64 pc = sp.n0l / c.chunks, crow = pc * sp.n1;
+            double2* H = sp.H.as<double2>();
+            const size_t w = (size_t)sp.n1b * sp.Pp * 16;
+            for (int q = 0; q < c.chunks; ++q) {
+                const fsx::RowLayout lay{sp.Pp, 0, crow};
+                double2* Hq = H + q * crow * sp.Pp;
+                FSX_CK(fsx::launch_r2c_rows(mr.in.as<double>() + q * crow * sp.L, Hq, crow, sp.L, lay, tw, mr.st));
+                fsx::AxisGeom g = sp.axy;
+                g.outer = pc;
+                fsx::FusedSymbol none;
+                fsx::StepTwiddle nt;
+                if (mr.ytma[q]) FSX_CK(fsx::launch_cols_tma(mr.ymaps[q].b, g, 0, none, tw, mr.st));
+                else FSX_CK(fsx::launch_axis_pow2(Hq, Hq, g, -1, nt, tw, mr.st));
+                FSX_CK(cudaEventRecord(mr.ev_chunk[q], mr.st));
+                FSX_CK(cudaStreamWaitEvent(mr.cst, mr.ev_chunk[q], 0));
+                for (int d = 0; d < P; ++d) {
+                    double2* dst = c.ranks[d]->recv.as<double2>() + ((i64)r * sp.n0l + q * pc) * sp.n1b * sp.Pp;
+                    FSX_CK(cudaMemcpy2DAsync(dst, w, Hq + d * sp.n1b * sp.Pp, (size_t)sp.n1 * sp.Pp * 16, w,
+                                             (size_t)pc, cudaMemcpyDefault, mr.cst));
+                }
+            }
+            FSX_CK(cudaEventRecord(mr.ev_fwd, mr.cst));
+        }
+    }
+    if (c.exchange == kExNccl) nccl_all_to_all(c, false);
+    else multi_barrier(c, &MultiRank::ev_fwd);
+    FSX_CK(cudaSetDevice(c.ranks[0]->ordinal));
+    if (stt) FSX_CK(cudaEventRecord(c.tev[1], c.ranks[0]->st));
+    for (auto& mr : c.ranks) {
+        FSX_CK(cudaSetDevice(mr->ordinal));
+        slab_spectral(*mr->sp, *mr->dev, taps, T, mr->recv.as<double2>(), mr->st);
+        FSX_CK(cudaEventRecord(mr->ev_spec, mr->st));
+    }
+    FSX_CK(cudaSetDevice(c.ranks[0]->ordinal));
+    if (stt) FSX_CK(cudaEventRecord(c.tev[2], c.ranks[0]->st));
+    if (c.exchange == kExNccl) nccl_all_to_all(c, true);
+    else multi_barrier(c, &MultiRank::ev_spec, three);
+    for (int r = 0; r < P; ++r) {
+        MultiRank& mr = *c.ranks[r];
+        SlabPlan& sp = *mr.sp;
+        const double2* tw = mr.dev->tw_all.as<double2>();
+        fsx::Flags* fl = mr.flags.as<fsx::Flags>();
+        FSX_CK(cudaSetDevice(mr.ordinal));
+        if (c.exchange == kExNccl) {
+            slab_inverse(sp, *mr.dev, mr.send.as<double2>(), mr.out.as<double>(), mr.st, fl);
+        } else if (!three) {
+            const fsx::RowLayout lay{0, sp.CB, sp.n0l, mr.peers.as<double2* const>(), (i64)r * sp.n0l};
+            FSX_CK(fsx::launch_c2r_rows(nullptr, mr.out.as<double>(), sp.n0l, sp.L, lay, tw, fl, mr.st));
+        } else {
+            // chunked pulls of this rank's blocks ahead of the inverse y pass and C2R rows
+            const i64 pc = sp.n0l / c.chunks, crow = pc * sp.n1;
+            double2* H = sp.H.as<double2>();
+            const size_t w = (size_t)sp.n1b * sp.Pp * 16;
+            for (int q = 0; q < c.chunks; ++q) {
+                double2* Hq = H + q * crow * sp.Pp;
+                for (int d = 0; d < P; ++d) {
+                    const double2* src = c.ranks[d]->recv.as<double2>() + ((i64)r * sp.n0l + q * pc) * sp.n1b * sp.Pp;
+                    FSX_CK(cudaMemcpy2DAsync(Hq + d * sp.n1b * sp.Pp, (size_t)sp.n1 * sp.Pp * 16, src, w, w, (size_t)pc,
+                                             cudaMemcpyDefault, mr.cst));
+                }
+                FSX_CK(cudaEventRecord(mr.ev_chunk[q], mr.cst));
+                FSX_CK(cudaStreamWaitEvent(mr.st, mr.ev_chunk[q], 0));
+                fsx::AxisGeom g = sp.axy;
+                g.outer = pc;
+                fsx::FusedSymbol none;
+                fsx::StepTwiddle nt;
+                if (mr.ytma[q]) FSX_CK(fsx::launch_cols_tma(mr.ymaps[q].b, g, 1, none, tw, mr.st));
+                else FSX_CK(fsx::launch_axis_pow2(Hq, Hq, g, +1, nt, tw, mr.st));
+                const fsx::RowLayout lay{sp.Pp, 0, crow};
+                FSX_CK(fsx::launch_c2r_rows(Hq, mr.out.as<double>() + q * crow * sp.L, crow, sp.L, lay, tw, fl, mr.st));
+            }
+        }
+        FSX_CK(cudaMemcpyAsync(out + (size_t)r * c.local_values, mr.out.p, lbytes, cudaMemcpyDeviceToHost, mr.st));
+        FSX_CK(cudaEventRecord(mr.ev_done, mr.st));
+    }
+    FSX_CK(cudaSetDevice(c.ranks[0]->ordinal));
+    if (stt) FSX_CK(cudaEventRecord(c.tev[3], c.ranks[0]->st));
+    c.fresh = false;
+    // synchronize, then the reference's realize check on every slab
+    std::string err;
+    for (int r = 0; r < P; ++r) {
+        MultiRank& mr = *c.ranks[r];
+        FSX_CK(cudaSetDevice(mr.ordinal));
+        FSX_CK(cudaStreamSynchronize(mr.st));
+        fsx::Flags h;
+        FSX_CK(cudaMemcpy(&h, mr.flags.p, sizeof(h), cudaMemcpyDeviceToHost));
+        FSX_CK(cudaMemset(mr.flags.p, 0, sizeof(h)));
+        if (h.nonfinite && err.empty()) err = " (slab " + std::to_string(r) + " of " + std::to_string(P) + ")";
+    }
+    if (!err.empty()) throw NumErr("solve_periodic: non-finite value after inverse FFT" + err);
+    if (stt) {
+        // wait for rank 0's last stamp: every rank's stream joined it through the barriers
+        FSX_CK(cudaSetDevice(c.ranks[0]->ordinal));
+        FSX_CK(cudaEventSynchronize(c.tev[3]));
+        float t01 = 0, t12 = 0, t23 = 0;
+        FSX_CK(cudaEventElapsedTime(&t01, c.tev[0], c.tev[1]));
+        FSX_CK(cudaEventElapsedTime(&t12, c.tev[1], c.tev[2]));
+        FSX_CK(cudaEventElapsedTime(&t23, c.tev[2], c.tev[3]));
+        const double setup = std::chrono::duration<double>(t_enq - t_entry).count();
+        const double total = std::chrono::duration<double>(clk::now() - t_entry).count();
+        const double gpu = (t01 + t12 + t23) * 1e-3;
+        stt->forward_fft += setup + t01 * 1e-3;
+        stt->squaring += t12 * 1e-3;
+        stt->inverse_fft += t23 * 1e-3 + std::max(0.0, total - setup - gpu);
+    }
+}
+
+// Routes a host solve to the multi-GPU path; false when it runs on one GPU.
+bool try_multi(const fsx_shape* shape, const Shape& s, const Taps& taps, u64 T, const double* a0, double* out,
+               const fsx_options* opt, fsx_stage_timings* stt, std::chrono::steady_clock::time_point t_entry) {
+    const std::vector<int> devs = multi_devices(opt);
+    if (devs.empty() || !multi_eligible(s, taps, (int)devs.size())) return false;
+    const int exchange = opt ? opt->exchange : kExAuto;
+    if (exchange < kExAuto || exchange > kExNccl) throw SpecErr("fsx_options.exchange: 0 auto, 1 p2p, 2 nccl");
+    // every involved device's lock, in ordinal order (no lock-order inversion)
+    std::set<int> distinct(devs.begin(), devs.end());
+    std::vector<std::unique_ptr<DevLock>> locks;
+    for (int d : distinct) locks.push_back(std::make_unique<DevLock>(d));
+    MultiCtx& c = multi_ctx(shape, s, devs, exchange);
+    std::lock_guard<std::mutex> lk(c.mu);
+    multi_solve(c, taps, T, a0, out, stt, t_entry);
+    return true;
+}
+
 struct SolveReq {
     const fsx_shape* shape;
     const double* a0;
@@ -1387,6 +1834,10 @@ void solve(const SolveReq& rq) {
         if (out != in) std::memmove(out, in, bytes);
         return;
     }
+    // host-pointer explicit scalar solves of slab-decomposable grids go to the
+    // multi-GPU path when more than one device is asked for
+    if (!rq.device_ptrs && !f32 && !rq.q && try_multi(rq.shape, s, taps, rq.T, rq.a0, rq.out, rq.opt, rq.st, t_entry))
+        return;
     DevLock dlk(ordinal);
     Device& dev = dlk.dev;
     cudaStream_t st = stream_of(dev, rq.opt);
@@ -1539,6 +1990,9 @@ fsx_status guarded(F&& f) {
     } catch (const CudaErr& e) {
         g_err = e.what();
         return e.code == cudaErrorMemoryAllocation ? FSX_ERR_OOM : FSX_ERR_CUDA;
+    } catch (const NcclErr& e) {
+        g_err = e.what();
+        return FSX_ERR_NCCL;
     } catch (const std::bad_alloc&) {
         g_err = "fsx: host allocation failed";
         return FSX_ERR_OOM;
@@ -1566,6 +2020,33 @@ __attribute__((visibility("hidden"))) void fsx_internal_set_error(const char* ms
 
 const char* fsx_last_error(void) { return g_err.c_str(); }
 int32_t fsx_version(void) { return 100; }
+
+fsx_status fsx_set_devices(const int32_t* devices, int32_t n) {
+    return guarded([&] {
+        if (n < 0 || n > 1024) throw SpecErr("fsx_set_devices: bad device count");
+        std::vector<int> devs;
+        if (n > 1 || (n == 1 && devices)) {
+            int count = 0;
+            if (cudaGetDeviceCount(&count) != cudaSuccess) {
+                cudaGetLastError();
+                count = 0;
+            }
+            for (int r = 0; r < n; ++r) {
+                const int d = devices ? devices[r] : r;
+                if (d < 0 || d >= count) throw SpecErr("fsx_set_devices: device ordinal out of range");
+                devs.push_back(d);
+            }
+        }
+        std::lock_guard<std::mutex> lk(g_multi_default_mu);
+        g_multi_default = devs;
+    });
+}
+
+int32_t fsx_get_devices(int32_t* devices, int32_t cap) {
+    std::lock_guard<std::mutex> lk(g_multi_default_mu);
+    for (int32_t r = 0; devices && r < cap && r < (int32_t)g_multi_default.size(); ++r) devices[r] = g_multi_default[r];
+    return (int32_t)g_multi_default.size();
+}
 
 int32_t fsx_device_count(void) {
     int n = 0;
@@ -1829,6 +2310,23 @@ fsx_status fsx_plan_describe(const fsx_shape* shape, const fsx_kernel* k, const 
         info->alg_bytes = p.alg_bytes;
         info->fused_bytes = p.fused_bytes;
         info->work_bytes = (int64_t)p.work.bytes;
+        info->ranks = 1;
+        info->exchange = 0;
+        const std::vector<int> devs = multi_devices(opt);
+        if (!devs.empty() && multi_eligible(s, taps, (int)devs.size())) {
+            info->ranks = (int32_t)devs.size();
+            int ex = opt ? opt->exchange : kExAuto;
+            if (ex == kExAuto) {
+                ex = kExP2P;
+                for (int a : devs)
+                    for (int b : devs) {
+                        int can = 1;
+                        if (a != b) FSX_CK(cudaDeviceCanAccessPeer(&can, a, b));
+                        if (!can) ex = kExNccl;
+                    }
+            }
+            info->exchange = ex;
+        }
     });
 }
 

@@ -313,25 +313,55 @@ CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: the NULL stream's explicit handle
 _OPTS: dict = {}  # option structs are read-only for the library: reuse them
 
 
-def _opts(device: int = 0, path: int = 0, stream: int | None = None, stage_events: int = 0, spectral_cut: int = 0):
+def _opts(device: int = 0, path: int = 0, stream: int | None = None, stage_events: int = 0, spectral_cut: int = 0,
+          num_gpus: int = 0, exchange: int = 0, devices=None):
     """fsx_options.  stream None -> the library's own stream; a handle of 0
     (torch's default stream) is passed as cudaStreamLegacy so the work is
-    ordered with the caller's NULL-stream work instead of the library stream."""
-    key = (device, path, stream, stage_events, spectral_cut)
+    ordered with the caller's NULL-stream work instead of the library stream.
+    num_gpus / exchange / devices: the single-process multi-GPU path (fsx.h)."""
+    devices = tuple(int(d) for d in devices) if devices is not None else None
+    key = (device, path, stream, stage_events, spectral_cut, num_gpus, exchange, devices)
     o = _OPTS.get(key)
     if o is None:
         o = _lib.FsxOptions()
         o.device, o.path, o.stage_events, o.spectral_cut = device, path, stage_events, int(bool(spectral_cut))
         o.stream = None if stream is None else (stream or CUDA_STREAM_LEGACY)
+        o.num_gpus, o.exchange = num_gpus, exchange
+        if devices is not None:
+            o._devs = (ctypes.c_int32 * len(devices))(*devices)  # kept alive with the struct
+            o.devices = ctypes.cast(o._devs, ctypes.POINTER(ctypes.c_int32))
+            o.num_gpus = len(devices)
         if len(_OPTS) > 256:
             _OPTS.clear()
         _OPTS[key] = o
     return o
 
 
+def set_devices(devices=None, n: int | None = None) -> None:
+    """Process default device list of host solves (fsx_set_devices): eligible
+    2D/3D grids are then slab-decomposed over these devices by every
+    solve_periodic call that does not pass its own ``devices``.  ``[]`` or
+    one device -> single GPU.  A repeated ordinal emulates ranks on one GPU."""
+    L = _lib.load()
+    if devices is None:
+        _lib.check(L.fsx_set_devices(None, ctypes.c_int32(int(n or 0))))
+        return
+    devs = [int(d) for d in devices]
+    arr = (ctypes.c_int32 * max(1, len(devs)))(*devs)
+    _lib.check(L.fsx_set_devices(arr, ctypes.c_int32(len(devs))))
+
+
+def get_devices() -> list:
+    L = _lib.load()
+    n = L.fsx_get_devices(None, ctypes.c_int32(0))
+    arr = (ctypes.c_int32 * max(1, n))()
+    L.fsx_get_devices(arr, ctypes.c_int32(n))
+    return [int(arr[i]) for i in range(n)]
+
+
 # ---------------------------------------------------------------- solvers
 def _solve(fn, a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None, path: int, extra=(), out=None,
-           spectral_cut: int = 0):
+           spectral_cut: int = 0, multi: dict | None = None):
     L = _lib.load()
     if T < 0 or T >= 1 << 64:
         raise SpecError("T must be a nonnegative 64-bit integer")
@@ -344,7 +374,7 @@ def _solve(fn, a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None,
     stc = st._push() if st is not None else None
     status = getattr(L, fn)(ctypes.byref(shape_c), a0.data.ctypes.data_as(_DP), ctypes.byref(kc),
                             _u64_T(T), *extra, out.ctypes.data_as(_DP),
-                            ctypes.byref(_opts(path=path, spectral_cut=spectral_cut)),
+                            ctypes.byref(_opts(path=path, spectral_cut=spectral_cut, **(multi or {}))),
                             ctypes.byref(stc) if stc is not None else None)
     del keep
     _lib.check(status)
@@ -354,11 +384,16 @@ def _solve(fn, a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None,
 
 
 def solve_periodic(a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None = None, *, path: int = 0,
-                   out: np.ndarray | None = None, spectral_cut: int = 0):
+                   out: np.ndarray | None = None, spectral_cut: int = 0, num_gpus: int = 0, devices=None,
+                   exchange: int = 0):
     """proj/src/periodic.cpp:76-86 on the B200 path (fsx_solve_periodic).
     ``out`` optionally supplies the (e.g. pinned) host array the result is written to.
-    ``spectral_cut=1``: the exact spectral cut (fsx_options.spectral_cut; same result)."""
-    return _solve("fsx_solve_periodic", a0, k, T, st, path, out=out, spectral_cut=spectral_cut)
+    ``spectral_cut=1``: the exact spectral cut (fsx_options.spectral_cut; same result).
+    ``num_gpus`` / ``devices`` / ``exchange`` (0 auto, 1 p2p, 2 nccl): slab-decompose an
+    eligible 2D/3D grid over several GPUs of this process (fsx_options; 0 = the
+    process default of set_devices)."""
+    multi = {"num_gpus": num_gpus, "exchange": exchange, "devices": devices}
+    return _solve("fsx_solve_periodic", a0, k, T, st, path, out=out, spectral_cut=spectral_cut, multi=multi)
 
 
 def solve_periodic_vector(a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None = None, *, path: int = 0):
@@ -582,15 +617,17 @@ def spectral_cut_columns(shape: GridShape, k: StencilKernel, T: int) -> tuple:
     return kept.value, total.value
 
 
-def plan_describe(shape: GridShape, k: StencilKernel, path: int = 0) -> dict:
+def plan_describe(shape: GridShape, k: StencilKernel, path: int = 0, num_gpus: int = 0, devices=None,
+                  exchange: int = 0) -> dict:
     L = _lib.load()
     info = _lib.FsxPlanInfo()
     kc, keep = k._c()
-    _lib.check(L.fsx_plan_describe(ctypes.byref(shape._c()), ctypes.byref(kc), ctypes.byref(_opts(path=path)),
-                                   ctypes.byref(info)))
+    o = _opts(path=path, num_gpus=num_gpus, exchange=exchange, devices=devices)
+    _lib.check(L.fsx_plan_describe(ctypes.byref(shape._c()), ctypes.byref(kc), ctypes.byref(o), ctypes.byref(info)))
     del keep
     return {"path": info.path, "launches": info.launches, "alg_bytes": info.alg_bytes,
-            "fused_bytes": info.fused_bytes, "work_bytes": info.work_bytes}
+            "fused_bytes": info.fused_bytes, "work_bytes": info.work_bytes, "ranks": info.ranks,
+            "exchange": info.exchange}
 
 
 # ---------------------------------------------------------------- building blocks

@@ -70,6 +70,37 @@ int main(int argc, char** argv) {
         FieldGrid c = solve_periodic_cached(a, k, 1, cache, &st);
         for (int i = 0; i < 4; ++i) CHECK(std::fabs(c.data[i] - want[i]) <= 1e-12);
         CHECK(st.sum() > 0);
+        // multi-GPU through the unchanged drop-in call: the process default
+        // device list (two ranks emulated on device 0) slab-decomposes a 2D
+        // and a 3D grid; the result matches the single-GPU solve
+        StencilKernel k2(2), k3(3);
+        for (int o = -1; o <= 1; ++o) {
+            k2.add_tap({o, 0}, 0.2);
+            k2.add_tap({0, o}, 0.2);
+            k3.add_tap({o, 0, 0}, 0.1);
+            k3.add_tap({0, o, 0}, 0.1);
+            k3.add_tap({0, 0, o}, 0.1);
+        }
+        FieldGrid g2(GridShape({64, 128})), g3(GridShape({16, 8, 32}));
+        for (size_t i = 0; i < g2.data.size(); ++i) g2.data[i] = std::cos(0.37 * i);
+        for (size_t i = 0; i < g3.data.size(); ++i) g3.data[i] = std::sin(0.11 * i);
+        const FieldGrid s2 = solve_periodic(g2, k2, 50), s3 = solve_periodic(g3, k3, 20);
+        set_devices({0, 0});
+        StageTimings mst;
+        const FieldGrid m2 = solve_periodic(g2, k2, 50, &mst), m3 = solve_periodic(g3, k3, 20);
+        set_devices({});
+        CHECK(mst.sum() > 0);
+        double e2 = 0, n2 = 0, e3 = 0, n3 = 0;
+        for (size_t i = 0; i < s2.data.size(); ++i) {
+            e2 += (m2.data[i] - s2.data[i]) * (m2.data[i] - s2.data[i]);
+            n2 += s2.data[i] * s2.data[i];
+        }
+        for (size_t i = 0; i < s3.data.size(); ++i) {
+            e3 += (m3.data[i] - s3.data[i]) * (m3.data[i] - s3.data[i]);
+            n3 += s3.data[i] * s3.data[i];
+        }
+        CHECK(std::sqrt(e2 / n2) <= 1e-12);
+        CHECK(std::sqrt(e3 / n3) <= 1e-12);
     }
     std::printf("%s: %d failure(s)\n", gpu ? "gpu" : "cpu", failures);
     return failures ? 1 : 0;
