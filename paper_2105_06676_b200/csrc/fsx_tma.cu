@@ -828,15 +828,314 @@ k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol s
     }
 }
 
-// FSX_F8192: "c" (default) the CTA-pair kernel, "h" the one-CTA parity-halves kernel
-static bool f8192_pair() {
+// ------------------------------------------------------------------ persistent CTA pairs, TMEM-prefetched columns
+// k_fused8192c loads its column half when the CTA starts and stores it when
+// it ends, so each CTA's TMA load and store latency is exposed to the SM
+// except for what the one other resident CTA happens to overlap (ncu: ~20 %
+// of the stall samples wait for the tile).  Shared memory has no room for a
+// second 64 KB tile per CTA, but tensor memory (256 KB per SM, unused by an
+// FFT) does: here each CTA pair is persistent over columns c, c + G, ... and
+// while it transforms column c its thread 0 streams the next column's half
+// through a 12 KB shared-memory stage into TMEM (TMA box loads -> mbarrier ->
+// tcgen05.cp 128x128b -> tcgen05.commit), a chunk per checkpoint between the
+// compute phases.  The next iteration starts with one tcgen05.ld.32x32b.x64
+// per thread (its 16 values: lane = thread mod 128, 64 contiguous columns).
+// The per-column symbol tap terms are computed one column ahead (double
+// buffered), and the TMA store of the result drains while the next column's
+// data comes out of TMEM.  Arithmetic, exchanges and results are those of
+// k_fused8192c (bitwise).
+__device__ __forceinline__ unsigned long long tmem_cp_desc(const void* smem) {
+    // no-swizzle K-major matrix of 128 rows x 16 B: 8-row core matrices 128 B apart
+    const unsigned a = smem_u32(smem);
+    return (unsigned long long)((a >> 4) & 0x3FFF) | (1ull << 16) | ((unsigned long long)(128 >> 4) << 32) | (1ull << 46);
+}
+__device__ __forceinline__ void tmem_cp_128x128b(unsigned taddr, const void* smem) {
+    asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;\n" ::"r"(taddr), "l"(tmem_cp_desc(smem)) : "memory");
+}
+__device__ __forceinline__ void tmem_commit(unsigned long long* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+// 16 complex values (64 x 32-bit TMEM columns) of this thread's lane
+__device__ __forceinline__ void tmem_ld16(unsigned taddr, double2 (&v)[16]) {
+    unsigned r[64];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+        "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,"
+        "%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]),
+          "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]),
+          "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]),
+          "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]),
+          "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        v[q].x = __hiloint2double((int)r[4 * q + 1], (int)r[4 * q]);
+        v[q].y = __hiloint2double((int)r[4 * q + 3], (int)r[4 * q + 2]);
+    }
+}
+
+// Thread 0's column-half prefetch: chunks of PF_BOX TMA boxes (256 rows of
+// 16 B) land in the stage, then tcgen05.cp moves each 128-element block b
+// (half-column elements 128 b .. 128 b + 127) to lanes 0..127, columns
+// 64 (b % 2) + 4 (b / 2): thread th then finds elements th + 256 q at lane
+// th % 128, columns 64 (th / 128) + 4 q.
+__device__ __forceinline__ bool mbar_test(unsigned long long* bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+struct PrefetchPipe {
+    static constexpr int PF_BOX = 3;                              // boxes per chunk (12 KB stage)
+    static constexpr int NCH = (16 + PF_BOX - 1) / PF_BOX;        // chunks per 4096-element half
+    int pend = NCH;      // chunk in flight (NCH: nothing pending)
+    int state = 0;       // 0 idle, 1 TMA landing in the stage, 2 tcgen05.cp reading the stage
+    i64 col = 0;         // column being prefetched
+    unsigned lpar = 0, cpar = 0;
+    __device__ __forceinline__ void issue(const CUtensorMap* map, double2* stage, unsigned long long* lbar, unsigned h,
+                                          int k) {
+        const int b0 = k * PF_BOX, b1 = b0 + PF_BOX < 16 ? b0 + PF_BOX : 16;
+        mbar_expect_tx(lbar, (unsigned)((b1 - b0) * 256 * sizeof(double2)));
+        for (int b = b0; b < b1; ++b) tma_load_4d(stage + (b - b0) * 256, map, (int)(2 * col), (int)h, b * 256, 0, lbar);
+        state = 1;
+    }
+    __device__ __forceinline__ void start(const CUtensorMap* map, double2* stage, unsigned long long* lbar, unsigned h,
+                                          i64 c) {
+        col = c;
+        pend = 0;
+        issue(map, stage, lbar, h, 0);
+    }
+    // Advance as far as possible without waiting (block = true: to the end):
+    // a landed chunk is copied into TMEM, a finished copy frees the stage for
+    // the next chunk's TMA loads.
+    __device__ __forceinline__ void poll(const CUtensorMap* map, double2* stage, unsigned long long* lbar,
+                                         unsigned long long* cbar, unsigned h, unsigned tbase, bool block = false) {
+        while (state != 0) {
+            if (state == 1) {
+                if (!block && !mbar_test(lbar, lpar)) return;
+                mbar_wait(lbar, lpar);
+                lpar ^= 1u;
+                tc_fence_after();
+                const int b0 = pend * PF_BOX, b1 = b0 + PF_BOX < 16 ? b0 + PF_BOX : 16;
+                for (int blk = 2 * b0; blk < 2 * b1; ++blk)
+                    tmem_cp_128x128b(tbase + 64u * (unsigned)(blk & 1) + 4u * (unsigned)(blk >> 1),
+                                     stage + (blk - 2 * b0) * 128);
+                tmem_commit(cbar);
+                state = 2;
+            } else {
+                if (!block && !mbar_test(cbar, cpar)) return;
+                mbar_wait(cbar, cpar);
+                cpar ^= 1u;
+                if (++pend < NCH) issue(map, stage, lbar, h, pend);
+                else state = 0;
+            }
+        }
+    }
+};
+
+// Symbol group coefficients of one column: tap terms (threads j < ntaps),
+// then their per-group sums (threads gi < ngroups) after a barrier.
+__device__ __forceinline__ i64 next_fused_col(const FusedSymbol& sym, i64 c, i64 step, i64 ncols) {
+    for (c += step; c < ncols; c += step)
+        if (sym.rank != 3 || c - (c / sym.P) * sym.P <= sym.M) return c;
+    return -1;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
+k_fused8192p(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
+    constexpr int N = 8192, NH = 4096, TH = 256;
+    using FF = LineFFT<NH, -1>;
+    using FI = LineFFT<NH, +1>;
+    extern __shared__ __align__(1024) double2 tile[];  // [NH] tile, [NH / 2] exchange-1 landing, prefetch stage
+    double2* recv = tile + NH;
+    double2* stage = recv + NH / 2;
+    __shared__ __align__(8) unsigned long long lbar, cbar, bx1, bx2, bok;
+    __shared__ double2 acoef[2][kMaxGroups];
+    __shared__ double2 tapterm[2][kMaxFusedTaps];
+    __shared__ unsigned tmem_base;
+    const int th = threadIdx.x;
+    const unsigned h = cluster_rank(), peer = h ^ 1u;
+    const i64 ncl = (i64)gridDim.x >> 1;
+    i64 c = next_fused_col(sym, (i64)(blockIdx.x >> 1) - ncl, ncl, g.ncols);
+    if (c < 0) return;  // (both CTAs of the pair)
+    PrefetchPipe pf;
+    if (th < 32) {  // 128 TMEM columns: one 4096-element half (lanes x 64 B)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n" ::"r"(smem_u32(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (th == 0) {
+        mbar_init(&lbar, 1);
+        mbar_init(&cbar, 1);
+        mbar_init(&bx1, 1);
+        mbar_init(&bx2, 1);
+        mbar_init(&bok, 1);
+        mbar_init_fence();
+        mbar_expect_tx(&bx1, (unsigned)(NH / 2 * sizeof(double2)));
+        mbar_expect_tx(&bx2, (unsigned)(NH / 2 * sizeof(double2)));
+    }
+    tc_fence_before();
+    cluster_arrive_relaxed();  // publishes the barrier initialisation to the peer
+    // the first column's tap terms and group sums
+    {
+        i64 kx, ky;
+        fused_col_freqs(sym, c, kx, ky);
+        for (int j = th; j < sym.ntaps; j += TH) tapterm[0][j] = tap_term(sym, tw_all, j, kx, ky);
+    }
+    __syncthreads();
+    tc_fence_after();
+    const unsigned tbase = tmem_base;
+    for (int gi = th; gi < sym.ngroups; gi += TH) {
+        double2 a = make_double2(0.0, 0.0);
+        for (int j = 0; j < sym.ntaps; ++j)
+            if (sym.tap_group[j] == gi) a = cadd(a, tapterm[0][j]);
+        acoef[0][gi] = a;
+    }
+    if (th == 0) {
+        pdl_wait();  // H is the predecessor's output
+        pf.start(&map2, stage, &lbar, h, c);
+        pf.poll(&map2, stage, &lbar, &cbar, h, tbase, true);
+    }
+    tc_fence_before();
+    cluster_wait();  // the peer's barriers exist
+    __syncthreads();  // the first column is in TMEM; acoef[0] written
+    tc_fence_after();
+    const unsigned my_taddr = tbase + ((unsigned)(32 * ((th >> 5) & 3)) << 16) + 64u * (unsigned)(th >> 7);
+    const double2 wt = __ldg(tw_all + N + th);  // W_8192^th; W_8192^(th + 256 q) = wt W_32^q
+    for (unsigned it = 0; c >= 0; ++it) {
+        const unsigned s = it & 1u, par = it & 1u;
+        const i64 cn = next_fused_col(sym, c, ncl, g.ncols);
+        double2 v[16];
+        tmem_ld16(my_taddr, v);
+        tc_fence_before();
+        if (th == 0) bulk_wait_read0();  // the previous column's store has read the tile
+        if (cn < 0) pdl_trigger();
+        __syncthreads();  // TMEM read by every thread; tile free
+        if (th == 0 && cn >= 0) {
+            tc_fence_after();
+            pf.start(&map2, stage, &lbar, h, cn);
+        }
+        FF::run(v, th, tile, tw_all + NH);
+        if (th == 0) pf.poll(&map2, stage, &lbar, &cbar, h, tbase);
+        if (h == 1) {
+            static_for<0, 16>([&](auto Q) {
+                constexpr int q = decltype(Q)::value;
+                v[q] = cmul(v[q], cmul_const<q, 32, -1>(wt));
+            });
+        }
+        // exchange 1: the half of the k range the peer keeps, into its recv
+        {
+            const unsigned dst = peer_smem(recv + th, peer), pbar = peer_smem(&bx1, peer);
+#pragma unroll
+            for (int b = 0; b < 8; ++b) st_async_peer(dst + 256u * 16u * b, h == 0 ? v[8 + b] : v[b], pbar);
+        }
+        if (th == 0) pf.poll(&map2, stage, &lbar, &cbar, h, tbase);
+        // the next column's tap terms (their table reads overlap the wait below)
+        if (cn >= 0) {
+            i64 kx, ky;
+            fused_col_freqs(sym, cn, kx, ky);
+            for (int j = th; j < sym.ntaps; j += TH) tapterm[s ^ 1u][j] = tap_term(sym, tw_all, j, kx, ky);
+        }
+        __syncthreads();  // every thread is past the forward FFT's tile reads
+        if (th == 0) mbar_arrive_peer(peer_smem(&bok, peer));  // the peer may write into this tile
+        mbar_wait(&bx1, par);
+        double2 u[16];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const double2 r = recv[th + 256 * b];
+            const double2 e = h == 0 ? v[b] : r;
+            const double2 o = h == 0 ? r : v[8 + b];
+            u[b] = cadd(e, o);
+            u[b + 8] = csub(e, o);
+        }
+        if (th == 0) {
+            mbar_expect_tx(&bx1, (unsigned)(NH / 2 * sizeof(double2)));  // next column's exchange 1
+            pf.poll(&map2, stage, &lbar, &cbar, h, tbase);
+        }
+        spectral_pair8192(u, th, (int)h, sym, tw_all, acoef[s]);
+        double2 keep[8], send[8];
+        static_for<0, 8>([&](auto B) {
+            constexpr int b = decltype(B)::value;
+            const double2 e = cadd(u[b], u[b + 8]);
+            const double2 d = csub(u[b], u[b + 8]);
+            const double2 o = h == 0 ? cmulc(d, cmul_const<b, 32, -1>(wt)) : cmulc(d, cmul_const<b + 8, 32, -1>(wt));
+            keep[b] = h == 0 ? e : o;
+            send[b] = h == 0 ? o : e;
+        });
+        if (th == 0) pf.poll(&map2, stage, &lbar, &cbar, h, tbase);
+        // exchange 2 into the peer's tile, once the peer's forward FFT is done with it
+        mbar_wait_cluster(&bok, par);
+        {
+            const unsigned dst = peer_smem(tile + th, peer), pbar = peer_smem(&bx2, peer);
+#pragma unroll
+            for (int b = 0; b < 8; ++b) st_async_peer(dst + 256u * 16u * b, send[b], pbar);
+        }
+        if (th == 0) pf.poll(&map2, stage, &lbar, &cbar, h, tbase);
+        mbar_wait(&bx2, par);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const double2 r = tile[th + 256 * b];
+            v[b] = h == 0 ? keep[b] : r;
+            v[8 + b] = h == 0 ? r : keep[b];
+        }
+        if (th == 0) mbar_expect_tx(&bx2, (unsigned)(NH / 2 * sizeof(double2)));
+        FI::run(v, th, tile, tw_all + NH);
+        if (th == 0) pf.poll(&map2, stage, &lbar, &cbar, h, tbase);
+        __syncthreads();  // the last exchange reads are done before the tile is overwritten
+#pragma unroll
+        for (int q = 0; q < 16; ++q) tile[th + 256 * q] = v[q];
+        fence_proxy_async();
+        // the next column's group sums (its tap terms were written before two barriers)
+        if (cn >= 0)
+            for (int gi = th; gi < sym.ngroups; gi += TH) {
+                double2 a = make_double2(0.0, 0.0);
+                for (int j = 0; j < sym.ntaps; ++j)
+                    if (sym.tap_group[j] == gi) a = cadd(a, tapterm[s ^ 1u][j]);
+                acoef[s ^ 1u][gi] = a;
+            }
+        __syncthreads();
+        if (th == 0) {
+#pragma unroll 1
+            for (int b = 0; b < NH / 256; ++b) tma_store_4d(&map2, tile + b * 256, (int)(2 * c), (int)h, b * 256, 0);
+            bulk_commit();
+            pf.poll(&map2, stage, &lbar, &cbar, h, tbase, true);
+        }
+        tc_fence_before();
+        __syncthreads();  // the next column is in TMEM
+        tc_fence_after();
+        c = cn;
+    }
+    if (th == 0) bulk_wait_read0();
+    tc_fence_before();
+    __syncthreads();
+    if (th < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;\n" ::"r"(tbase));
+}
+
+// FSX_F8192: "c" (default) the one-column-per-pair kernel, "p" the persistent
+// TMEM-prefetched pairs (measured slower on cfg3: 0.672 ms with blocking
+// chunk steps, 0.811 ms polled, against 0.584 -- a 12 KB stage keeps too few
+// bytes in flight to hide the 16-byte-row TMA latency), "h" the one-CTA
+// parity-halves kernel
+static int f8192_kind() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("FSX_F8192");
-        v = (e && e[0] == 'h') ? 0 : 1;
+        v = (e && e[0] == 'h') ? 0 : (e && e[0] == 'p') ? 2 : 1;
     }
-    return v != 0;
+    return v;
 }
+static bool f8192_pair() { return f8192_kind() != 0; }
 
 static int fused_halves() {
     static int v = -1;
@@ -852,6 +1151,19 @@ bool halves_ok(const AxisGeom& g) { return g.n == 8192 && g.outer == 1 && fused_
 cudaError_t launch_fused_halves(const void* tensor_map2, const AxisGeom& g, const FusedSymbol& sym,
                                 const double2* tw, cudaStream_t s) {
     const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(tensor_map2);
+    if (f8192_kind() == 2) {
+        // one persistent pair per SM (two CTAs of 256 threads per SM)
+        const size_t smem = (4096 + 2048 + 256 * PrefetchPipe::PF_BOX) * sizeof(double2);
+        kernel_prepare((const void*)k_fused8192p, smem);
+        static int nsm = 0;
+        if (!nsm) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        }
+        const i64 pairs = std::min<i64>(nsm, g.ncols);
+        return launch_pdl(k_fused8192p, dim3((unsigned)(2 * pairs)), dim3(256), smem, s, map, g, sym, tw);
+    }
     if (f8192_pair()) {
         const size_t smem2 = (4096 + 2048) * sizeof(double2);
         kernel_prepare((const void*)k_fused8192c, smem2);
