@@ -157,6 +157,25 @@ fsx_status fsx_solve_periodic_implicit(const fsx_shape* shape, const double* a0,
 fsx_status fsx_solve_periodic_batch(const fsx_shape* shape, int64_t nbatch, const double* const* a0s,
                                     const fsx_kernel* k, uint64_t T, double* const* outs, const fsx_options* opt);
 
+/* One recursion level's slab solves (the aperiodic recursion's rb_run, which
+ * calls solve_periodic_cached on each of the 2d face slabs of a level in turn,
+ * proj/src/aperiodic.cpp:224-228,240-244): nslabs grids of possibly different
+ * shapes (shapes[i], host pointers a0s[i] -> outs[i], each may alias), one
+ * kernel and T.  Slabs of equal shape are stacked and solved as one batched
+ * plan (one launch per pass for all of them, the stack an outer dimension of
+ * every pass); different shapes run on the device's two lanes so their
+ * copies and kernels overlap.  cache (may be NULL): SpectrumCache semantics of
+ * fsx_solve_periodic_cached -- the first kernel seen for a dims vector is used
+ * for every later slab with those dims.  Plans stay resident per device
+ * (keyed by shape and stack size) across calls.  Returns synchronized;
+ * FSX_ERR_NUMERIC names the first failing slab in argument order (the other
+ * outputs are valid).  st (may be NULL): the call's wall time is accumulated
+ * into boundary_recursion (the reference's stage for the recursion's solves,
+ * proj/src/aperiodic.cpp:310-313). */
+fsx_status fsx_solve_periodic_slabs(int64_t nslabs, const fsx_shape* shapes, const double* const* a0s,
+                                    const fsx_kernel* k, uint64_t T, fsx_spectrum_cache* cache, double* const* outs,
+                                    const fsx_options* opt, fsx_stage_timings* st);
+
 /* Device-resident variant: d_a0 / d_out are device pointers (may alias);
  * the work is enqueued on opt->stream and the call returns without
  * synchronizing.  The non-finite check is deferred: fsx_device_check()

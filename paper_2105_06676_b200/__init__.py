@@ -42,6 +42,7 @@ from .fftstencil import (  # noqa: F401
     solve_periodic_device_f32,
     solve_periodic_f32,
     solve_periodic_implicit,
+    solve_periodic_slabs,
     solve_periodic_vector,
     spectral_cut_columns,
     spectrum_from_kernel,

@@ -97,6 +97,7 @@ EXPORTS = (
     "fsx_solve_periodic_implicit",
     "fsx_solve_periodic_device",
     "fsx_solve_periodic_batch",
+    "fsx_solve_periodic_slabs",
     "fsx_solve_periodic_f32",
     "fsx_solve_periodic_device_f32",
     "fsx_solve_periodic_batch_f32",

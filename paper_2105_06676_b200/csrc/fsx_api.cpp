@@ -306,6 +306,11 @@ struct Plan {
     int launches = 0;
     i64 alg_bytes = 0, fused_bytes = 0;
     const char* kernel = "";  // the dominant (fused) kernel of a solve, for measurement
+    // batch > 1: that many grids of this shape stacked [batch][cells][m] and
+    // solved together (fsx_solve_periodic_slabs): one launch per pass, the
+    // batch as an outer dimension of every pass (plan 1 or plan 3)
+    i64 batch = 1;
+    int pins = 0;  // > 0: in use by a multi-plan call, exempt from cache eviction
     // Cross-stream ordering of the plan's workspaces: `done` is recorded after
     // every enqueue on `last`; a solve on another stream first waits on it, so
     // two solves that share this plan's buffers never overlap on the GPU.
@@ -522,7 +527,7 @@ void setup_bluestein(Plan& p, Device& dev) {
         if (ga.blue) {
             ga.bhat_off = total;
             total += ga.P;
-            work = std::max<i64>(work, p.cells * p.m / ga.n * ga.P);
+            work = std::max<i64>(work, p.cells * p.m * p.batch / ga.n * ga.P);
         }
     if (!total) return;
     p.blue_bhat.ensure((size_t)total * sizeof(double2));
@@ -545,7 +550,7 @@ void setup_bluestein(Plan& p, Device& dev) {
 
 // lane > 0: an independent copy of the plan (own workspaces and tensor maps)
 // for the pipelined batch solve, which keeps two solves in flight.
-Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general, int lane = 0) {
+Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general, int lane = 0, i64 batch = 1) {
     // squeeze length-1 axes (their offsets are 0 by require_fits)
     Plan probe;
     probe.full = s;
@@ -559,14 +564,15 @@ Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general,
         probe.dims.push_back(1);
         probe.axes.push_back(0);
     }
-    const int kind = choose_kind(probe, taps, force_general);
-    const std::string base = plan_key(s, kind);
+    int kind = choose_kind(probe, taps, force_general);
+    if (batch > 1 && kind == kRowPair1D) kind = kGeneral;  // stacked 1D grids: the general passes
+    const std::string base = plan_key(s, kind) + (batch > 1 ? "|b" + std::to_string(batch) : "");
     const std::string key = lane ? base + "|lane" + std::to_string(lane) : base;
     auto it = dev.plans.find(key);
     if (it != dev.plans.end()) return *it->second;
-    if (dev.plans.size() >= 8) {  // bounded cache; keep this shape's other lanes (a batch holds them)
+    if (dev.plans.size() >= 8) {  // bounded cache; keep this shape's other lanes (a batch holds them) and pinned plans
         for (auto e = dev.plans.begin(); e != dev.plans.end();)
-            e = e->first.rfind(base, 0) == 0 ? std::next(e) : dev.plans.erase(e);
+            e = (e->first.rfind(base, 0) == 0 || e->second->pins > 0) ? std::next(e) : dev.plans.erase(e);
     }
 
     auto p = std::make_unique<Plan>();
@@ -576,25 +582,26 @@ Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general,
     p->m = probe.m;
     p->kind = kind;
     p->cells = s.cells;
+    p->batch = batch;
     const int r = (int)p->dims.size();
-    const i64 R = s.values() * 8;  // real bytes
+    const i64 R = s.values() * 8 * batch;  // real bytes
     if (kind == kFusedR2C) {
         p->L = p->dims[r - 1];
         p->M = p->L / 2;
         p->P = p->M + 8;
-        p->rows = s.cells / p->L;
+        p->rows = s.cells / p->L * batch;
         p->work.ensure((size_t)p->rows * p->P * sizeof(double2));
         const i64 plane = (r == 3) ? p->dims[1] * p->P : p->P;
         if (r == 3) {
             p->ax1.n = p->dims[1];
             p->ax1.inner = p->P;
-            p->ax1.outer = p->dims[0];
+            p->ax1.outer = p->dims[0] * batch;
             p->ax1.block = p->dims[1] * p->P;
             p->ax1.ncols = p->M + 1;
         }
         p->ax0.n = p->dims[0];
         p->ax0.inner = plane;
-        p->ax0.outer = 1;
+        p->ax0.outer = batch;
         p->ax0.block = p->dims[0] * plane;
         p->ax0.ncols = (r == 3) ? plane : p->M + 1;
         if (tma_enabled()) {
@@ -644,7 +651,7 @@ Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general,
     } else {
         // general: complex Z of cells * m (block kernels instantiated for m <= 8)
         if (p->m > 8) throw SpecErr("fsx: more than 8 fields per cell is not supported on the GPU path");
-        p->work.ensure((size_t)s.values() * sizeof(double2));
+        p->work.ensure((size_t)s.values() * batch * sizeof(double2));
         i64 nl = 0;
         for (int a = 0; a < r; ++a) {
             GenAxis ga;
@@ -677,7 +684,7 @@ Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general,
         p->tables.upload();
         setup_bluestein(*p, dev);
         p->launches = (int)nl + 3;
-        const i64 Z = s.values() * 16;
+        const i64 Z = s.values() * 16 * batch;
         p->fused_bytes = 2 * Z;
         p->alg_bytes = R + Z + (nl) * 2 * Z / 1 + 2 * Z + Z + R;
     }
@@ -853,6 +860,7 @@ fsx::GeneralSymbol general_symbol(Plan& p, const Taps& taps, const Taps* q, u64 
     }
     s.T = T;
     s.scale = 1.0 / (double)p.cells;
+    s.batch = p.batch;
     const int mm = p.m * p.m;
     auto pack = [&](const Taps& t, std::vector<long long>& off, std::vector<double>& blk) {
         for (const auto& kv : t.map) {
@@ -895,7 +903,7 @@ void general_axes(Plan& p, const Device& dev, double2* Z, bool inverse, cudaStre
     auto run_axis = [&](int a) {
         const GenAxis& ga = p.gax[a];
         if (ga.n <= 1) return;
-        i64 inner = p.m, outer = 1;
+        i64 inner = p.m, outer = p.batch;  // stacked grids are outer blocks of every axis
         for (int b = a + 1; b < r; ++b) inner *= p.dims[b];
         for (int b = 0; b < a; ++b) outer *= p.dims[b];
         fsx::StepTwiddle none;
@@ -1057,7 +1065,7 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
         sp.mark();
     } else {
         double2* Z = p.work.as<double2>();
-        FSX_CK(fsx::launch_promote(d_a0, Z, p.cells * p.m, st));
+        FSX_CK(fsx::launch_promote(d_a0, Z, p.cells * p.m * p.batch, st));
         general_axes(p, dev, Z, false, st);
         sp.mark();
         fsx::GeneralSymbol sym = general_symbol(p, taps, q, T, st);
@@ -1068,7 +1076,9 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
         FSX_CK(fsx::launch_spectral_general(Z, sym, st));
         sp.mark();
         general_axes(p, dev, Z, true, st);
-        FSX_CK(fsx::launch_extract(Z, d_out, p.cells * p.m, flags, st));
+        // realize_checked per stacked grid: flags[b] (the residue test is per solve)
+        const i64 nv = p.cells * p.m;
+        for (i64 b = 0; b < p.batch; ++b) FSX_CK(fsx::launch_extract(Z + b * nv, d_out + b * nv, nv, flags + b, st));
         sp.mark();
     }
 }
@@ -1975,6 +1985,20 @@ void solve_batch(const fsx_shape* shape, i64 nb, const TE* const* a0s, const fsx
     for (i64 i = 0; i < nb; ++i) judge_flags(h[(size_t)i], pl[0]->kind, " (batch item " + std::to_string(i) + ")");
 }
 
+// One recursion level's slab solves (the aperiodic recursion's rb_run issues
+// the 2d face-slab solve_periodic_cached calls of a level one after another,
+// proj/src/aperiodic.cpp:224-228,240-244): slabs of equal shape are stacked
+// and solved as one batched plan -- one launch per pass for all of them, the
+// stack an outer dimension of every pass -- and the shape groups run on the
+// device's two lanes (H2D, kernels and D2H of different groups overlap).
+// The spectrum follows SpectrumCache semantics when a cache is given: the
+// first kernel seen for a dims vector is the one used for every later slab of
+// those dims (proj/src/periodic.cpp:67-74, 88-99).  Plans stay resident in
+// the device's plan cache (keyed by shape and stack size) across levels.
+// NumericError names the first failing slab in argument order.
+void solve_slabs(i64 n, const fsx_shape* shapes, const double* const* a0s, const fsx_kernel* k, u64 T,
+                 fsx_spectrum_cache* cache, double* const* outs, const fsx_options* opt, fsx_stage_timings* stt);
+
 template <class F>
 fsx_status guarded(F&& f) {
     try {
@@ -2012,6 +2036,137 @@ struct fsx_spectrum_cache {
     std::mutex mu;
     std::map<std::vector<i64>, Taps> by_dims;  // the first kernel seen for a dims vector (Taps::m = its fields)
 };
+
+namespace {
+
+// The kernel a dims vector uses under SpectrumCache semantics (the first one
+// seen); without a cache, the passed kernel.
+Taps cached_taps(fsx_spectrum_cache* cache, const Shape& sh, const Taps& taps) {
+    if (!cache) return taps;
+    Taps cached;
+    {
+        std::lock_guard<std::mutex> lk(cache->mu);
+        auto it = cache->by_dims.find(sh.dims);
+        if (it == cache->by_dims.end()) it = cache->by_dims.emplace(sh.dims, taps).first;
+        cached = it->second;
+    }
+    // the cached spectrum keeps its own block size: a grid with another
+    // field count fails in hadamard, as in the reference (spectrum.cpp:111-116)
+    if (cached.m != sh.fields) throw SpecErr("hadamard: shape mismatch");
+    return cached;
+}
+
+struct PlanPin {
+    Plan* p;
+    explicit PlanPin(Plan* q) : p(q) { ++p->pins; }
+    ~PlanPin() { --p->pins; }
+    PlanPin(const PlanPin&) = delete;
+    PlanPin& operator=(const PlanPin&) = delete;
+};
+
+void solve_slabs(i64 n, const fsx_shape* shapes, const double* const* a0s, const fsx_kernel* k, u64 T,
+                 fsx_spectrum_cache* cache, double* const* outs, const fsx_options* opt, fsx_stage_timings* stt) {
+    using clk = std::chrono::steady_clock;
+    const auto t_entry = clk::now();
+    if (n < 0) throw SpecErr("fsx_solve_periodic_slabs: negative slab count");
+    if (n > 0 && (!shapes || !a0s || !outs)) throw SpecErr("fsx: null grid pointer");
+    const Taps taps = parse_kernel(k);
+    std::vector<Shape> sh((size_t)n);
+    for (i64 i = 0; i < n; ++i) {
+        sh[i] = parse_shape(&shapes[i]);
+        require_fits(taps, sh[i]);  // the passed kernel is checked (periodic.cpp:91)
+        if (!a0s[i] || !outs[i]) throw SpecErr("fsx: null grid pointer");
+    }
+    // shape groups in first-seen order, each with its (cached) kernel
+    std::vector<std::string> order;
+    std::map<std::string, std::vector<i64>> groups;
+    std::map<std::string, Taps> gtaps;
+    for (i64 i = 0; i < n; ++i) {
+        const std::string key = plan_key(sh[i], 0);
+        if (!groups.count(key)) {
+            order.push_back(key);
+            gtaps.emplace(key, cached_taps(cache, sh[i], taps));
+        }
+        groups[key].push_back(i);
+    }
+    if (T == 0) {  // proj/src/periodic.cpp:79 per slab
+        for (i64 i = 0; i < n; ++i)
+            if (outs[i] != a0s[i]) std::memmove(outs[i], a0s[i], (size_t)sh[i].values() * 8);
+        return;
+    }
+    if (n == 0) return;
+    DevLock dlk(opt ? opt->device : 0);
+    Device& dev = dlk.dev;
+    for (int l = 0; l < 2; ++l)
+        if (!dev.lanes[l]) {
+            FSX_CK(cudaStreamCreateWithFlags(&dev.lanes[l], cudaStreamNonBlocking));
+            FSX_CK(cudaEventCreateWithFlags(&dev.lane_ev[l], cudaEventDisableTiming));
+        }
+    dev.bflags.ensure((size_t)n * sizeof(fsx::Flags));
+    fsx::Flags* fl = dev.bflags.as<fsx::Flags>();
+    FSX_CK(cudaMemsetAsync(fl, 0, (size_t)n * sizeof(fsx::Flags), dev.lanes[0]));
+    if (opt && opt->stream) {
+        FSX_CK(cudaEventRecord(dev.lane_ev[1], reinterpret_cast<cudaStream_t>(opt->stream)));
+        FSX_CK(cudaStreamWaitEvent(dev.lanes[0], dev.lane_ev[1], 0));
+    }
+    FSX_CK(cudaEventRecord(dev.lane_ev[0], dev.lanes[0]));
+    FSX_CK(cudaStreamWaitEvent(dev.lanes[1], dev.lane_ev[0], 0));
+    // every group's plan first (pinned: a later group's plan must not evict an earlier one)
+    std::vector<Plan*> plans;
+    std::vector<std::unique_ptr<PlanPin>> pins;
+    for (const std::string& key : order) {
+        const std::vector<i64>& idx = groups[key];
+        Plan* p = &get_plan(dev, sh[idx[0]], gtaps[key], 0, 0, (i64)idx.size());
+        pins.push_back(std::make_unique<PlanPin>(p));
+        plans.push_back(p);
+    }
+    // flag slots: group gi owns the contiguous range [gofs, gofs + B) -- one per
+    // stacked grid on the general plan (the residue test is per solve), the
+    // first one for a stacked plan-1 group (its C2R pass sets one flag)
+    std::vector<i64> flag_of((size_t)n);
+    i64 gofs = 0;
+    for (size_t gi = 0; gi < order.size(); ++gi) {
+        const std::vector<i64>& idx = groups[order[gi]];
+        Plan& p = *plans[gi];
+        cudaStream_t st = dev.lanes[gi & 1];
+        const i64 B = (i64)idx.size();
+        const size_t bytes = (size_t)sh[idx[0]].values() * 8;
+        p.d_in.ensure(bytes * B);
+        p.d_out.ensure(bytes * B);
+        plan_enter(p, st);
+        for (i64 b = 0; b < B; ++b)
+            FSX_CK(cudaMemcpyAsync(p.d_in.as<char>() + b * bytes, a0s[idx[b]], bytes, cudaMemcpyHostToDevice, st));
+        Stamps sp{&dev, false, st};
+        run_plan(p, dev, gtaps[order[gi]], nullptr, T, p.d_in.as<double>(), p.d_out.as<double>(), st, sp, fl + gofs);
+        for (i64 b = 0; b < B; ++b) {
+            FSX_CK(cudaMemcpyAsync(outs[idx[b]], p.d_out.as<char>() + b * bytes, bytes, cudaMemcpyDeviceToHost, st));
+            flag_of[idx[b]] = gofs + (p.kind == kGeneral ? b : 0);
+        }
+        plan_leave(p, st);
+        gofs += B;
+    }
+    std::vector<fsx::Flags> h((size_t)n);
+    FSX_CK(cudaStreamSynchronize(dev.lanes[1]));
+    FSX_CK(cudaMemcpyAsync(h.data(), fl, (size_t)n * sizeof(fsx::Flags), cudaMemcpyDeviceToHost, dev.lanes[0]));
+    FSX_CK(cudaStreamSynchronize(dev.lanes[0]));
+    for (i64 i = 0; i < n; ++i) {
+        const fsx::Flags& f = h[(size_t)flag_of[i]];
+        int kind = kGeneral;
+        for (size_t gi = 0; gi < order.size(); ++gi)
+            if (plan_key(sh[i], 0) == order[gi]) kind = plans[gi]->kind;
+        if (kind != kGeneral && f.nonfinite) {
+            // one flag for a stacked plan-1 group: name the slab whose output is non-finite
+            const double* o = outs[i];
+            bool bad = false;
+            for (i64 j = 0; j < sh[i].values() && !bad; ++j) bad = !std::isfinite(o[j]);
+            if (!bad) continue;
+        }
+        judge_flags(f, kind, " (slab " + std::to_string(i) + ")");
+    }
+    if (stt) stt->boundary_recursion += std::chrono::duration<double>(clk::now() - t_entry).count();
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -2082,16 +2237,7 @@ fsx_status fsx_solve_periodic_cached(const fsx_shape* shape, const double* a0, c
         const Shape sh = parse_shape(shape);
         const Taps taps = parse_kernel(k);
         require_fits(taps, sh);  // the passed kernel is checked (periodic.cpp:91)
-        Taps cached;
-        {
-            std::lock_guard<std::mutex> lk(cache->mu);
-            auto it = cache->by_dims.find(sh.dims);
-            if (it == cache->by_dims.end()) it = cache->by_dims.emplace(sh.dims, taps).first;
-            cached = it->second;
-        }
-        // the cached spectrum keeps its own block size: a grid with another
-        // field count fails in hadamard, as in the reference (spectrum.cpp:111-116)
-        if (cached.m != sh.fields) throw SpecErr("hadamard: shape mismatch");
+        const Taps cached = cached_taps(cache, sh, taps);
         SolveReq rq{shape, a0, k, nullptr, T, out, opt, st};
         rq.cached = &cached;
         solve(rq);
@@ -2156,6 +2302,12 @@ fsx_status fsx_solve_periodic_device_f32(const fsx_shape* shape, const float* d_
         rq.device_ptrs = true;
         solve(rq);
     });
+}
+
+fsx_status fsx_solve_periodic_slabs(int64_t nslabs, const fsx_shape* shapes, const double* const* a0s,
+                                    const fsx_kernel* k, uint64_t T, fsx_spectrum_cache* cache, double* const* outs,
+                                    const fsx_options* opt, fsx_stage_timings* st) {
+    return guarded([&] { solve_slabs(nslabs, shapes, a0s, k, T, cache, outs, opt, st); });
 }
 
 fsx_status fsx_solve_periodic_batch_f32(const fsx_shape* shape, int64_t nbatch, const float* const* a0s,

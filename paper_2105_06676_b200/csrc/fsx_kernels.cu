@@ -874,21 +874,27 @@ __global__ void k_spectral_general(double2* z, GeneralSymbol s) {
                 t >>= 1;
                 if (t) sq = cmul(sq, sq);
             }
-            z[cell] = cscale(cmul(acc, z[cell]), s.scale);
+            for (i64 b = 0; b < s.batch; ++b) {  // stacked grids share the symbol
+                double2* zc = z + b * s.cells + cell;
+                *zc = cscale(cmul(acc, *zc), s.scale);
+            }
         } else {
             pow_block<MM>(lam, s.T);
-            double2 x[MM], y[MM];
+            for (i64 b = 0; b < s.batch; ++b) {
+                double2* zc = z + (b * s.cells + cell) * MM;
+                double2 x[MM], y[MM];
 #pragma unroll
-            for (int f = 0; f < MM; ++f) x[f] = z[cell * MM + f];
+                for (int f = 0; f < MM; ++f) x[f] = zc[f];
 #pragma unroll
-            for (int r = 0; r < MM; ++r) {
-                double2 acc = make_double2(0.0, 0.0);
+                for (int r = 0; r < MM; ++r) {
+                    double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-                for (int c = 0; c < MM; ++c) acc = cadd(acc, cmul(lam[r][c], x[c]));
-                y[r] = cscale(acc, s.scale);
+                    for (int c = 0; c < MM; ++c) acc = cadd(acc, cmul(lam[r][c], x[c]));
+                    y[r] = cscale(acc, s.scale);
+                }
+#pragma unroll
+                for (int f = 0; f < MM; ++f) zc[f] = y[f];
             }
-#pragma unroll
-            for (int f = 0; f < MM; ++f) z[cell * MM + f] = y[f];
         }
     }
 }

@@ -164,6 +164,7 @@ struct GeneralSymbol {
     const double* qmax = nullptr;        // device scalar: max |lamQ|
     u64 T = 1;
     double scale = 1.0;
+    i64 batch = 1;                       // independent grids stacked [batch][cells][m] (one symbol)
 };
 
 // 1D fused row-pair pass (four-step row stage + pairing + spectral + inverse rows).

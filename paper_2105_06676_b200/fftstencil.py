@@ -472,6 +472,43 @@ def solve_periodic_batch(a0s, k: StencilKernel, T: int, outs=None, spectral_cut:
     return outs
 
 
+def solve_periodic_slabs(a0s, k: StencilKernel, T: int, cache: SpectrumCache | None = None,
+                         st: StageTimings | None = None, outs=None) -> list:
+    """One recursion level's slab solves (fsx_solve_periodic_slabs): the
+    aperiodic recursion's rb_run solves the 2d face slabs of a level with
+    solve_periodic_cached one after another (proj/src/aperiodic.cpp:224-228,
+    240-244); here the FieldGrids ``a0s`` (shapes may differ) are solved in one
+    call -- equal shapes stacked into one batched plan, shape groups
+    overlapped on two lanes.  ``cache``: SpectrumCache semantics (first kernel
+    per dims).  Returns the output arrays (``outs`` optionally supplies them)."""
+    if T < 0 or T >= 1 << 64:
+        raise SpecError("T must be a nonnegative 64-bit integer")
+    grids = list(a0s)
+    n = len(grids)
+    if outs is None:
+        outs = [np.empty_like(g.data) for g in grids]
+    outs = list(outs)
+    if len(outs) != n:
+        raise SpecError("solve_periodic_slabs: one output per input")
+    for g, o in zip(grids, outs):
+        if o.dtype != np.float64 or o.size != g.data.size or not o.flags.c_contiguous:
+            raise SpecError("out must be a contiguous float64 array of the grid's size")
+    shapes = (_lib.FsxShape * max(1, n))(*[g.shape._c() for g in grids])
+    ins = (ctypes.c_void_p * max(1, n))(*[g.data.ctypes.data for g in grids])
+    ous = (ctypes.c_void_p * max(1, n))(*[o.ctypes.data for o in outs])
+    L = _lib.load()
+    kc, keep = k._c()
+    stc = st._push() if st is not None else None
+    status = L.fsx_solve_periodic_slabs(ctypes.c_int64(n), shapes, ins, ctypes.byref(kc), _u64_T(T),
+                                        cache._h if cache is not None else None, ous, ctypes.byref(_opts()),
+                                        ctypes.byref(stc) if stc is not None else None)
+    del keep
+    _lib.check(status)
+    if st is not None:
+        st._pull(stc)
+    return outs
+
+
 def solve_periodic_device(shape: GridShape, d_a0: int, k: StencilKernel, T: int, d_out: int,
                           stream: int | None = None, device: int = 0, path: int = 0, stage_events: int = 0,
                           spectral_cut: int = 0) -> None:
