@@ -602,6 +602,7 @@ def run_gpu(args, cfg):
     alg_step = info["alg_bytes"]
     if f32:  # plan 1 reads / writes the grid as floats; the others widen (R/2 + R) and narrow (R + R/2)
         alg_step += -n * 8 if info["path"] == 1 else 3 * n * 8
+    sched_step = alg_step + (info.get("sched_bytes", info["alg_bytes"]) - info["alg_bytes"])  # bytes the launched passes move
     pipe_gbs = alg_step / (ms * 1e-3) / 1e9
     kernel_name = dominant_kernel(info, cfg)
     traffic, traffic_src = load_traffic(cfg.name, kernel_name)
@@ -643,7 +644,10 @@ def run_gpu(args, cfg):
             "fp64": None if f32 else load_fp64(cfg.name, fms, kernel_name),  # the fp32 mode's fused pass has its own counts
         },
         "pipeline": {"alg_bytes_per_step": alg_step, "achieved_gbs": pipe_gbs, "frac": pipe_gbs / peak,
-                     "frac_vs_nominal_8tbs": pipe_gbs / NOMINAL_HBM_GBS},
+                     "frac_vs_nominal_8tbs": pipe_gbs / NOMINAL_HBM_GBS,
+                     "alg_bytes_source": "SURVEY.md 8(d) minimal schedule (2D 2R+4H, 3D 2R+8H, 1D 6R)",
+                     "schedule_bytes_per_step": sched_step,
+                     "schedule_frac": sched_step / (ms * 1e-3) / 1e9 / peak},
         "gpu_launches": info["launches"] * args.steps,
         "host_enqueue_us": sorted(host_us)[len(host_us) // 2],
         "clocks": clocks,

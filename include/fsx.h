@@ -330,9 +330,11 @@ int32_t fsx_device_count(void);
 typedef struct fsx_plan_info {
     int32_t path;            /* 1 = fused R2C (rank 2/3), 2 = 1D four-step row-pair, 3 = general */
     int32_t launches;        /* kernels per solve */
-    int64_t alg_bytes;       /* algorithmic bytes per solve (all passes) */
+    int64_t alg_bytes;       /* algorithmic bytes of the minimal pass schedule */
     int64_t fused_bytes;     /* algorithmic bytes of the dominant (fused) kernel */
     int64_t work_bytes;      /* device workspace of the plan */
+    int64_t sched_bytes;     /* bytes the launched pass schedule moves (> alg_bytes when a pass is split,
+                                e.g. the 1D plan's two-level column FFT above 8192 columns) */
     int32_t ranks;           /* devices a host solve is decomposed over (1 = single GPU) */
     int32_t exchange;        /* ranks > 1: FSX_EXCHANGE_P2P or FSX_EXCHANGE_NCCL as resolved */
 } fsx_plan_info;

@@ -82,6 +82,7 @@ class FsxPlanInfo(ctypes.Structure):
         ("alg_bytes", ctypes.c_int64),
         ("fused_bytes", ctypes.c_int64),
         ("work_bytes", ctypes.c_int64),
+        ("sched_bytes", ctypes.c_int64),
         ("ranks", ctypes.c_int32),
         ("exchange", ctypes.c_int32),
     ]

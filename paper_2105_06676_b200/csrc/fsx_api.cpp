@@ -311,6 +311,7 @@ struct Plan {
     // batch as an outer dimension of every pass (plan 1 or plan 3)
     i64 batch = 1;
     int pins = 0;  // > 0: in use by a multi-plan call, exempt from cache eviction
+    i64 sched_bytes = 0;  // bytes the launched pass schedule moves (0: = alg_bytes)
     // Cross-stream ordering of the plan's workspaces: `done` is recorded after
     // every enqueue on `last`; a solve on another stream first waits on it, so
     // two solves that share this plan's buffers never overlap on the GPU.
@@ -646,7 +647,11 @@ Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general,
         }
         p->tables.upload();
         p->fused_bytes = 2 * R;
-        p->alg_bytes = (2 + 4 * col_passes) * R + R;
+        // the minimal 1D four-step schedule is 3 passes (column,
+        // row-pair, inverse column) = 6R; a split column FFT (N1 > 8192, e.g.
+        // cfg5) launches 5 passes = 10R (sched_bytes)
+        p->alg_bytes = 6 * R;
+        p->sched_bytes = (i64)(2 + 4 * col_passes) * R;
         p->launches = 2 * col_passes + 1 + 1;
     } else {
         // general: complex Z of cells * m (block kernels instantiated for m <= 8)
@@ -2462,6 +2467,7 @@ fsx_status fsx_plan_describe(const fsx_shape* shape, const fsx_kernel* k, const 
         info->alg_bytes = p.alg_bytes;
         info->fused_bytes = p.fused_bytes;
         info->work_bytes = (int64_t)p.work.bytes;
+        info->sched_bytes = p.sched_bytes ? p.sched_bytes : p.alg_bytes;
         info->ranks = 1;
         info->exchange = 0;
         const std::vector<int> devs = multi_devices(opt);

@@ -663,7 +663,8 @@ def plan_describe(shape: GridShape, k: StencilKernel, path: int = 0, num_gpus: i
     _lib.check(L.fsx_plan_describe(ctypes.byref(shape._c()), ctypes.byref(kc), ctypes.byref(o), ctypes.byref(info)))
     del keep
     return {"path": info.path, "launches": info.launches, "alg_bytes": info.alg_bytes,
-            "fused_bytes": info.fused_bytes, "work_bytes": info.work_bytes, "ranks": info.ranks,
+            "fused_bytes": info.fused_bytes, "work_bytes": info.work_bytes, "sched_bytes": info.sched_bytes,
+            "ranks": info.ranks,
             "exchange": info.exchange}
 
 
