@@ -364,6 +364,158 @@ k_c2r_bulk(const double2* __restrict__ H, TO* __restrict__ x, i64 nrows, i64 L, 
     if (any && (threadIdx.x & 31) == 0) atomicOr(&flags->nonfinite, 1u);
 }
 
+// ------------------------------------------------------------------ rows, two groups per CTA
+// The bulk-staged row kernels at M = 4096 (cfg3's 8192-real rows) run one
+// 256-thread CTA per SM (three 64 KB stages fill shared memory): 8 warps,
+// ncu 12 % warps active, latency-bound at ~4.5 TB/s.  Here the same three
+// stages feed TWO 256-thread groups of one CTA (16 warps per SM): row j of
+// the CTA (global row blockIdx + j G) lands in stage j % 3 and is transformed
+// by group j % 2 with named-barrier exchanges; the group that frees a stage
+// refills it with row j + 3 at once.  A stage's row tag (written when its
+// refill is issued) tells the consumer which load the stage's mbarrier phase
+// belongs to, so a group never mistakes an older phase for its row's.
+template <int NG>
+__device__ __forceinline__ void grp_wait_stage(volatile int* tag, int s, int j, unsigned long long* bar, int ST) {
+    while (tag[s] != j) {
+    }
+    mbar_wait(bar, (unsigned)(j / ST) & 1u);
+}
+
+template <int M, int NG, int ST>
+__global__ void __launch_bounds__(NG * PCfg<M>::TPL, 1)
+k_r2c_grp(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, RowLayout lay,
+          const double2* __restrict__ tw_all) {
+    constexpr int TPL = PCfg<M>::TPL, R = 16;
+    using F = LineFFT<M, -1, false, false, 0, TPL>;  // named barriers per group
+    static_assert(!F::PAIRED, "k_r2c_grp: split through the exchange line (M = 2^(4a))");
+    constexpr unsigned BYTES = 2 * M * sizeof(double);
+    extern __shared__ __align__(128) double2 sm[];
+    __shared__ __align__(8) unsigned long long bar[ST];
+    __shared__ int tag[ST];
+    const int g = threadIdx.x / TPL, t = threadIdx.x % TPL;
+    const i64 G = gridDim.x;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int b = 0; b < ST; ++b) mbar_init(&bar[b], 1);
+        mbar_init_fence();
+        pdl_wait();  // x may be the predecessor's output
+#pragma unroll
+        for (int j = 0; j < ST; ++j) {
+            tag[j] = j;
+            const i64 row = blockIdx.x + (i64)j * G;
+            if (row < nrows) {
+                mbar_expect_tx(&bar[j], BYTES);
+                bulk_load(sm + j * M, x + row * L, BYTES, &bar[j]);
+            }
+        }
+    }
+    __syncthreads();
+    for (int j = g;; j += NG) {
+        const i64 row = blockIdx.x + (i64)j * G;
+        if (row >= nrows) break;
+        const int s = j % ST;
+        if (row + (i64)NG * G >= nrows) pdl_trigger();  // this group's last row
+        grp_wait_stage<NG>(tag, s, j, &bar[s], ST);
+        double2* line = sm + s * M;
+        double2 v[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = line[t + q * TPL];
+        F::run(v, t, line, tw_all + M);
+        group_sync<TPL>();
+#pragma unroll
+        for (int q = 0; q < R; ++q) line[swz(t + q * TPL)] = v[q];
+        group_sync<TPL>();
+        const double2 wt = __ldg(tw_all + 2 * M + t);  // W_L^(t + q M/16) = W_L^t * W_32^q
+        static_for<0, R>([&](auto Q) {
+            constexpr int q = decltype(Q)::value;
+            const int k = t + q * TPL;
+            const double2 zk = v[q];
+            const double2 zm = cconj(line[swz((M - k) & (M - 1))]);
+            const double2 e = cscale(cadd(zk, zm), 0.5);
+            const double2 od = cscale(cmul_si<-1>(csub(zk, zm)), 0.5);
+            if (lay.kcut < 0 || k <= lay.kcut) H[row * lay.P + k] = cadd(e, cmul(cmul_const<q, 32, -1>(wt), od));
+            if (k == 0 && (lay.kcut < 0 || lay.kcut >= M)) H[row * lay.P + M] = make_double2(zk.x - zk.y, 0.0);
+        });
+        fence_proxy_async();  // generic writes of this stage before its next bulk fill
+        group_sync<TPL>();
+        const i64 nrow = blockIdx.x + (i64)(j + ST) * G;
+        if (t == 0 && nrow < nrows) {
+            mbar_expect_tx(&bar[s], BYTES);
+            bulk_load(sm + s * M, x + nrow * L, BYTES, &bar[s]);
+            __threadfence_block();
+            tag[s] = j + ST;
+        }
+    }
+}
+
+template <int M, int NG, int ST>
+__global__ void __launch_bounds__(NG * PCfg<M>::TPL, 1)
+k_c2r_grp(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, RowLayout lay,
+          const double2* __restrict__ tw_all, Flags* flags) {
+    constexpr int TPL = PCfg<M>::TPL, R = 16;
+    using F = LineFFT<M, +1, false, false, 0, TPL>;
+    constexpr int SS = M + 8;  // stage stride: M + 1 elements, 128 B aligned
+    extern __shared__ __align__(128) double2 sm[];
+    __shared__ __align__(8) unsigned long long bar[ST];
+    __shared__ int tag[ST];
+    const int g = threadIdx.x / TPL, t = threadIdx.x % TPL;
+    const i64 G = gridDim.x;
+    bool bad = false;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int b = 0; b < ST; ++b) mbar_init(&bar[b], 1);
+        mbar_init_fence();
+        pdl_wait();  // H is the predecessor's output
+#pragma unroll
+        for (int j = 0; j < ST; ++j) {
+            tag[j] = j;
+            const i64 row = blockIdx.x + (i64)j * G;
+            if (row < nrows) load_hrow<M, false>(sm + j * SS, H, lay, row, &bar[j]);
+        }
+    }
+    __syncthreads();
+    for (int j = g;; j += NG) {
+        const i64 row = blockIdx.x + (i64)j * G;
+        if (row >= nrows) break;
+        const int s = j % ST;
+        if (row + (i64)NG * G >= nrows) pdl_trigger();
+        grp_wait_stage<NG>(tag, s, j, &bar[s], ST);
+        double2* line = sm + s * SS;
+        if (lay.kcut >= 0 && lay.kcut < M) {  // exact spectral cut: the dropped columns are 0
+            for (i64 k = lay.kcut + 1 + t; k <= M; k += TPL) line[k] = make_double2(0.0, 0.0);
+            group_sync<TPL>();
+        }
+        double2 v[R];
+        const double2 wt = __ldg(tw_all + 2 * M + t);  // W_L^(t + q M/16) = W_L^t * W_32^q
+        static_for<0, R>([&](auto Q) {
+            constexpr int q = decltype(Q)::value;
+            const int k = t + q * TPL;
+            const double2 xk = line[k];
+            const double2 xm = cconj(line[M - k]);
+            const double2 e = cadd(xk, xm);
+            const double2 od = cmulc(csub(xk, xm), cmul_const<q, 32, -1>(wt));
+            v[q] = cadd(e, cmul_si<+1>(od));
+        });
+        F::run(v, t, line, tw_all + M);
+        double2* dst = reinterpret_cast<double2*>(x + row * L);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            dst[t + q * TPL] = v[q];
+            bad |= !isfinite(v[q].x) || !isfinite(v[q].y);
+        }
+        fence_proxy_async();
+        group_sync<TPL>();
+        const i64 nrow = blockIdx.x + (i64)(j + ST) * G;
+        if (t == 0 && nrow < nrows) {
+            load_hrow<M, false>(sm + s * SS, H, lay, nrow, &bar[s]);
+            __threadfence_block();
+            tag[s] = j + ST;
+        }
+    }
+    const unsigned any = __ballot_sync(0xffffffffu, bad);
+    if (any && (threadIdx.x & 31) == 0) atomicOr(&flags->nonfinite, 1u);
+}
+
 // FSX_ROWS: 0 = one-row-per-CTA kernels, 1 = cp.async staged (cfg2 r2c 70 us /
 // c2r 64 us at the time), 3 = bulk-copy staged (default: 67 / 63 us then, 52 / 51 us
 // with the later twiddle work).  A register double-buffered variant (86 / 109 us)
@@ -526,10 +678,28 @@ static cudaError_t r2c_bulk_ms(const double* x, double2* H, i64 nrows, i64 L, co
     return launch_pdl(kf, dim3(grid), dim3(PCfg<M>::TPL), smem, s, x, H, nrows, L, lay, tw);
 }
 
+// FSX_ROW_GROUPS=0 keeps the one-group kernels at M = 4096 (A/B)
+static bool row_groups() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_ROW_GROUPS");
+        v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+}
+
 template <int M>
 static cudaError_t r2c_bulk_m(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
                               cudaStream_t s) {
     if (lay.blk) return r2c_bulk_ms<M, 2, true>(x, H, nrows, L, lay, tw, s);
+    if constexpr (M == 4096)
+        if (row_groups()) {  // two 256-thread groups on three 64 KB stages
+            const size_t smem = (size_t)3 * M * sizeof(double2);
+            auto kf = k_r2c_grp<M, 2, 3>;
+            kernel_prepare((const void*)kf, smem);
+            const int grid = persistent_grid(kf, 2 * PCfg<M>::TPL, smem, (nrows + 1) / 2);
+            return launch_pdl(kf, dim3(grid), dim3(2 * PCfg<M>::TPL), smem, s, x, H, nrows, L, lay, tw);
+        }
     if constexpr (M == 4096)  // FSX_ROW_STAGES=3: three 64 KB stages (two rows in flight)
         if (row_stages(M) == 3) return r2c_bulk_ms<M, 3, false>(x, H, nrows, L, lay, tw, s);
     return row_stages(M) == 1 ? r2c_bulk_ms<M, 1, false>(x, H, nrows, L, lay, tw, s)
@@ -550,6 +720,14 @@ template <int M>
 static cudaError_t c2r_bulk_m(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
                               Flags* f, cudaStream_t s) {
     if (lay.blk) return c2r_bulk_ms<M, 2, true>(H, x, nrows, L, lay, tw, f, s);
+    if constexpr (M == 4096)
+        if (row_groups()) {
+            const size_t smem = (size_t)3 * (M + 8) * sizeof(double2);
+            auto kf = k_c2r_grp<M, 2, 3>;
+            kernel_prepare((const void*)kf, smem);
+            const int grid = persistent_grid(kf, 2 * PCfg<M>::TPL, smem, (nrows + 1) / 2);
+            return launch_pdl(kf, dim3(grid), dim3(2 * PCfg<M>::TPL), smem, s, H, x, nrows, L, lay, tw, f);
+        }
     if constexpr (M == 4096)
         if (row_stages(M) == 3) return c2r_bulk_ms<M, 3, false>(H, x, nrows, L, lay, tw, f, s);
     return row_stages(M) == 1 ? c2r_bulk_ms<M, 1, false>(H, x, nrows, L, lay, tw, f, s)
