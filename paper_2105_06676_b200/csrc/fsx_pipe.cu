@@ -381,8 +381,8 @@ __device__ __forceinline__ void grp_wait_stage(volatile int* tag, int s, int j, 
     mbar_wait(bar, (unsigned)(j / ST) & 1u);
 }
 
-template <int M, int NG, int ST>
-__global__ void __launch_bounds__(NG * PCfg<M>::TPL, 1)
+template <int M, int NG, int ST, int MINB = 1>
+__global__ void __launch_bounds__(NG * PCfg<M>::TPL, MINB)
 k_r2c_grp(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, RowLayout lay,
           const double2* __restrict__ tw_all) {
     constexpr int TPL = PCfg<M>::TPL, R = 16;
@@ -448,8 +448,8 @@ k_r2c_grp(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 
     }
 }
 
-template <int M, int NG, int ST>
-__global__ void __launch_bounds__(NG * PCfg<M>::TPL, 1)
+template <int M, int NG, int ST, int MINB = 1>
+__global__ void __launch_bounds__(NG * PCfg<M>::TPL, MINB)
 k_c2r_grp(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, RowLayout lay,
           const double2* __restrict__ tw_all, Flags* flags) {
     constexpr int TPL = PCfg<M>::TPL, R = 16;
@@ -688,10 +688,28 @@ static bool row_groups() {
     return v != 0;
 }
 
+// FSX_ROW_GROUPS=2 also runs the M = 2048 rows as groups (A/B)
+static bool row_groups_m2048() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_ROW_GROUPS");
+        v = e ? atoi(e) : 1;
+    }
+    return v == 2;
+}
+
 template <int M>
 static cudaError_t r2c_bulk_m(const double* x, double2* H, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
                               cudaStream_t s) {
     if (lay.blk) return r2c_bulk_ms<M, 2, true>(x, H, nrows, L, lay, tw, s);
+    if constexpr (M == 2048)
+        if (row_groups_m2048()) {  // two 128-thread groups on three 32 KB stages, two CTAs per SM
+            const size_t smem = (size_t)3 * M * sizeof(double2);
+            auto kf = k_r2c_grp<M, 2, 3, 2>;
+            kernel_prepare((const void*)kf, smem);
+            const int grid = persistent_grid(kf, 2 * PCfg<M>::TPL, smem, (nrows + 1) / 2);
+            return launch_pdl(kf, dim3(grid), dim3(2 * PCfg<M>::TPL), smem, s, x, H, nrows, L, lay, tw);
+        }
     if constexpr (M == 4096)
         if (row_groups()) {  // two 256-thread groups on three 64 KB stages
             const size_t smem = (size_t)3 * M * sizeof(double2);
@@ -720,6 +738,14 @@ template <int M>
 static cudaError_t c2r_bulk_m(const double2* H, double* x, i64 nrows, i64 L, const RowLayout& lay, const double2* tw,
                               Flags* f, cudaStream_t s) {
     if (lay.blk) return c2r_bulk_ms<M, 2, true>(H, x, nrows, L, lay, tw, f, s);
+    if constexpr (M == 2048)
+        if (row_groups_m2048()) {
+            const size_t smem = (size_t)3 * (M + 8) * sizeof(double2);
+            auto kf = k_c2r_grp<M, 2, 3, 2>;
+            kernel_prepare((const void*)kf, smem);
+            const int grid = persistent_grid(kf, 2 * PCfg<M>::TPL, smem, (nrows + 1) / 2);
+            return launch_pdl(kf, dim3(grid), dim3(2 * PCfg<M>::TPL), smem, s, H, x, nrows, L, lay, tw, f);
+        }
     if constexpr (M == 4096)
         if (row_groups()) {
             const size_t smem = (size_t)3 * (M + 8) * sizeof(double2);
