@@ -1312,8 +1312,174 @@ cudaError_t launch_fused_r2c(double2* H, const AxisGeom& g, const FusedSymbol& s
     }
 }
 
+// ------------------------------------------------------------------ row pairs on a CTA pair
+// k_rowpair holds rows r and N1 - r in one CTA (2 x 64 KB at N2 = 4096): one
+// 512-thread CTA per SM, whose row loads, pairing and stores no other CTA
+// overlaps (cfg5: 1.6 ms, FP64 pipe 42 %, warps 25 %).  Here a 2-CTA cluster
+// takes the pair, one row per CTA (64 KB tile + 32 KB landing: two CTAs per
+// SM), the row arriving by one bulk copy:
+//   1. forward row FFT; thread th holds X[th + TPL q];
+//   2. exchange 1 over DSMEM: each CTA sends the upper half of its row
+//      (positions >= N2/2, q >= 8) into the peer's landing zone;
+//   3. CTA h pairs its own positions p < N2/2 with the peer's N2 - 1 - p
+//      (landing index N2/2 - 1 - p): CTA 0 (row r) owns frequencies
+//      k = r + N1 p, CTA 1 (row N1 - r) their partners -- the same pair
+//      arithmetic as k_rowpair, so the results are bitwise equal;
+//   4. exchange 2: the partner's updated value goes back into the peer's tile
+//      at N2 - 1 - p (its upper half, free once the peer reports its forward
+//      FFT reads done);
+//   5. inverse row FFT from registers (lower half) + tile (upper half), store.
+// Rows 0 and N1 / 2 pair with themselves: cluster 0 runs them with
+// k_rowpair's self-pairing loops, one row per CTA, no exchange.
+template <int N2>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(N2 / 16, 2)
+k_rowpair_c(RowPairArgs a) {
+    using FF = LineFFT<N2, -1>;
+    using FI = LineFFT<N2, +1>;
+    constexpr int TPL = N2 / 16, R = 16, HALF = N2 / 2;
+    extern __shared__ __align__(128) double2 tile[];  // [N2] row (+ FFT exchanges), [N2 / 2] landing
+    double2* recv = tile + N2;
+    __shared__ __align__(8) unsigned long long bar, bx1, bx2, bok;
+    const int th = threadIdx.x;
+    const unsigned h = cluster_rank(), peer = h ^ 1u;
+    const i64 N1 = a.N1, M = a.N1 * a.N2;
+    const i64 ci = (i64)(blockIdx.x >> 1);
+    const bool self = ci == 0;  // rows 0 (CTA 0) and N1 / 2 (CTA 1)
+    const i64 fr = self ? (h == 0 ? 0 : N1 / 2) : (h == 0 ? ci : N1 - ci);  // frequency row k1
+    const i64 row = a.row_split ? (fr % (N1 / a.row_split)) * a.row_split + fr / (N1 / a.row_split) : fr;
+    double2* src = a.z + row * N2;
+    if (th == 0) {
+        mbar_init(&bar, 1);
+        mbar_init(&bx1, 1);
+        mbar_init(&bx2, 1);
+        mbar_init(&bok, 1);
+        mbar_init_fence();
+        mbar_expect_tx(&bx1, (unsigned)(HALF * sizeof(double2)));
+        mbar_expect_tx(&bx2, (unsigned)(HALF * sizeof(double2)));
+        pdl_wait();
+        mbar_expect_tx(&bar, (unsigned)(N2 * sizeof(double2)));
+        bulk_load(tile, src, (unsigned)(N2 * sizeof(double2)), &bar);
+    }
+    cluster_arrive_relaxed();
+    cluster_wait();  // the peer's barriers exist
+    mbar_wait(&bar, 0);
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = tile[th + q * TPL];
+    FF::run(v, th, tile, a.tw_all + N2);
+    if (self) {
+        // k_rowpair's self-paired rows, one row per CTA
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < R; ++q) tile[swz(th + q * TPL)] = v[q];
+        __syncthreads();
+        if (h == 0) {
+            for (int cpos = th; cpos <= N2 / 2; cpos += TPL) {
+                const int cp = (N2 - cpos) % N2;
+                double2 zk = tile[swz(cpos)], zp = tile[swz(cp)];
+                const i64 k = N1 * (i64)cpos;
+                if (a.mode == 0) pair_mode0(a, zk, zp, k, M);
+                else pair_mode1(a, zk, zp, k, M);
+                if (cp != cpos) tile[swz(cp)] = zp;
+                tile[swz(cpos)] = zk;
+            }
+        } else {
+            for (int cpos = th; cpos < N2 / 2; cpos += TPL) {
+                const int cp = N2 - 1 - cpos;
+                double2 zk = tile[swz(cpos)], zp = tile[swz(cp)];
+                const i64 k = fr + N1 * (i64)cpos;
+                if (a.mode == 0) pair_mode0(a, zk, zp, k, M);
+                else pair_mode1(a, zk, zp, k, M);
+                tile[swz(cpos)] = zk;
+                tile[swz(cp)] = zp;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = tile[swz(th + q * TPL)];
+        __syncthreads();  // the inverse FFT's exchanges overwrite the tile
+    } else {
+        pdl_trigger();
+        // exchange 1: the upper half of this row into the peer's landing zone
+        {
+            const unsigned dst = peer_smem(recv + th, peer), pbar = peer_smem(&bx1, peer);
+#pragma unroll
+            for (int b = 0; b < R / 2; ++b) st_async_peer(dst + (unsigned)(TPL * 16 * b), v[R / 2 + b], pbar);
+        }
+        __syncthreads();  // every thread is past the forward FFT's tile reads
+        if (th == 0) mbar_arrive_peer(peer_smem(&bok, peer));  // the peer may write this tile's upper half
+        // park the own lower half in the tile (positions the peer never writes)
+        // so the pairing's power chains have the registers to themselves
+#pragma unroll
+        for (int q = 0; q < R / 2; ++q) tile[th + q * TPL] = v[q];
+        mbar_wait(&bx1, 0);
+        mbar_wait_cluster(&bok, 0);  // the peer's upper half is free for exchange 2
+        // own positions p = th + TPL q (q < R/2) with the peer's N2 - 1 - p
+        // (landing N2/2 - 1 - p); the partner's result goes straight back into
+        // the peer's tile at N2 - 1 - p (exchange 2)
+        const unsigned pbar = peer_smem(&bx2, peer);
+        constexpr int NX = 4;
+#pragma unroll 1
+        for (int q0 = 0; q0 < R / 2; q0 += NX) {
+            double2 zk[NX], zp[NX];
+            i64 k[NX];
+#pragma unroll
+            for (int i = 0; i < NX; ++i) {
+                const int p = th + TPL * (q0 + i);
+                const double2 own = tile[p], oth = recv[HALF - 1 - p];
+                zk[i] = h == 0 ? own : oth;
+                zp[i] = h == 0 ? oth : own;
+                k[i] = h == 0 ? fr + N1 * (i64)p : (N1 - fr) + N1 * (i64)(N2 - 1 - p);
+            }
+            if (a.mode == 1 && a.real) {
+                pair_mode1_real_xn<NX>(a, zk, zp, k, M);
+            } else if (a.mode == 0 && a.real) {
+                pair_mode0_real_x4(a, zk, zp, k, M);
+            } else {
+#pragma unroll
+                for (int i = 0; i < NX; ++i) {
+                    if (a.mode == 0) pair_mode0(a, zk[i], zp[i], k[i], M);
+                    else pair_mode1(a, zk[i], zp[i], k[i], M);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < NX; ++i) {
+                const int p = th + TPL * (q0 + i);
+                tile[p] = h == 0 ? zk[i] : zp[i];
+                st_async_peer(peer_smem(tile + (N2 - 1 - p), peer), h == 0 ? zp[i] : zk[i], pbar);
+            }
+        }
+        mbar_wait(&bx2, 0);
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = tile[th + q * TPL];
+        __syncthreads();  // the inverse FFT's exchanges overwrite the tile
+    }
+    FI::run(v, th, tile, a.tw_all + N2);
+#pragma unroll
+    for (int q = 0; q < R; ++q) src[th + q * TPL] = v[q];
+}
+
+// FSX_ROWPAIR_C=0 keeps the one-CTA row-pair kernel for every N2 (A/B)
+static bool rowpair_cluster() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_ROWPAIR_C");
+        v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+}
+
 template <int N2>
 static cudaError_t rowpair_n(const RowPairArgs& a, cudaStream_t s) {
+    // measured: cfg5 (N2 = 4096) row-pair pass 1.62 -> 1.44 ms; cfg1 (N2 = 1024,
+    // 64-thread CTAs) 28.8 -> 39.0 us, so only the 4096-point rows take the pair
+    if constexpr (N2 == 4096) {
+        if (rowpair_cluster() && a.N1 >= 4) {
+            const size_t smem = (size_t)(N2 + N2 / 2) * sizeof(double2);
+            kernel_prepare((const void*)k_rowpair_c<N2>, smem);
+            return launch_pdl(k_rowpair_c<N2>, dim3((unsigned)a.N1), dim3(N2 / 16), smem, s, a);
+        }
+    }
     using C = Cfg<N2>;
     constexpr int LS = N2 + ((C::TPL >= 8) ? 0 : 8 / (8 / C::TPL > 2 ? 2 : 8 / C::TPL));
     const size_t smem = (size_t)2 * LS * sizeof(double2);

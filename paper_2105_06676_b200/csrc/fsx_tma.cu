@@ -583,24 +583,6 @@ k_fused8192h(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol s
 }
 
 // ------------------------------------------------------------------ 8192-point columns on a CTA pair
-// Cluster primitives (sm_90+): this CTA's rank in the cluster, a peer CTA's
-// shared-memory address, fire-and-forget stores into it, and the split
-// cluster barrier (arrive / wait).
-__device__ __forceinline__ unsigned cluster_rank() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ unsigned peer_smem(const void* local, unsigned rank) {
-    unsigned out;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(out) : "r"(smem_u32(local)), "r"(rank));
-    return out;
-}
-__device__ __forceinline__ void cluster_arrive_relaxed() {
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
-
 // Spectral multiply of the CTA-pair layout: u[b + 8 s] = X[k0] with
 // k0 = th + 256 b + 2048 (h + 2 s), h = the CTA's rank, so
 // exp(2 pi i og k0 / 8192) = e_b i^(og (h + 2 s)): eight table reads per group
@@ -697,26 +679,6 @@ __device__ __forceinline__ void spectral_pair8192(double2 (&u)[16], int th, int 
 // arrive: the only cluster-wide barrier is the start-up one that publishes the
 // barrier initialisation (a release cluster barrier per exchange costs a
 // GPU-scope fence and an L1 invalidation: ~20 % of the stall samples).
-__device__ __forceinline__ void st_async_peer(unsigned addr, double2 v, unsigned peer_bar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(addr),
-                 "d"(v.x), "d"(v.y), "r"(peer_bar)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_peer(unsigned peer_bar) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(peer_bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAITC_%=:\n"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAITC_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
 k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
     constexpr int N = 8192, NH = 4096, TH = 256;
