@@ -16,6 +16,7 @@
 // (fsx_api.cpp) with cuTensorMapEncodeTiled.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
