@@ -149,7 +149,11 @@ def main():
         T = int(rng.choice([1, 10, 1000]))
         n = int(np.prod(dims))
         a0 = orc.splitmix_fill(8000 + i, n, True)
-        want = orc.solve_periodic(a0, dims, 1, *k.arrays(), T)
+        try:
+            want = orc.solve_periodic(a0, dims, 1, *k.arrays(), T)
+        except orc.OracleSpecError as ex:  # the shrunken last axis is shorter than the kernel's reach
+            print("slab skip", dims, P, ex)
+            continue
         da = torch.from_numpy(a0).cuda()
         try:
             got = slab_solve_emulated(fs.GridShape(dims), da, K(k), T, P).cpu().numpy()
