@@ -1512,7 +1512,11 @@ bool multi_eligible(const Shape& s, const Taps& taps, int P) {
     return (int)groups.size() <= fsx::kMaxGroups;
 }
 
-MultiCtx& multi_ctx(const fsx_shape* global, const Shape& s, const std::vector<int>& devs, int exchange) {
+// The context for (device list, dims, exchange), created on first use; returned
+// with its mutex held (taken under g_multi_mu, so the bounded cache cannot
+// evict a context between its lookup and its use).
+MultiCtx& multi_ctx(const fsx_shape* global, const Shape& s, const std::vector<int>& devs, int exchange,
+                    std::unique_lock<std::mutex>& held) {
     const int P = (int)devs.size();
     std::set<int> distinct(devs.begin(), devs.end());
     if (exchange == kExAuto) {
@@ -1529,7 +1533,10 @@ MultiCtx& multi_ctx(const fsx_shape* global, const Shape& s, const std::vector<i
     for (i64 d : s.dims) key += ":" + std::to_string(d);
     std::lock_guard<std::mutex> lk(g_multi_mu);
     auto it = g_multi.find(key);
-    if (it != g_multi.end()) return *it->second;
+    if (it != g_multi.end()) {
+        held = std::unique_lock<std::mutex>(it->second->mu);
+        return *it->second;
+    }
     if (g_multi.size() >= 4) {  // bounded: drop idle contexts
         for (auto e = g_multi.begin(); e != g_multi.end();) {
             std::unique_lock<std::mutex> busy(e->second->mu, std::try_to_lock);
@@ -1619,6 +1626,7 @@ MultiCtx& multi_ctx(const fsx_shape* global, const Shape& s, const std::vector<i
     for (cudaEvent_t& e : c->tev) FSX_CK(cudaEventCreate(&e));
     auto& ref = *c;
     g_multi.emplace(key, std::move(c));
+    held = std::unique_lock<std::mutex>(ref.mu);
     return ref;
 }
 
@@ -1794,8 +1802,8 @@ bool try_multi(const fsx_shape* shape, const Shape& s, const Taps& taps, u64 T, 
     std::set<int> distinct(devs.begin(), devs.end());
     std::vector<std::unique_ptr<DevLock>> locks;
     for (int d : distinct) locks.push_back(std::make_unique<DevLock>(d));
-    MultiCtx& c = multi_ctx(shape, s, devs, exchange);
-    std::lock_guard<std::mutex> lk(c.mu);
+    std::unique_lock<std::mutex> held;
+    MultiCtx& c = multi_ctx(shape, s, devs, exchange, held);
     multi_solve(c, taps, T, a0, out, stt, t_entry);
     return true;
 }
