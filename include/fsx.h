@@ -101,7 +101,20 @@ typedef struct fsx_options {
     int32_t num_gpus;
     int32_t exchange;
     const int32_t* devices;
+    /* decomp: FSX_DECOMP_AUTO (slabs when axis 0 -- and in 3D axis 1 -- divide
+     * by P, else pencils when they apply), FSX_DECOMP_SLAB, FSX_DECOMP_PENCIL
+     * (3D only: a Pr x Pc grid; rank (pr, pc) owns planes [pr n0/Pr, ...) and
+     * rows [pc n1/Pc, ...) of axis 1; four transposes per solve, over peer
+     * memory by the copy engines; pencil_rows = Pr, 0 = the most square
+     * factorization of P).  Slabs are pencils with Pr = 1 and need two
+     * transposes: they are the better choice whenever they apply. */
+    int32_t decomp;
+    int32_t pencil_rows;
 } fsx_options;
+
+#define FSX_DECOMP_AUTO 0
+#define FSX_DECOMP_SLAB 1
+#define FSX_DECOMP_PENCIL 2
 
 #define FSX_EXCHANGE_AUTO 0
 #define FSX_EXCHANGE_P2P 1
@@ -337,6 +350,8 @@ typedef struct fsx_plan_info {
                                 e.g. the 1D plan's two-level column FFT above 8192 columns) */
     int32_t ranks;           /* devices a host solve is decomposed over (1 = single GPU) */
     int32_t exchange;        /* ranks > 1: FSX_EXCHANGE_P2P or FSX_EXCHANGE_NCCL as resolved */
+    int32_t decomp;          /* ranks > 1: FSX_DECOMP_SLAB or FSX_DECOMP_PENCIL as resolved */
+    int32_t pencil_rows;     /* pencils: Pr (the grid is Pr x ranks / Pr) */
 } fsx_plan_info;
 /* Columns the exact spectral cut keeps for this solve (kept <= total = L/2 + 1;
  * kept == total when the cut does not apply: other plans, rank 3, T == 1, ...). */

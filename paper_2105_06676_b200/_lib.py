@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("FSX_LIB") or os.path.join(HERE, "libfsx.so")  # FSX_L
 FSX_OK, FSX_ERR_SPEC, FSX_ERR_NUMERIC, FSX_ERR_CUDA, FSX_ERR_NCCL, FSX_ERR_OOM, FSX_ERR_IO = 0, 1, 2, 3, 4, 5, 6
 FSX_GRID_CSV, FSX_GRID_RAW = 0, 1
 FSX_EXCHANGE_AUTO, FSX_EXCHANGE_P2P, FSX_EXCHANGE_NCCL = 0, 1, 2
+FSX_DECOMP_AUTO, FSX_DECOMP_SLAB, FSX_DECOMP_PENCIL = 0, 1, 2
 MAX_RANK = 8
 
 
@@ -72,6 +73,8 @@ class FsxOptions(ctypes.Structure):
         ("num_gpus", ctypes.c_int32),
         ("exchange", ctypes.c_int32),
         ("devices", ctypes.POINTER(ctypes.c_int32)),
+        ("decomp", ctypes.c_int32),
+        ("pencil_rows", ctypes.c_int32),
     ]
 
 
@@ -85,6 +88,8 @@ class FsxPlanInfo(ctypes.Structure):
         ("sched_bytes", ctypes.c_int64),
         ("ranks", ctypes.c_int32),
         ("exchange", ctypes.c_int32),
+        ("decomp", ctypes.c_int32),
+        ("pencil_rows", ctypes.c_int32),
     ]
 
 

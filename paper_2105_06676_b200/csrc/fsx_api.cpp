@@ -1445,14 +1445,18 @@ struct MultiRank {
     cudaStream_t cst = nullptr;  // 3D p2p: chunk puts / pulls (copy engines)
     std::unique_ptr<SlabPlan> sp;
     DevBuf in, out, send, recv, peers, flags;
+    DevBuf H1, H2, H3;                  // pencils: x-, y- and z-pencil half spectra
+    TmaMap map_y, map_z, map_z2;        // pencils: y pass over H2, fused pass over H3 (map_z2: parity view)
+    bool tma_y = false, tma_z = false, halves_z = false;
     cudaEvent_t ev_fwd = nullptr, ev_spec = nullptr, ev_done = nullptr;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // pencils: transposes A and B (reverse) written
     std::vector<cudaEvent_t> ev_chunk;  // 3D p2p: per plane chunk
     std::vector<TmaMap> ymaps;          // 3D: y-pass tensor map per plane chunk
     std::vector<bool> ytma;
     ncclComm_t comm = nullptr;
     ~MultiRank() {
         cudaSetDevice(ordinal);
-        for (cudaEvent_t e : {ev_fwd, ev_spec, ev_done})
+        for (cudaEvent_t e : {ev_fwd, ev_spec, ev_done, ev_a, ev_b})
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : ev_chunk) cudaEventDestroy(e);
         if (st) cudaStreamDestroy(st);
@@ -1466,7 +1470,12 @@ struct MultiCtx {
     std::vector<i64> dims;
     int exchange = kExP2P;
     int P = 1, chunks = 1;
-    i64 local_values = 0;  // real values per rank's slab
+    int decomp = 1;        // 1 slabs, 2 pencils
+    // pencils: grid Pr x Pc; local sizes n0r = n0/Pr planes, n1c = n1/Pc rows (x pencils),
+    // n1r = n1/Pr (z pencils); kx blocks of CBx columns; H1 row pitch Pp1
+    int Pr = 1, Pc = 1;
+    i64 n0r = 0, n1c = 0, n1r = 0, CBx = 0, Pp1 = 0, L = 0, M = 0;
+    i64 local_values = 0;  // real values per rank's slab / pencil
     std::vector<std::unique_ptr<MultiRank>> ranks;
     bool fresh = true;         // no solve enqueued yet (no ev_done to wait on)
     cudaEvent_t tev[4] = {};   // stage stamps on rank 0's stream
@@ -1496,39 +1505,64 @@ std::vector<int> multi_devices(const fsx_options* opt) {
     return g_multi_default;
 }
 
-// Whether a problem decomposes into slabs over P ranks (else it runs on one
-// GPU: same result contract, the decomposition is a performance choice).
-bool multi_eligible(const Shape& s, const Taps& taps, int P) {
+// How a problem decomposes over P ranks: 0 = it does not (it runs on one GPU:
+// same result contract, the decomposition is a performance choice), 1 = slabs
+// along axis 0, 2 = a Pr x Pc pencil grid (3D; Pr returned).  Slabs whenever
+// they apply (two transposes against a pencil grid's four), unless pencils
+// are asked for.
+int multi_decomp(const Shape& s, const Taps& taps, int P, const fsx_options* opt, int exchange, int& Pr) {
+    Pr = 1;
     const int rk = s.rank();
-    if ((rk != 2 && rk != 3) || s.fields != 1 || P < 1) return false;
+    if ((rk != 2 && rk != 3) || s.fields != 1 || P < 1) return 0;
     for (i64 d : s.dims)
-        if (!is_pow2(d)) return false;
+        if (!is_pow2(d)) return 0;
     const i64 L = s.dims[rk - 1];
-    if (L < 16 || L > 2 * fsx::kMaxLine || s.dims[0] < 8 || s.dims[0] > fsx::kMaxLine || s.dims[0] % P) return false;
-    if (rk == 3 && (s.dims[1] < 2 || s.dims[1] % P || s.dims[1] > fsx::kMaxLine)) return false;
-    if ((i64)taps.map.size() > fsx::kMaxFusedTaps) return false;
+    if (L < 16 || L > 2 * fsx::kMaxLine || s.dims[0] < 8 || s.dims[0] > fsx::kMaxLine) return 0;
+    if (rk == 3 && (s.dims[1] < 2 || s.dims[1] > fsx::kMaxLine)) return 0;
+    if ((i64)taps.map.size() > fsx::kMaxFusedTaps) return 0;
     std::set<i64> groups;
     for (const auto& kv : taps.map) groups.insert(kv.first[0]);
-    return (int)groups.size() <= fsx::kMaxGroups;
+    if ((int)groups.size() > fsx::kMaxGroups) return 0;
+    const int want = opt ? opt->decomp : 0;
+    if (want < 0 || want > 2) throw SpecErr("fsx_options.decomp: 0 auto, 1 slab, 2 pencil");
+    const bool slab_ok = s.dims[0] % P == 0 && (rk == 2 || s.dims[1] % P == 0);
+    if (want != 2 && slab_ok) return 1;
+    if (want == 1 || rk != 3 || exchange == kExNccl) return 0;
+    // pencils: Pr from the options, else the most square factorization (Pr <= Pc)
+    int pr = opt ? opt->pencil_rows : 0;
+    if (pr <= 0)
+        for (int d = 1; d * d <= P; ++d)
+            if (P % d == 0) pr = d;
+    if (pr < 1 || P % pr) return 0;
+    const int pc = P / pr;
+    const i64 n0 = s.dims[0], n1 = s.dims[1];
+    if (n0 % pr || n1 % pc || n1 % pr || (L / 2 + 1) < pc) return 0;
+    Pr = pr;
+    return 2;
 }
+
 
 // The context for (device list, dims, exchange), created on first use; returned
 // with its mutex held (taken under g_multi_mu, so the bounded cache cannot
 // evict a context between its lookup and its use).
-MultiCtx& multi_ctx(const fsx_shape* global, const Shape& s, const std::vector<int>& devs, int exchange,
-                    std::unique_lock<std::mutex>& held) {
+// p2p when every pair of the devices has peer access, else NCCL
+int resolve_exchange(const std::vector<int>& devs, int exchange) {
+    if (exchange != kExAuto) return exchange;
+    std::set<int> distinct(devs.begin(), devs.end());
+    for (int a : distinct)
+        for (int b : distinct) {
+            int can = 1;
+            if (a != b) FSX_CK(cudaDeviceCanAccessPeer(&can, a, b));
+            if (!can) return kExNccl;
+        }
+    return kExP2P;
+}
+
+MultiCtx& multi_ctx(const fsx_shape* global, const Shape& s, const std::vector<int>& devs, int exchange, int decomp,
+                    int Pr, std::unique_lock<std::mutex>& held) {
     const int P = (int)devs.size();
     std::set<int> distinct(devs.begin(), devs.end());
-    if (exchange == kExAuto) {
-        exchange = kExP2P;
-        for (int a : distinct)
-            for (int b : distinct) {
-                int can = 1;
-                if (a != b) FSX_CK(cudaDeviceCanAccessPeer(&can, a, b));
-                if (!can) exchange = kExNccl;
-            }
-    }
-    std::string key = std::to_string(exchange) + "|";
+    std::string key = std::to_string(exchange) + "|" + std::to_string(decomp) + "x" + std::to_string(Pr) + "|";
     for (int d : devs) key += std::to_string(d) + ",";
     for (i64 d : s.dims) key += ":" + std::to_string(d);
     std::lock_guard<std::mutex> lk(g_multi_mu);
@@ -1554,7 +1588,19 @@ MultiCtx& multi_ctx(const fsx_shape* global, const Shape& s, const std::vector<i
     c->exchange = exchange;
     c->P = P;
     c->local_values = s.cells / P;
+    c->decomp = decomp;
     const bool three = s.rank() == 3;
+    if (decomp == 2) {
+        c->Pr = Pr;
+        c->Pc = P / Pr;
+        c->L = s.dims[2];
+        c->M = c->L / 2;
+        c->n0r = s.dims[0] / c->Pr;
+        c->n1c = s.dims[1] / c->Pc;
+        c->n1r = s.dims[1] / c->Pr;
+        c->CBx = (c->M + 1 + c->Pc - 1) / c->Pc;
+        c->Pp1 = (std::max<i64>(c->M + 8, c->Pc * c->CBx) + 7) / 8 * 8;
+    }
     // peer access between every pair of distinct devices (NVLink / NVSwitch)
     if (exchange == kExP2P)
         for (int a : distinct)
@@ -1575,8 +1621,29 @@ MultiCtx& multi_ctx(const fsx_shape* global, const Shape& s, const std::vector<i
         mr->dev = &device_for(devs[r]);  // selects the device
         FSX_CK(cudaStreamCreateWithFlags(&mr->st, cudaStreamNonBlocking));
         FSX_CK(cudaStreamCreateWithFlags(&mr->cst, cudaStreamNonBlocking));
-        for (cudaEvent_t* e : {&mr->ev_fwd, &mr->ev_spec, &mr->ev_done})
+        for (cudaEvent_t* e : {&mr->ev_fwd, &mr->ev_spec, &mr->ev_done, &mr->ev_a, &mr->ev_b})
             FSX_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        if (decomp == 2) {
+            // pencils: x (H1 [n0r][n1c][Pp1]), y (H2 [n0r][n1][CBx]), z (H3 [n0][n1r][CBx])
+            mr->in.ensure((size_t)c->local_values * 8);
+            mr->out.ensure((size_t)c->local_values * 8);
+            mr->H1.ensure((size_t)c->n0r * c->n1c * c->Pp1 * 16);
+            mr->H2.ensure((size_t)c->n0r * s.dims[1] * c->CBx * 16);
+            mr->H3.ensure((size_t)s.dims[0] * c->n1r * c->CBx * 16);
+            FSX_CK(cudaMemset(mr->H1.p, 0, mr->H1.bytes));  // the kx padding of the last block stays finite
+            mr->flags.ensure(sizeof(fsx::Flags));
+            FSX_CK(cudaMemset(mr->flags.p, 0, sizeof(fsx::Flags)));
+            const fsx::AxisGeom gy{s.dims[1], c->CBx, c->n0r, s.dims[1] * c->CBx, c->CBx};
+            mr->tma_y = tma_enabled() && fsx::tma_cols_ok(s.dims[1]) && c->CBx % fsx::tma_cols_width(s.dims[1]) == 0 &&
+                        fsx::make_cols_tensor_map(mr->map_y.b, mr->H2.p, gy) == 0;
+            const i64 inz = c->n1r * c->CBx;
+            const fsx::AxisGeom gz{s.dims[0], inz, 1, s.dims[0] * inz, inz};
+            mr->halves_z = tma_enabled() && fsx::halves_ok(gz) && fsx::make_cols_tensor_map_par(mr->map_z2.b, mr->H3.p, gz) == 0;
+            mr->tma_z = tma_enabled() && fsx::tma_cols_ok(s.dims[0]) && inz % fsx::tma_cols_width(s.dims[0]) == 0 &&
+                        fsx::make_cols_tensor_map(mr->map_z.b, mr->H3.p, gz) == 0;
+            c->ranks.push_back(std::move(mr));
+            continue;
+        }
         mr->sp = make_slab_plan(global, P, r);
         const SlabPlan& sp = *mr->sp;
         mr->in.ensure((size_t)c->local_values * 8);
@@ -1603,7 +1670,7 @@ MultiCtx& multi_ctx(const fsx_shape* global, const Shape& s, const std::vector<i
         }
         c->ranks.push_back(std::move(mr));
     }
-    if (exchange == kExP2P && !three) {
+    if (exchange == kExP2P && !three && decomp == 1) {
         // 2D: each rank's device array of every rank's exchange buffer
         std::vector<void*> ptrs(P);
         for (int d = 0; d < P; ++d) ptrs[d] = c->ranks[d]->recv.p;
@@ -1791,20 +1858,201 @@ void multi_solve(MultiCtx& c, const Taps& taps, u64 T, const double* a0, double*
     }
 }
 
+// 3D grid on a Pr x Pc pencil grid (rank r = pr Pc + pc): x pencils (planes
+// [pr n0r, ...), rows [pc n1c, ...), full L) -> R2C rows -> transpose A within
+// the row group (kx blocks of CBx columns; full y lines) -> y pass ->
+// transpose B within the column group (y blocks of n1r rows; full z lines) ->
+// fused axis-0 pass with the tile's (ky, kx) offsets -> the reverse.  Every
+// transpose is one pitched copy per peer by the copy engines straight into
+// the peer's buffer (no pack buffers); each is closed by an event barrier
+// before its data is read.  Same kernels per line as the single-GPU solve.
+void multi_solve_pencil(MultiCtx& c, const Taps& taps, u64 T, const double* a0, double* out, fsx_stage_timings* stt,
+                        std::chrono::steady_clock::time_point t_entry) {
+    using clk = std::chrono::steady_clock;
+    const int P = c.P, Pc = c.Pc;
+    const i64 n0 = c.dims[0], n1 = c.dims[1], L = c.L;
+    const auto t_enq = clk::now();
+    auto copy3d = [](void* dst, size_t dpitch, size_t dysize, const void* src, size_t spitch, size_t sysize, size_t w,
+                     size_t h, size_t d, cudaStream_t st) {
+        cudaMemcpy3DParms p = {};
+        p.srcPtr = make_cudaPitchedPtr(const_cast<void*>(src), spitch, w, sysize);
+        p.dstPtr = make_cudaPitchedPtr(dst, dpitch, w, dysize);
+        p.extent = make_cudaExtent(w, h, d);
+        p.kind = cudaMemcpyDefault;
+        FSX_CK(cudaMemcpy3DAsync(&p, st));
+    };
+    if (!c.fresh) multi_barrier(c, &MultiRank::ev_done);
+    FSX_CK(cudaSetDevice(c.ranks[0]->ordinal));
+    if (stt) FSX_CK(cudaEventRecord(c.tev[0], c.ranks[0]->st));
+    // x pencils: H2D, R2C rows, transpose A (kx block pc' to rank (pr, pc'), at its y offset pc n1c)
+    for (int r = 0; r < P; ++r) {
+        MultiRank& mr = *c.ranks[r];
+        const int pr = r / Pc, pc = r % Pc;
+        const double2* tw = mr.dev->tw_all.as<double2>();
+        FSX_CK(cudaSetDevice(mr.ordinal));
+        const double* src = a0 + ((size_t)pr * c.n0r * n1 + (size_t)pc * c.n1c) * L;
+        FSX_CK(cudaMemcpy2DAsync(mr.in.p, (size_t)c.n1c * L * 8, src, (size_t)n1 * L * 8, (size_t)c.n1c * L * 8,
+                                 (size_t)c.n0r, cudaMemcpyHostToDevice, mr.st));
+        const fsx::RowLayout lay{c.Pp1, 0, c.n0r * c.n1c};
+        FSX_CK(fsx::launch_r2c_rows(mr.in.as<double>(), mr.H1.as<double2>(), c.n0r * c.n1c, L, lay, tw, mr.st));
+        for (int q = 0; q < Pc; ++q) {
+            MultiRank& dst = *c.ranks[pr * Pc + q];
+            copy3d(dst.H2.as<double2>() + (size_t)pc * c.n1c * c.CBx, (size_t)c.CBx * 16, (size_t)n1,
+                   mr.H1.as<double2>() + (size_t)q * c.CBx, (size_t)c.Pp1 * 16, (size_t)c.n1c, (size_t)c.CBx * 16,
+                   (size_t)c.n1c, (size_t)c.n0r, mr.st);
+        }
+        FSX_CK(cudaEventRecord(mr.ev_a, mr.st));
+    }
+    multi_barrier(c, &MultiRank::ev_a);
+    // y pass, transpose B (y block pr' to rank (pr', pc), at its plane offset pr n0r)
+    fsx::StepTwiddle nt;
+    fsx::FusedSymbol none;
+    for (int r = 0; r < P; ++r) {
+        MultiRank& mr = *c.ranks[r];
+        const int pr = r / Pc, pc = r % Pc;
+        const double2* tw = mr.dev->tw_all.as<double2>();
+        FSX_CK(cudaSetDevice(mr.ordinal));
+        const fsx::AxisGeom gy{n1, c.CBx, c.n0r, n1 * c.CBx, c.CBx};
+        if (mr.tma_y) FSX_CK(fsx::launch_cols_tma(mr.map_y.b, gy, 0, none, tw, mr.st));
+        else FSX_CK(fsx::launch_axis_pow2(mr.H2.as<double2>(), mr.H2.as<double2>(), gy, -1, nt, tw, mr.st));
+        const size_t w = (size_t)c.n1r * c.CBx * 16;
+        for (int q = 0; q < c.Pr; ++q) {
+            MultiRank& dst = *c.ranks[q * Pc + pc];
+            FSX_CK(cudaMemcpy2DAsync(dst.H3.as<double2>() + (size_t)pr * c.n0r * c.n1r * c.CBx, w,
+                                     mr.H2.as<double2>() + (size_t)q * c.n1r * c.CBx, (size_t)n1 * c.CBx * 16, w,
+                                     (size_t)c.n0r, cudaMemcpyDefault, mr.st));
+        }
+        FSX_CK(cudaEventRecord(mr.ev_fwd, mr.st));
+    }
+    multi_barrier(c, &MultiRank::ev_fwd);
+    FSX_CK(cudaSetDevice(c.ranks[0]->ordinal));
+    if (stt) FSX_CK(cudaEventRecord(c.tev[1], c.ranks[0]->st));
+    // fused axis-0 pass on the z pencils: local tile [ky][kx] of pitch CBx at (pr n1r, pc CBx)
+    Plan view;
+    view.dims = c.dims;
+    view.axes = {0, 1, 2};
+    view.L = L;
+    view.M = c.M;
+    view.P = c.CBx;
+    view.cells = n0 * n1 * L;
+    for (int r = 0; r < P; ++r) {
+        MultiRank& mr = *c.ranks[r];
+        const int pr = r / Pc, pc = r % Pc;
+        const double2* tw = mr.dev->tw_all.as<double2>();
+        FSX_CK(cudaSetDevice(mr.ordinal));
+        fsx::FusedSymbol sym = fused_symbol(view, taps, T);
+        sym.c_off = (i64)pr * c.n1r;
+        sym.c_off_x = (i64)pc * c.CBx;
+        const i64 inz = c.n1r * c.CBx;
+        const fsx::AxisGeom gz{n0, inz, 1, n0 * inz, inz};
+        if (mr.halves_z) FSX_CK(fsx::launch_fused_halves(mr.map_z2.b, gz, sym, tw, mr.st));
+        else if (mr.tma_z) FSX_CK(fsx::launch_cols_tma(mr.map_z.b, gz, 2, sym, tw, mr.st));
+        else FSX_CK(fsx::launch_fused_r2c(mr.H3.as<double2>(), gz, sym, tw, mr.st));
+        FSX_CK(cudaEventRecord(mr.ev_spec, mr.st));
+    }
+    multi_barrier(c, &MultiRank::ev_spec);
+    FSX_CK(cudaSetDevice(c.ranks[0]->ordinal));
+    if (stt) FSX_CK(cudaEventRecord(c.tev[2], c.ranks[0]->st));
+    // reverse transpose B: my planes block pr' back to rank (pr', pc)'s y block pr
+    for (int r = 0; r < P; ++r) {
+        MultiRank& mr = *c.ranks[r];
+        const int pr = r / Pc, pc = r % Pc;
+        FSX_CK(cudaSetDevice(mr.ordinal));
+        const size_t w = (size_t)c.n1r * c.CBx * 16;
+        for (int q = 0; q < c.Pr; ++q) {
+            MultiRank& dst = *c.ranks[q * Pc + pc];
+            FSX_CK(cudaMemcpy2DAsync(dst.H2.as<double2>() + (size_t)pr * c.n1r * c.CBx, (size_t)n1 * c.CBx * 16,
+                                     mr.H3.as<double2>() + (size_t)q * c.n0r * c.n1r * c.CBx, w, w, (size_t)c.n0r,
+                                     cudaMemcpyDefault, mr.st));
+        }
+        FSX_CK(cudaEventRecord(mr.ev_b, mr.st));
+    }
+    multi_barrier(c, &MultiRank::ev_b);
+    // inverse y pass, reverse transpose A: my y block pc' back to rank (pr, pc')'s kx block pc
+    for (int r = 0; r < P; ++r) {
+        MultiRank& mr = *c.ranks[r];
+        const int pr = r / Pc, pc = r % Pc;
+        const double2* tw = mr.dev->tw_all.as<double2>();
+        FSX_CK(cudaSetDevice(mr.ordinal));
+        const fsx::AxisGeom gy{n1, c.CBx, c.n0r, n1 * c.CBx, c.CBx};
+        if (mr.tma_y) FSX_CK(fsx::launch_cols_tma(mr.map_y.b, gy, 1, none, tw, mr.st));
+        else FSX_CK(fsx::launch_axis_pow2(mr.H2.as<double2>(), mr.H2.as<double2>(), gy, +1, nt, tw, mr.st));
+        for (int q = 0; q < Pc; ++q) {
+            MultiRank& dst = *c.ranks[pr * Pc + q];
+            copy3d(dst.H1.as<double2>() + (size_t)pc * c.CBx, (size_t)c.Pp1 * 16, (size_t)c.n1c,
+                   mr.H2.as<double2>() + (size_t)q * c.n1c * c.CBx, (size_t)c.CBx * 16, (size_t)n1, (size_t)c.CBx * 16,
+                   (size_t)c.n1c, (size_t)c.n0r, mr.st);
+        }
+        FSX_CK(cudaEventRecord(mr.ev_a, mr.st));
+    }
+    multi_barrier(c, &MultiRank::ev_a);
+    // C2R rows, D2H of the x pencil
+    for (int r = 0; r < P; ++r) {
+        MultiRank& mr = *c.ranks[r];
+        const int pr = r / Pc, pc = r % Pc;
+        const double2* tw = mr.dev->tw_all.as<double2>();
+        FSX_CK(cudaSetDevice(mr.ordinal));
+        const fsx::RowLayout lay{c.Pp1, 0, c.n0r * c.n1c};
+        FSX_CK(fsx::launch_c2r_rows(mr.H1.as<double2>(), mr.out.as<double>(), c.n0r * c.n1c, L, lay, tw,
+                                    mr.flags.as<fsx::Flags>(), mr.st));
+        double* dsth = out + ((size_t)pr * c.n0r * n1 + (size_t)pc * c.n1c) * L;
+        FSX_CK(cudaMemcpy2DAsync(dsth, (size_t)n1 * L * 8, mr.out.p, (size_t)c.n1c * L * 8, (size_t)c.n1c * L * 8,
+                                 (size_t)c.n0r, cudaMemcpyDeviceToHost, mr.st));
+        FSX_CK(cudaEventRecord(mr.ev_done, mr.st));
+    }
+    FSX_CK(cudaSetDevice(c.ranks[0]->ordinal));
+    if (stt) FSX_CK(cudaEventRecord(c.tev[3], c.ranks[0]->st));
+    c.fresh = false;
+    std::string err;
+    for (int r = 0; r < P; ++r) {
+        MultiRank& mr = *c.ranks[r];
+        FSX_CK(cudaSetDevice(mr.ordinal));
+        FSX_CK(cudaStreamSynchronize(mr.st));
+        fsx::Flags h;
+        FSX_CK(cudaMemcpy(&h, mr.flags.p, sizeof(h), cudaMemcpyDeviceToHost));
+        FSX_CK(cudaMemset(mr.flags.p, 0, sizeof(h)));
+        if (h.nonfinite && err.empty())
+            err = " (pencil " + std::to_string(r / Pc) + "," + std::to_string(r % Pc) + " of " + std::to_string(c.Pr) +
+                  "x" + std::to_string(Pc) + ")";
+    }
+    if (!err.empty()) throw NumErr("solve_periodic: non-finite value after inverse FFT" + err);
+    if (stt) {
+        FSX_CK(cudaSetDevice(c.ranks[0]->ordinal));
+        FSX_CK(cudaEventSynchronize(c.tev[3]));
+        float t01 = 0, t12 = 0, t23 = 0;
+        FSX_CK(cudaEventElapsedTime(&t01, c.tev[0], c.tev[1]));
+        FSX_CK(cudaEventElapsedTime(&t12, c.tev[1], c.tev[2]));
+        FSX_CK(cudaEventElapsedTime(&t23, c.tev[2], c.tev[3]));
+        const double setup = std::chrono::duration<double>(t_enq - t_entry).count();
+        const double total = std::chrono::duration<double>(clk::now() - t_entry).count();
+        const double gpu = (t01 + t12 + t23) * 1e-3;
+        stt->forward_fft += setup + t01 * 1e-3;
+        stt->squaring += t12 * 1e-3;
+        stt->inverse_fft += t23 * 1e-3 + std::max(0.0, total - setup - gpu);
+    }
+}
+
 // Routes a host solve to the multi-GPU path; false when it runs on one GPU.
 bool try_multi(const fsx_shape* shape, const Shape& s, const Taps& taps, u64 T, const double* a0, double* out,
                const fsx_options* opt, fsx_stage_timings* stt, std::chrono::steady_clock::time_point t_entry) {
     const std::vector<int> devs = multi_devices(opt);
-    if (devs.empty() || !multi_eligible(s, taps, (int)devs.size())) return false;
-    const int exchange = opt ? opt->exchange : kExAuto;
-    if (exchange < kExAuto || exchange > kExNccl) throw SpecErr("fsx_options.exchange: 0 auto, 1 p2p, 2 nccl");
-    // every involved device's lock, in ordinal order (no lock-order inversion)
+    if (devs.empty()) return false;
+    const int ex_opt = opt ? opt->exchange : kExAuto;
+    if (ex_opt < kExAuto || ex_opt > kExNccl) throw SpecErr("fsx_options.exchange: 0 auto, 1 p2p, 2 nccl");
+    // validate the ordinals (DevLock below) before any peer query
     std::set<int> distinct(devs.begin(), devs.end());
+    for (int d : distinct) device_for(d);
+    const int exchange = resolve_exchange(devs, ex_opt);
+    int Pr = 1;
+    const int decomp = multi_decomp(s, taps, (int)devs.size(), opt, exchange, Pr);
+    if (!decomp) return false;
+    // every involved device's lock, in ordinal order (no lock-order inversion)
     std::vector<std::unique_ptr<DevLock>> locks;
     for (int d : distinct) locks.push_back(std::make_unique<DevLock>(d));
     std::unique_lock<std::mutex> held;
-    MultiCtx& c = multi_ctx(shape, s, devs, exchange, held);
-    multi_solve(c, taps, T, a0, out, stt, t_entry);
+    MultiCtx& c = multi_ctx(shape, s, devs, exchange, decomp, Pr, held);
+    if (decomp == 2) multi_solve_pencil(c, taps, T, a0, out, stt, t_entry);
+    else multi_solve(c, taps, T, a0, out, stt, t_entry);
     return true;
 }
 
@@ -2479,19 +2727,20 @@ fsx_status fsx_plan_describe(const fsx_shape* shape, const fsx_kernel* k, const 
         info->ranks = 1;
         info->exchange = 0;
         const std::vector<int> devs = multi_devices(opt);
-        if (!devs.empty() && multi_eligible(s, taps, (int)devs.size())) {
-            info->ranks = (int32_t)devs.size();
-            int ex = opt ? opt->exchange : kExAuto;
-            if (ex == kExAuto) {
-                ex = kExP2P;
-                for (int a : devs)
-                    for (int b : devs) {
-                        int can = 1;
-                        if (a != b) FSX_CK(cudaDeviceCanAccessPeer(&can, a, b));
-                        if (!can) ex = kExNccl;
-                    }
+        info->decomp = 0;
+        info->pencil_rows = 0;
+        if (!devs.empty()) {
+            std::set<int> distinct(devs.begin(), devs.end());
+            for (int d : distinct) device_for(d);
+            const int ex = resolve_exchange(devs, opt ? opt->exchange : kExAuto);
+            int Pr = 1;
+            const int dc = multi_decomp(s, taps, (int)devs.size(), opt, ex, Pr);
+            if (dc) {
+                info->ranks = (int32_t)devs.size();
+                info->exchange = ex;
+                info->decomp = dc;
+                info->pencil_rows = dc == 2 ? Pr : 0;
             }
-            info->exchange = ex;
         }
     });
 }

@@ -84,13 +84,15 @@ struct FusedSymbol {
     const unsigned long long* qmax_bits = nullptr;
     i64 c_off = 0;               // slab decomposition: global frequency of local column block start
                                  // (rank 2: kx offset; rank 3: ky offset)
+    i64 c_off_x = 0;             // rank 3 pencil decomposition: kx of the local tile's first column
+                                 // (the local [ky][kx] tile has pitch P = its kx block width)
 };
 
 // Local column c of a fused-pass tile -> global (kx, ky); valid iff kx <= M.
 __host__ __device__ inline void fused_col_freqs(const FusedSymbol& s, i64 c, i64& kx, i64& ky) {
     if (s.rank == 3) {
         ky = c / s.P;
-        kx = c - ky * s.P;
+        kx = c - ky * s.P + s.c_off_x;
         ky += s.c_off;
     } else {
         ky = 0;

@@ -314,19 +314,20 @@ _OPTS: dict = {}  # option structs are read-only for the library: reuse them
 
 
 def _opts(device: int = 0, path: int = 0, stream: int | None = None, stage_events: int = 0, spectral_cut: int = 0,
-          num_gpus: int = 0, exchange: int = 0, devices=None):
+          num_gpus: int = 0, exchange: int = 0, devices=None, decomp: int = 0, pencil_rows: int = 0):
     """fsx_options.  stream None -> the library's own stream; a handle of 0
     (torch's default stream) is passed as cudaStreamLegacy so the work is
     ordered with the caller's NULL-stream work instead of the library stream.
     num_gpus / exchange / devices: the single-process multi-GPU path (fsx.h)."""
     devices = tuple(int(d) for d in devices) if devices is not None else None
-    key = (device, path, stream, stage_events, spectral_cut, num_gpus, exchange, devices)
+    key = (device, path, stream, stage_events, spectral_cut, num_gpus, exchange, devices, decomp, pencil_rows)
     o = _OPTS.get(key)
     if o is None:
         o = _lib.FsxOptions()
         o.device, o.path, o.stage_events, o.spectral_cut = device, path, stage_events, int(bool(spectral_cut))
         o.stream = None if stream is None else (stream or CUDA_STREAM_LEGACY)
         o.num_gpus, o.exchange = num_gpus, exchange
+        o.decomp, o.pencil_rows = decomp, pencil_rows
         if devices is not None:
             o._devs = (ctypes.c_int32 * len(devices))(*devices)  # kept alive with the struct
             o.devices = ctypes.cast(o._devs, ctypes.POINTER(ctypes.c_int32))
@@ -385,14 +386,15 @@ def _solve(fn, a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None,
 
 def solve_periodic(a0: FieldGrid, k: StencilKernel, T: int, st: StageTimings | None = None, *, path: int = 0,
                    out: np.ndarray | None = None, spectral_cut: int = 0, num_gpus: int = 0, devices=None,
-                   exchange: int = 0):
+                   exchange: int = 0, decomp: int = 0, pencil_rows: int = 0):
     """proj/src/periodic.cpp:76-86 on the B200 path (fsx_solve_periodic).
     ``out`` optionally supplies the (e.g. pinned) host array the result is written to.
     ``spectral_cut=1``: the exact spectral cut (fsx_options.spectral_cut; same result).
     ``num_gpus`` / ``devices`` / ``exchange`` (0 auto, 1 p2p, 2 nccl): slab-decompose an
     eligible 2D/3D grid over several GPUs of this process (fsx_options; 0 = the
     process default of set_devices)."""
-    multi = {"num_gpus": num_gpus, "exchange": exchange, "devices": devices}
+    multi = {"num_gpus": num_gpus, "exchange": exchange, "devices": devices, "decomp": decomp,
+             "pencil_rows": pencil_rows}
     return _solve("fsx_solve_periodic", a0, k, T, st, path, out=out, spectral_cut=spectral_cut, multi=multi)
 
 
@@ -655,17 +657,17 @@ def spectral_cut_columns(shape: GridShape, k: StencilKernel, T: int) -> tuple:
 
 
 def plan_describe(shape: GridShape, k: StencilKernel, path: int = 0, num_gpus: int = 0, devices=None,
-                  exchange: int = 0) -> dict:
+                  exchange: int = 0, decomp: int = 0, pencil_rows: int = 0) -> dict:
     L = _lib.load()
     info = _lib.FsxPlanInfo()
     kc, keep = k._c()
-    o = _opts(path=path, num_gpus=num_gpus, exchange=exchange, devices=devices)
+    o = _opts(path=path, num_gpus=num_gpus, exchange=exchange, devices=devices, decomp=decomp, pencil_rows=pencil_rows)
     _lib.check(L.fsx_plan_describe(ctypes.byref(shape._c()), ctypes.byref(kc), ctypes.byref(o), ctypes.byref(info)))
     del keep
     return {"path": info.path, "launches": info.launches, "alg_bytes": info.alg_bytes,
             "fused_bytes": info.fused_bytes, "work_bytes": info.work_bytes, "sched_bytes": info.sched_bytes,
             "ranks": info.ranks,
-            "exchange": info.exchange}
+            "exchange": info.exchange, "decomp": info.decomp, "pencil_rows": info.pencil_rows}
 
 
 # ---------------------------------------------------------------- building blocks

@@ -136,3 +136,51 @@ def test_multi_numeric_error_and_aliasing(orc):
     assert np.linalg.norm(buf - want) / np.linalg.norm(want) <= 1e-10
     same = fs.solve_periodic(fs.FieldGrid(shape, a0.copy()), _k(kern), 0, devices=[0, 0]).data
     assert np.array_equal(same, a0)
+
+
+PENCIL_CASES = [
+    ([32, 64, 128], 4, 0),      # 2 x 2 (most square)
+    ([64, 32, 64], 8, 2),       # 2 x 4
+    ([64, 32, 64], 8, 4),       # 4 x 2
+    ([32, 16, 32], 2, 1),       # 1 x 2: pencils along axis 1 only
+    ([8, 16, 32], 16, 0),       # slabs impossible (8 planes < 16 ranks): auto picks 4 x 4 pencils
+    ([1024, 64, 32], 4, 2),     # 1024-point fused columns (TMA), 2 x 2
+]
+
+
+@pytest.mark.parametrize("dims,P,pr", PENCIL_CASES)
+def test_multi_pencils_emulated_vs_oracle(orc, dims, P, pr):
+    """Pr x Pc pencil grid (fsx_options.decomp = FSX_DECOMP_PENCIL): four
+    copy-engine transposes per solve; against the oracle and bit for bit
+    against the single-GPU solve (the same kernels per line)."""
+    kern = R.random_kernel(R.Rng(sum(dims) + P), 3, 1, 1, 0.95)
+    a0 = orc.splitmix_fill(13, int(np.prod(dims)), True)
+    T = 11
+    want = orc.solve_periodic(a0, dims, 1, *kern.arrays(), T)
+    shape = fs.GridShape(dims)
+    single = fs.solve_periodic(fs.FieldGrid(shape, a0.copy()), _k(kern), T).data
+    devs = [0] * P
+    decomp = 2 if dims[0] >= P else 0
+    info = fs.plan_describe(shape, _k(kern), devices=devs, decomp=decomp, pencil_rows=pr)
+    assert info["ranks"] == P and info["decomp"] == 2, info
+    if pr:
+        assert info["pencil_rows"] == pr
+    got = fs.solve_periodic(fs.FieldGrid(shape, a0.copy()), _k(kern), T, devices=devs, decomp=decomp,
+                            pencil_rows=pr).data
+    err = np.linalg.norm(got - want) / np.linalg.norm(want)
+    print(f"{dims} pencils {info['pencil_rows']}x{P // info['pencil_rows']}: rel L2 vs oracle {err:.3e}")
+    assert err <= 1e-10, (dims, P, err)
+    assert np.array_equal(got, single)
+
+
+def test_multi_pencil_numeric_error(orc):
+    dims = [32, 16, 32]
+    kern = R.random_kernel(R.Rng(44), 3, 1, 1, 0.95)
+    bad = orc.splitmix_fill(2, int(np.prod(dims)), True)
+    bad[-3] = np.inf
+    with pytest.raises(fs.NumericError, match="pencil"):
+        fs.solve_periodic(fs.FieldGrid(fs.GridShape(dims), bad), _k(kern), 3, devices=[0] * 4, decomp=2)
+    # 2D grids have no pencils: decomp = pencil there means one GPU
+    info = fs.plan_describe(fs.GridShape([64, 64]), _k(R.random_kernel(R.Rng(45), 2, 1, 1, 0.9)), devices=[0, 0],
+                            decomp=2)
+    assert info["ranks"] == 1
