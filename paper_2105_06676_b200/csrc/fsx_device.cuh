@@ -261,7 +261,11 @@ __device__ __forceinline__ void group_sync() {
 
 // CT: the complex element type (double2; float2 for the fp32 mode's fused
 // pass, with a float2 copy of the twiddle tables).
-template <int N, int SIGN, bool PF = false, bool PAIR = false, int FT = 0, int NB = 0, class CT = double2>
+// LPF = true: the four base twiddles (W^1, W^2, W^4, W^8) of the next radix-16
+// derived-twiddle pass are loaded before the exchange barrier (8 extra live
+// registers instead of PF's 30), so their latency overlaps the barrier wait.
+template <int N, int SIGN, bool PF = false, bool PAIR = false, int FT = 0, int NB = 0, class CT = double2,
+          bool LPF = false>
 struct LineFFT {
     static constexpr int LOGN = ilog2c(N);
     static constexpr int R = N < 16 ? N : 16;
@@ -345,11 +349,27 @@ struct LineFFT {
     // are the generic path's (w3 = w1 w2, w5 = w1 w4, w6 = w2 w4, w7 = w3 w4,
     // w(u + 8) = w(u) w8): bitwise the same results.
     template <int S>
-    __device__ __forceinline__ static void tw16_apply(CT (&a)[16], int t, const CT* __restrict__ tw) {
+    __device__ __forceinline__ static void tw16_base(int t, const CT* __restrict__ tw, CT (&b)[4]) {
         constexpr int Ns = ns<S>();
         const int k = item<S>(t, 0) & (Ns - 1);
         const CT* pt = tw + (kPassTabBase + 15 * N + 16 * Ns) + k;
-        const CT w1 = __ldg(pt), w2 = __ldg(pt + Ns), w4 = __ldg(pt + 3 * Ns), w8 = __ldg(pt + 7 * Ns);
+        b[0] = __ldg(pt);
+        b[1] = __ldg(pt + Ns);
+        b[2] = __ldg(pt + 3 * Ns);
+        b[3] = __ldg(pt + 7 * Ns);
+    }
+
+    template <int S>
+    __device__ __forceinline__ static void tw16_apply(CT (&a)[16], int t, const CT* __restrict__ tw,
+                                                      const CT* pre = nullptr) {
+        CT b[4];
+        if (pre) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) b[i] = pre[i];
+        } else {
+            tw16_base<S>(t, tw, b);
+        }
+        const CT w1 = b[0], w2 = b[1], w4 = b[2], w8 = b[3];
         a[1] = ctw<SIGN>(a[1], w1);
         a[2] = ctw<SIGN>(a[2], w2);
         a[4] = ctw<SIGN>(a[4], w4);
@@ -372,12 +392,19 @@ struct LineFFT {
     }
 
     template <int S>
-    __device__ __forceinline__ static void pass(CT (&v)[R], int t, CT* line, const CT* __restrict__ tw, CT (&w)[R]) {
+    __host__ __device__ static constexpr bool inc_pass() {
+        return !PF && radix<S>() == 16 && R / radix<S>() == 1 && ns<S>() > 1 && ((FT >> S) & 1) == 0 &&
+               !(PAIRED && S == NPASS - 1);
+    }
+
+    template <int S>
+    __device__ __forceinline__ static void pass(CT (&v)[R], int t, CT* line, const CT* __restrict__ tw, CT (&w)[R],
+                                                const CT* pre = nullptr) {
         constexpr int r = radix<S>();
         constexpr int Ns = ns<S>();
         constexpr int C = R / r;
         // radix-16 items with derived twiddles: formed and applied on the fly
-        constexpr bool INC = !PF && r == 16 && C == 1 && Ns > 1 && ((FT >> S) & 1) == 0 && !(PAIRED && S == NPASS - 1);
+        constexpr bool INC = inc_pass<S>();
         if constexpr (!PF && !INC) load_tw<S>(t, tw, w);
 #pragma unroll
         for (int i = 0; i < C; ++i) {
@@ -385,7 +412,7 @@ struct LineFFT {
 #pragma unroll
             for (int u = 0; u < r; ++u) a[u] = v[i + u * C];
             if constexpr (INC) {
-                tw16_apply<S>(a, t, tw);
+                tw16_apply<S>(a, t, tw, pre);
             } else if constexpr (Ns > 1) {
 #pragma unroll
                 for (int u = 1; u < r; ++u) a[u] = ctw<SIGN>(a[u], w[i * r + u]);
@@ -396,6 +423,9 @@ struct LineFFT {
         }
         if constexpr (S + 1 < NPASS) {
             if constexpr (PF) load_tw<S + 1>(t, tw, w);
+            CT nb[4];
+            constexpr bool LP = LPF && inc_pass<S + 1>();
+            if constexpr (LP) tw16_base<S + 1>(t, tw, nb);
             group_sync<NB>();
 #pragma unroll
             for (int i = 0; i < C; ++i) {
@@ -414,7 +444,8 @@ struct LineFFT {
 #pragma unroll
                 for (int u = 0; u < r2; ++u) v[i + u * C2] = line[swz(j + u * (N / r2))];
             }
-            pass<S + 1>(v, t, line, tw, w);
+            if constexpr (LP) pass<S + 1>(v, t, line, tw, w, nb);
+            else pass<S + 1>(v, t, line, tw, w);
         }
     }
 

@@ -386,7 +386,10 @@ __global__ void __launch_bounds__(NG * PCfg<M>::TPL, MINB)
 k_r2c_grp(const double* __restrict__ x, double2* __restrict__ H, i64 nrows, i64 L, RowLayout lay,
           const double2* __restrict__ tw_all) {
     constexpr int TPL = PCfg<M>::TPL, R = 16;
-    using F = LineFFT<M, -1, false, false, 0, TPL>;  // named barriers per group
+    #ifndef FSX_ROWS_LPF
+#define FSX_ROWS_LPF 1  // cfg3 rows ~1 % (r02v)
+#endif
+    using F = LineFFT<M, -1, false, false, 0, TPL, double2, FSX_ROWS_LPF != 0>;  // named barriers per group
     static_assert(!F::PAIRED, "k_r2c_grp: split through the exchange line (M = 2^(4a))");
     constexpr unsigned BYTES = 2 * M * sizeof(double);
     extern __shared__ __align__(128) double2 sm[];
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(NG * PCfg<M>::TPL, MINB)
 k_c2r_grp(const double2* __restrict__ H, double* __restrict__ x, i64 nrows, i64 L, RowLayout lay,
           const double2* __restrict__ tw_all, Flags* flags) {
     constexpr int TPL = PCfg<M>::TPL, R = 16;
-    using F = LineFFT<M, +1, false, false, 0, TPL>;
+    using F = LineFFT<M, +1, false, false, 0, TPL, double2, FSX_ROWS_LPF != 0>;
     constexpr int SS = M + 8;  // stage stride: M + 1 elements, 128 B aligned
     extern __shared__ __align__(128) double2 sm[];
     __shared__ __align__(8) unsigned long long bar[ST];

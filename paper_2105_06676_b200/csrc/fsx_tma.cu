@@ -60,8 +60,11 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
 #define FSX_FT4096 0
 #endif
     constexpr int FT = N < 4096 ? ~0 : FSX_FT4096;
-    using FF = LineFFT<N, -1, false, false, FT>;
-    using FI = LineFFT<N, +1, false, false, FT>;
+#ifndef FSX_COLS_LPF
+#define FSX_COLS_LPF 0
+#endif
+    using FF = LineFFT<N, -1, false, false, FT, 0, double2, FSX_COLS_LPF != 0>;
+    using FI = LineFFT<N, +1, false, false, FT, 0, double2, FSX_COLS_LPF != 0>;
     extern __shared__ __align__(128) double2 tile[];
     __shared__ __align__(8) unsigned long long bar;
     __shared__ double2 acoef[kMaxGroups][W];
@@ -683,8 +686,11 @@ __device__ __forceinline__ void spectral_pair8192(double2 (&u)[16], int th, int 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
 k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
     constexpr int N = 8192, NH = 4096, TH = 256;
-    using FF = LineFFT<NH, -1>;
-    using FI = LineFFT<NH, +1>;
+#ifndef FSX_F8192_LPF
+#define FSX_F8192_LPF 1  // cfg3: fused 0.5829 -> 0.5800 ms (r02v)
+#endif
+    using FF = LineFFT<NH, -1, false, false, 0, 0, double2, FSX_F8192_LPF != 0>;
+    using FI = LineFFT<NH, +1, false, false, 0, 0, double2, FSX_F8192_LPF != 0>;
     extern __shared__ __align__(128) double2 tile[];  // [NH] tile + [NH / 2] exchange-1 landing
     double2* recv = tile + NH;
     // bar: TMA load; bx1 / bx2: the peer's exchange-1 / exchange-2 stores
