@@ -95,7 +95,7 @@ def load_traffic(cfg_name, kernel):
     name = t.get(cfg_name + "_kernel", "")
     if t.get(cfg_name) is None or not kernel.startswith(name.split("<")[0]) or name.split("<")[0] == "":
         return None, f"no capture of {kernel} in profiles/ncu_traffic.json"
-    return t.get(cfg_name), f"ncu --set full of {name} at {t.get(cfg_name + '_head', 'round-1 HEAD')}"
+    return t.get(cfg_name), f"ncu dram__bytes_read.sum + dram__bytes_write.sum of {name} at {t.get(cfg_name + '_head', 'round-1 HEAD')}"
 
 
 def dominant_kernel(info, cfg):
@@ -105,7 +105,15 @@ def dominant_kernel(info, cfg):
         if n0 == 8192 and len(cfg.dims) == 2:
             return "k_fused8192c (8192-point columns, 2-CTA cluster)"
         return f"k_cols_tma<{n0}, 2>"
-    return {2: "k_rowpair", 3: "k_spectral_general"}[info["path"]]
+    if info["path"] == 2:
+        n = cfg.dims[0]
+        mc = n // 2 if cfg.fields == 1 else n  # complex points of the 1D row-pair plan
+        b = mc.bit_length() - 1
+        n2 = mc if mc <= 256 else 1 << min(12, (b + 1) // 2)
+        n1 = mc // n2
+        # 4096-point rows run on a CTA pair (k_rowpair_c), the others one row pair per CTA
+        return f"k_rowpair_c<{n2}>" if (n2 == 4096 and n1 >= 4) else f"k_rowpair<{n2}>"
+    return "k_spectral_general"
 
 
 class ClockSampler:
