@@ -24,6 +24,11 @@
 namespace fsx {
 
 // ------------------------------------------------------------------ helpers
+// a mod n for a power-of-two n (two's complement: exact for negative a too);
+// the 1D row-pair symbols' phase indices (their lengths are powers of two) --
+// the generic 64-bit modp is a ~40-instruction software sequence per call
+__device__ __forceinline__ i64 modp2(i64 a, i64 n) { return a & (n - 1); }
+
 __device__ __forceinline__ i64 modp(i64 a, i64 n) {
     const i64 r = a % n;
     return r < 0 ? r + n : r;
@@ -430,7 +435,7 @@ k_fused_r2c(double2* H, AxisGeom g, FusedSymbol sym, const double2* __restrict__
 __device__ __forceinline__ double2 sym1(const RowPairArgs& a, i64 k, i64 n) {
     double2 lam = make_double2(0.0, 0.0);
     for (int j = 0; j < a.ntaps; ++j) {
-        const double2 e = cconj(phase_at(a.wk, modp(k * (i64)a.tap_off[j], n)));
+        const double2 e = cconj(phase_at(a.wk, modp2(k * (i64)a.tap_off[j], n)));
         lam = make_double2(fma(a.tap_b[j][0], e.x, lam.x), fma(a.tap_b[j][0], e.y, lam.y));
     }
     return lam;
@@ -484,7 +489,7 @@ __device__ __forceinline__ void pair_mode0_real_x4(const RowPairArgs& a, double2
         const double b = a.tap_b[j][0], bp = (o & 1) ? -b : b;
         if (ao != 0 && ao != last) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) lastc[i] = phase_at(a.wk, modp(k[i] * (i64)ao, L)).x;
+            for (int i = 0; i < 4; ++i) lastc[i] = phase_at(a.wk, modp2(k[i] * (i64)ao, L)).x;
             last = ao;
         }
 #pragma unroll
@@ -520,7 +525,7 @@ __device__ __forceinline__ void pair_mode1(const RowPairArgs& a, double2& zk, do
         // matrix; same binary-exponentiation loop in real arithmetic
         double l00 = 0, l01 = 0, l10 = 0, l11 = 0;
         for (int j = 0; j < a.ntaps; ++j) {
-            const double c = phase_at(a.wk, modp(k * (i64)a.tap_off[j], N)).x;
+            const double c = phase_at(a.wk, modp2(k * (i64)a.tap_off[j], N)).x;
             l00 = fma(a.tap_b[j][0], c, l00);
             l01 = fma(a.tap_b[j][1], c, l01);
             l10 = fma(a.tap_b[j][2], c, l10);
@@ -557,7 +562,7 @@ __device__ __forceinline__ void pair_mode1(const RowPairArgs& a, double2& zk, do
     }
     double2 lam[2][2] = {{make_double2(0, 0), make_double2(0, 0)}, {make_double2(0, 0), make_double2(0, 0)}};
     for (int j = 0; j < a.ntaps; ++j) {
-        const double2 e = cconj(phase_at(a.wk, modp(k * (i64)a.tap_off[j], N)));
+        const double2 e = cconj(phase_at(a.wk, modp2(k * (i64)a.tap_off[j], N)));
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
@@ -587,7 +592,7 @@ __device__ __forceinline__ void real_block_symbol(const RowPairArgs& a, i64 k, i
     for (int j = 0; j < a.ntaps; ++j) {
         const int o = a.tap_off[j] < 0 ? -a.tap_off[j] : a.tap_off[j];
         if (o != 0 && o != last) {
-            lastc = phase_at(a.wk, modp(k * (i64)o, N)).x;
+            lastc = phase_at(a.wk, modp2(k * (i64)o, N)).x;
             last = o;
         }
         const double c = o == 0 ? 1.0 : lastc;
