@@ -334,6 +334,10 @@ fsx_status fsx_format_stage_table(const fsx_stage_timings* st, double total, dou
 
 /* ---------------------------------------------------------------- introspection */
 const char* fsx_last_error(void);
+/* ABI version: 200 = round 2 (fsx_options grew num_gpus / exchange / devices /
+ * decomp / pencil_rows, fsx_plan_info grew sched_bytes / ranks / exchange /
+ * decomp / pencil_rows; callers built against 100 must be rebuilt). */
+#define FSX_ABI_VERSION 200
 int32_t fsx_version(void);
 int32_t fsx_device_count(void);
 

@@ -17,6 +17,7 @@ FSX_GRID_CSV, FSX_GRID_RAW = 0, 1
 FSX_EXCHANGE_AUTO, FSX_EXCHANGE_P2P, FSX_EXCHANGE_NCCL = 0, 1, 2
 FSX_DECOMP_AUTO, FSX_DECOMP_SLAB, FSX_DECOMP_PENCIL = 0, 1, 2
 MAX_RANK = 8
+ABI_VERSION = 200  # include/fsx.h FSX_ABI_VERSION: the struct layouts below
 
 
 class Error(RuntimeError):
@@ -155,6 +156,9 @@ def load():
     L.fsx_version.restype = ctypes.c_int32
     L.fsx_device_count.restype = ctypes.c_int32
     L.fsx_get_devices.restype = ctypes.c_int32
+    if L.fsx_version() != ABI_VERSION:
+        raise ImportError(f"{LIB_PATH}: ABI version {L.fsx_version()}, this binding expects {ABI_VERSION} "
+                          "(rebuild with `make`)")
     L.fsx_spectrum_cache_create.restype = ctypes.c_void_p
     L.fsx_spectrum_cache_destroy.argtypes = [ctypes.c_void_p]
     _lib = L

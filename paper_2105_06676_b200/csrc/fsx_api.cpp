@@ -2435,7 +2435,7 @@ extern "C" {
 __attribute__((visibility("hidden"))) void fsx_internal_set_error(const char* msg) { g_err = msg ? msg : ""; }
 
 const char* fsx_last_error(void) { return g_err.c_str(); }
-int32_t fsx_version(void) { return 100; }
+int32_t fsx_version(void) { return FSX_ABI_VERSION; }
 
 fsx_status fsx_set_devices(const int32_t* devices, int32_t n) {
     return guarded([&] {

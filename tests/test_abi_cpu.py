@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(_lib.EXPORTS)
-    assert L.fsx_version() >= 100
+    assert L.fsx_version() == 200
 
 
 def test_library_is_sm100a():
