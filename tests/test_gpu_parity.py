@@ -610,9 +610,11 @@ def test_cfg5_protocol(orc):
             # residue exceeds 1e-6 max|real| (proj/src/periodic.cpp:60-63) --
             # measured at n = 2^16; the real-to-complex GPU path has no
             # imaginary part and stays close to the truth
+            print(f"cfg5 protocol n={n}: GPU vs truth {e_gpu:.3e} (fp64 oracle raises NumericError)")
             assert e_gpu <= 1e-2, (n, e_gpu)
             continue
         e_orc = rel_l2(want, truth)
+        print(f"cfg5 protocol n={n}: GPU vs truth {e_gpu:.3e}, fp64 oracle vs truth {e_orc:.3e}")
         assert e_gpu <= max(1e-12, 1.5 * e_orc), (n, e_gpu, e_orc)
 
 
