@@ -10,7 +10,7 @@ PIPE_O = $(CSRC)/fsx_pipe.o
 
 all: $(LIB) oracle
 
-$(CSRC)/fsx_kernels.o: $(CSRC)/fsx_kernels.cu $(CSRC)/fsx_kernels.h $(CSRC)/fsx_device.cuh $(CSRC)/fsx_spectral.cuh
+$(CSRC)/fsx_kernels.o: $(CSRC)/fsx_kernels.cu $(CSRC)/fsx_kernels.h $(CSRC)/fsx_device.cuh $(CSRC)/fsx_spectral.cuh $(CSRC)/fsx_async.cuh
 	$(NVCC) $(NVFLAGS) -c $< -o $@ > build_ptxas.log 2>&1 || (cat build_ptxas.log; false)
 
 $(CSRC)/fsx_pipe.o: $(CSRC)/fsx_pipe.cu $(CSRC)/fsx_kernels.h $(CSRC)/fsx_device.cuh $(CSRC)/fsx_spectral.cuh $(CSRC)/fsx_async.cuh
