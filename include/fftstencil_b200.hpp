@@ -224,6 +224,32 @@ inline FieldGrid solve_periodic_implicit(const StencilKernel& q, const StencilKe
     return out;
 }
 
+// One recursion level's slab solves in one call (fsx_solve_periodic_slabs):
+// the 2d face slabs rb_run hands to solve_periodic_cached one after another
+// (proj/src/aperiodic.cpp:224-228,240-244); shapes may differ, equal shapes
+// are stacked into one batched plan.  Same results as the sequential calls.
+inline std::vector<FieldGrid> solve_periodic_slabs(const std::vector<FieldGrid>& slabs, const StencilKernel& k,
+                                                   std::uint64_t T, SpectrumCache* cache = nullptr,
+                                                   StageTimings* st = nullptr) {
+    std::vector<FieldGrid> out;
+    out.reserve(slabs.size());
+    std::vector<fsx_shape> shapes;
+    std::vector<const double*> ins;
+    std::vector<double*> outs;
+    for (const FieldGrid& g : slabs) {
+        out.emplace_back(g.shape);
+        shapes.push_back(g.shape.c());
+        ins.push_back(g.data.data());
+    }
+    for (FieldGrid& g : out) outs.push_back(g.data.data());
+    auto kv = k.c();
+    fsx_stage_timings t = detail::to_c(st);
+    check(fsx_solve_periodic_slabs((int64_t)slabs.size(), shapes.data(), ins.data(), &kv.k, T,
+                                   cache ? cache->handle() : nullptr, outs.data(), nullptr, st ? &t : nullptr));
+    detail::from_c(t, st);
+    return out;
+}
+
 // fp32 storage mode (no reference counterpart: the reference is fp64 only):
 // float cells in and out, fp64 arithmetic inside (fsx_solve_periodic_f32).
 inline std::vector<float> solve_periodic_f32(const GridShape& shape, const std::vector<float>& a0,

@@ -101,6 +101,21 @@ int main(int argc, char** argv) {
         }
         CHECK(std::sqrt(e2 / n2) <= 1e-12);
         CHECK(std::sqrt(e3 / n3) <= 1e-12);
+        // one recursion level's face slabs (different shapes) in one call =
+        // the sequential solve_periodic_cached calls, bit for bit
+        std::vector<FieldGrid> level;
+        for (int ax = 0; ax < 2; ++ax)
+            for (int side = 0; side < 2; ++side) {
+                FieldGrid sl(GridShape(ax == 0 ? std::vector<Index>{12, 128} : std::vector<Index>{64, 12}));
+                for (size_t i = 0; i < sl.data.size(); ++i) sl.data[i] = std::sin(0.3 * i + ax + 2 * side);
+                level.push_back(sl);
+            }
+        SpectrumCache c1, c2;
+        StageTimings bst;
+        const std::vector<FieldGrid> batched = solve_periodic_slabs(level, k2, 7, &c1, &bst);
+        CHECK(batched.size() == level.size());
+        CHECK(bst.boundary_recursion > 0);
+        for (size_t i = 0; i < level.size(); ++i) CHECK(batched[i].data == solve_periodic_cached(level[i], k2, 7, c2).data);
     }
     std::printf("%s: %d failure(s)\n", gpu ? "gpu" : "cpu", failures);
     return failures ? 1 : 0;
