@@ -7,7 +7,9 @@
 //      loads half of the rows of BOTH columns (64 KB), then swaps 32 KB with
 //      CTA (1 - j, h) over DSMEM (st.async, receiver-side mbarrier) so it holds
 //      one column's rows, and the reverse before its 32-byte-row store;
+//   A2 as A with half the rows read by the threads (LDG.128) instead of TMA;
 //   C  two adjacent columns per CTA, 32-byte rows, 128 KB tile (1 CTA/SM).
+// Measured (B200): A 304 us (3.5 TB/s), A2 354 us, B 336 us, C 236 us (4.6 TB/s).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I../../paper_2105_06676_b200/csrc tma_cluster.cu -o tma_cluster
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -125,6 +127,45 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 2) k_b(const __
     }
 }
 
+// A2: as A, but only the first half of the rows by TMA; the second half is
+// read by the threads themselves (LDG.128, one 16-byte element each, the
+// values a thread would own in registers): does a second path raise the
+// 16-byte-row request rate?
+__global__ void __launch_bounds__(256, 2) k_a2(const __grid_constant__ CUtensorMap map, const double2* __restrict__ H,
+                                               int ncols, long long P) {
+    extern __shared__ __align__(128) double2 tile[];
+    __shared__ __align__(8) unsigned long long bar;
+    const int c = blockIdx.x % ncols, h = blockIdx.x / ncols;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_init_fence();
+        mbar_expect_tx(&bar, 2048 * 16);
+        for (int b = 0; b < 8; ++b) tma_load_3d(tile + b * 256, &map, 2 * c, h * 4096 + b * 256, 0, &bar);
+    }
+    double2 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __ldg(H + (long long)(h * 4096 + 2048 + threadIdx.x + 256 * q) * P + c);
+    __syncthreads();
+    mbar_wait(&bar, 0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        v[q].x += 1.0;
+        tile[2048 + threadIdx.x + 256 * q] = v[q];
+    }
+    for (int i = threadIdx.x; i < 2048; i += 256) {
+        double2 u = tile[i];
+        u.x += 1.0;
+        tile[i] = u;
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 16; ++b) tma_store_3d(&map, tile + b * 256, 2 * c, h * 4096 + b * 256, 0);
+        bulk_commit();
+        bulk_wait_read0();
+    }
+}
+
 // C: two columns x 4096 rows per CTA (128 KB), 32-byte rows
 __global__ void __launch_bounds__(512, 1) k_c(const __grid_constant__ CUtensorMap map2, int npair) {
     extern __shared__ __align__(128) double2 tile[];
@@ -203,6 +244,8 @@ int main() {
     const size_t sa = 96 * 1024;  // the shipped kernel's 64 KB tile + 32 KB exchange landing (2 CTAs/SM)
     cudaFuncSetAttribute(k_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa);
     timeit("A  16 B rows, 64 KB tile/CTA, 2 CTAs/SM", [&] { k_a<<<2 * ncols, 256, sa>>>(m1, ncols); }, bytes);
+    cudaFuncSetAttribute(k_a2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa);
+    timeit("A2 16 B rows, half TMA / half per-thread LDG", [&] { k_a2<<<2 * ncols, 256, sa>>>(m1, H, ncols, P); }, bytes);
     const size_t sb = 96 * 1024;
     cudaFuncSetAttribute(k_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
     timeit("B  32 B rows, 4-CTA cluster + 2 DSMEM swaps", [&] { k_b<<<2 * ncols, 256, sb>>>(m2); }, bytes);
