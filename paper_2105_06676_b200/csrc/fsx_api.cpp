@@ -15,6 +15,7 @@
 //   3  general: complex promotion, per-axis passes (pow2 <= 8192 in one CTA,
 //      pow2 up to 2^26 as a four-step split, other lengths by direct DFT),
 //      m x m spectral kernel, inverse passes, real part + residue scan.
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -847,6 +848,23 @@ fsx::RowPairArgs rowpair_args(const Plan& p, const Taps& taps, u64 T, double2* z
     }
     a.ntaps = j;
     a.real = symmetric_taps(taps) ? 1 : 0;
+    if (a.real && a.mode == 1) {
+        // real block symbol B(0) + sum_{o>0} (B(o) + B(-o)) cos(2 pi k o / N): the
+        // +-o taps folded into one cosine term each (one phase read and one
+        // fma per entry per |o|; cfg5's three taps become two)
+        std::map<int, std::array<double, 4>> fold;
+        for (int t = 0; t < a.ntaps; ++t) {
+            auto& b = fold[a.tap_off[t] < 0 ? -a.tap_off[t] : a.tap_off[t]];
+            for (int i = 0; i < 4; ++i) b[i] += a.tap_b[t][i];
+        }
+        j = 0;
+        for (const auto& kv : fold) {
+            a.tap_off[j] = kv.first;
+            for (int i = 0; i < 4; ++i) a.tap_b[j][i] = kv.second[i];
+            ++j;
+        }
+        a.ntaps = j;
+    }
     a.row_split = p.N1b;
     return a;
 }

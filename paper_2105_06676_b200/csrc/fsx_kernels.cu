@@ -482,7 +482,7 @@ __device__ __forceinline__ void pair_mode0_real_x4(const RowPairArgs& a, double2
         wk[i] = phase_at(a.wk, k[i]);
         x[i] = x[4 + i] = 0.0;
     }
-    int last = 0;  // cos is even in o: offset 0 reads nothing, +-o share one read (see real_block_symbol)
+    int last = 0;  // cos is even in o: offset 0 reads nothing, +-o share one read
     double lastc[4] = {1.0, 1.0, 1.0, 1.0};
     for (int j = 0; j < a.ntaps; ++j) {
         const int o = a.tap_off[j], ao = o < 0 ? -o : o;
@@ -516,43 +516,105 @@ __device__ __forceinline__ void pair_mode0_real_x4(const RowPairArgs& a, double2
     }
 }
 
+// Real 2x2 symbol power by Cayley-Hamilton, NX independent chains.
+// A^n = p_n A + q_n I (A^2 = t A - d I, t = trace, d = det), tracked as
+// (p_n, tr_n = trace A^n, d^n) by left-to-right binary exponentiation:
+//   A^2n  : p <- p tr,             tr <- tr^2 - 2 d^n,      d^n <- (d^n)^2
+//   A^n+1 : p' = (p t + tr) / 2,   tr <- p' t - 2 d p,      d^n <- d^n d
+// and q_T = (tr_T - p_T t) / 2 at the end.  4 ops per squaring and 5 per
+// multiply against the matrix loop's 6 and 8 (proj/src/spectrum.cpp:66-82);
+// for det A = 1 (area-preserving schemes: cfg5's leapfrog) d^n stays 1 and a
+// squaring is 2 ops -- the same arithmetic as the general branch, so the fast
+// branch changes no bit.  Accuracy: near a double eigenvalue (the wave
+// equation's low frequencies) the matrix product cancels n^2-sized terms
+// while tr_n stays bounded; against an exact (60-digit) power of the same
+// fp64 symbol the worst relative error at cfg5 (N = 2^26, T = 1e6) is 6.4e-5
+// here and 12 for the matrix loop (scripts/pow_accuracy.py).
+template <int NX>
+__device__ __forceinline__ void pow_real2_ch(const double (&l)[NX][4], u64 T, double (&acc)[NX][4]) {
+    if (T == 0) {
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            acc[i][0] = acc[i][3] = 1.0;
+            acc[i][1] = acc[i][2] = 0.0;
+        }
+        return;
+    }
+    double t[NX], m2d[NX], p[NX], tr[NX], dn[NX];
+    bool unit = true;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+        t[i] = l[i][0] + l[i][3];
+        const double d = fma(l[i][0], l[i][3], -(l[i][1] * l[i][2]));
+        m2d[i] = -2.0 * d;
+        p[i] = 1.0;
+        tr[i] = t[i];
+        dn[i] = d;
+        unit = unit && d == 1.0;
+    }
+    const int top = 63 - __clzll((long long)T);
+    if (unit) {
+#pragma unroll 1
+        for (int b = top - 1; b >= 0; --b) {
+#pragma unroll
+            for (int i = 0; i < NX; ++i) {
+                p[i] *= tr[i];
+                tr[i] = fma(tr[i], tr[i], -2.0);
+            }
+            if ((T >> b) & 1) {
+#pragma unroll
+                for (int i = 0; i < NX; ++i) {
+                    const double pn = 0.5 * fma(p[i], t[i], tr[i]);
+                    tr[i] = fma(pn, t[i], -2.0 * p[i]);
+                    p[i] = pn;
+                }
+            }
+        }
+    } else {
+#pragma unroll 1
+        for (int b = top - 1; b >= 0; --b) {
+#pragma unroll
+            for (int i = 0; i < NX; ++i) {
+                p[i] *= tr[i];
+                tr[i] = fma(tr[i], tr[i], -2.0 * dn[i]);
+                dn[i] *= dn[i];
+            }
+            if ((T >> b) & 1) {
+#pragma unroll
+                for (int i = 0; i < NX; ++i) {
+                    const double pn = 0.5 * fma(p[i], t[i], tr[i]);
+                    tr[i] = fma(pn, t[i], m2d[i] * p[i]);
+                    p[i] = pn;
+                    dn[i] *= -0.5 * m2d[i];
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+        const double q = 0.5 * fma(-p[i], t[i], tr[i]);
+        acc[i][0] = fma(p[i], l[i][0], q);
+        acc[i][1] = p[i] * l[i][1];
+        acc[i][2] = p[i] * l[i][2];
+        acc[i][3] = fma(p[i], l[i][3], q);
+    }
+}
+
 __device__ __forceinline__ void pair_mode1(const RowPairArgs& a, double2& zk, double2& zp, i64 k, i64 N) {
     const double2 cz = cconj(zp);
     const double2 u = cscale(cadd(zk, cz), 0.5);
     const double2 vv = cscale(cmul_si<-1>(csub(zk, cz)), 0.5);
     if (a.real) {
         // symmetric block stencil: lam(k) = sum B cos(2 pi k o / N) is a real 2x2
-        // matrix; same binary-exponentiation loop in real arithmetic
-        double l00 = 0, l01 = 0, l10 = 0, l11 = 0;
+        // matrix, raised by the Cayley-Hamilton chain in real arithmetic
+        double l[1][4] = {{0.0, 0.0, 0.0, 0.0}}, A[1][4];
         for (int j = 0; j < a.ntaps; ++j) {
             const double c = phase_at(a.wk, modp2(k * (i64)a.tap_off[j], N)).x;
-            l00 = fma(a.tap_b[j][0], c, l00);
-            l01 = fma(a.tap_b[j][1], c, l01);
-            l10 = fma(a.tap_b[j][2], c, l10);
-            l11 = fma(a.tap_b[j][3], c, l11);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) l[0][e] = fma(a.tap_b[j][e], c, l[0][e]);
         }
-        double a00 = 1, a01 = 0, a10 = 0, a11 = 1;
-        u64 t = a.T;
-        while (t) {
-            if (t & 1) {
-                const double b00 = fma(a00, l00, a01 * l10), b01 = fma(a00, l01, a01 * l11);
-                const double b10 = fma(a10, l00, a11 * l10), b11 = fma(a10, l01, a11 * l11);
-                a00 = b00;
-                a01 = b01;
-                a10 = b10;
-                a11 = b11;
-            }
-            t >>= 1;
-            if (t) {
-                // L^2 = [[l00^2 + p, l01 tr], [l10 tr, l11^2 + p]], p = l01 l10, tr = l00 + l11
-                const double pp = l01 * l10, tr = l00 + l11;
-                const double s00 = fma(l00, l00, pp), s11 = fma(l11, l11, pp);
-                l01 *= tr;
-                l10 *= tr;
-                l00 = s00;
-                l11 = s11;
-            }
-        }
+        pow_real2_ch<1>(l, a.T, A);
+        const double a00 = A[0][0], a01 = A[0][1], a10 = A[0][2], a11 = A[0][3];
         const double sc = a.scale;
         const double2 u2 = make_double2(sc * fma(a00, u.x, a01 * vv.x), sc * fma(a00, u.y, a01 * vv.y));
         const double2 v2 = make_double2(sc * fma(a10, u.x, a11 * vv.x), sc * fma(a10, u.y, a11 * vv.y));
@@ -578,24 +640,15 @@ __device__ __forceinline__ void pair_mode1(const RowPairArgs& a, double2& zk, do
     zp = cadd(cconj(u2), cmul_si<+1>(cconj(v2)));
 }
 
-// Real 2x2 symbols of two frequencies at once: the two binary-exponentiation
-// chains are independent, so interleaving them doubles the FP64 ILP of the
-// power (the row-pair pass of cfg5 is bound by this loop at T = 1e6).
-// cos(2 pi k o / N) is even in o: offset 0 needs no table read, and +-o share
-// one (the taps come in sorted order, so the two of a pair are looked up by
-// |o| from a one-entry cache of the last nonzero |o|; a symmetric 3-point
-// stencil reads one two-level phase per frequency instead of three).
+// Real 2x2 block symbols, NX frequencies per call (independent power chains:
+// the row-pair pass of cfg5 is bound by this arithmetic at T = 1e6).  The host
+// folds the +-o taps of a symmetric stencil into one cosine term per |o|
+// (rowpair_args), so offset 0 needs no table read and every other term one.
 __device__ __forceinline__ void real_block_symbol(const RowPairArgs& a, i64 k, i64 N, double (&l)[4]) {
     l[0] = l[1] = l[2] = l[3] = 0.0;
-    int last = 0;
-    double lastc = 1.0;
     for (int j = 0; j < a.ntaps; ++j) {
-        const int o = a.tap_off[j] < 0 ? -a.tap_off[j] : a.tap_off[j];
-        if (o != 0 && o != last) {
-            lastc = phase_at(a.wk, modp2(k * (i64)o, N)).x;
-            last = o;
-        }
-        const double c = o == 0 ? 1.0 : lastc;
+        const int o = a.tap_off[j];
+        const double c = o == 0 ? 1.0 : phase_at(a.wk, modp2(k * (i64)o, N)).x;
 #pragma unroll
         for (int e = 0; e < 4; ++e) l[e] = fma(a.tap_b[j][e], c, l[e]);
     }
@@ -606,39 +659,8 @@ __device__ __forceinline__ void pair_mode1_real_xn(const RowPairArgs& a, double2
                                                    const i64 (&k)[NX], i64 N) {
     double l[NX][4], acc[NX][4];
 #pragma unroll
-    for (int i = 0; i < NX; ++i) {
-        real_block_symbol(a, k[i], N, l[i]);
-        acc[i][0] = 1.0;
-        acc[i][1] = 0.0;
-        acc[i][2] = 0.0;
-        acc[i][3] = 1.0;
-    }
-    u64 t = a.T;
-    while (t) {
-        if (t & 1) {
-#pragma unroll
-            for (int i = 0; i < NX; ++i) {
-                const double b00 = fma(acc[i][0], l[i][0], acc[i][1] * l[i][2]), b01 = fma(acc[i][0], l[i][1], acc[i][1] * l[i][3]);
-                const double b10 = fma(acc[i][2], l[i][0], acc[i][3] * l[i][2]), b11 = fma(acc[i][2], l[i][1], acc[i][3] * l[i][3]);
-                acc[i][0] = b00;
-                acc[i][1] = b01;
-                acc[i][2] = b10;
-                acc[i][3] = b11;
-            }
-        }
-        t >>= 1;
-        if (t) {
-#pragma unroll
-            for (int i = 0; i < NX; ++i) {
-                const double pp = l[i][1] * l[i][2], tr = l[i][0] + l[i][3];
-                const double s00 = fma(l[i][0], l[i][0], pp), s11 = fma(l[i][3], l[i][3], pp);
-                l[i][1] *= tr;
-                l[i][2] *= tr;
-                l[i][0] = s00;
-                l[i][3] = s11;
-            }
-        }
-    }
+    for (int i = 0; i < NX; ++i) real_block_symbol(a, k[i], N, l[i]);
+    pow_real2_ch<NX>(l, a.T, acc);
     const double sc = a.scale;
 #pragma unroll
     for (int i = 0; i < NX; ++i) {
