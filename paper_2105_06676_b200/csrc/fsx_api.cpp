@@ -1023,7 +1023,7 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
         const bool f32c = (fin || fout) && !q && sym.real && p.tma0 && !p.halves && p.ax0.n <= 4096 &&
                           fsx::f32_compute_enabled();
         if (f32c) FSX_CK(fsx::launch_cols_tma_f32(p.map0, ax0, 2, sym, tw, dev.tw_all_f.as<float2>(), st));
-        else if (p.halves) FSX_CK(fsx::launch_fused_halves(p.map2, ax0, sym, tw, st));
+        else if (p.halves) FSX_CK(fsx::launch_fused_halves(p.map2, ax0, sym, tw, st, H));
         else if (p.tma0) FSX_CK(fsx::launch_cols_tma(p.map0, ax0, 2, sym, tw, st));
         else FSX_CK(fsx::launch_fused_r2c(H, ax0, sym, tw, st));
         sp.mark();

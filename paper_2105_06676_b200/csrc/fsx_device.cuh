@@ -223,6 +223,88 @@ struct Dft<16, SIGN> {
     __device__ __forceinline__ static void run(CT* v) { DftCT<4, 4, SIGN>::run(v); }
 };
 
+// ------------------------------------------------------------------ radix-16 with the pass twiddles folded in
+// X[k] = sum_u a[u] w^u W16^(u k), w = the pass twiddle of this item (the
+// table value for SIGN = -1, its conjugate for +1), as four radix-2 layers in
+// which the twiddle rides on the butterfly: with u = u' + 8 b,
+//   X[p + 2 k'] = sum_u' (w W16^p)^u' W8^(u' k') (a[u'] + (-1)^p w^8 a[u' + 8]),
+// an 8-point transform of the same form with base twiddle w W16^p, and so on.
+// Layer 1 multiplies by w^8, layer 2 by w^4 (SIGN i)^p, layer 3 by
+// w^2 W8^p (SIGN i)^p', layer 4 by w W16^(p + 2 p') (SIGN i)^p''.  Each
+// butterfly is s = a + m b (4 FMA), d = 2 a - s (2 FMA): 32 x 6 + 4 constant
+// products = 208 FP64 instructions against 264 for twiddles (15 products + 11
+// derived powers) followed by the plain transform.  Only w, w^2, w^4, w^8 are
+// needed -- the four values the gathered tables hold.  Output in natural order
+// (the bit reversal is a compile-time renaming).
+#ifndef FSX_FUSED16
+#define FSX_FUSED16 0  // 1: measured slower (cfg3 0.983 -> 1.017 ms, r04e): fewer FP64 instructions, longer FMA chains
+#endif
+template <class CT>
+__device__ __forceinline__ void bfly_tw(CT& a, CT& b, typename CScalar<CT>::T mx, typename CScalar<CT>::T my) {
+    using T = typename CScalar<CT>::T;
+    const T sx = fma(mx, b.x, fma(-my, b.y, a.x));
+    const T sy = fma(mx, b.y, fma(my, b.x, a.y));
+    b = CScalar<CT>::make(fma((T)2, a.x, -sx), fma((T)2, a.y, -sy));
+    a = CScalar<CT>::make(sx, sy);
+}
+
+template <int SIGN, class CT>
+__device__ __forceinline__ void dft16_tw_fused(CT (&a)[16], CT w1, CT w2, CT w4, CT w8) {
+    if constexpr (SIGN > 0) {
+        w1 = cconj(w1);
+        w2 = cconj(w2);
+        w4 = cconj(w4);
+        w8 = cconj(w8);
+    }
+    // layer 1: (u, u + 8), multiplier w^8
+#pragma unroll
+    for (int u = 0; u < 8; ++u) bfly_tw(a[u], a[u + 8], w8.x, w8.y);
+    // layer 2: group p, (u, u + 4), multiplier w^4 (SIGN i)^p
+    {
+        const CT m1 = cmul_si<SIGN>(w4);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            bfly_tw(a[u], a[u + 4], w4.x, w4.y);
+            bfly_tw(a[8 + u], a[12 + u], m1.x, m1.y);
+        }
+    }
+    // layer 3: group (p, p'), (u, u + 2), multiplier w^2 W8^p (SIGN i)^p'
+    {
+        const CT m0 = w2, m1 = cmul_const<1, 8, SIGN>(w2);
+        const CT m0i = cmul_si<SIGN>(m0), m1i = cmul_si<SIGN>(m1);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            bfly_tw(a[u], a[u + 2], m0.x, m0.y);
+            bfly_tw(a[4 + u], a[6 + u], m0i.x, m0i.y);
+            bfly_tw(a[8 + u], a[10 + u], m1.x, m1.y);
+            bfly_tw(a[12 + u], a[14 + u], m1i.x, m1i.y);
+        }
+    }
+    // layer 4: group (p, p', p''), (0, 1), multiplier w W16^(p + 2 p') (SIGN i)^p''
+    {
+        const CT n0 = w1, n1 = cmul_const<1, 16, SIGN>(w1), n2 = cmul_const<2, 16, SIGN>(w1),
+                 n3 = cmul_const<3, 16, SIGN>(w1);
+        const CT n0i = cmul_si<SIGN>(n0), n1i = cmul_si<SIGN>(n1), n2i = cmul_si<SIGN>(n2), n3i = cmul_si<SIGN>(n3);
+        // index 8 p + 4 p' + 2 p'': j = p + 2 p'
+        bfly_tw(a[0], a[1], n0.x, n0.y);
+        bfly_tw(a[2], a[3], n0i.x, n0i.y);
+        bfly_tw(a[4], a[5], n2.x, n2.y);
+        bfly_tw(a[6], a[7], n2i.x, n2i.y);
+        bfly_tw(a[8], a[9], n1.x, n1.y);
+        bfly_tw(a[10], a[11], n1i.x, n1i.y);
+        bfly_tw(a[12], a[13], n3.x, n3.y);
+        bfly_tw(a[14], a[15], n3i.x, n3i.y);
+    }
+    // position 8 p + 4 p' + 2 p'' + p''' holds X[p + 2 p' + 4 p'' + 8 p''']
+    CT t;
+    t = a[1], a[1] = a[8], a[8] = t;
+    t = a[2], a[2] = a[4], a[4] = t;
+    t = a[3], a[3] = a[12], a[12] = t;
+    t = a[5], a[5] = a[10], a[10] = t;
+    t = a[7], a[7] = a[14], a[14] = t;
+    t = a[11], a[11] = a[13], a[13] = t;
+}
+
 // ------------------------------------------------------------------ smem swizzle
 // 16-byte elements: 8 per 128-byte bank row.  XOR the low 3 bits with bits
 // 3..5 and 4..6 so the Stockham scatter strides 2, 4, 8, 16 and the unit
@@ -411,13 +493,24 @@ struct LineFFT {
             CT a[r];
 #pragma unroll
             for (int u = 0; u < r; ++u) a[u] = v[i + u * C];
-            if constexpr (INC) {
-                tw16_apply<S>(a, t, tw, pre);
-            } else if constexpr (Ns > 1) {
+            if constexpr (INC && FSX_FUSED16 != 0) {
+                CT b[4];
+                if (pre) {
 #pragma unroll
-                for (int u = 1; u < r; ++u) a[u] = ctw<SIGN>(a[u], w[i * r + u]);
+                    for (int q = 0; q < 4; ++q) b[q] = pre[q];
+                } else {
+                    tw16_base<S>(t, tw, b);
+                }
+                dft16_tw_fused<SIGN>(a, b[0], b[1], b[2], b[3]);
+            } else {
+                if constexpr (INC) {
+                    tw16_apply<S>(a, t, tw, pre);
+                } else if constexpr (Ns > 1) {
+#pragma unroll
+                    for (int u = 1; u < r; ++u) a[u] = ctw<SIGN>(a[u], w[i * r + u]);
+                }
+                Dft<r, SIGN>::run(a);
             }
-            Dft<r, SIGN>::run(a);
 #pragma unroll
             for (int u = 0; u < r; ++u) v[i + u * C] = a[u];
         }

@@ -286,8 +286,9 @@ cudaError_t launch_axis_tma(const double2* in, double2* out, const AxisGeom& g, 
 // 8192-point fused pass as two parity halves (fsx_tma.cu)
 bool halves_ok(const AxisGeom& g);
 int make_cols_tensor_map_par(void* out_map, void* base, const AxisGeom& g);
+// base: the half spectrum the map describes (enables the optional L2 strip prefetch), or nullptr
 cudaError_t launch_fused_halves(const void* tensor_map2, const AxisGeom& g, const FusedSymbol& sym,
-                                const double2* tw_all, cudaStream_t s);
+                                const double2* tw_all, cudaStream_t s, const double2* base = nullptr);
 // TMA column passes (fsx_tma.cu); tensor_map points at a 64-byte aligned CUtensorMap
 bool tma_cols_ok(i64 N);
 int tma_cols_width(i64 N);  // columns per TMA tile (the box width the host encodes)

@@ -684,7 +684,8 @@ __device__ __forceinline__ void spectral_pair8192(double2 (&u)[16], int th, int 
 // barrier initialisation (a release cluster barrier per exchange costs a
 // GPU-scope fence and an L1 invalidation: ~20 % of the stall samples).
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
-k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all) {
+k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol sym, const double2* __restrict__ tw_all,
+             const double2* __restrict__ pf_base, int pf_dist) {
     constexpr int N = 8192, NH = 4096, TH = 256;
 #ifndef FSX_F8192_LPF
 #define FSX_F8192_LPF 1  // cfg3: fused 0.5829 -> 0.5800 ms (r02v)
@@ -718,6 +719,15 @@ k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol s
         for (int b = 0; b < NH / 256; ++b) tma_load_4d(tile + b * 256, &map2, (int)(2 * c), (int)h, b * 256, 0, &bar);
     }
     cluster_arrive_relaxed();  // publishes the barrier initialisation (fence above) to the peer
+    // L2 prefetch in full 128-byte lines: every eighth pair pulls the strip of
+    // eight columns pf_dist ahead (the rows of its parity) into L2, so the
+    // 16-byte-row TMA loads of the pairs that follow are L2 hits and DRAM sees
+    // whole lines instead of one 32-byte sector per row and column pair.
+    if (pf_base != nullptr && (c & 7) == 0 && c + pf_dist < g.ncols) {
+        const double2* a = pf_base + (i64)(2 * th + (int)h) * g.inner + (c + pf_dist);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) l2_prefetch_bulk(a + (i64)(512 * q) * g.inner, 128u);
+    }
     for (int j = th; j < sym.ntaps; j += TH) tapterm[j] = tap_term(sym, tw_all, j, kx, ky);
     __syncthreads();
     for (int gi = th; gi < sym.ngroups; gi += TH) {
@@ -1117,8 +1127,18 @@ static int fused_halves() {
 
 bool halves_ok(const AxisGeom& g) { return g.n == 8192 && g.outer == 1 && fused_halves(); }
 
+// FSX_F8192_PFD: L2 prefetch distance of k_fused8192c in columns (a multiple of 8; 0: off)
+static int f8192_pfd() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_F8192_PFD");
+        v = e ? atoi(e) & ~7 : 0;
+    }
+    return v;
+}
+
 cudaError_t launch_fused_halves(const void* tensor_map2, const AxisGeom& g, const FusedSymbol& sym,
-                                const double2* tw, cudaStream_t s) {
+                                const double2* tw, cudaStream_t s, const double2* base) {
     const CUtensorMap& map = *reinterpret_cast<const CUtensorMap*>(tensor_map2);
     if (f8192_kind() == 2) {
         // one persistent pair per SM (two CTAs of 256 threads per SM)
@@ -1136,7 +1156,9 @@ cudaError_t launch_fused_halves(const void* tensor_map2, const AxisGeom& g, cons
     if (f8192_pair()) {
         const size_t smem2 = (4096 + 2048) * sizeof(double2);
         kernel_prepare((const void*)k_fused8192c, smem2);
-        return launch_pdl(k_fused8192c, dim3((unsigned)(2 * g.ncols)), dim3(256), smem2, s, map, g, sym, tw);
+        const int pfd = base != nullptr && g.inner % 8 == 0 ? f8192_pfd() : 0;
+        return launch_pdl(k_fused8192c, dim3((unsigned)(2 * g.ncols)), dim3(256), smem2, s, map, g, sym, tw,
+                          pfd > 0 ? base : (const double2*)nullptr, pfd);
     }
     const size_t smem = 8192 * sizeof(double2);
     kernel_prepare((const void*)k_fused8192h, smem);
