@@ -19,8 +19,10 @@ metric is quoted on at 1/2/4/8 GPUs and the largest 2D one that fits a B200;
 `roofline` the fused spectral kernel (k_cols_tma for plan 1): its
          algorithmic bytes / its CUDA-event duration (separate steps with the
          library's stage events on the solve stream).
-`cpu_baseline` the reference path (oracle restatement, test infrastructure)
-         timed on this host, rank 0 at N = 1 only.
+`cpu_baseline` the reference's CPU path timed on this host, rank 0 at N = 1
+         only: oracle/_ref (the reference's own sources compiled against a
+         stand-in for the absent Eigen3, kind "reference") when built, else
+         the oracle restatement (kind "port"); both are test infrastructure.
 
 Multi-GPU (torchrun, one rank per GPU): 2D/3D configs are slab-decomposed
 over the ranks (strong scaling; two NCCL all-to-alls per step, reported
@@ -206,6 +208,24 @@ def oracle_peak_bytes(cells, m):
     return cells * (96 if m == 1 else 32 * m * m + 80 * m)
 
 
+def cpu_impl():
+    """The CPU implementation the baseline legs time: oracle/_ref (the
+    reference's own periodic-path sources compiled against oracle/eigen_shim,
+    `kind` "reference") when it was built, else the oracle restatement
+    ("port").  Returns (binding module, kind, one-line description)."""
+    from oracle import ref as refmod
+
+    if refmod.available() or refmod.build():
+        return (refmod.module(), "reference",
+                "oracle/_ref: the reference's own fft/spectrum/periodic/parallel/grid/kernel sources, unmodified, "
+                "built with its flags (-O3 -DNDEBUG, C++20) against a stand-in for the absent Eigen3")
+    from oracle import oracle as orc
+
+    orc.build()
+    return (orc, "port", "oracle (CPU restatement of the reference solve_periodic; radix-2/Bluestein FFT, "
+            "FFT-of-generator spectrum, std::thread chunks)")
+
+
 def cpu_sample(cfg, budget_s=None):
     """The CPU reference's workload: the FULL configured grid whenever the
     host has the RAM for the reference pipeline (and, if `budget_s` is given,
@@ -220,8 +240,7 @@ def cpu_sample(cfg, budget_s=None):
     use = dims
     est = None
     if budget_s is not None:
-        from oracle import oracle as orc
-
+        orc = cpu_impl()[0]
         small = [max(8, d // (16 if len(dims) > 1 else 64)) for d in dims]
         sc = cfg.scaled(small)
         off, blk = sc.kernel().arrays()
@@ -241,18 +260,16 @@ def cpu_sample(cfg, budget_s=None):
 
 
 def run_reference(args, cfg):
-    """--impl reference: the reference's CPU path (the oracle restatement of
-    proj/src/periodic.cpp; the reference itself cannot be built here, DESIGN
-    section 1) on all host threads, on the SAME grid as our arm (no sample
-    shrink unless the host lacks the RAM), K timed solves after W warm-ups."""
+    """--impl reference: the reference's CPU path (cpu_impl(): its own sources
+    from oracle/_ref when built, else the restatement) on all host threads, on
+    the SAME grid as our arm (no sample shrink unless the host lacks the RAM),
+    K timed solves after W warm-ups."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     import numpy as np
 
-    from oracle import oracle as orc
-
-    orc.build()
+    orc, kind, what = cpu_impl()
     cores = orc.thread_count()
     sample, off, blk, a = cpu_sample(cfg)
     for _ in range(args.warmup):
@@ -264,8 +281,7 @@ def run_reference(args, cfg):
         times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
     value = sample.cells() * sample.T / t
-    desc = (f"oracle (CPU restatement of the reference solve_periodic; radix-2/Bluestein FFT, FFT-of-generator "
-            f"spectrum, std::thread chunks) on grid {sample.dims} x{sample.fields}, T={sample.T}, "
+    desc = (f"{what} on grid {sample.dims} x{sample.fields}, T={sample.T}, "
             f"{cores} threads on {cpu_model()}; mean of {args.steps} solves (best {min(times):.3f} s)"
             + ("" if sample.dims == cfg.dims else f" (bounded sample of {cfg.dims}: host RAM)"))
     line = {
@@ -274,7 +290,7 @@ def run_reference(args, cfg):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (SplitMix64, reference init)",
         "config": {"workload": cfg.name + ": " + cfg.description, "grid": cfg.dims, "fields": cfg.fields,
                    "T": cfg.T, "sample_grid": sample.dims, "same_grid": sample.dims == cfg.dims},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc,
                          "cpu_model": cpu_model(), "best_s": min(times), "mean_s": t},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -413,9 +429,7 @@ def cpu_baseline(cfg):
     solves of the configured grid on all host threads (BASELINE.md section 2;
     a halved-grid sample only when the host lacks the RAM or one solve would
     exceed ~30 s by an N log N estimate), plus a 1-thread solve of a bounded sample."""
-    from oracle import oracle as orc
-
-    orc.build()
+    orc, kind, what = cpu_impl()
     cores = orc.thread_count()
     sample, off, blk, a = cpu_sample(cfg, budget_s=30.0)
     ts = []
@@ -434,9 +448,9 @@ def cpu_baseline(cfg):
     finally:
         orc.set_threads(0)
     return {
-        "value": sample.cells() * sample.T / tc, "unit": UNIT, "cores": cores, "kind": "port",
-        "cpu_model": cpu_model(),
-        "sample": f"best of 3 oracle solve_periodic on grid {sample.dims} x{sample.fields}, T={sample.T}, "
+        "value": sample.cells() * sample.T / tc, "unit": UNIT, "cores": cores, "kind": kind,
+        "cpu_model": cpu_model(), "impl": what,
+        "sample": f"best of 3 solve_periodic on grid {sample.dims} x{sample.fields}, T={sample.T}, "
                   f"{cores} threads ({', '.join(f'{x:.2f}' for x in ts)} s)"
                   + ("" if sample.dims == cfg.dims else f" (bounded sample of {cfg.dims})"),
         "one_thread": {"value": s1.cells() * s1.T / t1, "unit": UNIT, "cores": 1, "grid": s1.dims,

@@ -2,8 +2,8 @@
 // fftstencil ORACLE — TEST INFRASTRUCTURE, NOT PRODUCT CODE.
 //
 // A CPU restatement of the reference library's StencilFFT-P hot path
-// (/root/reference/proj, C++20 + Eigen; not buildable here: Eigen3 and
-// vendor/ are absent).  It follows the reference
+// (/root/reference/proj, C++20 + Eigen; its own build needs Eigen3 and
+// vendor/, both absent).  It follows the reference
 // algorithm for algorithm so that it can stand in for the reference both as
 // the parity checker and as the timed CPU baseline:
 //
@@ -21,7 +21,10 @@
 //     lambda^T (accuracy-parity criterion)             (proj/src/modal.cpp:13-145)
 //
 // It is pinned against the reference's own known-answer and property tests
-// (tests/golden/reference_known_answers.json, tests/test_oracle_cpu.py).
+// (tests/golden/reference_known_answers.json, tests/test_oracle_cpu.py) and,
+// bit for bit, against the reference's own sources compiled against a
+// stand-in for Eigen (oracle/_ref, `make -C oracle ref`;
+// tests/test_oracle_vs_ref_cpu.py, tests/golden/reference_outputs.npz).
 //
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 // `--impl reference` leg may load this library; the product path never does.

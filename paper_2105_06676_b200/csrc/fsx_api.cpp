@@ -623,7 +623,9 @@ Plan& get_plan(Device& dev, const Shape& s, const Taps& taps, int force_general,
             p->N2 = p->Mc;
         } else {
             const int b = ilog2(p->Mc);
-            const int b2 = std::min(12, (b + 1) / 2);
+            int b2 = std::min(12, (b + 1) / 2);
+            // FSX_N2LOG: row length 2^b2 of the four-step split (A/B of the split of small grids)
+            if (const char* e = getenv("FSX_N2LOG")) b2 = std::max(8, std::min(std::min(12, b - 1), atoi(e)));
             p->N2 = i64(1) << b2;
             p->N1 = p->Mc / p->N2;
         }
