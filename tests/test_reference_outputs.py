@@ -107,11 +107,20 @@ def test_gpu_matches_reference_library():
         m = cfg.fields
         off, blk = cfg.kernel().arrays()
         a0 = cfg.initial()
-        T = cfg.T if name != "cfg5" else 2000  # cfg5 at T = 1e6 is the truth protocol's job
+        T = cfg.T if name != "cfg5" else 2000  # cfg5 at T = 1e6 is the full truth protocol's job
         want = ref.solve_periodic(a0, dims, m, off, blk, T, vector=m > 1)
         g = fs.FieldGrid(fs.GridShape(dims, m), a0)
         got = (fs.solve_periodic_vector if m > 1 else fs.solve_periodic)(g, cfg.kernel(), T).data
         worst[name] = rel_l2(got, want)
+        if name == "cfg5":
+            # neutrally stable leapfrog symbol: two correct fp64 pipelines differ by more than 1e-10
+            # (SURVEY section 0.2), so both are measured against the long-double truth
+            from oracle import oracle as orc
+            truth = orc.solve_periodic_ld(a0, dims, m, off, blk, T)
+            e_ref, e_gpu = rel_l2(want, truth), rel_l2(got, truth)
+            print(f"cfg5 reduced, T={T}: reference vs truth {e_ref:.2e}, GPU vs truth {e_gpu:.2e}")
+            assert e_gpu <= max(1.5 * e_ref, 1e-10), (e_gpu, e_ref)
     print("GPU vs reference library (reduced BASELINE configs): " + ", ".join(f"{k} {v:.2e}" for k, v in worst.items()))
     for name, e in worst.items():
-        assert e <= (1e-10 if name != "cfg5" else 1e-8), (name, e)
+        if name != "cfg5":
+            assert e <= 1e-10, (name, e)
