@@ -809,6 +809,13 @@ i64 compute_kcut(const Plan& p, const Taps& taps, u64 T) {
     return 0;
 }
 
+// FSX_ZEROCOL=0: the fused pass evaluates the symbol of every column (A/B and the bitwise
+// test; read per solve so a test can flip it in-process)
+static bool zero_columns_enabled() {
+    const char* e = getenv("FSX_ZEROCOL");
+    return !e || atoi(e) != 0;
+}
+
 i64 plan_kcut(Plan& p, const Taps& taps, u64 T) {
     if (!(p.cut_valid && p.cut_T == T && p.cut_taps.map == taps.map)) {
         p.kcut = compute_kcut(p, taps, T);
@@ -1009,7 +1016,13 @@ void run_plan(Plan& p, Device& dev, const Taps& taps, const Taps* q, u64 T, cons
         if (fin) FSX_CK(fsx::launch_r2c_rows_f32(fin, H, p.rows, p.L, lay, tw, twf, st));
         else FSX_CK(fsx::launch_r2c_rows(d_a0, H, p.rows, p.L, lay, tw, st));
         fsx::StepTwiddle none;
-        const fsx::FusedSymbol sym = fused_symbol(p, taps, T, q, q ? p.qmax.as<unsigned long long>() : nullptr);
+        fsx::FusedSymbol sym = fused_symbol(p, taps, T, q, q ? p.qmax.as<unsigned long long>() : nullptr);
+        if (!q && zero_columns_enabled()) {
+            // columns whose multipliers all underflow to exactly 0: known from the host-side column
+            // bound (cached per taps and T), so the fused pass need not evaluate the symbol there
+            const i64 kz = plan_kcut(p, taps, T);
+            if (kz >= 0) sym.kzero = kz;
+        }
         fsx::FusedSymbol nosym;
         if (r == 3) {
             if (p.tma1 && twf && p.ax1.n <= 4096) FSX_CK(fsx::launch_cols_tma_f32(p.map1, p.ax1, 0, nosym, tw, twf, st));

@@ -76,6 +76,10 @@ struct FusedSymbol {
     double scale = 1.0;          // 1 / prod(dims)
     int real = 0;                // taps symmetric under o -> -o: lam is real
     double neg_mag2 = 0.0;       // |lam|^2 below this: |lam|^T < 2^-1100 (power skipped, 0)
+    // rank 2: every multiplier of a half-spectrum column kx > kzero is exactly 0 -- the host proved
+    // |lam(k0, kx)|^2 < neg_mag2 for every k0 (compute_kcut's column bound) -- so the fused pass
+    // takes 0 without evaluating the symbol (same bits as evaluating it); default: no such column
+    i64 kzero = 0x7fffffffffffffffLL;
     // implicit solve (solve_periodic_implicit): groups of the mass kernel Q
     // carry group_set = 1; lam = pinv(lamQ) * lamS with the pinv threshold
     // 1e-12 * max |lamQ| (*qmax_bits, filled by launch_fused_qmax first)

@@ -100,6 +100,17 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
     // them in tensor memory instead measured neutral.
     constexpr bool PRE = FUSED && C::PRE;
     double* mult = reinterpret_cast<double*>(tile + W * C::LSW);
+    // every multiplier of this warp's columns is a host-proved 0 (FusedSymbol::kzero); warp-uniform,
+    // because the power's short cut votes across the warp
+    // (evaluated where it is used, so that no flag stays live across the FFTs)
+    auto is_dead = [&]() -> bool {
+        // one-column tiles only: in the multi-column kernels (N < 4096; cfg4's 1024-point columns,
+        // where no column is provably 0 anyway) the extra branch costs spills (ptxas: 168 -> 448 B)
+        if constexpr (MODE != 2 || W != 1) return false;
+        i64 kx2 = c, ky2 = 0;
+        fused_col_freqs(sym, c, kx2, ky2);
+        return __all_sync(0xffffffffu, kx2 > sym.kzero);
+    };
     if constexpr (FUSED) {
         for (int j = t; j < sym.ntaps; j += C::TPL) tapterm[j][w] = tap_term(sym, tw_all, j, kx, ky);
     }
@@ -113,11 +124,17 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
         }
         __syncthreads();
         if (PRE && sym.real) {
-            double lam[C::R];
-            symbol_real<N, C::R, C::TPL, MODE == 4>(lam, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
-            pow_real_vec_skip<C::R, 4>(lam, sym.T, sym.neg_mag2);
+            if (is_dead()) {
+                const double z = 0.0 * sym.scale;
 #pragma unroll
-            for (int q = 0; q < C::R; ++q) mult[q * C::NT + threadIdx.x] = lam[q] * sym.scale;
+                for (int q = 0; q < C::R; ++q) mult[q * C::NT + threadIdx.x] = z;
+            } else {
+                double lam[C::R];
+                symbol_real<N, C::R, C::TPL, MODE == 4>(lam, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
+                pow_real_vec_skip<C::R, 4>(lam, sym.T, sym.neg_mag2);
+#pragma unroll
+                for (int q = 0; q < C::R; ++q) mult[q * C::NT + threadIdx.x] = lam[q] * sym.scale;
+            }
         }
     }
     mbar_wait(&bar, 0);
@@ -137,6 +154,11 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
         if (PRE && sym.real) {
 #pragma unroll
             for (int q = 0; q < C::R; ++q) v[q] = cscale(v[q], mult[q * C::NT + threadIdx.x]);
+        } else if (is_dead()) {
+            // lam = 0 for the whole column: the products spectral_regs would form with it
+#pragma unroll
+            for (int q = 0; q < C::R; ++q)
+                v[q] = sym.real ? cscale(v[q], 0.0 * sym.scale) : cscale(cmul(make_double2(0.0, 0.0), v[q]), sym.scale);
         } else {
             spectral_regs<N, C::R, C::TPL>(v, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
         }
@@ -768,7 +790,14 @@ k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol s
         u[b] = cadd(e, o);
         u[b + 8] = csub(e, o);
     }
-    spectral_pair8192(u, th, (int)h, sym, tw_all, acoef);
+    if (kx > sym.kzero) {
+        // a column of host-proved zero multipliers (FusedSymbol::kzero): the products with lam = 0
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            u[j] = sym.real ? cscale(u[j], 0.0 * sym.scale) : cscale(cmul(make_double2(0.0, 0.0), u[j]), sym.scale);
+    } else {
+        spectral_pair8192(u, th, (int)h, sym, tw_all, acoef);
+    }
     // inverse split for the own k = th + 256 b + 2048 h: CTA 0 keeps e and sends o, CTA 1 the reverse
     double2 keep[8], send[8];
     static_for<0, 8>([&](auto B) {

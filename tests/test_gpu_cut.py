@@ -70,6 +70,22 @@ def test_cut_bitwise_equal_and_vs_oracle(orc, dims, taps, T, expect_cut):
         assert rel_l2(cut, want) <= 1e-10
 
 
+@pytest.mark.parametrize("dims,taps,T,expect_cut", CASES + [([8192, 2048], box9(5), 100000, True)])
+def test_zero_column_shortcut_is_bitwise(orc, dims, taps, T, expect_cut, monkeypatch):
+    """The default fused pass takes the multipliers of host-proved zero columns as 0 without
+    evaluating the symbol (FusedSymbol::kzero); FSX_ZEROCOL=0 evaluates every column.  Same
+    bits, including the sign of every zero."""
+    k = R.kern_from(taps, 2)
+    n = int(np.prod(dims))
+    a0 = orc.splitmix_fill(5 + T % 11, n, True)
+    g = fs.FieldGrid(fs.GridShape(dims), a0)
+    monkeypatch.setenv("FSX_ZEROCOL", "1")
+    fast = fs.solve_periodic(g, K(k), T).data
+    monkeypatch.setenv("FSX_ZEROCOL", "0")
+    slow = fs.solve_periodic(g, K(k), T).data
+    assert np.array_equal(fast.view(np.int64), slow.view(np.int64))
+
+
 def test_cut_does_not_apply():
     shape = fs.GridShape([64, 64, 64])
     k3 = R.kern_from({(0, 0, 0): 0.4, (1, 0, 0): 0.3, (-1, 0, 0): 0.3}, 3)
