@@ -546,6 +546,19 @@ def run_gpu(args, cfg):
     cells_T = cfg.cells() * cfg.T
     value = cells_T * ws / (ms * 1e-3)
 
+    # disclosure: in the default 2D fused path the multipliers of half-spectrum columns the host
+    # proved to be exactly 0 are taken as 0 without evaluating the symbol (DESIGN 4b'); every
+    # column is still loaded, transformed both ways and stored
+    symbol_shortcut = None
+    if info["path"] == 1 and len(cfg.dims) == 2 and not f32 and max(cfg.dims[0], 0) >= 4096:
+        zc_on = os.environ.get("FSX_ZEROCOL", "1") != "0"
+        kept0, total0 = fs.spectral_cut_columns(shape, kern, cfg.T)
+        symbol_shortcut = {
+            "enabled": zc_on, "columns_proved_zero": (total0 - kept0) if zc_on else 0, "columns": total0,
+            "what": "multiplier 0 taken for host-proved zero columns without evaluating the symbol there; all "
+                    "columns still loaded, transformed forward and back, and stored; bit-identical result; "
+                    "FSX_ZEROCOL=0 evaluates every column"}
+
     # exact spectral cut (opt-in, fsx_options.spectral_cut): reported beside the
     # headline, which keeps the reference's full work.  Same steps, same flush;
     # the result must equal the full solve bit for bit.
@@ -656,6 +669,7 @@ def run_gpu(args, cfg):
             "storage": "f32 (fp32 storage mode: float grids in and out, fp64 arithmetic)" if f32 else "f64",
             "plan": info["path"],
             "wall_s_timed_region": wall,
+            "symbol_shortcut": symbol_shortcut,
         },
         "roofline": {
             "bound": "hbm",
