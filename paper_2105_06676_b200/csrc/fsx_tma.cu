@@ -766,13 +766,9 @@ k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol s
     for (int q = 0; q < 16; ++q) v[q] = tile[th + 256 * q];
     FF::run(v, th, tile, tw_all + NH);
     const double2 wt = __ldg(tw_all + N + th);  // W_8192^th; W_8192^(th + 256 q) = wt W_32^q
-    if (h == 1) {
-        static_for<0, 16>([&](auto Q) {
-            constexpr int q = decltype(Q)::value;
-            v[q] = cmul(v[q], cmul_const<q, 32, -1>(wt));
-        });
-    }
-    // exchange 1: the half of the k range the peer keeps, into its recv
+    // exchange 1: the half of the k range the peer keeps, into its recv -- O goes out raw and
+    // each CTA forms W^k O for the k it joins (the same products CTA 1 alone used to form for
+    // all 16 values before sending: the pair's critical path loses 64 FP64 instructions)
     {
         const unsigned dst = peer_smem(recv + th, peer), pbar = peer_smem(&bx1, peer);
 #pragma unroll
@@ -782,14 +778,15 @@ k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol s
     if (th == 0) mbar_arrive_peer(peer_smem(&bok, peer));  // the peer may write into this tile
     mbar_wait(&bx1, 0);
     double2 u[16];
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
+    static_for<0, 8>([&](auto B) {
+        constexpr int b = decltype(B)::value;
         const double2 r = recv[th + 256 * b];
         const double2 e = h == 0 ? v[b] : r;
-        const double2 o = h == 0 ? r : v[8 + b];
+        const double2 oraw = h == 0 ? r : v[8 + b];
+        const double2 o = h == 0 ? cmul(oraw, cmul_const<b, 32, -1>(wt)) : cmul(oraw, cmul_const<b + 8, 32, -1>(wt));
         u[b] = cadd(e, o);
         u[b + 8] = csub(e, o);
-    }
+    });
     if (kx > sym.kzero) {
         // a column of host-proved zero multipliers (FusedSymbol::kzero): the products with lam = 0
 #pragma unroll
