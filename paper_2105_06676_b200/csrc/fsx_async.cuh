@@ -106,6 +106,37 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+int cluster_policy();  // FSX_CLUSTER_POLICY: 0 driver default, 1 spread, 2 load balancing
+
+// launch_pdl for a __cluster_dims__ kernel, with the cluster scheduling policy preference
+// (where the CTAs of a cluster land relative to one another) selectable for A/B
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                      Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    if (pdl_enabled()) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    const int pol = cluster_policy();
+    if (pol == 1 || pol == 2) {
+        attr[n].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+        attr[n].val.clusterSchedulingPolicyPreference =
+            pol == 1 ? cudaClusterSchedulingPolicySpread : cudaClusterSchedulingPolicyLoadBalancing;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 }  // namespace fsx
 
 // ------------------------------------------------------------------ CTA-pair (cluster) helpers

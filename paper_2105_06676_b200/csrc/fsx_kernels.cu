@@ -1213,6 +1213,15 @@ bool pdl_enabled() {
     return v == 1;
 }
 
+int cluster_policy() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("FSX_CLUSTER_POLICY");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
 int kernel_prepare(const void* fn, size_t smem, int threads) {
     struct Info {
         size_t smem = 0;
@@ -1504,7 +1513,7 @@ static cudaError_t rowpair_n(const RowPairArgs& a, cudaStream_t s) {
         if (rowpair_cluster() && a.N1 >= 4) {
             const size_t smem = (size_t)(N2 + N2 / 2) * sizeof(double2);
             kernel_prepare((const void*)k_rowpair_c<N2>, smem);
-            return launch_pdl(k_rowpair_c<N2>, dim3((unsigned)a.N1), dim3(N2 / 16), smem, s, a);
+            return launch_pdl_cluster(k_rowpair_c<N2>, dim3((unsigned)a.N1), dim3(N2 / 16), smem, s, a);
         }
     }
     using C = Cfg<N2>;

@@ -1183,7 +1183,7 @@ cudaError_t launch_fused_halves(const void* tensor_map2, const AxisGeom& g, cons
         const size_t smem2 = (4096 + 2048) * sizeof(double2);
         kernel_prepare((const void*)k_fused8192c, smem2);
         const int pfd = base != nullptr && g.inner % 8 == 0 ? f8192_pfd() : 0;
-        return launch_pdl(k_fused8192c, dim3((unsigned)(2 * g.ncols)), dim3(256), smem2, s, map, g, sym, tw,
+        return launch_pdl_cluster(k_fused8192c, dim3((unsigned)(2 * g.ncols)), dim3(256), smem2, s, map, g, sym, tw,
                           pfd > 0 ? base : (const double2*)nullptr, pfd);
     }
     const size_t smem = 8192 * sizeof(double2);

@@ -25,7 +25,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) k_place(int*
     }
 }
 
-int main() {
+static void run(int policy, const char* name) {
     const int n = 8194;
     int* d;
     long long* t;
@@ -33,12 +33,31 @@ int main() {
     cudaMalloc(&t, n * sizeof(long long));
     const size_t smem = (4096 + 2048) * 16;
     cudaFuncSetAttribute(k_place, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_place<<<n, 256, smem>>>(d, t);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+    attr[0].val.clusterSchedulingPolicyPreference =
+        policy == 1 ? cudaClusterSchedulingPolicySpread : cudaClusterSchedulingPolicyLoadBalancing;
+    cfg.attrs = attr;
+    cfg.numAttrs = policy ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k_place, d, t);
     cudaError_t e = cudaDeviceSynchronize();
     std::vector<int> h(n);
     cudaMemcpy(h.data(), d, n * sizeof(int), cudaMemcpyDeviceToHost);
     int same = 0;
     for (int i = 0; i < n; i += 2) same += h[i] == h[i + 1];
-    printf("%s: %d of %d pairs on one SM (%.1f %%)\n", cudaGetErrorString(e), same, n / 2, 100.0 * same / (n / 2));
+    printf("%-16s %s: %d of %d pairs on one SM (%.1f %%)\n", name, cudaGetErrorString(e), same, n / 2,
+           100.0 * same / (n / 2));
+    cudaFree(d);
+    cudaFree(t);
+}
+
+int main() {
+    run(0, "default");
+    run(1, "spread");
+    run(2, "load balancing");
     return 0;
 }
