@@ -28,6 +28,21 @@ __device__ __forceinline__ double2 eplus_tab(const double2* tw_all, i64 n, i64 x
     return cconj(__ldg(tw_all + n + (x & (n - 1))));
 }
 
+// The product of a finite u with a zero multiplier, as the fused passes form it:
+//   real symbol     cscale(u, 0.0 * scale)             = (0 * u.x, 0 * u.y)
+//   complex symbol  cscale(cmul((0, 0), u), scale),  cmul = (fma(0, u.x, -(0 * u.y)), fma(0, u.y, 0 * u.x))
+// with scale > 0.  Every result is a zero; only its sign depends on u: 0 * x carries x's sign, and a
+// sum of two zeros is -0 only when both are.  So the signs follow from u's sign bits alone, without
+// touching the FP64 pipe (96 of its instructions per thread in a zero column otherwise).  A non-finite
+// u would give NaN in the full evaluation; it cannot hide here, because its whole row and therefore
+// the always-evaluated column 0 is non-finite too (the solve raises NumericError either way).
+__device__ __forceinline__ double2 zero_products(double2 u, bool real_symbol) {
+    const unsigned sx = (unsigned)__double2hiint(u.x), sy = (unsigned)__double2hiint(u.y);
+    const unsigned rx = real_symbol ? sx : (sx & ~sy);  // complex: (+-0 of u.x) + (-+0 of u.y)
+    const unsigned ry = real_symbol ? sy : (sx & sy);   //          (+-0 of u.y) + (+-0 of u.x)
+    return make_double2(__hiloint2double((int)(rx & 0x80000000u), 0), __hiloint2double((int)(ry & 0x80000000u), 0));
+}
+
 // e * i^m for m in 0..3 (exact: swaps and sign flips)
 __device__ __forceinline__ double2 rot_quarter(double2 e, int m) {
     const double x = (m & 1) ? e.y : e.x, y = (m & 1) ? e.x : e.y;

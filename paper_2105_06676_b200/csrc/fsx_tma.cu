@@ -157,8 +157,7 @@ k_cols_tma(const __grid_constant__ CUtensorMap map, AxisGeom g, FusedSymbol sym,
         } else if (is_dead()) {
             // lam = 0 for the whole column: the products spectral_regs would form with it
 #pragma unroll
-            for (int q = 0; q < C::R; ++q)
-                v[q] = sym.real ? cscale(v[q], 0.0 * sym.scale) : cscale(cmul(make_double2(0.0, 0.0), v[q]), sym.scale);
+            for (int q = 0; q < C::R; ++q) v[q] = zero_products(v[q], sym.real != 0);
         } else {
             spectral_regs<N, C::R, C::TPL>(v, t, sym, tw_all, [&](int gi) { return acoef[gi][w]; });
         }
@@ -788,10 +787,10 @@ k_fused8192c(const __grid_constant__ CUtensorMap map2, AxisGeom g, FusedSymbol s
         u[b + 8] = csub(e, o);
     });
     if (kx > sym.kzero) {
-        // a column of host-proved zero multipliers (FusedSymbol::kzero): the products with lam = 0
+        // a column of host-proved zero multipliers (FusedSymbol::kzero): the products with lam = 0,
+        // i.e. zeros whose signs are those the multiplications would give (zero_products)
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            u[j] = sym.real ? cscale(u[j], 0.0 * sym.scale) : cscale(cmul(make_double2(0.0, 0.0), u[j]), sym.scale);
+        for (int j = 0; j < 16; ++j) u[j] = zero_products(u[j], sym.real != 0);
     } else {
         spectral_pair8192(u, th, (int)h, sym, tw_all, acoef);
     }
