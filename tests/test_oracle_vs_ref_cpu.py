@@ -7,7 +7,6 @@ Bar: bit-for-bit.  The restatement follows the reference operation for
 operation and both are built with the reference's flags, so every case below
 is required to be identical, not merely close.
 """
-import os
 
 import numpy as np
 import pytest

@@ -16,7 +16,6 @@ import sys
 import numpy as np
 import pytest
 
-import refutil as R
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.join(HERE, "golden"))
