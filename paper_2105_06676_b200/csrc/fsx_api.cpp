@@ -1131,6 +1131,11 @@ struct SlabPlan {
     alignas(64) unsigned char mapH[128];
     bool tmaH = false;
     fsx::AxisGeom axy;  // 3D local y pass
+    // 2D: the largest global column not provably zero for (kz_taps, kz_T) (FusedSymbol::kzero), cached
+    bool kz_valid = false;
+    Taps kz_taps;
+    u64 kz_T = 0;
+    i64 kz = -1;
 };
 
 std::mutex g_slab_mu;  // guards the g_slabs map (entries are per device, used under that device's lock)
@@ -1260,6 +1265,19 @@ void slab_spectral(SlabPlan& sp, Device& dev, const Taps& taps, u64 T, double2* 
     for (i64 d : sp.dims) view.cells *= d;
     fsx::FusedSymbol sym = fused_symbol(view, taps, T);
     sym.c_off = (i64)sp.r * sp.CB;
+    if (rk == 2 && zero_columns_enabled()) {
+        // host-proved zero columns (global kx, as fused_col_freqs gives it with c_off): same shortcut
+        // and same bits as the single-GPU fused pass
+        if (!(sp.kz_valid && sp.kz_T == T && sp.kz_taps.map == taps.map)) {
+            view.kind = kFusedR2C;
+            view.m = 1;
+            sp.kz = compute_kcut(view, taps, T);
+            sp.kz_taps = taps;
+            sp.kz_T = T;
+            sp.kz_valid = true;
+        }
+        if (sp.kz >= 0) sym.kzero = sp.kz;
+    }
     const i64 inner = rk == 3 ? sp.n1b * sp.Pp : sp.CB;
     const fsx::AxisGeom g{sp.dims[0], inner, 1, sp.dims[0] * inner, inner};
     alignas(64) unsigned char map[128];
