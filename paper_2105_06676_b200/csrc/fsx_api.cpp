@@ -22,6 +22,7 @@
 #include <cstring>
 #include <map>
 #include <set>
+#include <algorithm>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -279,11 +280,8 @@ struct Plan {
     TableSet tables;
     // kind 1
     i64 L = 0, M = 0, P = 0, rows = 0;
-    // exact spectral cut (fsx_options.spectral_cut): kcut for (cut_taps, cut_T), cached
-    bool cut_valid = false;
-    Taps cut_taps;
-    u64 cut_T = 0;
-    i64 kcut = -1;
+    // exact spectral cut / zero columns: column bounds per taps and the cut per T, cached (ColumnCut)
+    std::shared_ptr<struct ColumnCut> cut;
     fsx::AxisGeom ax1, ax0;
     alignas(64) unsigned char map0[128], map1[128];  // CUtensorMaps for TMA column passes
     alignas(64) unsigned char map2[128];             // parity-split view (8192-point halves pass)
@@ -785,29 +783,83 @@ fsx::FusedSymbol fused_symbol(const Plan& p, const Taps& taps, u64 T, const Taps
 // with it a non-finite input -- always goes through), or -1 when the cut does
 // not apply.  Columns above it are neither stored by the forward rows, nor
 // transformed, nor read by the inverse rows (which take them as 0).
-i64 compute_kcut(const Plan& p, const Taps& taps, u64 T) {
-    if (p.kind != kFusedR2C || p.dims.size() != 2 || p.m != 1 || !fsx::rows_f32_ok(p.L)) return -1;
-    const double neg = std::exp2(-2200.0 / (double)T);
-    if (!(neg > 0.0)) return -1;
-    const double thr = neg * (1.0 - 1e-9);
+// The bounds B(kx)^2 do not depend on T, so they are computed once per (plan, taps) --
+// exact integer phase reduction, one cos/sin pair per distinct last-axis offset and column --
+// and a new T costs only the threshold scan (a caller stepping T pays microseconds, not the
+// ~M trigonometric evaluations, on every solve).
+bool column_cut_applies(const Plan& p) {
+    return p.kind == kFusedR2C && p.dims.size() == 2 && p.m == 1 && fsx::rows_f32_ok(p.L);
+}
+
+std::vector<double> column_bounds_sq(const Plan& p, const Taps& taps) {
     std::map<i64, std::vector<std::pair<i64, double>>> groups;  // O_g -> (o_last, c)
-    for (const auto& kv : taps.map) groups[kv.first[p.axes[0]]].push_back({kv.first[p.axes[1]], kv.second[0]});
+    std::vector<i64> offs;                                      // distinct o_last
+    for (const auto& kv : taps.map) {
+        const i64 ol = kv.first[p.axes[1]];
+        groups[kv.first[p.axes[0]]].push_back({ol, kv.second[0]});
+        if (std::find(offs.begin(), offs.end(), ol) == offs.end()) offs.push_back(ol);
+    }
+    // each group's taps as (index into offs, c)
+    std::vector<std::vector<std::pair<size_t, double>>> gs;
+    for (const auto& g : groups) {
+        gs.emplace_back();
+        for (const auto& oc : g.second)
+            gs.back().push_back({(size_t)(std::find(offs.begin(), offs.end(), oc.first) - offs.begin()), oc.second});
+    }
     const double w = 2.0 * 3.14159265358979323846 / (double)p.L;
-    for (i64 kx = p.M; kx > 0; --kx) {
+    std::vector<double> bsq((size_t)p.M + 1, 0.0), cs(offs.size()), sn(offs.size());
+    for (i64 kx = 0; kx <= p.M; ++kx) {
+        for (size_t a = 0; a < offs.size(); ++a) {
+            const i64 ph = ((kx * offs[a]) % p.L + p.L) % p.L;  // exact integer phase
+            cs[a] = std::cos(w * (double)ph);
+            sn[a] = std::sin(w * (double)ph);
+        }
         double B = 0.0;
-        for (const auto& g : groups) {
+        for (const auto& g : gs) {
             double re = 0.0, im = 0.0;
-            for (const auto& oc : g.second) {
-                const i64 ph = ((kx * oc.first) % p.L + p.L) % p.L;  // exact integer phase
-                re += oc.second * std::cos(w * (double)ph);
-                im += oc.second * std::sin(w * (double)ph);
+            for (const auto& oc : g) {
+                re += oc.second * cs[oc.first];
+                im += oc.second * sn[oc.first];
             }
             B += std::sqrt(re * re + im * im);
         }
-        if (B * B >= thr) return kx;
+        bsq[(size_t)kx] = B * B;
     }
+    return bsq;
+}
+
+i64 cut_from_bounds(const std::vector<double>& bsq, u64 T) {
+    const double neg = std::exp2(-2200.0 / (double)T);
+    if (!(neg > 0.0)) return -1;
+    const double thr = neg * (1.0 - 1e-9);
+    for (i64 kx = (i64)bsq.size() - 1; kx > 0; --kx)
+        if (bsq[(size_t)kx] >= thr) return kx;
     return 0;
 }
+
+// cache of the above: bounds per taps, cut per T
+struct ColumnCut {
+    bool taps_valid = false, t_valid = false;
+    Taps taps;
+    std::vector<double> bsq;
+    u64 T = 0;
+    i64 kcut = -1;
+    i64 get(const Plan& p, const Taps& tp, u64 t) {
+        if (!column_cut_applies(p)) return -1;
+        if (!(taps_valid && taps.map == tp.map)) {
+            bsq = column_bounds_sq(p, tp);
+            taps = tp;
+            taps_valid = true;
+            t_valid = false;
+        }
+        if (!(t_valid && T == t)) {
+            kcut = cut_from_bounds(bsq, t);
+            T = t;
+            t_valid = true;
+        }
+        return kcut;
+    }
+};
 
 // FSX_ZEROCOL=0: the fused pass evaluates the symbol of every column (A/B and the bitwise
 // test; read per solve so a test can flip it in-process)
@@ -817,13 +869,8 @@ static bool zero_columns_enabled() {
 }
 
 i64 plan_kcut(Plan& p, const Taps& taps, u64 T) {
-    if (!(p.cut_valid && p.cut_T == T && p.cut_taps.map == taps.map)) {
-        p.kcut = compute_kcut(p, taps, T);
-        p.cut_taps = taps;
-        p.cut_T = T;
-        p.cut_valid = true;
-    }
-    return p.kcut;
+    if (!p.cut) p.cut = std::make_shared<ColumnCut>();
+    return p.cut->get(p, taps, T);
 }
 
 // The implicit solve fuses into plan 1 when the symbol is real and the fused
@@ -1131,11 +1178,8 @@ struct SlabPlan {
     alignas(64) unsigned char mapH[128];
     bool tmaH = false;
     fsx::AxisGeom axy;  // 3D local y pass
-    // 2D: the largest global column not provably zero for (kz_taps, kz_T) (FusedSymbol::kzero), cached
-    bool kz_valid = false;
-    Taps kz_taps;
-    u64 kz_T = 0;
-    i64 kz = -1;
+    // 2D: the largest global column not provably zero (FusedSymbol::kzero), cached (ColumnCut)
+    std::shared_ptr<struct ColumnCut> cut;
 };
 
 std::mutex g_slab_mu;  // guards the g_slabs map (entries are per device, used under that device's lock)
@@ -1268,15 +1312,11 @@ void slab_spectral(SlabPlan& sp, Device& dev, const Taps& taps, u64 T, double2* 
     if (rk == 2 && zero_columns_enabled()) {
         // host-proved zero columns (global kx, as fused_col_freqs gives it with c_off): same shortcut
         // and same bits as the single-GPU fused pass
-        if (!(sp.kz_valid && sp.kz_T == T && sp.kz_taps.map == taps.map)) {
-            view.kind = kFusedR2C;
-            view.m = 1;
-            sp.kz = compute_kcut(view, taps, T);
-            sp.kz_taps = taps;
-            sp.kz_T = T;
-            sp.kz_valid = true;
-        }
-        if (sp.kz >= 0) sym.kzero = sp.kz;
+        view.kind = kFusedR2C;
+        view.m = 1;
+        if (!sp.cut) sp.cut = std::make_shared<ColumnCut>();
+        const i64 kz = sp.cut->get(view, taps, T);
+        if (kz >= 0) sym.kzero = kz;
     }
     const i64 inner = rk == 3 ? sp.n1b * sp.Pp : sp.CB;
     const fsx::AxisGeom g{sp.dims[0], inner, 1, sp.dims[0] * inner, inner};
